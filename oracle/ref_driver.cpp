@@ -1,0 +1,453 @@
+// Oracle driver (TEST INFRASTRUCTURE ONLY — never linked into the product).
+//
+// Runs the UNMODIFIED reference library (proj/src/*.cpp, compiled by
+// oracle/Makefile into oracle/_ref/) through its public API on a system read
+// from the reference's external formats, and exports every setup product and
+// apply/solve result as .npy files so the GPU path can be checked against it
+// (SURVEY.md §8c protocol: exported-factor apply parity + end-to-end gates).
+//
+// Composition mirrors ProblemContext + run_with_context
+// (proj/src/harness.cpp:63-139) without harness.cpp itself (which needs the
+// absent vendor/json.hpp):
+//   read_matrix_market / read_vector / read_partition   sparse.cpp:89-138, partition.cpp:212-233
+//   check_minimal_overlap                               partition.cpp:137-156 (harness.cpp:85-91)
+//   build_pou, Splitting, GeneoContext                  partition.cpp:94-108, splitting.cpp:86-105
+//   OneLevel(NN), build_coarse | fixed-k coarse, TwoLevel(HYBRID)   preconditioner.cpp:20-82, coarse.cpp:113-154
+//   build_w, AwgPreconditioner                          preconditioner.cpp:84-147
+//   pcg                                                 krylov.cpp:36-124
+// The fixed-k selection (BASELINE.json configs 3 and 5) is built from public
+// API exactly like build_coarse, with k_s = max(k, n_nonpos(s)) extended over
+// clusters |lambda_{k+1} - lambda_k| <= 1e-8.
+#include <chrono>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "awg/coarse.hpp"
+#include "awg/dense.hpp"
+#include "awg/krylov.hpp"
+#include "awg/partition.hpp"
+#include "awg/preconditioner.hpp"
+#include "awg/sparse.hpp"
+#include "awg/splitting.hpp"
+
+using namespace awg;
+
+namespace {
+
+double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// --- minimal .npy writer (v1.0, little-endian) -------------------------------
+void write_npy(const std::string& path, const char* descr, const std::vector<long>& shape,
+               bool fortran, const void* data, size_t elem_size) {
+  std::string sh = "(";
+  size_t count = 1;
+  for (size_t i = 0; i < shape.size(); ++i) {
+    sh += std::to_string(shape[i]);
+    sh += (shape.size() == 1) ? "," : (i + 1 < shape.size() ? ", " : "");
+    count *= size_t(shape[i]);
+  }
+  sh += ")";
+  std::string header = std::string("{'descr': '") + descr + "', 'fortran_order': " +
+                       (fortran ? "True" : "False") + ", 'shape': " + sh + ", }";
+  size_t total = 10 + header.size() + 1;
+  size_t pad = (64 - total % 64) % 64;
+  header += std::string(pad, ' ');
+  header += '\n';
+  FILE* f = std::fopen(path.c_str(), "wb");
+  if (!f) {
+    std::fprintf(stderr, "cannot write %s\n", path.c_str());
+    std::exit(2);
+  }
+  const unsigned char magic[8] = {0x93, 'N', 'U', 'M', 'P', 'Y', 1, 0};
+  std::fwrite(magic, 1, 8, f);
+  uint16_t hl = uint16_t(header.size());
+  std::fwrite(&hl, 2, 1, f);
+  std::fwrite(header.data(), 1, header.size(), f);
+  if (count) std::fwrite(data, elem_size, count, f);
+  std::fclose(f);
+}
+void npy_d(const std::string& dir, const std::string& name, const std::vector<double>& v) {
+  write_npy(dir + "/" + name + ".npy", "<f8", {long(v.size())}, false, v.data(), 8);
+}
+void npy_i(const std::string& dir, const std::string& name, const std::vector<int>& v) {
+  write_npy(dir + "/" + name + ".npy", "<i4", {long(v.size())}, false, v.data(), 4);
+}
+void npy_mat(const std::string& dir, const std::string& name, const DenseMatrix& m) {
+  write_npy(dir + "/" + name + ".npy", "<f8", {long(m.rows), long(m.cols)}, true, m.a.data(), 8);
+}
+void npy_rows(const std::string& dir, const std::string& name, const std::vector<std::vector<double>>& rows) {
+  std::vector<double> flat;
+  for (auto& r : rows) flat.insert(flat.end(), r.begin(), r.end());
+  long n = rows.empty() ? 0 : long(rows[0].size());
+  write_npy(dir + "/" + name + ".npy", "<f8", {long(rows.size()), n}, false, flat.data(), 8);
+}
+
+// SplitMix64 uniform stream, identical to paper_2106_10913_b200/problems.py.
+std::vector<double> uniform_vec(uint64_t seed, int n, double a, double b) {
+  std::vector<double> v(n);
+  uint64_t state = seed;
+  for (int i = 0; i < n; ++i) {
+    state += 0x9E3779B97F4A7C15ull;
+    uint64_t z = state;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z = z ^ (z >> 31);
+    double u = double(z >> 11) * 0x1.0p-53;
+    v[i] = a + (b - a) * u;
+  }
+  return v;
+}
+
+struct Args {
+  std::string prefix, out;
+  double tau = -1.0;
+  int fixed_k = -1;
+  std::string awg = "ad";
+  std::string comp = "hybrid";
+  double rtol = 1e-8;
+  double w_rtol = 1e-10;
+  int maxit = 10000;
+  int n_apply = 3;
+  int export_factors = 1;
+  int apply_reps = 0;
+  int no_solve = 0;
+  int export_dense = 0;
+};
+
+Args parse(int argc, char** argv) {
+  Args a;
+  if (argc < 3) {
+    std::fprintf(stderr,
+                 "usage: ref_driver <prefix> <outdir> [--tau T | --fixed-k K] [--awg ad|hyb|inex|none]\n"
+                 "       [--comp hybrid|additive] [--rtol R] [--w-rtol W] [--maxit M] [--n-apply M]\n"
+                 "       [--export-factors 0|1] [--apply-reps R] [--no-solve]\n");
+    std::exit(2);
+  }
+  a.prefix = argv[1];
+  a.out = argv[2];
+  for (int i = 3; i < argc; ++i) {
+    std::string k = argv[i];
+    auto next = [&]() -> std::string {
+      if (i + 1 >= argc) {
+        std::fprintf(stderr, "missing value for %s\n", k.c_str());
+        std::exit(2);
+      }
+      return argv[++i];
+    };
+    if (k == "--tau") a.tau = std::stod(next());
+    else if (k == "--fixed-k") a.fixed_k = std::stoi(next());
+    else if (k == "--awg") a.awg = next();
+    else if (k == "--comp") a.comp = next();
+    else if (k == "--rtol") a.rtol = std::stod(next());
+    else if (k == "--w-rtol") a.w_rtol = std::stod(next());
+    else if (k == "--maxit") a.maxit = std::stoi(next());
+    else if (k == "--n-apply") a.n_apply = std::stoi(next());
+    else if (k == "--export-factors") a.export_factors = std::stoi(next());
+    else if (k == "--apply-reps") a.apply_reps = std::stoi(next());
+    else if (k == "--no-solve") a.no_solve = 1;
+    else if (k == "--export-dense") a.export_dense = std::stoi(next());
+    else {
+      std::fprintf(stderr, "unknown flag %s\n", k.c_str());
+      std::exit(2);
+    }
+  }
+  return a;
+}
+
+AwgMode mode_of(const std::string& s) {
+  if (s == "none") return AwgMode::NONE;
+  if (s == "ad") return AwgMode::AD;
+  if (s == "hyb") return AwgMode::HYB;
+  if (s == "inex") return AwgMode::INEX;
+  std::fprintf(stderr, "bad awg mode %s\n", s.c_str());
+  std::exit(2);
+}
+
+// Fixed-k GenEO coarse space from public API, mirroring build_coarse
+// (coarse.cpp:113-154) with a different per-subdomain column count.
+CoarseSpace fixed_k_coarse(GeneoContext& ctx, int k, std::vector<int>& ks) {
+  const Splitting& split = ctx.splitting();
+  const Partition& part = split.partition();
+  const int n = split.n();
+  std::vector<std::pair<int, DenseMatrix>> picked;
+  ks.clear();
+  for (int s = 0; s < part.count(); ++s) {
+    const EigenDecomposition& e = ctx.pencil_nn(s);
+    const int ns = int(e.eigenvalues.size());
+    int kk = std::max(k, split.splits()[s].n_nonpos);
+    kk = std::min(kk, ns);
+    while (kk > 0 && kk < ns && std::abs(e.eigenvalues[kk] - e.eigenvalues[kk - 1]) <= 1e-8) ++kk;
+    DenseMatrix y(e.eigenvectors.rows, kk);
+    for (int c = 0; c < kk; ++c) std::copy_n(e.eigenvectors.col(c), e.eigenvectors.rows, y.col(c));
+    picked.emplace_back(s, std::move(y));
+    ks.push_back(kk);
+  }
+  int n0 = 0;
+  for (auto& p : picked) n0 += p.second.cols;
+  CoarseSpace cs;
+  cs.z = DenseMatrix(n, n0);
+  int col = 0;
+  for (auto& [s, y] : picked)
+    for (int c = 0; c < y.cols; ++c, ++col) split.prolong_add(s, y.col(c), cs.z.col(col));
+  DenseMatrix g(n0, n0);
+  std::vector<double> tmp(n);
+  for (int j = 0; j < n0; ++j) {
+    split.apply_Aplus(cs.z.col(j), tmp.data());
+    matvec_transpose(cs.z, tmp.data(), g.col(j));
+  }
+  symmetrize(g);
+  cs.k0 = rank_revealing_sym_factor(g);
+  return cs;
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+  const Args args = parse(argc, argv);
+  std::string cmd = "mkdir -p '" + args.out + "'";
+  if (std::system(cmd.c_str()) != 0) return 2;
+  const std::string& out = args.out;
+  FILE* js = std::fopen((out + "/summary.json").c_str(), "w");
+  std::fprintf(js, "{\n");
+
+  double t0 = now_s();
+  SparseSymMatrix a = read_matrix_market(args.prefix + ".mtx");
+  std::vector<double> b = read_vector(args.prefix + ".rhs");
+  Partition part = read_partition(args.prefix + ".part", a.n);
+  const auto violations = check_minimal_overlap(a, part);
+  if (!violations.empty()) {
+    std::fprintf(stderr, "minimal overlap violated\n");
+    return 3;
+  }
+  double t_read = now_s() - t0;
+
+  t0 = now_s();
+  PartitionOfUnity pou = build_pou(part);
+  Splitting split(a, part, pou);
+  GeneoContext geneo(split);
+  double t_split = now_s() - t0;
+
+  const int N = part.count();
+  const int n = a.n;
+  std::vector<int> sizes(N), n_nonpos(N), n_zero(N);
+  std::vector<double> eps(N);
+  for (int s = 0; s < N; ++s) {
+    sizes[s] = part.size_of(s);
+    n_nonpos[s] = split.splits()[s].n_nonpos;
+    n_zero[s] = split.splits()[s].n_zero;
+    eps[s] = split.splits()[s].eps_zero;
+  }
+
+  t0 = now_s();
+  std::vector<int> ks;
+  CoarseSpace cs;
+  if (args.fixed_k > 0) {
+    cs = fixed_k_coarse(geneo, args.fixed_k, ks);
+  } else {
+    const double tau = args.tau > 0 ? args.tau : 0.1;
+    // build_coarse with ThresholdSpec::nn; ks recovered from the pencils.
+    for (int s = 0; s < N; ++s) {
+      const auto& e = geneo.pencil_nn(s);
+      int m = 0;
+      while (m < int(e.eigenvalues.size()) && e.eigenvalues[m] < tau) ++m;
+      ks.push_back(m);
+    }
+    cs = build_coarse(ThresholdSpec::nn(tau), geneo);
+  }
+  double t_coarse = now_s() - t0;
+  const Composition comp = args.comp == "additive" ? Composition::ADDITIVE : Composition::HYBRID;
+  auto h2 = std::make_shared<TwoLevel>(OneLevel(OneLevelKind::NN, split), cs, comp, split);
+
+  t0 = now_s();
+  const AwgMode mode = mode_of(args.awg);
+  std::shared_ptr<const SecondCoarse> sc;
+  if (mode != AwgMode::NONE) sc = std::make_shared<SecondCoarse>(build_w(split, *h2, args.w_rtol));
+  double t_w = now_s() - t0;
+  t0 = now_s();
+  AwgPreconditioner h3(mode, h2, sc, split);
+  std::unique_ptr<AwgPreconditioner> h3_ad, h3_hyb, h3_inex;
+  if (sc) {
+    h3_ad = std::make_unique<AwgPreconditioner>(AwgMode::AD, h2, sc, split);
+    h3_hyb = std::make_unique<AwgPreconditioner>(AwgMode::HYB, h2, sc, split);
+    h3_inex = std::make_unique<AwgPreconditioner>(AwgMode::INEX, h2, sc, split);
+  }
+  double t_h3 = now_s() - t0;
+
+  std::fprintf(js, "  \"n\": %d, \"nnz\": %d, \"n_sub\": %d,\n", n, a.nnz(), N);
+  std::fprintf(js, "  \"n0\": %d, \"r0\": %d, \"n_minus\": %d, \"rw\": %d,\n", cs.dim(), cs.retained_rank(),
+               sc ? sc->n_minus() : 0, sc ? sc->kw.rank() : 0);
+  std::fprintf(js, "  \"t_read\": %.6f, \"t_splitting\": %.6f, \"t_coarse\": %.6f, \"t_w\": %.6f, \"t_h3\": %.6f,\n",
+               t_read, t_split, t_coarse, t_w, t_h3);
+
+  // ---- exports -----------------------------------------------------------
+  npy_i(out, "sizes", sizes);
+  npy_i(out, "n_nonpos", n_nonpos);
+  npy_i(out, "n_zero", n_zero);
+  npy_d(out, "eps_zero", eps);
+  npy_i(out, "ks", ks);
+  npy_i(out, "multiplicity", pou.multiplicity);
+  {
+    std::vector<double> lam, plam;
+    for (int s = 0; s < N; ++s) {
+      auto& e = split.splits()[s].eig.eigenvalues;
+      lam.insert(lam.end(), e.begin(), e.end());
+      auto& pe = geneo.pencil_nn(s).eigenvalues;
+      plam.insert(plam.end(), pe.begin(), pe.end());
+    }
+    npy_d(out, "lam", lam);
+    npy_d(out, "pencil_lam", plam);
+  }
+  npy_i(out, "k0_retained", cs.k0.retained);
+  npy_mat(out, "k0_l11", cs.k0.l11);
+  {
+    // The coarse operator fed to rank_revealing_sym_factor, recomputed with
+    // the same operations as coarse.cpp:145-151 (deterministic, identical).
+    const int n0 = cs.dim();
+    DenseMatrix g(n0, n0);
+    std::vector<double> tmp(n);
+    for (int j = 0; j < n0; ++j) {
+      split.apply_Aplus(cs.z.col(j), tmp.data());
+      matvec_transpose(cs.z, tmp.data(), g.col(j));
+    }
+    symmetrize(g);
+    npy_mat(out, "k0_G", g);
+  }
+  if (args.export_dense) {
+    // B^s, weighted A+^s and R A+ R^T per subdomain (tiny problems only).
+    std::vector<double> bs, ma, mb;
+    auto bsv = build_Bs(a, part);
+    for (int s = 0; s < N; ++s) {
+      bs.insert(bs.end(), bsv[s].a.begin(), bsv[s].a.end());
+      DenseMatrix w = geneo.weighted_asplus(s);
+      ma.insert(ma.end(), w.a.begin(), w.a.end());
+      const DenseMatrix& b2 = geneo.aplus_block(s);
+      mb.insert(mb.end(), b2.a.begin(), b2.a.end());
+    }
+    npy_d(out, "Bs", bs);
+    npy_d(out, "pencil_MA", ma);
+    npy_d(out, "pencil_MB", mb);
+  }
+  if (args.export_factors) {
+    std::vector<double> V, Y;
+    for (int s = 0; s < N; ++s) {
+      auto& m = split.splits()[s].eig.eigenvectors.a;
+      V.insert(V.end(), m.begin(), m.end());
+      auto& pm = geneo.pencil_nn(s).eigenvectors;
+      Y.insert(Y.end(), pm.a.begin(), pm.a.begin() + size_t(pm.rows) * ks[s]);
+    }
+    npy_d(out, "V", V);
+    npy_d(out, "Y", Y);
+    // The reference keeps Z dense (n x n0); export it too for cross-checks
+    // on small problems only.
+    if (size_t(n) * cs.dim() <= (size_t(1) << 24)) npy_mat(out, "Z", cs.z);
+  }
+  if (sc) {
+    npy_d(out, "neg_weights", sc->neg_weights);
+    npy_i(out, "w_inner_iterations", sc->inner_iterations);
+    npy_i(out, "kw_retained", sc->kw.retained);
+    npy_mat(out, "kw_l11", sc->kw.l11);
+    {
+      // W^T A W as in preconditioner.cpp:119-125.
+      const int m = sc->n_minus();
+      DenseMatrix g(m, m);
+      std::vector<double> tmp(n);
+      for (int j = 0; j < m; ++j) {
+        spmv(a, sc->w.col(j), tmp.data());
+        matvec_transpose(sc->w, tmp.data(), g.col(j));
+      }
+      symmetrize(g);
+      npy_mat(out, "kw_G", g);
+    }
+    if (args.export_factors) {
+      npy_mat(out, "W", sc->w);
+      npy_mat(out, "v_minus", sc->v_minus);
+    }
+  }
+
+  // ---- applies on seeded vectors -----------------------------------------
+  {
+    std::vector<std::vector<double>> X, yA, yAm, yAp, yH1, yQ, yQW, yH2, yAD, yHYB, yINEX, yPI3, yPI3T;
+    OneLevel h1(OneLevelKind::NN, split);
+    for (int m = 0; m < args.n_apply; ++m) {
+      std::vector<double> x = uniform_vec(1000 + m, n, -1.0, 1.0), y(n);
+      X.push_back(x);
+      spmv(a, x.data(), y.data()); yA.push_back(y);
+      split.apply_Aminus(x.data(), y.data()); yAm.push_back(y);
+      split.apply_Aplus(x.data(), y.data()); yAp.push_back(y);
+      h1.apply(x.data(), y.data()); yH1.push_back(y);
+      coarse_correct(cs, x.data(), y.data()); yQ.push_back(y);
+      h2->apply(x.data(), y.data()); yH2.push_back(y);
+      if (sc) {
+        // second_correct (preconditioner.cpp:149-159) is private: same ops
+        // through the public SecondCoarse members.
+        const int nm = sc->n_minus();
+        std::vector<double> wx(nm), c(nm);
+        matvec_transpose(sc->w, x.data(), wx.data());
+        rank_revealing_solve(sc->kw, wx.data(), c.data());
+        matvec(sc->w, c.data(), y.data());
+        yQW.push_back(y);
+        h3_ad->apply(x.data(), y.data()); yAD.push_back(y);
+        h3_hyb->apply(x.data(), y.data()); yHYB.push_back(y);
+        h3_inex->apply(x.data(), y.data()); yINEX.push_back(y);
+        h3_ad->apply_pi3(x.data(), y.data()); yPI3.push_back(y);
+        h3_ad->apply_pi3_transpose(x.data(), y.data()); yPI3T.push_back(y);
+      }
+    }
+    npy_rows(out, "x_apply", X);
+    npy_rows(out, "y_A", yA);
+    npy_rows(out, "y_Aminus", yAm);
+    npy_rows(out, "y_Aplus", yAp);
+    npy_rows(out, "y_H1", yH1);
+    npy_rows(out, "y_Q", yQ);
+    npy_rows(out, "y_H2", yH2);
+    if (sc) {
+      npy_rows(out, "y_QW", yQW);
+      npy_rows(out, "y_H3ad", yAD);
+      npy_rows(out, "y_H3hyb", yHYB);
+      npy_rows(out, "y_H3inex", yINEX);
+      npy_rows(out, "y_PI3", yPI3);
+      npy_rows(out, "y_PI3T", yPI3T);
+    }
+  }
+
+  // ---- timed H3 apply loop (CPU baseline) --------------------------------
+  if (args.apply_reps > 0) {
+    std::vector<double> x = uniform_vec(77, n, -1.0, 1.0), y(n);
+    h3.apply(x.data(), y.data());
+    double ta = now_s();
+    for (int r = 0; r < args.apply_reps; ++r) h3.apply(x.data(), y.data());
+    double per = (now_s() - ta) / args.apply_reps;
+    std::fprintf(js, "  \"t_h3_apply\": %.9f, \"apply_reps\": %d,\n", per, args.apply_reps);
+  }
+
+  // ---- the solve (run_with_context, harness.cpp:137-139) ------------------
+  if (!args.no_solve) {
+    const ApplyFn apply_a = [&a](const double* x, double* y) { spmv(a, x, y); };
+    const ApplyFn apply_h = [&h3](const double* x, double* y) { h3.apply(x, y); };
+    double ts = now_s();
+    auto [x, rep] = pcg(apply_a, apply_h, b, args.rtol, args.maxit);
+    double t_solve = now_s() - ts;
+    npy_d(out, "pcg_x", x);
+    npy_d(out, "pcg_residuals", rep.residual_history);
+    npy_d(out, "pcg_lanczos_diag", rep.lanczos_diag);
+    npy_d(out, "pcg_lanczos_offdiag", rep.lanczos_offdiag);
+    std::fprintf(js, "  \"t_solve\": %.6f, \"iterations\": %d, \"converged\": %s,\n", t_solve, rep.iterations,
+                 rep.converged ? "true" : "false");
+    std::fprintf(js, "  \"final_relative_residual\": %.17g, \"recurrence_residual_at_exit\": %.17g,\n",
+                 rep.final_relative_residual, rep.recurrence_residual_at_exit);
+    std::fprintf(js, "  \"ritz_min\": %.17g, \"ritz_max\": %.17g, \"kappa\": %.17g,\n", rep.ritz_min,
+                 rep.ritz_max, rep.kappa_estimate);
+  }
+  std::fprintf(js, "  \"awg\": \"%s\", \"rtol\": %.17g, \"w_rtol\": %.17g, \"tau\": %.17g, \"fixed_k\": %d\n}\n",
+               args.awg.c_str(), args.rtol, args.w_rtol, args.tau, args.fixed_k);
+  std::fclose(js);
+  return 0;
+}

@@ -1,0 +1,611 @@
+// C ABI (include/awg_cuda.h): context lifecycle, problem input with the
+// reference's validation semantics, factor loading, operator dispatch, PCG.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <string>
+
+#include "awg_internal.cuh"
+
+using namespace awgb;
+
+namespace awgb {
+namespace {
+
+// Stored-entry multiplicities M_mu(i,j) = #{s : i,j in Omega^s}
+// (entry_multiplicities, splitting.cpp:20-33): for each owner subdomain of
+// row i, binary search j in the sorted Omega^s.  Records violations of the
+// minimal overlap condition for pairs j >= i (check_minimal_overlap,
+// partition.cpp:137-156).
+__global__ void k_entry_mult(int n, const int* __restrict__ rp, const int* __restrict__ ci,
+                             const int* __restrict__ own_off, const int* __restrict__ own_pos,
+                             const int* __restrict__ psub, const long long* __restrict__ poff,
+                             const int* __restrict__ pidx, int* __restrict__ emult,
+                             unsigned long long* __restrict__ first_bad, int* __restrict__ nbad) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    for (int e = rp[i]; e < rp[i + 1]; ++e) {
+      const int j = ci[e];
+      int count = 0;
+      for (int q = own_off[i]; q < own_off[i + 1]; ++q) {
+        const int s = psub[own_pos[q]];
+        long long lo = poff[s], hi = poff[s + 1] - 1;
+        while (lo <= hi) {
+          const long long mid = (lo + hi) >> 1;
+          const int v = pidx[mid];
+          if (v == j) {
+            ++count;
+            break;
+          }
+          if (v < j) lo = mid + 1;
+          else hi = mid - 1;
+        }
+      }
+      emult[e] = count;
+      if (count == 0 && j >= i) {
+        atomicAdd(nbad, 1);
+        atomicMin(first_bad, (unsigned long long)i * (unsigned long long)n + (unsigned long long)j);
+      }
+    }
+  }
+}
+
+// core = Lambda_-^-1 - V_-^T W   (AwgPreconditioner ctor, preconditioner.cpp:134-146);
+// warp per entry (i, j).
+__global__ void k_core(int nm, const int* __restrict__ neg_s, const int* __restrict__ neg_k,
+                       const double* __restrict__ V, const long long* __restrict__ voff, const int* __restrict__ ns,
+                       const int* __restrict__ ld, const long long* __restrict__ poff, const int* __restrict__ pidx,
+                       const double* __restrict__ W, int ldw, const double* __restrict__ negw,
+                       double* __restrict__ core) {
+  const int lane = threadIdx.x & 31;
+  const long long e = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (e >= (long long)nm * nm) return;
+  const int i = int(e % nm), j = int(e / nm);
+  const int s = neg_s[i], n = ns[s];
+  const double* v = V + voff[s] + (size_t)neg_k[i] * ld[s];
+  const int* idx = pidx + poff[s];
+  const double* w = W + (size_t)j * ldw;
+  double acc = 0.0;
+  for (int l = lane; l < n; l += 32) acc = fma(v[l], w[idx[l]], acc);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) core[i + (size_t)j * nm] = -acc + (i == j ? 1.0 / negw[j] : 0.0);
+}
+
+// lu_factor (dense.cpp:368-393): partial pivoting, first maximum, full row
+// swaps; single CTA (n_minus is small).
+__global__ void k_lu_factor(int m, double* __restrict__ a, int* __restrict__ perm, int* __restrict__ singular) {
+  __shared__ int piv;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) perm[i] = i;
+  __syncthreads();
+  for (int k = 0; k < m; ++k) {
+    if (threadIdx.x == 0) {
+      int p = k;
+      for (int i = k + 1; i < m; ++i)
+        if (fabs(a[i + (size_t)k * m]) > fabs(a[p + (size_t)k * m])) p = i;
+      piv = p;
+      if (a[p + (size_t)k * m] == 0.0) *singular = 1;
+    }
+    __syncthreads();
+    if (*singular) return;
+    const int p = piv;
+    if (p != k) {
+      for (int j = threadIdx.x; j < m; j += blockDim.x) {
+        const double t = a[k + (size_t)j * m];
+        a[k + (size_t)j * m] = a[p + (size_t)j * m];
+        a[p + (size_t)j * m] = t;
+      }
+      if (threadIdx.x == 0) {
+        const int t = perm[k];
+        perm[k] = perm[p];
+        perm[p] = t;
+      }
+    }
+    __syncthreads();
+    const double inv = 1.0 / a[k + (size_t)k * m];
+    for (int i = k + 1 + threadIdx.x; i < m; i += blockDim.x) a[i + (size_t)k * m] *= inv;
+    __syncthreads();
+    for (int j = k + 1; j < m; ++j) {
+      const double f = a[k + (size_t)j * m];
+      if (f == 0.0) continue;
+      for (int i = k + 1 + threadIdx.x; i < m; i += blockDim.x) a[i + (size_t)j * m] -= a[i + (size_t)k * m] * f;
+    }
+    __syncthreads();
+  }
+}
+
+void upload_padded(DArr<double>& dst, const std::vector<long long>& off, long long total, const double* src,
+                   const std::vector<int>& rows, const std::vector<int>& lds, const std::vector<int>& cols,
+                   cudaStream_t st) {
+  dst.alloc(size_t(std::max<long long>(total, 1)));
+  dst.zero(st);
+  size_t s_off = 0;
+  for (size_t s = 0; s < rows.size(); ++s) {
+    if (cols[s] > 0 && rows[s] > 0)
+      AWG_CUDA(cudaMemcpy2DAsync(dst.p + off[s], sizeof(double) * lds[s], src + s_off, sizeof(double) * rows[s],
+                                 sizeof(double) * rows[s], cols[s], cudaMemcpyHostToDevice, st));
+    s_off += size_t(rows[s]) * cols[s];
+  }
+}
+
+void set_factor(Ctx& c, CoarseFactor& f, int dim, int r, const int* ret, const double* l11) {
+  f.dim = dim;
+  f.rank = r;
+  f.h_retained.assign(ret, ret + r);
+  f.h_l11.assign(l11, l11 + size_t(r) * r);
+  f.retained.upload(f.h_retained, c.stream);
+  f.linv.alloc(size_t(std::max(r, 1)) * std::max(r, 1));
+  if (r) {
+    DArr<double> l;
+    l.upload(f.h_l11, c.stream);
+    k::tri_inverse(c, l.p, r, f.linv.p);
+  }
+}
+
+}  // namespace
+
+void finalize_factors(Ctx& c) {
+  const int N = c.N;
+  // local layout
+  c.h_ld.resize(N);
+  c.h_voff.assign(N + 1, 0);
+  c.h_yoff.assign(N + 1, 0);
+  for (int s = 0; s < N; ++s) {
+    c.h_ld[s] = round_up(c.h_ns[s], 4);
+    c.h_voff[s + 1] = c.h_voff[s] + (long long)c.h_ld[s] * c.h_ns[s];
+    c.h_yoff[s + 1] = c.h_yoff[s] + (long long)c.h_ld[s] * c.h_ks[s];
+  }
+  c.ns.upload(c.h_ns, c.stream);
+  c.ld.upload(c.h_ld, c.stream);
+  c.msz.upload(c.h_m, c.stream);
+  c.voff.upload(c.h_voff, c.stream);
+  c.yoff.upload(c.h_yoff, c.stream);
+  // NN task lists
+  std::vector<GemvTTask> tT;
+  std::vector<GemvTask> t;
+  for (int s = 0; s < N; ++s) {
+    for (int j0 = c.h_m[s]; j0 < c.h_ns[s]; j0 += 64) tT.push_back({s, j0, std::min(j0 + 64, c.h_ns[s]), 0});
+    for (int i0 = 0; i0 < c.h_ns[s]; i0 += c.rows_per_gemv) t.push_back({s, i0});
+  }
+  c.t_gemvT.upload(tT, c.stream);
+  c.t_gemv.upload(t, c.stream);
+  // A- modes: k < n_nonpos with lambda != 0 (splitting.cpp:129-131), ascending (s, k)
+  std::vector<int> ns_, nk_, noff(N + 1, 0);
+  std::vector<double> nw_;
+  for (int s = 0; s < N; ++s) {
+    for (int k = 0; k < c.h_m[s]; ++k) {
+      const double lam = c.h_lam[c.h_poff[s] + k];
+      if (lam == 0.0) continue;
+      ns_.push_back(s);
+      nk_.push_back(k);
+      nw_.push_back(-lam);
+    }
+    noff[s + 1] = int(ns_.size());
+  }
+  c.nneg = int(ns_.size());
+  c.neg_s.upload(ns_, c.stream);
+  c.neg_k.upload(nk_, c.stream);
+  c.neg_w.upload(nw_, c.stream);
+  c.negoff.upload(noff, c.stream);
+  c.neg_c.alloc(std::max(c.nneg, 1));
+  // coarse columns
+  std::vector<int> zs, zl, koff(N + 1, 0);
+  for (int s = 0; s < N; ++s) {
+    for (int k = 0; k < c.h_ks[s]; ++k) {
+      zs.push_back(s);
+      zl.push_back(k);
+    }
+    koff[s + 1] = int(zs.size());
+  }
+  c.n0 = int(zs.size());
+  c.zcol_s.upload(zs, c.stream);
+  c.zcol_loc.upload(zl, c.stream);
+  c.koff.upload(koff, c.stream);
+  c.alloc_work();
+  AWG_CUDA(cudaStreamSynchronize(c.stream));
+}
+
+void build_core(Ctx& c) {
+  if (c.nm == 0) return;
+  c.core_lu.alloc(size_t(c.nm) * c.nm);
+  c.core_perm.alloc(c.nm);
+  const long long pairs = (long long)c.nm * c.nm;
+  k_core<<<int((pairs + 7) / 8), 256, 0, c.stream>>>(c.nm, c.neg_s.p, c.neg_k.p, c.V.p, c.voff.p, c.ns.p, c.ld.p,
+                                                    c.poff.p, c.pidx.p, c.W.p, c.ldw, c.neg_weights.p,
+                                                    c.core_lu.p);
+  DArr<int> sing;
+  sing.alloc(1);
+  sing.zero(c.stream);
+  k_lu_factor<<<1, 1024, 0, c.stream>>>(c.nm, c.core_lu.p, c.core_perm.p, sing.p);
+  c.launches += 2;
+  check_launch("core");
+  int h = 0;
+  AWG_CUDA(cudaMemcpyAsync(&h, sing.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  AWG_CUDA(cudaStreamSynchronize(c.stream));
+  if (h) c.fail(AWG_E_ARG, "lu_factor: singular matrix");
+}
+
+}  // namespace awgb
+
+// ===========================================================================
+namespace {
+
+template <class F>
+int guarded(awg_ctx* ctx, F f) {
+  if (!ctx) return AWG_E_ARG;
+  Ctx& c = ctx->c;
+  try {
+    if (c.device >= 0) cudaSetDevice(c.device);
+    f(c);
+    c.err.clear();
+    c.err_index = -1;
+    return AWG_OK;
+  } catch (const AwgError& e) {
+    c.err = e.what();
+    c.err_index = e.index;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    c.err = "host allocation failed";
+    return AWG_E_CUDA;
+  } catch (const std::exception& e) {
+    c.err = e.what();
+    return AWG_E_CUDA;
+  }
+}
+
+void check_config(Ctx& c, const awg_config& cfg) {
+  if (cfg.one_level != 2)
+    c.fail(AWG_E_ARG, "one_level: only NN is implemented on the device (AS/AS_PLUS: SURVEY.md §8f)");
+  if (cfg.composition != 0 && cfg.composition != 1) c.fail(AWG_E_ARG, "composition must be 0 or 1");
+  if (cfg.awg_mode < 0 || cfg.awg_mode > 3) c.fail(AWG_E_ARG, "awg_mode must be 0..3");
+  if (cfg.use_coarse && cfg.fixed_k <= 0 && !(cfg.tau_sharp > 0.0 && cfg.tau_sharp < 1.0))
+    c.fail(AWG_E_ARG, "NN threshold requires 0 < tau_sharp < 1");
+}
+
+}  // namespace
+
+extern "C" {
+
+int awg_create(awg_ctx** out, int device) {
+  if (!out) return AWG_E_ARG;
+  *out = nullptr;
+  awg_ctx* ctx = new (std::nothrow) awg_ctx();
+  if (!ctx) return AWG_E_CUDA;
+  Ctx& c = ctx->c;
+  c.device = device;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    c.device = -1;
+    c.err = "no CUDA device visible (the AWG path has no CPU fallback)";
+    *out = ctx;
+    return AWG_E_CUDA;
+  }
+  int rc = guarded(ctx, [&](Ctx& cc) {
+    AWG_CUDA(cudaSetDevice(device));
+    AWG_CUDA(cudaStreamCreateWithFlags(&cc.stream, cudaStreamNonBlocking));
+    AWG_CUDA(cudaDeviceGetAttribute(&cc.sm_count, cudaDevAttrMultiProcessorCount, device));
+  });
+  *out = ctx;
+  return rc;
+}
+
+void awg_destroy(awg_ctx* ctx) {
+  if (!ctx) return;
+  if (ctx->c.device >= 0) {
+    cudaSetDevice(ctx->c.device);
+    if (ctx->c.stream) cudaStreamSynchronize(ctx->c.stream);
+  }
+  cudaStream_t s = ctx->c.stream;
+  delete ctx;
+  if (s) cudaStreamDestroy(s);
+}
+
+const char* awg_last_error(const awg_ctx* ctx) { return ctx ? ctx->c.err.c_str() : "null context"; }
+int awg_last_error_index(const awg_ctx* ctx) { return ctx ? ctx->c.err_index : -1; }
+long long awg_launch_count(const awg_ctx* ctx) { return ctx ? ctx->c.launches : 0; }
+
+int awg_set_matrix(awg_ctx* ctx, int n, const int* rp, const int* ci, const double* va) {
+  return guarded(ctx, [&](Ctx& c) {
+    if (c.device < 0) c.fail(AWG_E_CUDA, "no CUDA device");
+    if (n <= 0 || !rp || !ci || !va) c.fail(AWG_E_ARG, "set_matrix: bad arguments");
+    if (rp[0] != 0) c.fail(AWG_E_ARG, "set_matrix: row_offsets[0] must be 0");
+    for (int i = 0; i < n; ++i) {
+      if (rp[i + 1] < rp[i]) c.fail(AWG_E_ARG, "set_matrix: row_offsets not monotone");
+      for (int k = rp[i]; k < rp[i + 1]; ++k) {
+        if (ci[k] < 0 || ci[k] >= n) c.fail(AWG_E_ARG, "set_matrix: column index out of range");
+        if (k > rp[i] && ci[k] <= ci[k - 1]) c.fail(AWG_E_ARG, "set_matrix: column indices not strictly increasing");
+      }
+    }
+    c.n = n;
+    c.nnz = rp[n];
+    c.h_rp.assign(rp, rp + n + 1);
+    c.h_ci.assign(ci, ci + c.nnz);
+    c.h_va.assign(va, va + c.nnz);
+    c.rp.upload(c.h_rp, c.stream);
+    c.ci.upload(c.h_ci, c.stream);
+    c.va.upload(c.h_va, c.stream);
+    c.have_factors = false;
+    c.N = 0;
+    AWG_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int awg_set_partition(awg_ctx* ctx, int N, const long long* off, const int* idx) {
+  return guarded(ctx, [&](Ctx& c) {
+    if (c.n == 0) c.fail(AWG_E_STATE, "set_partition: set the matrix first");
+    if (N <= 0 || !off || !idx) c.fail(AWG_E_ARG, "set_partition: bad arguments");
+    if (off[0] != 0) c.fail(AWG_E_ARG, "set_partition: offsets[0] must be 0");
+    const int n = c.n;
+    std::vector<int> mult(n, 0);
+    std::vector<int> ns(N);
+    for (int s = 0; s < N; ++s) {
+      if (off[s + 1] <= off[s]) c.fail(AWG_E_ARG, "set_partition: empty subdomain " + std::to_string(s));
+      ns[s] = int(off[s + 1] - off[s]);
+      for (long long p = off[s]; p < off[s + 1]; ++p) {
+        if (idx[p] < 0 || idx[p] >= n) c.fail(AWG_E_ARG, "partition index out of range");
+        if (p > off[s] && idx[p] <= idx[p - 1]) c.fail(AWG_E_ARG, "set_partition: indices must be sorted and unique");
+        ++mult[idx[p]];
+      }
+    }
+    for (int i = 0; i < n; ++i)
+      if (mult[i] == 0) c.fail(AWG_E_OVERLAP, "partition does not cover dof " + std::to_string(i), i);
+    const long long P = off[N];
+    c.N = N;
+    c.P = P;
+    c.h_ns = ns;
+    c.h_poff.assign(off, off + N + 1);
+    c.h_pidx.assign(idx, idx + P);
+    c.h_mult = mult;
+    std::vector<int> psub(P), own_off(n + 1, 0), own_pos(P);
+    std::vector<double> ds(P);
+    for (int s = 0; s < N; ++s)
+      for (long long p = off[s]; p < off[s + 1]; ++p) {
+        psub[p] = s;
+        ds[p] = 1.0 / mult[idx[p]];
+        ++own_off[idx[p] + 1];
+      }
+    for (int i = 0; i < n; ++i) own_off[i + 1] += own_off[i];
+    std::vector<int> fill(own_off.begin(), own_off.end() - 1);
+    for (long long p = 0; p < P; ++p) own_pos[fill[idx[p]]++] = int(p);
+    c.pidx.upload(c.h_pidx, c.stream);
+    c.poff.upload(c.h_poff, c.stream);
+    c.psub.upload(psub, c.stream);
+    c.ds.upload(ds, c.stream);
+    c.own_off.upload(own_off, c.stream);
+    c.own_pos.upload(own_pos, c.stream);
+    c.mult.upload(mult, c.stream);
+    // minimal overlap / entry multiplicities on the device
+    c.emult.alloc(c.nnz);
+    DArr<unsigned long long> first;
+    DArr<int> nbad;
+    first.alloc(1);
+    nbad.alloc(1);
+    AWG_CUDA(cudaMemsetAsync(first.p, 0xff, sizeof(unsigned long long), c.stream));
+    nbad.zero(c.stream);
+    k_entry_mult<<<std::max(1, std::min((n + 255) / 256, c.sm_count * 8)), 256, 0, c.stream>>>(
+        n, c.rp.p, c.ci.p, c.own_off.p, c.own_pos.p, c.psub.p, c.poff.p, c.pidx.p, c.emult.p, first.p, nbad.p);
+    ++c.launches;
+    check_launch("entry_mult");
+    unsigned long long hf = 0;
+    int hb = 0;
+    AWG_CUDA(cudaMemcpyAsync(&hf, first.p, sizeof(hf), cudaMemcpyDeviceToHost, c.stream));
+    AWG_CUDA(cudaMemcpyAsync(&hb, nbad.p, sizeof(hb), cudaMemcpyDeviceToHost, c.stream));
+    AWG_CUDA(cudaStreamSynchronize(c.stream));
+    if (hb > 0) {
+      const long long fi = (long long)(hf / (unsigned long long)n), fj = (long long)(hf % (unsigned long long)n);
+      c.fail(AWG_E_OVERLAP, "external partition violates minimal overlap on " + std::to_string(hb) +
+                                " pair(s), first (" + std::to_string(fi) + "," + std::to_string(fj) + ")");
+    }
+    c.have_factors = false;
+  });
+}
+
+int awg_load_factors(awg_ctx* ctx, const awg_config* cfg, const awg_factors* f) {
+  return guarded(ctx, [&](Ctx& c) {
+    if (c.N == 0) c.fail(AWG_E_STATE, "load_factors: set matrix and partition first");
+    if (!cfg || !f || !f->lam || !f->V || !f->n_nonpos || !f->n_zero || !f->ks)
+      c.fail(AWG_E_ARG, "load_factors: missing arrays");
+    check_config(c, *cfg);
+    c.cfg = *cfg;
+    c.lu_semantics = cfg->lu_semantics;
+    const int N = c.N;
+    c.h_m.assign(f->n_nonpos, f->n_nonpos + N);
+    c.h_nzero.assign(f->n_zero, f->n_zero + N);
+    c.h_ks.assign(f->ks, f->ks + N);
+    if (!cfg->use_coarse) std::fill(c.h_ks.begin(), c.h_ks.end(), 0);
+    c.h_lam.assign(f->lam, f->lam + c.P);
+    c.h_eps.assign(N, 0.0);
+    c.h_plam.clear();
+    c.lam.upload(c.h_lam, c.stream);
+    finalize_factors(c);
+    std::vector<int> ns = c.h_ns;
+    upload_padded(c.V, c.h_voff, c.h_voff[N], f->V, ns, c.h_ld, ns, c.stream);
+    long long n0 = 0;
+    for (int s = 0; s < N; ++s) n0 += c.h_ks[s];
+    if (n0 > 0) {
+      if (!f->Y || !f->k0_retained || !f->k0_l11) c.fail(AWG_E_ARG, "load_factors: coarse factors missing");
+      upload_padded(c.Y, c.h_yoff, c.h_yoff[N], f->Y, ns, c.h_ld, c.h_ks, c.stream);
+      set_factor(c, c.k0, int(n0), f->r0, f->k0_retained, f->k0_l11);
+    } else {
+      c.k0.clear();
+    }
+    c.nm = (cfg->awg_mode != 0) ? f->n_minus : 0;
+    c.ldw = round_up(c.n, 4);
+    if (c.nm > 0) {
+      if (!f->W || !f->kw_retained || !f->kw_l11) c.fail(AWG_E_ARG, "load_factors: W factors missing");
+      std::vector<long long> woff = {0};
+      upload_padded(c.W, woff, (long long)c.ldw * c.nm, f->W, {c.n}, {c.ldw}, {c.nm}, c.stream);
+      set_factor(c, c.kw, c.nm, f->rw, f->kw_retained, f->kw_l11);
+      if (f->neg_weights) {
+        c.h_neg_weights.assign(f->neg_weights, f->neg_weights + c.nm);
+        c.neg_weights.upload(c.h_neg_weights, c.stream);
+      }
+    }
+    c.alloc_work();
+    if (cfg->awg_mode == 3 && c.nm > 0) {
+      if (!f->neg_weights) c.fail(AWG_E_ARG, "load_factors: INEX needs neg_weights");
+      build_core(c);
+    }
+    AWG_CUDA(cudaStreamSynchronize(c.stream));
+    c.have_factors = true;
+  });
+}
+
+int awg_setup(awg_ctx* ctx, const awg_config* cfg) {
+  return guarded(ctx, [&](Ctx& c) {
+    if (c.N == 0) c.fail(AWG_E_STATE, "setup: set matrix and partition first");
+    if (!cfg) c.fail(AWG_E_ARG, "setup: null config");
+    check_config(c, *cfg);
+    run_setup(c, *cfg);
+    c.have_factors = true;
+  });
+}
+
+int awg_apply(awg_ctx* ctx, int op, const double* x, double* y, int ptr_kind) {
+  return guarded(ctx, [&](Ctx& c) {
+    if (op != AWG_OP_A && !c.have_factors) c.fail(AWG_E_STATE, "apply: preconditioner not set up");
+    if (c.n == 0) c.fail(AWG_E_STATE, "apply: no matrix");
+    if (!x || !y) c.fail(AWG_E_ARG, "apply: null vector");
+    if (!c.pb.p) c.alloc_work();
+    if (ptr_kind == AWG_PTR_HOST) {
+      AWG_CUDA(cudaMemcpyAsync(c.pb.p, x, sizeof(double) * c.n, cudaMemcpyHostToDevice, c.stream));
+      op_apply(c, op, c.pb.p, c.pz.p, nullptr);
+      AWG_CUDA(cudaMemcpyAsync(y, c.pz.p, sizeof(double) * c.n, cudaMemcpyDeviceToHost, c.stream));
+    } else {
+      op_apply(c, op, x, y, nullptr);
+    }
+    AWG_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int awg_time_apply(awg_ctx* ctx, int op, int reps, double* ms) {
+  return guarded(ctx, [&](Ctx& c) {
+    if (!c.have_factors) c.fail(AWG_E_STATE, "time_apply: preconditioner not set up");
+    if (reps < 1 || !ms) c.fail(AWG_E_ARG, "time_apply: bad arguments");
+    cudaEvent_t e0, e1;
+    AWG_CUDA(cudaEventCreate(&e0));
+    AWG_CUDA(cudaEventCreate(&e1));
+    op_apply(c, op, c.pb.p, c.pz.p, nullptr);
+    AWG_CUDA(cudaEventRecord(e0, c.stream));
+    for (int r = 0; r < reps; ++r) op_apply(c, op, c.pb.p, c.pz.p, nullptr);
+    AWG_CUDA(cudaEventRecord(e1, c.stream));
+    AWG_CUDA(cudaEventSynchronize(e1));
+    float t = 0.f;
+    AWG_CUDA(cudaEventElapsedTime(&t, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *ms = double(t) / reps;
+  });
+}
+
+int awg_pcg(awg_ctx* ctx, const double* b, double* x, double rtol, int maxit, int ptr_kind, awg_solve_report* rep) {
+  return guarded(ctx, [&](Ctx& c) {
+    if (!c.have_factors) c.fail(AWG_E_STATE, "pcg: preconditioner not set up");
+    if (!b || !x || !rep) c.fail(AWG_E_ARG, "pcg: null argument");
+    if (ptr_kind == AWG_PTR_HOST) {
+      AWG_CUDA(cudaMemcpyAsync(c.pb.p, b, sizeof(double) * c.n, cudaMemcpyHostToDevice, c.stream));
+      run_pcg(c, c.pb.p, rtol, maxit, rep);
+      AWG_CUDA(cudaMemcpyAsync(x, c.px.p, sizeof(double) * c.n, cudaMemcpyDeviceToHost, c.stream));
+    } else {
+      run_pcg(c, b, rtol, maxit, rep);
+      AWG_CUDA(cudaMemcpyAsync(x, c.px.p, sizeof(double) * c.n, cudaMemcpyDeviceToDevice, c.stream));
+    }
+    AWG_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int awg_query(awg_ctx* ctx, awg_stats* st) {
+  return guarded(ctx, [&](Ctx& c) {
+    if (!st) c.fail(AWG_E_ARG, "query: null");
+    std::memset(st, 0, sizeof(*st));
+    st->n = c.n;
+    st->nnz = c.nnz;
+    st->n_sub = c.N;
+    st->n0 = c.n0;
+    st->r0 = c.k0.rank;
+    st->n_minus = c.nm;
+    st->rw = c.kw.rank;
+    for (int s = 0; s < c.N && s < (int)c.h_ns.size(); ++s) {
+      const long long n_s = c.h_ns[s];
+      st->sum_ns += n_s;
+      st->sum_ns2 += n_s * n_s;
+      if (s < (int)c.h_ks.size()) st->sum_ns_ks += n_s * c.h_ks[s];
+      if (s < (int)c.h_m.size()) {
+        st->sum_ns_ms += n_s * c.h_m[s];
+        st->sum_ns_qs += n_s * (c.h_m[s] - c.h_nzero[s]);
+      }
+    }
+    for (int i = 0; i < 8; ++i) st->t_setup_ms[i] = c.t_setup_ms[i];
+    for (int v : c.h_w_inner) st->w_inner_total += v;
+    st->w_batches = c.w_batches;
+  });
+}
+
+int awg_get_history(awg_ctx* ctx, int which, double* out, int cap) {
+  if (!ctx) return -1;
+  Ctx& c = ctx->c;
+  const std::vector<double>& v = which == 0 ? c.h_hist_res : which == 1 ? c.h_hist_diag : c.h_hist_off;
+  const int k = std::min<int>(cap, int(v.size()));
+  if (out) std::copy(v.begin(), v.begin() + k, out);
+  return int(v.size());
+}
+
+int awg_get_array(awg_ctx* ctx, int which, void* out, long long cap, long long* n_elems) {
+  return guarded(ctx, [&](Ctx& c) {
+    std::vector<double> dv;
+    std::vector<int> iv;
+    bool is_int = false;
+    switch (which) {
+      case 0: dv = c.h_lam; break;
+      case 1: iv = c.h_m; is_int = true; break;
+      case 2: iv = c.h_nzero; is_int = true; break;
+      case 3: iv = c.h_ks; is_int = true; break;
+      case 4: dv = c.h_plam; break;
+      case 5: iv = c.h_mult; is_int = true; break;
+      case 6: iv = c.k0.h_retained; is_int = true; break;
+      case 7: dv = c.k0.h_l11; break;
+      case 8: iv = c.kw.h_retained; is_int = true; break;
+      case 9: dv = c.kw.h_l11; break;
+      case 10: {
+        dv.assign(size_t(c.n) * c.nm, 0.0);
+        for (int j = 0; j < c.nm; ++j)
+          AWG_CUDA(cudaMemcpy(dv.data() + size_t(j) * c.n, c.W.p + size_t(j) * c.ldw, sizeof(double) * c.n,
+                              cudaMemcpyDeviceToHost));
+        break;
+      }
+      case 11: dv = c.h_neg_weights; break;
+      case 12: iv = c.h_w_inner; is_int = true; break;
+      case 13: {
+        for (int s = 0; s < c.N; ++s)
+          for (int k = 0; k < c.h_ks[s]; ++k) {
+            std::vector<double> col(c.h_ns[s]);
+            AWG_CUDA(cudaMemcpy(col.data(), c.Y.p + c.h_yoff[s] + size_t(k) * c.h_ld[s],
+                                sizeof(double) * c.h_ns[s], cudaMemcpyDeviceToHost));
+            dv.insert(dv.end(), col.begin(), col.end());
+          }
+        break;
+      }
+      case 14: {
+        for (int s = 0; s < c.N; ++s) {
+          std::vector<double> blk(size_t(c.h_ns[s]) * c.h_ns[s]);
+          AWG_CUDA(cudaMemcpy2D(blk.data(), sizeof(double) * c.h_ns[s], c.V.p + c.h_voff[s],
+                                sizeof(double) * c.h_ld[s], sizeof(double) * c.h_ns[s], c.h_ns[s],
+                                cudaMemcpyDeviceToHost));
+          dv.insert(dv.end(), blk.begin(), blk.end());
+        }
+        break;
+      }
+      case 15: dv = c.h_eps; break;
+      default: c.fail(AWG_E_ARG, "get_array: unknown array");
+    }
+    const long long cnt = is_int ? (long long)iv.size() : (long long)dv.size();
+    if (n_elems) *n_elems = cnt;
+    if (out) {
+      const long long k = std::min(cap, cnt);
+      if (is_int) std::memcpy(out, iv.data(), sizeof(int) * k);
+      else std::memcpy(out, dv.data(), sizeof(double) * k);
+    }
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,235 @@
+// Internal declarations of the B200-native AWG-PCG library (not part of the
+// C ABI).  Device data layout (HBM), per context:
+//
+//   CSR A            rp[n+1] int32, ci[nnz] int32, va[nnz] f64    (sparse.hpp:12-21)
+//   Partition        pidx[P] int32 (P = sum n_s, subdomains concatenated, each sorted),
+//                    poff[N+1] int64; psub[P] subdomain of entry p
+//   POU              ds[P] = 1/mu(pidx[p])  (partition.cpp:94-108)
+//   Owner lists      own_off[n+1], own_pos[P]: entries p with pidx[p] == i in
+//                    ascending s — the deterministic prolongation order of
+//                    OneLevel::apply (preconditioner.cpp:37-55)
+//   V^s              column-major, leading dimension ld_s = round_up(n_s, 4) (32-byte
+//                    aligned columns, zero padding rows), block offsets voff[s]
+//   lam              [P] eigenvalues of B^s, ascending, snapped (splitting.cpp:64-84)
+//   A- modes         list of (s, k, -lambda_k) for k < n_nonpos(s), lambda_k != 0
+//   Z (block sparse) Y_s column-major with the same ld_s, offsets yoff[s]; column
+//                    j of Z = R^s^T Y_s(:, j - koff[s]) (coarse.cpp:136-141)
+//   K0, KW           retained index lists and the inverse of the l11 factor (lower,
+//                    r x r column-major) — the triangular solves of
+//                    rank_revealing_solve (dense.cpp:348-366) become two triangular
+//                    matrix-vector products
+//   W                n x n_minus column-major, leading dimension round_up(n, 4)
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/awg_cuda.h"
+
+namespace awgb {
+
+struct AwgError : std::runtime_error {
+  int code;
+  int index;
+  AwgError(int c, const std::string& m, int idx = -1) : std::runtime_error(m), code(c), index(idx) {}
+};
+
+#define AWG_CUDA(x)                                                                              \
+  do {                                                                                           \
+    cudaError_t e_ = (x);                                                                        \
+    if (e_ != cudaSuccess)                                                                       \
+      throw ::awgb::AwgError(AWG_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));       \
+  } while (0)
+
+inline void check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw AwgError(AWG_E_CUDA, std::string("launch ") + what + ": " + cudaGetErrorString(e));
+}
+
+template <class T>
+struct DArr {
+  T* p = nullptr;
+  size_t n = 0;
+  DArr() = default;
+  DArr(const DArr&) = delete;
+  DArr& operator=(const DArr&) = delete;
+  ~DArr() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(size_t count) {
+    release();
+    n = count;
+    if (count) AWG_CUDA(cudaMalloc(&p, count * sizeof(T)));
+  }
+  void zero(cudaStream_t s) {
+    if (n) AWG_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+  }
+  void upload(const T* h, size_t count, cudaStream_t s) {
+    alloc(count);
+    if (count) AWG_CUDA(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+  void upload(const std::vector<T>& h, cudaStream_t s) { upload(h.data(), h.size(), s); }
+  std::vector<T> download(cudaStream_t s) const {
+    std::vector<T> h(n);
+    if (n) AWG_CUDA(cudaMemcpyAsync(h.data(), p, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+    AWG_CUDA(cudaStreamSynchronize(s));
+    return h;
+  }
+};
+
+inline int round_up(int v, int m) { return (v + m - 1) / m * m; }
+
+// Work items of the batched NN local solve.
+struct GemvTTask {  // columns [j0, j1) of V^s
+  int s, j0, j1, pad;
+};
+struct GemvTask {  // rows [i0, i0 + rows) of V^s
+  int s, i0;
+};
+
+// Triangular coarse factor with retained pivots (RankRevealingFactor,
+// dense.hpp:81-86), stored as the inverse of l11.
+struct CoarseFactor {
+  int dim = 0;   // original dimension (n0 or n_minus)
+  int rank = 0;  // r
+  DArr<int> retained;
+  DArr<double> linv;  // r x r, column-major, lower
+  std::vector<int> h_retained;
+  std::vector<double> h_l11;  // r x r, as produced (for exports)
+  void clear() {
+    dim = rank = 0;
+    retained.release();
+    linv.release();
+    h_retained.clear();
+    h_l11.clear();
+  }
+};
+
+// PCG state in device memory; every iteration kernel is gated on `done`.
+struct PcgState {
+  double bnorm, rz, pq, alpha, beta, relres, true_rel, alpha_prev, beta_prev;
+  double final_rel, rec_exit, rtol;
+  int it, maxit, done, converged, past_rtol, need_true, error, force_true;
+};
+
+enum PcgError { PCG_OK = 0, PCG_BAD_OPERATOR = 1, PCG_BAD_PRECOND = 2 };
+
+struct Ctx;
+
+// ---- launchers (kernels.cu) -------------------------------------------------
+namespace k {
+void spmv(Ctx& c, const double* x, double* y, int mode, const double* add, const double* sub, const int* gate);
+void gather(Ctx& c, const double* x, const double* scale, double* xs, const int* gate);
+void prolong(Ctx& c, const double* w, double* y, const int* gate);
+void nn_local(Ctx& c, const double* xs, double* w, const int* gate);  // w = D V mask(1/lam) V^T xs
+void aminus(Ctx& c, const double* x, double* y, const int* gate);     // y = A- x
+void coarse_q(Ctx& c, const double* x, double* y, const int* gate);   // y = Z K0+ Z^T x
+void second_q(Ctx& c, const double* x, double* y, const int* gate);   // y = W KW+ W^T x
+void inex_q(Ctx& c, const double* x, double* y, const int* gate);     // y = W core^-1 W^T x
+void axpby(Ctx& c, int n, const double* a, const double* b, const double* d, double* y, int mode, const int* gate);
+void rr_solve(Ctx& c, const CoarseFactor& f, const double* b, double* x, const int* gate);
+void tri_inverse(Ctx& c, const double* l, int r, double* linv);
+}  // namespace k
+
+// ---- the context --------------------------------------------------------------
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  int err_index = -1;
+  long long launches = 0;
+  int sm_count = 148;
+
+  // problem
+  int n = 0, nnz = 0, N = 0;
+  long long P = 0;  // sum n_s
+  std::vector<int> h_rp, h_ci;
+  std::vector<double> h_va;
+  std::vector<long long> h_poff;
+  std::vector<int> h_pidx, h_mult, h_ns, h_ld;
+  DArr<int> rp, ci;
+  DArr<double> va;
+  DArr<int> pidx, psub, own_off, own_pos, mult;
+  DArr<long long> poff;
+  DArr<double> ds;
+  DArr<int> emult;  // multiplicity of each stored entry (splitting.cpp:20-33)
+
+  // local factors
+  bool have_factors = false;
+  std::vector<int> h_m, h_nzero, h_ks;
+  std::vector<long long> h_voff, h_yoff;
+  std::vector<double> h_lam, h_eps, h_plam;
+  DArr<int> ns, ld, msz;
+  DArr<long long> voff;
+  DArr<double> V, lam;
+  DArr<GemvTTask> t_gemvT;
+  DArr<GemvTask> t_gemv;
+  int rows_per_gemv = 512;
+
+  // A- modes
+  int nneg = 0;
+  DArr<int> neg_s, neg_k, negoff;
+  DArr<double> neg_w, neg_c;
+
+  // coarse space
+  int n0 = 0;
+  DArr<long long> yoff;
+  DArr<double> Y;
+  DArr<int> zcol_s, zcol_loc, koff;
+  CoarseFactor k0;
+
+  // second coarse space
+  int nm = 0;
+  int ldw = 0;
+  DArr<double> W, neg_weights, vminus;
+  CoarseFactor kw;
+  std::vector<int> h_w_inner;
+  std::vector<double> h_neg_weights;
+  // INEX core: LU of Lambda^-1 - V-^T W (dense.cpp:368-393)
+  DArr<double> core_lu;
+  DArr<int> core_perm;
+  int lu_semantics = 0;
+
+  // configuration
+  awg_config cfg{};
+  double t_setup_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int w_batches = 0;
+
+  // work buffers
+  DArr<double> xs, uh, wl;                          // P each
+  DArr<double> t0, t1, t2, t3, t4, t5, t6, t7, t8;  // n each
+  DArr<double> cz, cz2;                             // max(n0, nm) each
+  DArr<double> wpart;                               // split-K partials of W^T x
+  DArr<double> red;                                 // reduction partials
+  DArr<unsigned> red_count;
+
+  // pcg
+  DArr<PcgState> pcg;
+  DArr<double> px, pr, pz, pp, pq, pb, pt;
+  DArr<double> hist_res, hist_diag, hist_off;
+  int hist_cap = 0;
+  std::vector<double> h_hist_res, h_hist_diag, h_hist_off;
+
+  void alloc_work();
+  void fail(int code, const std::string& m, int idx = -1) { throw AwgError(code, m, idx); }
+};
+
+// ---- operators (ops.cu) -------------------------------------------------------
+void op_apply(Ctx& c, int op, const double* x, double* y, const int* gate);
+void run_pcg(Ctx& c, const double* b_dev, double rtol, int maxit, awg_solve_report* rep);
+void finalize_factors(Ctx& c);  // task lists, A- modes, inverses, work buffers
+void build_core(Ctx& c);        // INEX core LU
+void run_setup(Ctx& c, const awg_config& cfg);  // setup.cu
+
+}  // namespace awgb
+
+struct awg_ctx {
+  awgb::Ctx c;
+};

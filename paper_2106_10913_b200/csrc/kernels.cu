@@ -1,0 +1,598 @@
+// Apply-path kernels of the AWG preconditioner (sm_100a, fp64, HBM-bound).
+//
+// Every kernel takes a `gate` pointer: when non-null and *gate != 0 the kernel
+// returns immediately.  The PCG driver points it at its device-side `done`
+// flag, so iterations can be enqueued ahead of the host's convergence check
+// without changing any state after the stopping rule fired.
+//
+// Summation-order notes (parity): the CSR SpMV accumulates in ascending
+// column order with fused multiply-adds exactly like sparse.cpp:49-56
+// compiled with GCC's default FP contraction (bit-identical results); the
+// prolongation sums subdomain contributions in ascending s like
+// OneLevel::apply (preconditioner.cpp:37-55).  Dense dot products use
+// fixed-shape warp trees (deterministic, not sequential): the parity bar for
+// the applies is 1e-11 relative.
+#include <algorithm>
+
+#include "awg_internal.cuh"
+
+namespace awgb {
+namespace {
+
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ bool gated(const int* gate) { return gate != nullptr && *gate != 0; }
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+int grid_for(const Ctx& c, long long work, int threads = kThreads) {
+  long long g = (work + threads - 1) / threads;
+  long long cap = (long long)c.sm_count * 16;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return int(g);
+}
+
+// ---------------------------------------------------------------------------
+// CSR SpMV  (sparse.cpp:49-56), thread per row, fused epilogues:
+//   mode 0: y = A x      mode 1: y = add + A x   (A+ = A- x + A x, splitting.cpp:142-147)
+//   mode 2: y = sub - (add + A x)                (projector transpose, coarse.cpp:180-191)
+//   mode 3: y = sub - A x                        (Pi3^T, preconditioner.cpp:173-183)
+__global__ void k_spmv(const int* __restrict__ gate, int n, const int* __restrict__ rp,
+                       const int* __restrict__ ci, const double* __restrict__ va,
+                       const double* __restrict__ x, double* __restrict__ y, int mode,
+                       const double* __restrict__ add, const double* __restrict__ sub) {
+  if (gated(gate)) return;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int k0 = rp[i], k1 = rp[i + 1];
+    double acc = 0.0;
+    for (int k = k0; k < k1; ++k) acc = fma(va[k], __ldg(x + ci[k]), acc);
+    double out;
+    if (mode == 0) out = acc;
+    else if (mode == 1) out = add[i] + acc;
+    else if (mode == 2) out = sub[i] - (add[i] + acc);
+    else out = sub[i] - acc;
+    y[i] = out;
+  }
+}
+
+// xs[p] = x[pidx[p]] (* scale[p])      restrict_to (splitting.cpp:220-223) and the D^s
+// scaling of OneLevel::apply (preconditioner.cpp:48-49)
+__global__ void k_gather(const int* __restrict__ gate, long long total, const int* __restrict__ pidx,
+                         const double* __restrict__ x, const double* __restrict__ scale,
+                         double* __restrict__ xs) {
+  if (gated(gate)) return;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < total;
+       p += (long long)gridDim.x * blockDim.x) {
+    double v = __ldg(x + pidx[p]);
+    if (scale) v *= scale[p];
+    xs[p] = v;
+  }
+}
+
+// y[i] = sum over subdomains s containing i (ascending s) of w[p(s,i)]
+// (prolong_add, splitting.cpp:225-228, in OneLevel's ascending-s order)
+__global__ void k_prolong(const int* __restrict__ gate, int n, const int* __restrict__ own_off,
+                          const int* __restrict__ own_pos, const double* __restrict__ w,
+                          double* __restrict__ y) {
+  if (gated(gate)) return;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int q = own_off[i]; q < own_off[i + 1]; ++q) acc += w[own_pos[q]];
+    y[i] = acc;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Batched NN local solve, first half (local_Aplus_pinv_apply, splitting.cpp:211-218):
+//   uh[p_s + j] = (V^s(:, j) . xs_s) / lambda_j   for j >= n_nonpos(s)
+// One CTA per (s, column chunk); xs_s staged once in shared memory; one warp per
+// column, 16-byte coalesced loads down the column, 4 loads in flight per lane.
+template <int NW>
+__global__ void __launch_bounds__(NW * 32) k_nn_gemvT(const int* __restrict__ gate, const GemvTTask* __restrict__ tasks,
+                                                   const double* __restrict__ V, const long long* __restrict__ voff,
+                                                   const int* __restrict__ ns, const int* __restrict__ ld,
+                                                   const long long* __restrict__ poff, const double* __restrict__ xs,
+                                                   const double* __restrict__ lam, double* __restrict__ uh) {
+  if (gated(gate)) return;
+  extern __shared__ double sx[];
+  const GemvTTask t = tasks[blockIdx.x];
+  const int s = t.s, n = ns[s], L = ld[s];
+  const long long p0 = poff[s];
+  for (int i = threadIdx.x; i < L; i += blockDim.x) sx[i] = (i < n) ? xs[p0 + i] : 0.0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double* Vs = V + voff[s];
+  const double2* sx2 = reinterpret_cast<const double2*>(sx);
+  const int npair = L >> 1;
+  for (int j = t.j0 + warp; j < t.j1; j += NW) {
+    const double2* col = reinterpret_cast<const double2*>(Vs + (size_t)j * L);
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int q = lane;
+    for (; q + 96 < npair; q += 128) {
+      const double2 v0 = __ldcs(col + q), v1 = __ldcs(col + q + 32), v2 = __ldcs(col + q + 64),
+                    v3 = __ldcs(col + q + 96);
+      const double2 x0 = sx2[q], x1 = sx2[q + 32], x2 = sx2[q + 64], x3 = sx2[q + 96];
+      a0 = fma(v0.x, x0.x, a0); a0 = fma(v0.y, x0.y, a0);
+      a1 = fma(v1.x, x1.x, a1); a1 = fma(v1.y, x1.y, a1);
+      a2 = fma(v2.x, x2.x, a2); a2 = fma(v2.y, x2.y, a2);
+      a3 = fma(v3.x, x3.x, a3); a3 = fma(v3.y, x3.y, a3);
+    }
+    for (; q < npair; q += 32) {
+      const double2 v0 = __ldcs(col + q);
+      const double2 x0 = sx2[q];
+      a0 = fma(v0.x, x0.x, a0); a0 = fma(v0.y, x0.y, a0);
+    }
+    const double sum = warp_sum((a0 + a1) + (a2 + a3));
+    if (lane == 0) uh[p0 + j] = sum / lam[p0 + j];
+  }
+}
+
+// Second half: w[p_s + i] = D^s_i * sum_{j >= n_nonpos(s)} V^s(i, j) uh[p_s + j]
+// One CTA per (s, 2*blockDim row panel); each thread owns two adjacent rows
+// (16-byte loads, a warp reads 512 contiguous bytes of a column per step),
+// 8 column loads in flight per thread; uh_s staged in shared memory.
+__global__ void __launch_bounds__(kThreads) k_nn_gemv(const int* __restrict__ gate, const GemvTask* __restrict__ tasks,
+                                                   const double* __restrict__ V, const long long* __restrict__ voff,
+                                                   const int* __restrict__ ns, const int* __restrict__ ld,
+                                                   const int* __restrict__ msz, const long long* __restrict__ poff,
+                                                   const double* __restrict__ uh, const double* __restrict__ ds,
+                                                   double* __restrict__ w) {
+  if (gated(gate)) return;
+  extern __shared__ double su[];
+  const GemvTask t = tasks[blockIdx.x];
+  const int s = t.s, n = ns[s], L = ld[s], m = msz[s];
+  const long long p0 = poff[s];
+  for (int j = m + threadIdx.x; j < n; j += blockDim.x) su[j] = uh[p0 + j];
+  __syncthreads();
+  const int i = t.i0 + 2 * threadIdx.x;
+  if (i >= n) return;
+  const double* Vs = V + voff[s] + i;
+  double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+  int j = m;
+  for (; j + 8 <= n; j += 8) {
+    double2 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __ldcs(reinterpret_cast<const double2*>(Vs + (size_t)(j + u) * L));
+#pragma unroll
+    for (int u = 0; u < 8; u += 2) {
+      const double c0 = su[j + u], c1 = su[j + u + 1];
+      a0 = fma(v[u].x, c0, a0);
+      a1 = fma(v[u].y, c0, a1);
+      b0 = fma(v[u + 1].x, c1, b0);
+      b1 = fma(v[u + 1].y, c1, b1);
+    }
+  }
+  for (; j < n; ++j) {
+    const double2 v0 = __ldcs(reinterpret_cast<const double2*>(Vs + (size_t)j * L));
+    const double c0 = su[j];
+    a0 = fma(v0.x, c0, a0);
+    a1 = fma(v0.y, c0, a1);
+  }
+  w[p0 + i] = (a0 + b0) * ds[p0 + i];
+  if (i + 1 < n) w[p0 + i + 1] = (a1 + b1) * ds[p0 + i + 1];
+}
+
+// ---------------------------------------------------------------------------
+// A- x (splitting.cpp:119-140): per strictly negative mode (s,k):
+//   c = (-lambda_k) * (v_k . x[Omega^s]);   u_s = sum_k c_k v_k;   y = sum_s R^s^T u_s
+__global__ void k_neg_dot(const int* __restrict__ gate, int nneg, const int* __restrict__ neg_s,
+                          const int* __restrict__ neg_k, const double* __restrict__ neg_w,
+                          const double* __restrict__ V, const long long* __restrict__ voff,
+                          const int* __restrict__ ns, const int* __restrict__ ld,
+                          const long long* __restrict__ poff, const int* __restrict__ pidx,
+                          const double* __restrict__ x, double* __restrict__ cout) {
+  if (gated(gate)) return;
+  const int lane = threadIdx.x & 31;
+  const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (j >= nneg) return;
+  const int s = neg_s[j], k = neg_k[j], n = ns[s];
+  const double* v = V + voff[s] + (size_t)k * ld[s];
+  const int* idx = pidx + poff[s];
+  double acc = 0.0;
+  for (int i = lane; i < n; i += 32) acc = fma(v[i], __ldg(x + idx[i]), acc);
+  acc = warp_sum(acc);
+  if (lane == 0) cout[j] = neg_w[j] * acc;
+}
+
+// u[p] = sum over the negative modes of s(p), ascending k, of c_k v_k[i]
+// (Y-combine for Z c uses the same kernel on the Y blocks).
+__global__ void k_block_combine(const int* __restrict__ gate, long long P, const int* __restrict__ psub,
+                                const long long* __restrict__ poff, const int* __restrict__ coff,
+                                const int* __restrict__ ccol, const double* __restrict__ M,
+                                const long long* __restrict__ moff, const int* __restrict__ ld,
+                                const double* __restrict__ coef, double* __restrict__ u) {
+  if (gated(gate)) return;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < P;
+       p += (long long)gridDim.x * blockDim.x) {
+    const int s = psub[p];
+    const int i = int(p - poff[s]);
+    const double* Ms = M + moff[s] + i;
+    const int L = ld[s];
+    double acc = 0.0;
+    for (int q = coff[s]; q < coff[s + 1]; ++q) {
+      const int col = ccol ? ccol[q] : (q - coff[s]);
+      acc = fma(coef[q], Ms[(size_t)col * L], acc);
+    }
+    u[p] = acc;
+  }
+}
+
+// Z^T x with Z block sparse (coarse.cpp:136-141 + matvec_transpose, dense.cpp:47-54):
+// warp per coarse column j of subdomain s: zx[j] = Y_s(:, j - koff[s]) . x[Omega^s]
+__global__ void k_zT(const int* __restrict__ gate, int n0, const int* __restrict__ zcol_s,
+                     const int* __restrict__ zcol_loc, const double* __restrict__ Y,
+                     const long long* __restrict__ yoff, const int* __restrict__ ns,
+                     const int* __restrict__ ld, const long long* __restrict__ poff,
+                     const int* __restrict__ pidx, const double* __restrict__ x, double* __restrict__ zx) {
+  if (gated(gate)) return;
+  const int lane = threadIdx.x & 31;
+  const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (j >= n0) return;
+  const int s = zcol_s[j], n = ns[s];
+  const double* y = Y + yoff[s] + (size_t)zcol_loc[j] * ld[s];
+  const int* idx = pidx + poff[s];
+  double acc = 0.0;
+  for (int i = lane; i < n; i += 32) acc = fma(y[i], __ldg(x + idx[i]), acc);
+  acc = warp_sum(acc);
+  if (lane == 0) zx[j] = acc;
+}
+
+// ---------------------------------------------------------------------------
+// rank_revealing_solve (dense.cpp:348-366) with the inverse of l11:
+//   b_r = b[retained]; t = L^-1 b_r; y = L^-T t; x = 0, x[retained] = y
+__global__ void __launch_bounds__(kThreads) k_tri_lower(const int* __restrict__ gate, int r, const double* __restrict__ linv,
+                                                     const double* __restrict__ b, const int* __restrict__ ret,
+                                                     double* __restrict__ t) {
+  if (gated(gate)) return;
+  extern __shared__ double sb[];
+  constexpr int CH = 4096;
+  const int i0 = blockIdx.x * blockDim.x;
+  const int i = i0 + threadIdx.x;
+  const int jmax = min(r, i0 + (int)blockDim.x);  // columns j <= i needed
+  double acc = 0.0;
+  for (int c0 = 0; c0 < jmax; c0 += CH) {
+    const int c1 = min(jmax, c0 + CH);
+    __syncthreads();
+    for (int j = c0 + threadIdx.x; j < c1; j += blockDim.x) sb[j - c0] = b[ret[j]];
+    __syncthreads();
+    if (i < r) {
+      const int jend = min(c1, i + 1);
+      for (int j = c0; j < jend; ++j) acc = fma(linv[i + (size_t)j * r], sb[j - c0], acc);
+    }
+  }
+  if (i < r) t[i] = acc;
+}
+
+__global__ void k_tri_upperT(const int* __restrict__ gate, int r, const double* __restrict__ linv,
+                             const double* __restrict__ t, const int* __restrict__ ret, double* __restrict__ x) {
+  if (gated(gate)) return;
+  const int lane = threadIdx.x & 31;
+  const int k = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (k >= r) return;
+  const double* col = linv + (size_t)k * r;
+  double acc = 0.0;
+  for (int i = k + lane; i < r; i += 32) acc = fma(col[i], t[i], acc);
+  acc = warp_sum(acc);
+  if (lane == 0) x[ret[k]] = acc;
+}
+
+__global__ void k_zero(const int* __restrict__ gate, int n, double* __restrict__ y) {
+  if (gated(gate)) return;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) y[i] = 0.0;
+}
+
+// L^-1 of a lower-triangular r x r column-major l (setup; thread per column,
+// forward substitution against the identity, row-major scratch then transpose).
+__global__ void k_tri_inverse_rm(int r, const double* __restrict__ l, double* __restrict__ xrm) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= r) return;
+  for (int k = 0; k < j; ++k) xrm[(size_t)k * r + j] = 0.0;
+  for (int k = j; k < r; ++k) {
+    double acc = (k == j) ? 1.0 : 0.0;
+    for (int m = j; m < k; ++m) acc -= l[k + (size_t)m * r] * xrm[(size_t)m * r + j];
+    xrm[(size_t)k * r + j] = acc / l[k + (size_t)k * r];
+  }
+}
+
+__global__ void k_transpose(int r, const double* __restrict__ a, double* __restrict__ b) {
+  __shared__ double tile[32][33];
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  for (int yy = threadIdx.y; yy < 32; yy += blockDim.y) {
+    const int row = by + yy, col = bx + threadIdx.x;
+    if (row < r && col < r) tile[yy][threadIdx.x] = a[(size_t)row * r + col];
+  }
+  __syncthreads();
+  for (int yy = threadIdx.y; yy < 32; yy += blockDim.y) {
+    const int row = bx + yy, col = by + threadIdx.x;
+    if (row < r && col < r) b[(size_t)row * r + col] = tile[threadIdx.x][yy];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Tall-skinny W (n x nm, column-major, ld): split-K W^T x, then W c.
+__global__ void k_dense_gemvT_part(const int* __restrict__ gate, int n, int nm, int ldw, int chunk,
+                                   const double* __restrict__ W, const double* __restrict__ x,
+                                   double* __restrict__ part) {
+  if (gated(gate)) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int r0 = blockIdx.y * chunk;
+  const int r1 = min(n, r0 + chunk);
+  for (int j = blockIdx.x * nw + warp; j < nm; j += gridDim.x * nw) {
+    const double* col = W + (size_t)j * ldw;
+    double a0 = 0.0, a1 = 0.0;
+    int i = r0 + lane;
+    for (; i + 32 < r1; i += 64) {
+      a0 = fma(__ldcs(col + i), __ldg(x + i), a0);
+      a1 = fma(__ldcs(col + i + 32), __ldg(x + i + 32), a1);
+    }
+    for (; i < r1; i += 32) a0 = fma(__ldcs(col + i), __ldg(x + i), a0);
+    const double sum = warp_sum(a0 + a1);
+    if (lane == 0) part[(size_t)blockIdx.y * nm + j] = sum;
+  }
+}
+
+__global__ void k_colsum(const int* __restrict__ gate, int nm, int nchunks, const double* __restrict__ part,
+                         double* __restrict__ out) {
+  if (gated(gate)) return;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= nm) return;
+  double acc = 0.0;
+  for (int c = 0; c < nchunks; ++c) acc += part[(size_t)c * nm + j];
+  out[j] = acc;
+}
+
+__global__ void __launch_bounds__(kThreads) k_dense_gemv(const int* __restrict__ gate, int n, int nm, int ldw,
+                                                      const double* __restrict__ W, const double* __restrict__ c,
+                                                      double* __restrict__ y) {
+  if (gated(gate)) return;
+  extern __shared__ double scoef[];
+  for (int j = threadIdx.x; j < nm; j += blockDim.x) scoef[j] = c[j];
+  __syncthreads();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double* w = W + i;
+  double a0 = 0.0, a1 = 0.0;
+  int j = 0;
+  for (; j + 2 <= nm; j += 2) {
+    a0 = fma(__ldcs(w + (size_t)j * ldw), scoef[j], a0);
+    a1 = fma(__ldcs(w + (size_t)(j + 1) * ldw), scoef[j + 1], a1);
+  }
+  if (j < nm) a0 = fma(__ldcs(w + (size_t)j * ldw), scoef[j], a0);
+  y[i] = a0 + a1;
+}
+
+// ---------------------------------------------------------------------------
+// INEX core solve (preconditioner.cpp:208-216): LU with partial pivoting
+// (dense.cpp:368-393) and its solve; lu_semantics 0 reproduces the reference
+// back substitution (dense.cpp:404-409, reads lu(i,k) below the diagonal),
+// 1 the exact one (reads lu(k,i)).  Single CTA: n_minus is small.
+__global__ void k_lu_solve(const int* __restrict__ gate, int m, const double* __restrict__ lu,
+                           const int* __restrict__ perm, const double* __restrict__ b, double* __restrict__ x,
+                           int exact) {
+  if (gated(gate)) return;
+  extern __shared__ double sy[];
+  for (int i = threadIdx.x; i < m; i += blockDim.x) sy[i] = b[perm[i]];
+  __syncthreads();
+  for (int k = 0; k < m; ++k) {
+    const double f0 = sy[k];
+    __syncthreads();
+    if (f0 != 0.0)
+      for (int i = k + 1 + threadIdx.x; i < m; i += blockDim.x) sy[i] -= f0 * lu[i + (size_t)k * m];
+    __syncthreads();
+  }
+  // back substitution: sequential in k, parallel dot per k
+  __shared__ double red[32];
+  for (int k = m - 1; k >= 0; --k) {
+    double part = 0.0;
+    for (int i = k + 1 + threadIdx.x; i < m; i += blockDim.x) {
+      const double a = exact ? lu[k + (size_t)i * m] : lu[i + (size_t)k * m];
+      part = fma(a, sy[i], part);
+    }
+    part = warp_sum(part);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double acc = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) acc += red[w];
+      sy[k] = (sy[k] - acc) / lu[k + (size_t)k * m];
+    }
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < m; i += blockDim.x) x[i] = sy[i];
+}
+
+// elementwise compositions
+//   mode 0: y = (a - b) + d      (TwoLevel hybrid: Pi hp + corr, preconditioner.cpp:79-81)
+//   mode 1: y = a + b            (additive / AD sums)
+//   mode 2: y = a - b            (projectors)
+__global__ void k_axpby(const int* __restrict__ gate, int n, const double* __restrict__ a,
+                        const double* __restrict__ b, const double* __restrict__ d, double* __restrict__ y,
+                        int mode) {
+  if (gated(gate)) return;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double v;
+    if (mode == 0) v = (a[i] - b[i]) + d[i];
+    else if (mode == 1) v = a[i] + b[i];
+    else v = a[i] - b[i];
+    y[i] = v;
+  }
+}
+
+}  // namespace
+
+// ===========================================================================
+namespace k {
+
+void spmv(Ctx& c, const double* x, double* y, int mode, const double* add, const double* sub, const int* gate) {
+  k_spmv<<<grid_for(c, c.n), kThreads, 0, c.stream>>>(gate, c.n, c.rp.p, c.ci.p, c.va.p, x, y, mode, add, sub);
+  ++c.launches;
+  check_launch("spmv");
+}
+
+void gather(Ctx& c, const double* x, const double* scale, double* xs, const int* gate) {
+  k_gather<<<grid_for(c, c.P), kThreads, 0, c.stream>>>(gate, c.P, c.pidx.p, x, scale, xs);
+  ++c.launches;
+  check_launch("gather");
+}
+
+void prolong(Ctx& c, const double* w, double* y, const int* gate) {
+  k_prolong<<<grid_for(c, c.n), kThreads, 0, c.stream>>>(gate, c.n, c.own_off.p, c.own_pos.p, w, y);
+  ++c.launches;
+  check_launch("prolong");
+}
+
+void nn_local(Ctx& c, const double* xs, double* w, const int* gate) {
+  int ldmax = 0;
+  for (int v : c.h_ld) ldmax = std::max(ldmax, v);
+  const size_t smem = size_t(ldmax) * sizeof(double);
+  static size_t configured = 0;
+  if (smem > configured) {
+    AWG_CUDA(cudaFuncSetAttribute(k_nn_gemvT<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    AWG_CUDA(cudaFuncSetAttribute(k_nn_gemv, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    configured = smem;
+  }
+  if (c.t_gemvT.n) {
+    k_nn_gemvT<8><<<int(c.t_gemvT.n), 256, smem, c.stream>>>(gate, c.t_gemvT.p, c.V.p, c.voff.p, c.ns.p, c.ld.p,
+                                                             c.poff.p, xs, c.lam.p, c.uh.p);
+    ++c.launches;
+    check_launch("nn_gemvT");
+  }
+  k_nn_gemv<<<int(c.t_gemv.n), kThreads, smem, c.stream>>>(gate, c.t_gemv.p, c.V.p, c.voff.p, c.ns.p, c.ld.p,
+                                                           c.msz.p, c.poff.p, c.uh.p, c.ds.p, w);
+  ++c.launches;
+  check_launch("nn_gemv");
+}
+
+void aminus(Ctx& c, const double* x, double* y, const int* gate) {
+  if (c.nneg == 0) {
+    k_zero<<<grid_for(c, c.n), kThreads, 0, c.stream>>>(gate, c.n, y);
+    ++c.launches;
+    check_launch("zero");
+    return;
+  }
+  const int wpb = kThreads / 32;
+  k_neg_dot<<<(c.nneg + wpb - 1) / wpb, kThreads, 0, c.stream>>>(gate, c.nneg, c.neg_s.p, c.neg_k.p, c.neg_w.p,
+                                                                c.V.p, c.voff.p, c.ns.p, c.ld.p, c.poff.p, c.pidx.p,
+                                                                x, c.neg_c.p);
+  ++c.launches;
+  check_launch("neg_dot");
+  k_block_combine<<<grid_for(c, c.P), kThreads, 0, c.stream>>>(gate, c.P, c.psub.p, c.poff.p, c.negoff.p, c.neg_k.p,
+                                                               c.V.p, c.voff.p, c.ld.p, c.neg_c.p, c.wl.p);
+  ++c.launches;
+  check_launch("neg_combine");
+  prolong(c, c.wl.p, y, gate);
+}
+
+void rr_solve(Ctx& c, const CoarseFactor& f, const double* b, double* x, const int* gate) {
+  k_zero<<<grid_for(c, f.dim), kThreads, 0, c.stream>>>(gate, f.dim, x);
+  ++c.launches;
+  if (f.rank == 0) return;
+  const size_t smem = size_t(std::min(f.rank, 4096)) * sizeof(double);
+  k_tri_lower<<<(f.rank + kThreads - 1) / kThreads, kThreads, smem, c.stream>>>(gate, f.rank, f.linv.p, b,
+                                                                               f.retained.p, c.cz2.p);
+  ++c.launches;
+  check_launch("tri_lower");
+  const int wpb = kThreads / 32;
+  k_tri_upperT<<<(f.rank + wpb - 1) / wpb, kThreads, 0, c.stream>>>(gate, f.rank, f.linv.p, c.cz2.p, f.retained.p,
+                                                                   x);
+  ++c.launches;
+  check_launch("tri_upperT");
+}
+
+void coarse_q(Ctx& c, const double* x, double* y, const int* gate) {
+  if (c.n0 == 0) {
+    k_zero<<<grid_for(c, c.n), kThreads, 0, c.stream>>>(gate, c.n, y);
+    ++c.launches;
+    return;
+  }
+  const int wpb = kThreads / 32;
+  k_zT<<<(c.n0 + wpb - 1) / wpb, kThreads, 0, c.stream>>>(gate, c.n0, c.zcol_s.p, c.zcol_loc.p, c.Y.p, c.yoff.p,
+                                                         c.ns.p, c.ld.p, c.poff.p, c.pidx.p, x, c.cz.p);
+  ++c.launches;
+  check_launch("zT");
+  double* coef = c.cz.p + c.n0;  // second half of cz holds the solved coefficients
+  rr_solve(c, c.k0, c.cz.p, coef, gate);
+  k_block_combine<<<grid_for(c, c.P), kThreads, 0, c.stream>>>(gate, c.P, c.psub.p, c.poff.p, c.koff.p, nullptr,
+                                                               c.Y.p, c.yoff.p, c.ld.p, coef, c.wl.p);
+  ++c.launches;
+  check_launch("z_combine");
+  prolong(c, c.wl.p, y, gate);
+}
+
+static void w_transpose_apply(Ctx& c, const double* x, double* out, const int* gate) {
+  const int chunk = 4096;
+  const int nch = (c.n + chunk - 1) / chunk;
+  const int wpb = kThreads / 32;
+  dim3 grid((c.nm + wpb - 1) / wpb, nch);
+  k_dense_gemvT_part<<<grid, kThreads, 0, c.stream>>>(gate, c.n, c.nm, c.ldw, chunk, c.W.p, x, c.wpart.p);
+  ++c.launches;
+  check_launch("dense_gemvT_part");
+  k_colsum<<<(c.nm + kThreads - 1) / kThreads, kThreads, 0, c.stream>>>(gate, c.nm, nch, c.wpart.p, out);
+  ++c.launches;
+  check_launch("colsum");
+}
+
+static void w_apply(Ctx& c, const double* coef, double* y, const int* gate) {
+  const size_t smem = size_t(c.nm) * sizeof(double);
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    AWG_CUDA(cudaFuncSetAttribute(k_dense_gemv, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    configured = smem;
+  }
+  k_dense_gemv<<<(c.n + kThreads - 1) / kThreads, kThreads, smem, c.stream>>>(gate, c.n, c.nm, c.ldw, c.W.p, coef,
+                                                                              y);
+  ++c.launches;
+  check_launch("dense_gemv");
+}
+
+void second_q(Ctx& c, const double* x, double* y, const int* gate) {
+  if (c.nm == 0) {
+    k_zero<<<grid_for(c, c.n), kThreads, 0, c.stream>>>(gate, c.n, y);
+    ++c.launches;
+    return;
+  }
+  double* wx = c.cz.p;
+  double* coef = c.cz.p + c.nm;
+  w_transpose_apply(c, x, wx, gate);
+  rr_solve(c, c.kw, wx, coef, gate);
+  w_apply(c, coef, y, gate);
+}
+
+void inex_q(Ctx& c, const double* x, double* y, const int* gate) {
+  double* wx = c.cz.p;
+  double* coef = c.cz.p + c.nm;
+  w_transpose_apply(c, x, wx, gate);
+  k_lu_solve<<<1, 1024, size_t(c.nm) * sizeof(double), c.stream>>>(gate, c.nm, c.core_lu.p, c.core_perm.p, wx, coef,
+                                                                   c.lu_semantics);
+  ++c.launches;
+  check_launch("lu_solve");
+  w_apply(c, coef, y, gate);
+}
+
+void axpby(Ctx& c, int n, const double* a, const double* b, const double* d, double* y, int mode, const int* gate) {
+  k_axpby<<<grid_for(c, n), kThreads, 0, c.stream>>>(gate, n, a, b, d, y, mode);
+  ++c.launches;
+  check_launch("axpby");
+}
+
+void tri_inverse(Ctx& c, const double* l, int r, double* linv) {
+  if (r == 0) return;
+  DArr<double> scratch;
+  scratch.alloc(size_t(r) * r);
+  k_tri_inverse_rm<<<(r + 127) / 128, 128, 0, c.stream>>>(r, l, scratch.p);
+  ++c.launches;
+  check_launch("tri_inverse");
+  dim3 grid((r + 31) / 32, (r + 31) / 32);
+  k_transpose<<<grid, dim3(32, 8), 0, c.stream>>>(r, scratch.p, linv);
+  ++c.launches;
+  check_launch("transpose");
+  AWG_CUDA(cudaStreamSynchronize(c.stream));
+}
+
+}  // namespace k
+}  // namespace awgb

@@ -1,0 +1,477 @@
+// Operator composition (H1, H2, H3, projectors) and the device-resident PCG.
+//
+// Composition follows the reference exactly, operation by operation:
+//   TwoLevel::apply        preconditioner.cpp:64-82 (hybrid: Pi^T, H1, Pi, + Qx;
+//                          Q x is computed once and reused for Pi^T, which the
+//                          reference recomputes bit-identically, coarse.cpp:188)
+//   AwgPreconditioner      preconditioner.cpp:185-221 (AD, HYB, INEX), apply_pi3(_transpose) :161-183
+//   pcg                    krylov.cpp:36-124, including the recursive/true residual
+//                          stopping rule (:93-102), breakdown handling (:79-82, :107-110)
+//                          and the Lanczos coefficients (:90-91)
+#include <cmath>
+#include <cstring>
+
+#include "awg_internal.cuh"
+
+namespace awgb {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block partial -> fixed slot; the last block to arrive sums the slots in a
+// fixed order (deterministic single-pass grid reduction) and runs `fin`.
+template <class Fin>
+__device__ void grid_reduce(double v, double* part, unsigned* count, Fin fin) {
+  __shared__ double sred[32];
+  __shared__ int is_last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = warp_sum(v);
+  if (lane == 0) sred[warp] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double acc = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) acc += sred[w];
+    part[blockIdx.x] = acc;
+    __threadfence();
+    const unsigned t = atomicAdd(count, 1u);
+    is_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (is_last && warp == 0) {
+    __threadfence();
+    double acc = 0.0;
+    for (int b = lane; b < (int)gridDim.x; b += 32) acc += __ldcg(part + b);
+    acc = warp_sum(acc);
+    if (lane == 0) {
+      fin(acc);
+      *count = 0;
+    }
+  }
+}
+
+__global__ void k_pcg_init(PcgState* st, int n, const double* __restrict__ b, double* __restrict__ x,
+                           double* __restrict__ r, double* part, unsigned* count) {
+  double acc = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const double bi = b[i];
+    x[i] = 0.0;
+    r[i] = bi;
+    acc = fma(bi, bi, acc);
+  }
+  grid_reduce(acc, part, count, [&](double s) {
+    st->bnorm = sqrt(s);
+    st->it = 0;
+    st->error = 0;
+    st->past_rtol = 0;
+    st->need_true = 0;
+    st->converged = (s == 0.0);
+    st->done = (s == 0.0);
+  });
+}
+
+// rz = <r, z>; the initial check (krylov.cpp:51-53) or the beta step (:105-115).
+__global__ void k_pcg_rz(PcgState* st, int n, const double* __restrict__ r, const double* __restrict__ z,
+                         double* part, unsigned* count, int initial) {
+  if (st->done) return;
+  double acc = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) acc = fma(r[i], z[i], acc);
+  grid_reduce(acc, part, count, [&](double rz) {
+    if (initial) {
+      if (rz <= 0.0) {
+        st->error = PCG_BAD_PRECOND;
+        st->done = 1;
+      }
+      st->rz = rz;
+      st->beta = 0.0;
+      return;
+    }
+    if (rz <= 0.0) {
+      if (!st->past_rtol) st->error = PCG_BAD_PRECOND;
+      st->done = 1;
+      return;
+    }
+    const double beta = rz / st->rz;
+    st->beta = beta;
+    st->rz = rz;
+    st->beta_prev = beta;
+    st->alpha_prev = st->alpha;
+  });
+}
+
+// p = z + beta p   (p = z on the first step: beta = 0 and p zeroed)
+__global__ void k_pcg_p(const PcgState* st, int n, const double* __restrict__ z, double* __restrict__ p, int initial) {
+  if (st->done) return;
+  const double beta = st->beta;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    p[i] = initial ? z[i] : fma(beta, p[i], z[i]);
+}
+
+// q = A p and <p, q> (krylov.cpp:77-83)
+__global__ void k_pcg_spmv_dot(PcgState* st, int n, const int* __restrict__ rp, const int* __restrict__ ci,
+                               const double* __restrict__ va, const double* __restrict__ p, double* __restrict__ q,
+                               double* part, unsigned* count) {
+  if (st->done) return;
+  double acc = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int k = rp[i]; k < rp[i + 1]; ++k) s = fma(va[k], __ldg(p + ci[k]), s);
+    q[i] = s;
+    acc = fma(p[i], s, acc);
+  }
+  grid_reduce(acc, part, count, [&](double pq) {
+    st->pq = pq;
+    if (pq <= 0.0) {
+      if (!st->past_rtol) st->error = PCG_BAD_OPERATOR;
+      st->done = 1;
+      return;
+    }
+    st->alpha = st->rz / pq;
+  });
+}
+
+// x += alpha p; r -= alpha q; relres = ||r|| / ||b||, history and Lanczos
+// coefficients (krylov.cpp:84-92)
+__global__ void k_pcg_update(PcgState* st, int n, double* __restrict__ x, double* __restrict__ r,
+                             const double* __restrict__ p, const double* __restrict__ q, double* part,
+                             unsigned* count, double* hres, double* hdiag, double* hoff) {
+  if (st->done) return;
+  const double alpha = st->alpha;
+  double acc = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    x[i] = fma(alpha, p[i], x[i]);
+    const double ri = fma(-alpha, q[i], r[i]);
+    r[i] = ri;
+    acc = fma(ri, ri, acc);
+  }
+  grid_reduce(acc, part, count, [&](double rr) {
+    const double relres = sqrt(rr) / st->bnorm;
+    const int it = st->it + 1;
+    st->it = it;
+    st->relres = relres;
+    hres[it - 1] = relres;
+    hdiag[it - 1] = 1.0 / alpha + (it > 1 ? st->beta_prev / st->alpha_prev : 0.0);
+    if (it > 1) hoff[it - 2] = sqrt(st->beta_prev) / st->alpha_prev;
+    st->need_true = (relres <= st->rtol);
+    if (st->need_true) st->past_rtol = 1;
+    if (!st->need_true && it == st->maxit) st->done = 1;
+  });
+}
+
+// Recomputed residual ||b - A x|| / ||b|| and the acceptance rule (krylov.cpp:93-103).
+__global__ void k_pcg_true(PcgState* st, int n, const int* __restrict__ rp, const int* __restrict__ ci,
+                           const double* __restrict__ va, const double* __restrict__ x, const double* __restrict__ b,
+                           double* part, unsigned* count) {
+  const int force = st->force_true;
+  if (!force && (st->done || !st->need_true)) return;
+  double acc = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int k = rp[i]; k < rp[i + 1]; ++k) s = fma(va[k], __ldg(x + ci[k]), s);
+    const double d = b[i] - s;
+    acc = fma(d, d, acc);
+  }
+  grid_reduce(acc, part, count, [&](double dd) {
+    const double tr = sqrt(dd) / st->bnorm;
+    st->true_rel = tr;
+    if (force) {
+      st->final_rel = tr;
+      return;
+    }
+    if (tr <= st->rtol || fabs(tr - st->relres) <= 1e-8) {
+      st->converged = 1;
+      st->done = 1;
+      st->final_rel = tr;
+      st->rec_exit = st->relres;
+    } else if (st->it == st->maxit) {
+      st->done = 1;
+    }
+  });
+}
+
+__global__ void k_set_force(PcgState* st, int v) { st->force_true = v; }
+
+int red_grid(const Ctx& c) {
+  int g = (c.n + kThreads - 1) / kThreads;
+  return std::max(1, std::min(g, c.sm_count * 4));
+}
+
+// Extreme eigenvalues of the symmetric tridiagonal Lanczos matrix by Sturm
+// bisection (the reference uses dense Jacobi on it, krylov.cpp:126-139;
+// report-only quantity).
+int sturm_count(const std::vector<double>& d, const std::vector<double>& e, double x) {
+  int cnt = 0;
+  double q = 1.0;
+  for (size_t i = 0; i < d.size(); ++i) {
+    const double e2 = i ? e[i - 1] * e[i - 1] : 0.0;
+    q = d[i] - x - (i ? e2 / q : 0.0);
+    if (q == 0.0) q = -1e-300;
+    if (q < 0.0) ++cnt;
+  }
+  return cnt;
+}
+
+double tridiag_eig(const std::vector<double>& d, const std::vector<double>& e, int k) {
+  double lo = d[0], hi = d[0];
+  for (size_t i = 0; i < d.size(); ++i) {
+    const double r = (i ? std::fabs(e[i - 1]) : 0.0) + (i + 1 < d.size() ? std::fabs(e[i]) : 0.0);
+    lo = std::min(lo, d[i] - r);
+    hi = std::max(hi, d[i] + r);
+  }
+  for (int iter = 0; iter < 200; ++iter) {
+    const double mid = 0.5 * (lo + hi);
+    if (mid <= lo || mid >= hi) break;
+    if (sturm_count(d, e, mid) > k) hi = mid;
+    else lo = mid;
+  }
+  return 0.5 * (lo + hi);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+void Ctx::alloc_work() {
+  const size_t nn = size_t(n);
+  for (DArr<double>* b : {&t0, &t1, &t2, &t3, &t4, &t5, &t6, &t7, &t8}) b->alloc(nn);
+  xs.alloc(P);
+  uh.alloc(P);
+  wl.alloc(P);
+  const size_t cdim = size_t(std::max(n0, nm)) * 2 + 2;
+  cz.alloc(cdim);
+  cz2.alloc(cdim);
+  const int nch = (n + 4095) / 4096;
+  wpart.alloc(size_t(std::max(nm, 1)) * nch);
+  red.alloc(size_t(sm_count) * 16);
+  red_count.alloc(1);
+  red_count.zero(stream);
+  pcg.alloc(1);
+  for (DArr<double>* b : {&px, &pr, &pz, &pp, &pq, &pb, &pt}) b->alloc(nn);
+}
+
+static void h1(Ctx& c, const double* x, double* y, const int* gate) {
+  k::gather(c, x, c.ds.p, c.xs.p, gate);
+  k::nn_local(c, c.xs.p, c.wl.p, gate);
+  k::prolong(c, c.wl.p, y, gate);
+}
+
+static void aplus(Ctx& c, const double* x, double* y, const int* gate) {
+  k::aminus(c, x, y, gate);
+  k::spmv(c, x, y, 1, y, nullptr, gate);
+}
+
+static void h2(Ctx& c, const double* x, double* y, const int* gate) {
+  if (c.n0 == 0) {
+    h1(c, x, y, gate);
+    return;
+  }
+  k::coarse_q(c, x, c.t0.p, gate);  // corr
+  if (c.cfg.composition == 0) {
+    h1(c, x, c.t1.p, gate);
+    k::axpby(c, c.n, c.t1.p, c.t0.p, nullptr, y, 1, gate);
+    return;
+  }
+  k::aminus(c, c.t0.p, c.t1.p, gate);
+  k::spmv(c, c.t0.p, c.t2.p, 2, c.t1.p, x, gate);  // pt = x - A+ corr
+  h1(c, c.t2.p, c.t3.p, gate);                     // hp
+  aplus(c, c.t3.p, c.t4.p, gate);                  // A+ hp
+  k::coarse_q(c, c.t4.p, c.t5.p, gate);            // Q A+ hp
+  k::axpby(c, c.n, c.t3.p, c.t5.p, c.t0.p, y, 0, gate);
+}
+
+void op_apply(Ctx& c, int op, const double* x, double* y, const int* gate) {
+  if (x == y) c.fail(AWG_E_ARG, "apply: x and y must not alias (operators.hpp:7)");
+  const bool have_w = c.nm > 0;
+  switch (op) {
+    case AWG_OP_A:
+      k::spmv(c, x, y, 0, nullptr, nullptr, gate);
+      return;
+    case AWG_OP_AMINUS:
+      k::aminus(c, x, y, gate);
+      return;
+    case AWG_OP_APLUS:
+      aplus(c, x, y, gate);
+      return;
+    case AWG_OP_H1:
+      h1(c, x, y, gate);
+      return;
+    case AWG_OP_Q:
+      k::coarse_q(c, x, y, gate);
+      return;
+    case AWG_OP_QW:
+      k::second_q(c, x, y, gate);
+      return;
+    case AWG_OP_H2:
+      h2(c, x, y, gate);
+      return;
+    case AWG_OP_PI3:
+      if (!have_w) {
+        AWG_CUDA(cudaMemcpyAsync(y, x, sizeof(double) * c.n, cudaMemcpyDeviceToDevice, c.stream));
+        return;
+      }
+      k::spmv(c, x, c.t6.p, 0, nullptr, nullptr, gate);
+      k::second_q(c, c.t6.p, c.t7.p, gate);
+      k::axpby(c, c.n, x, c.t7.p, nullptr, y, 2, gate);
+      return;
+    case AWG_OP_PI3T:
+      if (!have_w) {
+        AWG_CUDA(cudaMemcpyAsync(y, x, sizeof(double) * c.n, cudaMemcpyDeviceToDevice, c.stream));
+        return;
+      }
+      k::second_q(c, x, c.t6.p, gate);
+      k::spmv(c, c.t6.p, y, 3, nullptr, x, gate);
+      return;
+    case AWG_OP_H3: {
+      const int mode = c.cfg.awg_mode;
+      if (mode == 0 || !have_w) {
+        h2(c, x, y, gate);
+        return;
+      }
+      if (mode == 1) {  // AD
+        k::second_q(c, x, c.t6.p, gate);
+        h2(c, x, c.t7.p, gate);
+        k::axpby(c, c.n, c.t7.p, c.t6.p, nullptr, y, 1, gate);
+      } else if (mode == 2) {  // HYB
+        k::second_q(c, x, c.t6.p, gate);                 // corr
+        k::spmv(c, c.t6.p, c.t7.p, 3, nullptr, x, gate);  // pt = x - A corr
+        h2(c, c.t7.p, c.t8.p, gate);                     // hp
+        k::spmv(c, c.t8.p, c.t7.p, 0, nullptr, nullptr, gate);
+        k::second_q(c, c.t7.p, c.t1.p, gate);  // QW A hp (t1 is free once h2 returned)
+        k::axpby(c, c.n, c.t8.p, c.t1.p, c.t6.p, y, 0, gate);
+      } else {  // INEX
+        k::inex_q(c, x, c.t6.p, gate);
+        h2(c, x, c.t7.p, gate);
+        k::axpby(c, c.n, c.t7.p, c.t6.p, nullptr, y, 1, gate);
+      }
+      return;
+    }
+    default:
+      c.fail(AWG_E_ARG, "apply: unknown operator");
+  }
+}
+
+// ---------------------------------------------------------------------------
+void run_pcg(Ctx& c, const double* b_dev, double rtol, int maxit, awg_solve_report* rep) {
+  if (!(rtol > 0.0 && rtol < 1.0)) c.fail(AWG_E_ARG, "pcg: rtol must be in (0,1)");
+  if (maxit < 1) c.fail(AWG_E_ARG, "pcg: maxit must be positive");
+  const int n = c.n;
+  if (c.hist_cap < maxit) {
+    c.hist_res.alloc(maxit);
+    c.hist_diag.alloc(maxit);
+    c.hist_off.alloc(maxit);
+    c.hist_cap = maxit;
+  }
+  PcgState h{};
+  h.rtol = rtol;
+  h.maxit = maxit;
+  AWG_CUDA(cudaMemcpyAsync(c.pcg.p, &h, sizeof(h), cudaMemcpyHostToDevice, c.stream));
+  if (b_dev != c.pb.p)
+    AWG_CUDA(cudaMemcpyAsync(c.pb.p, b_dev, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.stream));
+  PcgState* st = c.pcg.p;
+  const int* gate = &st->done;
+  const int g = red_grid(c);
+  cudaEvent_t e0, e1;
+  AWG_CUDA(cudaEventCreate(&e0));
+  AWG_CUDA(cudaEventCreate(&e1));
+  AWG_CUDA(cudaEventRecord(e0, c.stream));
+
+  k_pcg_init<<<g, kThreads, 0, c.stream>>>(st, n, c.pb.p, c.px.p, c.pr.p, c.red.p, c.red_count.p);
+  ++c.launches;
+  op_apply(c, AWG_OP_H3, c.pr.p, c.pz.p, gate);
+  k_pcg_rz<<<g, kThreads, 0, c.stream>>>(st, n, c.pr.p, c.pz.p, c.red.p, c.red_count.p, 1);
+  k_pcg_p<<<g, kThreads, 0, c.stream>>>(st, n, c.pz.p, c.pp.p, 1);
+  c.launches += 2;
+  check_launch("pcg init");
+
+  auto iteration = [&]() {
+    k_pcg_spmv_dot<<<g, kThreads, 0, c.stream>>>(st, n, c.rp.p, c.ci.p, c.va.p, c.pp.p, c.pq.p, c.red.p,
+                                                  c.red_count.p);
+    k_pcg_update<<<g, kThreads, 0, c.stream>>>(st, n, c.px.p, c.pr.p, c.pp.p, c.pq.p, c.red.p, c.red_count.p,
+                                               c.hist_res.p, c.hist_diag.p, c.hist_off.p);
+    k_pcg_true<<<g, kThreads, 0, c.stream>>>(st, n, c.rp.p, c.ci.p, c.va.p, c.px.p, c.pb.p, c.red.p,
+                                             c.red_count.p);
+    c.launches += 3;
+    op_apply(c, AWG_OP_H3, c.pr.p, c.pz.p, gate);
+    k_pcg_rz<<<g, kThreads, 0, c.stream>>>(st, n, c.pr.p, c.pz.p, c.red.p, c.red_count.p, 0);
+    k_pcg_p<<<g, kThreads, 0, c.stream>>>(st, n, c.pz.p, c.pp.p, 0);
+    c.launches += 2;
+    check_launch("pcg iteration");
+  };
+
+  // Enqueue iterations in batches; the device-side `done` flag turns every
+  // kernel after the stopping point into a no-op, so overshooting is free of
+  // side effects.  One CUDA graph holds one iteration.
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  bool use_graph = true;
+  if (use_graph) {
+    AWG_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+    iteration();
+    AWG_CUDA(cudaStreamEndCapture(c.stream, &graph));
+    AWG_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+  }
+  int batch = 2;
+  int issued = 0;
+  while (true) {
+    for (int b = 0; b < batch && issued < maxit; ++b, ++issued) {
+      if (use_graph) AWG_CUDA(cudaGraphLaunch(exec, c.stream));
+      else iteration();
+    }
+    AWG_CUDA(cudaMemcpyAsync(&h, st, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+    AWG_CUDA(cudaStreamSynchronize(c.stream));
+    if (h.done || issued >= maxit) break;
+    batch = std::min(batch * 2, 16);
+  }
+  if (exec) cudaGraphExecDestroy(exec);
+  if (graph) cudaGraphDestroy(graph);
+
+  if (!h.converged && h.it > 0 && !h.error) {
+    k_set_force<<<1, 1, 0, c.stream>>>(st, 1);
+    k_pcg_true<<<g, kThreads, 0, c.stream>>>(st, n, c.rp.p, c.ci.p, c.va.p, c.px.p, c.pb.p, c.red.p, c.red_count.p);
+    k_set_force<<<1, 1, 0, c.stream>>>(st, 0);
+    c.launches += 3;
+    AWG_CUDA(cudaMemcpyAsync(&h, st, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+  }
+  AWG_CUDA(cudaEventRecord(e1, c.stream));
+  AWG_CUDA(cudaStreamSynchronize(c.stream));
+  float ms = 0.f;
+  AWG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (h.error == PCG_BAD_OPERATOR) c.fail(AWG_E_BREAKDOWN, "pcg: operator not spd (<p, Ap> <= 0)");
+  if (h.error == PCG_BAD_PRECOND) c.fail(AWG_E_BREAKDOWN, "pcg: preconditioner not spd (<r, Hr> <= 0)");
+
+  const int it = h.it;
+  c.h_hist_res.assign(it, 0.0);
+  c.h_hist_diag.assign(it, 0.0);
+  c.h_hist_off.assign(it > 1 ? it - 1 : 0, 0.0);
+  if (it) {
+    AWG_CUDA(cudaMemcpy(c.h_hist_res.data(), c.hist_res.p, sizeof(double) * it, cudaMemcpyDeviceToHost));
+    AWG_CUDA(cudaMemcpy(c.h_hist_diag.data(), c.hist_diag.p, sizeof(double) * it, cudaMemcpyDeviceToHost));
+    if (it > 1)
+      AWG_CUDA(cudaMemcpy(c.h_hist_off.data(), c.hist_off.p, sizeof(double) * (it - 1), cudaMemcpyDeviceToHost));
+  }
+  std::memset(rep, 0, sizeof(*rep));
+  rep->iterations = it;
+  rep->converged = h.converged;
+  rep->solve_ms = ms;
+  if (h.converged && it == 0) return;  // b == 0
+  rep->final_relative_residual = h.final_rel;
+  rep->recurrence_residual_at_exit = h.converged ? h.rec_exit : (it ? c.h_hist_res.back() : 0.0);
+  // fill_ritz (krylov.cpp:21-32)
+  if (it == 1) {
+    rep->ritz_min = rep->ritz_max = c.h_hist_diag[0];
+    rep->kappa_estimate = 1.0;
+  } else if (it > 1) {
+    rep->ritz_min = tridiag_eig(c.h_hist_diag, c.h_hist_off, 0);
+    rep->ritz_max = tridiag_eig(c.h_hist_diag, c.h_hist_off, it - 1);
+    rep->kappa_estimate = rep->ritz_max / rep->ritz_min;
+  }
+}
+
+}  // namespace awgb
