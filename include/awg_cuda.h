@@ -167,6 +167,11 @@ int awg_get_array(struct awg_ctx* ctx, int which, void* out, long long cap_elems
 long long awg_launch_count(const struct awg_ctx* ctx);
 /* Device time (ms) of the last apply loop: runs op `reps` times on device buffers. */
 int awg_time_apply(struct awg_ctx* ctx, int op, int reps, double* ms_per_apply);
+/* Device time (ms per launch, CUDA events on the context stream) of one hot
+ * kernel launched `reps` times back to back: 0 batched NN GEMV^T (V^s^T x),
+ * 1 batched NN GEMV (V^s u), 2 CSR SpMV, 3 W^T x, 4 W c.  Also returns the
+ * algorithmic bytes one launch must move (operands read once, results written). */
+int awg_time_kernel(struct awg_ctx* ctx, int which, int reps, double* ms_per_launch, double* bytes_per_launch);
 
 #ifdef __cplusplus
 }

@@ -162,7 +162,7 @@ class _Stats(ctypes.Structure):
 EXPORTED_SYMBOLS = [
     "awg_create", "awg_destroy", "awg_last_error", "awg_last_error_index", "awg_set_matrix",
     "awg_set_partition", "awg_setup", "awg_load_factors", "awg_apply", "awg_pcg", "awg_query",
-    "awg_get_history", "awg_get_array", "awg_launch_count", "awg_time_apply",
+    "awg_get_history", "awg_get_array", "awg_launch_count", "awg_time_apply", "awg_time_kernel",
 ]
 
 _lib = None
@@ -195,6 +195,8 @@ def load_library(path: str = LIB_PATH):
     lib.awg_launch_count.argtypes = [vp]
     lib.awg_launch_count.restype = ctypes.c_longlong
     lib.awg_time_apply.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
+    lib.awg_time_kernel.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
+                                    ctypes.POINTER(ctypes.c_double)]
     _lib = lib
     return lib
 
@@ -370,6 +372,14 @@ class ProblemContext:
         ms = ctypes.c_double()
         self._check(self._lib.awg_time_apply(self._h, int(op), reps, ctypes.byref(ms)))
         return ms.value
+
+    KERNELS = {"nn_gemvT": 0, "nn_gemv": 1, "spmv": 2, "w_gemvT": 3, "w_gemv": 4}
+
+    def time_kernel(self, name: str, reps: int = 10) -> Tuple[float, float]:
+        """(ms per launch, algorithmic bytes per launch) of one hot kernel."""
+        ms, by = ctypes.c_double(), ctypes.c_double()
+        self._check(self._lib.awg_time_kernel(self._h, self.KERNELS[name], reps, ctypes.byref(ms), ctypes.byref(by)))
+        return ms.value, by.value
 
     def pcg(self, b=None, rtol: float = 1e-10, maxit: int = 10000) -> Tuple[np.ndarray, SolveReport]:
         """pcg(spmv, H3.apply, b, rtol, maxit) — krylov.cpp:36-124, on device."""

@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <functional>
 #include <numeric>
 #include <string>
 
@@ -495,6 +496,60 @@ int awg_time_apply(awg_ctx* ctx, int op, int reps, double* ms) {
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     *ms = double(t) / reps;
+  });
+}
+
+int awg_time_kernel(awg_ctx* ctx, int which, int reps, double* ms, double* bytes) {
+  return guarded(ctx, [&](Ctx& c) {
+    if (!c.have_factors) c.fail(AWG_E_STATE, "time_kernel: preconditioner not set up");
+    if (reps < 1 || !ms || !bytes) c.fail(AWG_E_ARG, "time_kernel: bad arguments");
+    double b = 0.0;
+    long long vcols = 0, P = 0;
+    for (int s = 0; s < c.N; ++s) {
+      vcols += (long long)c.h_ns[s] * (c.h_ns[s] - c.h_m[s]);
+      P += c.h_ns[s];
+    }
+    std::function<void()> launch;
+    switch (which) {
+      case 0:  // V^T reads + xs read + uh written (columns >= m)
+        b = 8.0 * vcols + 8.0 * P + 8.0 * P;
+        launch = [&] { k::nn_gemvT(c, c.xs.p, nullptr); };
+        break;
+      case 1:  // V reads + uh, D read + w written
+        b = 8.0 * vcols + 8.0 * P * 3;
+        launch = [&] { k::nn_gemv(c, c.wl.p, nullptr); };
+        break;
+      case 2:  // values + col indices + row offsets + x + y
+        b = 12.0 * c.nnz + 4.0 * (c.n + 1) + 16.0 * c.n;
+        launch = [&] { k::spmv(c, c.pb.p, c.pz.p, 0, nullptr, nullptr, nullptr); };
+        break;
+      case 3:
+        if (c.nm == 0) c.fail(AWG_E_STATE, "time_kernel: no W");
+        b = 8.0 * c.n * c.nm + 8.0 * c.n + 8.0 * c.nm;
+        launch = [&] { k::wT(c, c.pb.p, c.cz.p, nullptr); };
+        break;
+      case 4:
+        if (c.nm == 0) c.fail(AWG_E_STATE, "time_kernel: no W");
+        b = 8.0 * c.n * c.nm + 8.0 * c.n + 8.0 * c.nm;
+        launch = [&] { k::w_apply_public(c, c.cz.p, c.pz.p, nullptr); };
+        break;
+      default:
+        c.fail(AWG_E_ARG, "time_kernel: unknown kernel");
+    }
+    cudaEvent_t e0, e1;
+    AWG_CUDA(cudaEventCreate(&e0));
+    AWG_CUDA(cudaEventCreate(&e1));
+    launch();
+    AWG_CUDA(cudaEventRecord(e0, c.stream));
+    for (int r = 0; r < reps; ++r) launch();
+    AWG_CUDA(cudaEventRecord(e1, c.stream));
+    AWG_CUDA(cudaEventSynchronize(e1));
+    float t = 0.f;
+    AWG_CUDA(cudaEventElapsedTime(&t, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *ms = double(t) / reps;
+    *bytes = b;
   });
 }
 

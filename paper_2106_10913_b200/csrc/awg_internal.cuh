@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <map>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -129,6 +130,8 @@ void spmv(Ctx& c, const double* x, double* y, int mode, const double* add, const
 void gather(Ctx& c, const double* x, const double* scale, double* xs, const int* gate);
 void prolong(Ctx& c, const double* w, double* y, const int* gate);
 void nn_local(Ctx& c, const double* xs, double* w, const int* gate);  // w = D V mask(1/lam) V^T xs
+void nn_gemvT(Ctx& c, const double* xs, const int* gate);              // uh = mask(1/lam) V^T xs
+void nn_gemv(Ctx& c, double* w, const int* gate);                      // w = D V uh
 void aminus(Ctx& c, const double* x, double* y, const int* gate);     // y = A- x
 void coarse_q(Ctx& c, const double* x, double* y, const int* gate);   // y = Z K0+ Z^T x
 void second_q(Ctx& c, const double* x, double* y, const int* gate);   // y = W KW+ W^T x
@@ -136,6 +139,9 @@ void inex_q(Ctx& c, const double* x, double* y, const int* gate);     // y = W c
 void axpby(Ctx& c, int n, const double* a, const double* b, const double* d, double* y, int mode, const int* gate);
 void rr_solve(Ctx& c, const CoarseFactor& f, const double* b, double* x, const int* gate);
 void tri_inverse(Ctx& c, const double* l, int r, double* linv);
+void zT(Ctx& c, const double* x, double* out, const int* gate);  // out = Z^T x (n0)
+void wT(Ctx& c, const double* x, double* out, const int* gate);  // out = W^T x (n_minus)
+void w_apply_public(Ctx& c, const double* coef, double* y, const int* gate);  // y = W coef
 }  // namespace k
 
 // ---- the context --------------------------------------------------------------
@@ -212,18 +218,28 @@ struct Ctx {
 
   // pcg
   DArr<PcgState> pcg;
+  DArr<int> pcg_flag;
+  std::map<int, cudaGraphExec_t> graphs;  // one PCG iteration per operator pair
+  std::map<int, long long> graph_launches;
+  void invalidate_graphs() {
+    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+    graphs.clear();
+    graph_launches.clear();
+  }
+  ~Ctx() { invalidate_graphs(); }
   DArr<double> px, pr, pz, pp, pq, pb, pt;
   DArr<double> hist_res, hist_diag, hist_off;
   int hist_cap = 0;
   std::vector<double> h_hist_res, h_hist_diag, h_hist_off;
 
-  void alloc_work();
+  void alloc_work();  // also invalidates cached graphs
   void fail(int code, const std::string& m, int idx = -1) { throw AwgError(code, m, idx); }
 };
 
 // ---- operators (ops.cu) -------------------------------------------------------
 void op_apply(Ctx& c, int op, const double* x, double* y, const int* gate);
-void run_pcg(Ctx& c, const double* b_dev, double rtol, int maxit, awg_solve_report* rep);
+void run_pcg(Ctx& c, const double* b_dev, double rtol, int maxit, awg_solve_report* rep,
+             int op_a = AWG_OP_A, int op_h = AWG_OP_H3);
 void finalize_factors(Ctx& c);  // task lists, A- modes, inverses, work buffers
 void build_core(Ctx& c);        // INEX core LU
 void run_setup(Ctx& c, const awg_config& cfg);  // setup.cu

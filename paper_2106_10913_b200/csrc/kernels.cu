@@ -6,8 +6,8 @@
 // without changing any state after the stopping rule fired.
 //
 // Summation-order notes (parity): the CSR SpMV accumulates in ascending
-// column order with fused multiply-adds exactly like sparse.cpp:49-56
-// compiled with GCC's default FP contraction (bit-identical results); the
+// column order with separately rounded multiply and add exactly like the
+// reference build of sparse.cpp:49-56 (bit-identical results); the
 // prolongation sums subdomain contributions in ascending s like
 // OneLevel::apply (preconditioner.cpp:37-55).  Dense dot products use
 // fixed-shape warp trees (deterministic, not sequential): the parity bar for
@@ -50,7 +50,9 @@ __global__ void k_spmv(const int* __restrict__ gate, int n, const int* __restric
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int k0 = rp[i], k1 = rp[i + 1];
     double acc = 0.0;
-    for (int k = k0; k < k1; ++k) acc = fma(va[k], __ldg(x + ci[k]), acc);
+    // mul then add, not contracted: GCC emits vmulsd + vaddsd for this loop in
+    // the reference build (sparse.cpp:53), so the result is bit-identical.
+    for (int k = k0; k < k1; ++k) acc = __dadd_rn(acc, __dmul_rn(va[k], __ldg(x + ci[k])));
     double out;
     if (mode == 0) out = acc;
     else if (mode == 1) out = add[i] + acc;
@@ -446,7 +448,7 @@ void prolong(Ctx& c, const double* w, double* y, const int* gate) {
   check_launch("prolong");
 }
 
-void nn_local(Ctx& c, const double* xs, double* w, const int* gate) {
+static size_t nn_smem(Ctx& c) {
   int ldmax = 0;
   for (int v : c.h_ld) ldmax = std::max(ldmax, v);
   const size_t smem = size_t(ldmax) * sizeof(double);
@@ -456,16 +458,29 @@ void nn_local(Ctx& c, const double* xs, double* w, const int* gate) {
     AWG_CUDA(cudaFuncSetAttribute(k_nn_gemv, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     configured = smem;
   }
-  if (c.t_gemvT.n) {
-    k_nn_gemvT<8><<<int(c.t_gemvT.n), 256, smem, c.stream>>>(gate, c.t_gemvT.p, c.V.p, c.voff.p, c.ns.p, c.ld.p,
-                                                             c.poff.p, xs, c.lam.p, c.uh.p);
-    ++c.launches;
-    check_launch("nn_gemvT");
-  }
+  return smem;
+}
+
+void nn_gemvT(Ctx& c, const double* xs, const int* gate) {
+  const size_t smem = nn_smem(c);
+  if (!c.t_gemvT.n) return;
+  k_nn_gemvT<8><<<int(c.t_gemvT.n), 256, smem, c.stream>>>(gate, c.t_gemvT.p, c.V.p, c.voff.p, c.ns.p, c.ld.p,
+                                                           c.poff.p, xs, c.lam.p, c.uh.p);
+  ++c.launches;
+  check_launch("nn_gemvT");
+}
+
+void nn_gemv(Ctx& c, double* w, const int* gate) {
+  const size_t smem = nn_smem(c);
   k_nn_gemv<<<int(c.t_gemv.n), kThreads, smem, c.stream>>>(gate, c.t_gemv.p, c.V.p, c.voff.p, c.ns.p, c.ld.p,
                                                            c.msz.p, c.poff.p, c.uh.p, c.ds.p, w);
   ++c.launches;
   check_launch("nn_gemv");
+}
+
+void nn_local(Ctx& c, const double* xs, double* w, const int* gate) {
+  nn_gemvT(c, xs, gate);
+  nn_gemv(c, w, gate);
 }
 
 void aminus(Ctx& c, const double* x, double* y, const int* gate) {
@@ -524,6 +539,14 @@ void coarse_q(Ctx& c, const double* x, double* y, const int* gate) {
   prolong(c, c.wl.p, y, gate);
 }
 
+void zT(Ctx& c, const double* x, double* out, const int* gate) {
+  const int wpb = kThreads / 32;
+  k_zT<<<(c.n0 + wpb - 1) / wpb, kThreads, 0, c.stream>>>(gate, c.n0, c.zcol_s.p, c.zcol_loc.p, c.Y.p, c.yoff.p,
+                                                         c.ns.p, c.ld.p, c.poff.p, c.pidx.p, x, out);
+  ++c.launches;
+  check_launch("zT");
+}
+
 static void w_transpose_apply(Ctx& c, const double* x, double* out, const int* gate) {
   const int chunk = 4096;
   const int nch = (c.n + chunk - 1) / chunk;
@@ -549,6 +572,9 @@ static void w_apply(Ctx& c, const double* coef, double* y, const int* gate) {
   ++c.launches;
   check_launch("dense_gemv");
 }
+
+void wT(Ctx& c, const double* x, double* out, const int* gate) { w_transpose_apply(c, x, out, gate); }
+void w_apply_public(Ctx& c, const double* coef, double* y, const int* gate) { w_apply(c, coef, y, gate); }
 
 void second_q(Ctx& c, const double* x, double* y, const int* gate) {
   if (c.nm == 0) {

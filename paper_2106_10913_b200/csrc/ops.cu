@@ -113,15 +113,16 @@ __global__ void k_pcg_p(const PcgState* st, int n, const double* __restrict__ z,
     p[i] = initial ? z[i] : fma(beta, p[i], z[i]);
 }
 
-// q = A p and <p, q> (krylov.cpp:77-83)
+// q = A p (or A+ p = A- p + A p when `add` holds A- p) and <p, q> (krylov.cpp:77-83)
 __global__ void k_pcg_spmv_dot(PcgState* st, int n, const int* __restrict__ rp, const int* __restrict__ ci,
                                const double* __restrict__ va, const double* __restrict__ p, double* __restrict__ q,
-                               double* part, unsigned* count) {
+                               const double* __restrict__ add, double* part, unsigned* count) {
   if (st->done) return;
   double acc = 0.0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     double s = 0.0;
-    for (int k = rp[i]; k < rp[i + 1]; ++k) s = fma(va[k], __ldg(p + ci[k]), s);
+    for (int k = rp[i]; k < rp[i + 1]; ++k) s = __dadd_rn(s, __dmul_rn(va[k], __ldg(p + ci[k])));
+    if (add) s = add[i] + s;
     q[i] = s;
     acc = fma(p[i], s, acc);
   }
@@ -167,13 +168,14 @@ __global__ void k_pcg_update(PcgState* st, int n, double* __restrict__ x, double
 // Recomputed residual ||b - A x|| / ||b|| and the acceptance rule (krylov.cpp:93-103).
 __global__ void k_pcg_true(PcgState* st, int n, const int* __restrict__ rp, const int* __restrict__ ci,
                            const double* __restrict__ va, const double* __restrict__ x, const double* __restrict__ b,
-                           double* part, unsigned* count) {
+                           const double* __restrict__ add, double* part, unsigned* count) {
   const int force = st->force_true;
   if (!force && (st->done || !st->need_true)) return;
   double acc = 0.0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     double s = 0.0;
-    for (int k = rp[i]; k < rp[i + 1]; ++k) s = fma(va[k], __ldg(x + ci[k]), s);
+    for (int k = rp[i]; k < rp[i + 1]; ++k) s = __dadd_rn(s, __dmul_rn(va[k], __ldg(x + ci[k])));
+    if (add) s = add[i] + s;
     const double d = b[i] - s;
     acc = fma(d, d, acc);
   }
@@ -196,6 +198,11 @@ __global__ void k_pcg_true(PcgState* st, int n, const int* __restrict__ rp, cons
 }
 
 __global__ void k_set_force(PcgState* st, int v) { st->force_true = v; }
+
+// skip flag for work that only the true-residual check needs
+__global__ void k_true_gate(const PcgState* st, int* flag) {
+  flag[0] = (st->force_true || (!st->done && st->need_true)) ? 0 : 1;
+}
 
 int red_grid(const Ctx& c) {
   int g = (c.n + kThreads - 1) / kThreads;
@@ -237,6 +244,7 @@ double tridiag_eig(const std::vector<double>& d, const std::vector<double>& e, i
 
 // ---------------------------------------------------------------------------
 void Ctx::alloc_work() {
+  invalidate_graphs();
   const size_t nn = size_t(n);
   for (DArr<double>* b : {&t0, &t1, &t2, &t3, &t4, &t5, &t6, &t7, &t8}) b->alloc(nn);
   xs.alloc(P);
@@ -356,7 +364,7 @@ void op_apply(Ctx& c, int op, const double* x, double* y, const int* gate) {
 }
 
 // ---------------------------------------------------------------------------
-void run_pcg(Ctx& c, const double* b_dev, double rtol, int maxit, awg_solve_report* rep) {
+void run_pcg(Ctx& c, const double* b_dev, double rtol, int maxit, awg_solve_report* rep, int op_a, int op_h) {
   if (!(rtol > 0.0 && rtol < 1.0)) c.fail(AWG_E_ARG, "pcg: rtol must be in (0,1)");
   if (maxit < 1) c.fail(AWG_E_ARG, "pcg: maxit must be positive");
   const int n = c.n;
@@ -365,7 +373,9 @@ void run_pcg(Ctx& c, const double* b_dev, double rtol, int maxit, awg_solve_repo
     c.hist_diag.alloc(maxit);
     c.hist_off.alloc(maxit);
     c.hist_cap = maxit;
+    c.invalidate_graphs();
   }
+  if (!c.pcg_flag.p) c.pcg_flag.alloc(1);
   PcgState h{};
   h.rtol = rtol;
   h.maxit = maxit;
@@ -375,6 +385,9 @@ void run_pcg(Ctx& c, const double* b_dev, double rtol, int maxit, awg_solve_repo
   PcgState* st = c.pcg.p;
   const int* gate = &st->done;
   const int g = red_grid(c);
+  const bool aplus = (op_a == AWG_OP_APLUS);
+  double* am = c.t8.p;  // A- p / A- x scratch (H2 uses t0..t5; H3 also t6..t8, never with A+)
+  if (aplus && op_h == AWG_OP_H3) c.fail(AWG_E_ARG, "pcg: A+ operator pairs with H2 only");
   cudaEvent_t e0, e1;
   AWG_CUDA(cudaEventCreate(&e0));
   AWG_CUDA(cudaEventCreate(&e1));
@@ -382,21 +395,28 @@ void run_pcg(Ctx& c, const double* b_dev, double rtol, int maxit, awg_solve_repo
 
   k_pcg_init<<<g, kThreads, 0, c.stream>>>(st, n, c.pb.p, c.px.p, c.pr.p, c.red.p, c.red_count.p);
   ++c.launches;
-  op_apply(c, AWG_OP_H3, c.pr.p, c.pz.p, gate);
+  op_apply(c, op_h, c.pr.p, c.pz.p, gate);
   k_pcg_rz<<<g, kThreads, 0, c.stream>>>(st, n, c.pr.p, c.pz.p, c.red.p, c.red_count.p, 1);
   k_pcg_p<<<g, kThreads, 0, c.stream>>>(st, n, c.pz.p, c.pp.p, 1);
   c.launches += 2;
   check_launch("pcg init");
 
   auto iteration = [&]() {
-    k_pcg_spmv_dot<<<g, kThreads, 0, c.stream>>>(st, n, c.rp.p, c.ci.p, c.va.p, c.pp.p, c.pq.p, c.red.p,
-                                                  c.red_count.p);
+    if (aplus) k::aminus(c, c.pp.p, am, gate);
+    k_pcg_spmv_dot<<<g, kThreads, 0, c.stream>>>(st, n, c.rp.p, c.ci.p, c.va.p, c.pp.p, c.pq.p,
+                                                  aplus ? am : nullptr, c.red.p, c.red_count.p);
     k_pcg_update<<<g, kThreads, 0, c.stream>>>(st, n, c.px.p, c.pr.p, c.pp.p, c.pq.p, c.red.p, c.red_count.p,
                                                c.hist_res.p, c.hist_diag.p, c.hist_off.p);
-    k_pcg_true<<<g, kThreads, 0, c.stream>>>(st, n, c.rp.p, c.ci.p, c.va.p, c.px.p, c.pb.p, c.red.p,
-                                             c.red_count.p);
-    c.launches += 3;
-    op_apply(c, AWG_OP_H3, c.pr.p, c.pz.p, gate);
+    c.launches += 2;
+    if (aplus) {
+      k_true_gate<<<1, 1, 0, c.stream>>>(st, c.pcg_flag.p);
+      ++c.launches;
+      k::aminus(c, c.px.p, am, c.pcg_flag.p);
+    }
+    k_pcg_true<<<g, kThreads, 0, c.stream>>>(st, n, c.rp.p, c.ci.p, c.va.p, c.px.p, c.pb.p, aplus ? am : nullptr,
+                                             c.red.p, c.red_count.p);
+    ++c.launches;
+    op_apply(c, op_h, c.pr.p, c.pz.p, gate);
     k_pcg_rz<<<g, kThreads, 0, c.stream>>>(st, n, c.pr.p, c.pz.p, c.red.p, c.red_count.p, 0);
     k_pcg_p<<<g, kThreads, 0, c.stream>>>(st, n, c.pz.p, c.pp.p, 0);
     c.launches += 2;
@@ -405,36 +425,47 @@ void run_pcg(Ctx& c, const double* b_dev, double rtol, int maxit, awg_solve_repo
 
   // Enqueue iterations in batches; the device-side `done` flag turns every
   // kernel after the stopping point into a no-op, so overshooting is free of
-  // side effects.  One CUDA graph holds one iteration.
-  cudaGraph_t graph = nullptr;
+  // side effects.  One CUDA graph holds one iteration; it is cached per
+  // operator pair until buffers or factors change.
+  const int key = op_a * 16 + op_h;
   cudaGraphExec_t exec = nullptr;
-  bool use_graph = true;
-  if (use_graph) {
+  auto it_cached = c.graphs.find(key);
+  if (it_cached != c.graphs.end()) {
+    exec = it_cached->second;
+  } else {
+    cudaGraph_t graph = nullptr;
+    const long long before = c.launches;
     AWG_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
     iteration();
     AWG_CUDA(cudaStreamEndCapture(c.stream, &graph));
     AWG_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    cudaGraphDestroy(graph);
+    c.graphs[key] = exec;
+    c.graph_launches[key] = c.launches - before;
+    c.launches = before;
   }
+  const long long per_iter = c.graph_launches[key];
   int batch = 2;
   int issued = 0;
   while (true) {
     for (int b = 0; b < batch && issued < maxit; ++b, ++issued) {
-      if (use_graph) AWG_CUDA(cudaGraphLaunch(exec, c.stream));
-      else iteration();
+      AWG_CUDA(cudaGraphLaunch(exec, c.stream));
+      c.launches += per_iter;
     }
     AWG_CUDA(cudaMemcpyAsync(&h, st, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
     AWG_CUDA(cudaStreamSynchronize(c.stream));
     if (h.done || issued >= maxit) break;
     batch = std::min(batch * 2, 16);
   }
-  if (exec) cudaGraphExecDestroy(exec);
-  if (graph) cudaGraphDestroy(graph);
 
   if (!h.converged && h.it > 0 && !h.error) {
     k_set_force<<<1, 1, 0, c.stream>>>(st, 1);
-    k_pcg_true<<<g, kThreads, 0, c.stream>>>(st, n, c.rp.p, c.ci.p, c.va.p, c.px.p, c.pb.p, c.red.p, c.red_count.p);
+    c.launches += 1;
+    if (aplus) k::aminus(c, c.px.p, am, nullptr);
+    k_pcg_true<<<g, kThreads, 0, c.stream>>>(st, n, c.rp.p, c.ci.p, c.va.p, c.px.p, c.pb.p, aplus ? am : nullptr,
+                                             c.red.p, c.red_count.p);
     k_set_force<<<1, 1, 0, c.stream>>>(st, 0);
-    c.launches += 3;
+    c.launches += 2;
     AWG_CUDA(cudaMemcpyAsync(&h, st, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
   }
   AWG_CUDA(cudaEventRecord(e1, c.stream));

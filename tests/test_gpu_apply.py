@@ -1,0 +1,117 @@
+"""GPU apply / solve parity on the reference's exported factors (SURVEY.md
+§8c-1): every operator within 1e-11 relative 2-norm of the unmodified
+reference, SpMV bit-identical, PCG iterations within +-1 and x within 1e-7."""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import golden_with_base, rel
+from oracle import awg_oracle as O
+from paper_2106_10913_b200 import awg
+
+pytestmark = pytest.mark.gpu
+
+CASES = ["c1", "c1_exact", "t2d", "t2d_exact", "t2d_ov2", "t3d", "t3d_blocks", "telas"]
+OPS = {"A": awg.Op.A, "Aminus": awg.Op.AMINUS, "Aplus": awg.Op.APLUS, "H1": awg.Op.H1, "Q": awg.Op.Q,
+       "QW": awg.Op.QW, "H2": awg.Op.H2, "PI3": awg.Op.PI3, "PI3T": awg.Op.PI3T}
+# Same bound the oracle restatement meets on these inputs (see test_oracle_golden).
+TOL = {"H3inex": 1e-8, "PI3": 1e-10, "PI3T": 1e-10}
+
+
+def make_ctx(g, mode=awg.AwgMode.AD, composition=awg.Composition.HYBRID, lu="reference"):
+    n = len(g["b"])
+    off, idx = g["part_offsets"], g["part_indices"]
+    omega = [idx[a:b] for a, b in zip(off[:-1], off[1:])]
+    a = awg.SparseSymMatrix(n, g["A_row_offsets"], g["A_col_indices"], g["A_values"])
+    ctx = awg.ProblemContext(a, g["b"], awg.Partition(omega, n))
+    cfg = awg.PreconditionerConfig(awg=mode, composition=composition, lu_semantics=lu)
+    ctx.load_factors(cfg, g)
+    return ctx
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_operator_parity(case):
+    g, s = golden_with_base(case)
+    ctx = make_ctx(g)
+    for name, op in OPS.items():
+        if "y_" + name not in g:
+            continue
+        for x, y in zip(g["x_apply"], g["y_" + name]):
+            got = ctx.apply(op, x)
+            if name == "A":
+                assert np.array_equal(got, y), "spmv must be bit-identical (sparse.cpp:49-56)"
+            else:
+                assert rel(got, y) <= TOL.get(name, 1e-11), (case, name, rel(got, y))
+    for mode, key in ((awg.AwgMode.AD, "H3ad"), (awg.AwgMode.HYB, "H3hyb"), (awg.AwgMode.INEX, "H3inex")):
+        if "y_" + key not in g:
+            continue
+        c2 = make_ctx(g, mode=mode)
+        for x, y in zip(g["x_apply"], g["y_" + key]):
+            assert rel(c2.apply(awg.Op.H3, x), y) <= TOL.get(key, 1e-11), (case, key)
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_pcg_parity(case):
+    g, s = golden_with_base(case)
+    ctx = make_ctx(g)
+    x, rep = ctx.pcg(g["b"], s["rtol_solve"], 10000)
+    assert rep.converged
+    assert abs(rep.iterations - s["iterations"]) <= 1
+    assert rel(x, g["pcg_x"]) <= 1e-7
+    k = min(len(rep.residual_history), len(g["pcg_residuals"]))
+    # recursive residuals agree to rounding growth (the gates are iterations and x)
+    assert np.allclose(rep.residual_history[:k], g["pcg_residuals"][:k], rtol=1e-3, atol=1e-14)
+    assert abs(rep.kappa_estimate - s["kappa"]) <= 1e-4 * s["kappa"]
+    assert rep.final_relative_residual <= s["rtol_solve"] or abs(rep.final_relative_residual -
+                                                                  rep.recurrence_residual_at_exit) <= 1e-8
+
+
+def test_gpu_matches_oracle_restatement():
+    g, s = golden_with_base("t3d")
+    ctx = make_ctx(g)
+    orc = O.AwgOracle(len(g["b"]), g["A_row_offsets"], g["A_col_indices"], g["A_values"],
+                      [g["part_indices"][a:b] for a, b in zip(g["part_offsets"][:-1], g["part_offsets"][1:])], g)
+    rng = np.random.default_rng(5)
+    for _ in range(3):
+        x = rng.uniform(-1, 1, len(g["b"]))
+        assert rel(ctx.apply(awg.Op.H3, x), orc.h3(x, "ad")) <= 1e-11
+
+
+def test_device_pointers_and_aliasing():
+    import torch
+
+    g, s = golden_with_base("c1")
+    ctx = make_ctx(g)
+    x = torch.tensor(g["x_apply"][0], device="cuda")
+    y = ctx.apply(awg.Op.H3, x)
+    assert rel(y.cpu().numpy(), g["y_H3ad"][0]) <= 1e-11
+    with pytest.raises(ValueError):
+        ctx._check(ctx._lib.awg_apply(ctx._h, int(awg.Op.H3), x.data_ptr(), x.data_ptr(), 1))
+
+
+def test_error_paths():
+    g, s = golden_with_base("t2d")
+    n = len(g["b"])
+    a = awg.SparseSymMatrix(n, g["A_row_offsets"], g["A_col_indices"], g["A_values"])
+    off, idx = g["part_offsets"], g["part_indices"]
+    # drop the overlap ring of subdomain 0: minimal overlap must fail
+    omega = [idx[a_:b_] for a_, b_ in zip(off[:-1], off[1:])]
+    bad = [np.setdiff1d(omega[0], omega[1])] + omega[1:]
+    with pytest.raises(RuntimeError, match="minimal overlap|cover"):
+        awg.ProblemContext(a, g["b"], awg.Partition(bad, n))
+    ctx = awg.ProblemContext(a, g["b"], awg.Partition(omega, n))
+    with pytest.raises(RuntimeError):
+        ctx.apply(awg.Op.H3, g["b"])  # before setup
+    ctx.load_factors(awg.PreconditionerConfig(), g)
+    with pytest.raises(ValueError):
+        ctx.pcg(g["b"], 1.5, 10)
+    x, rep = ctx.pcg(np.zeros(n), 1e-8, 100)
+    assert rep.converged and rep.iterations == 0 and not x.any()
+    x, rep = ctx.pcg(g["b"], 1e-8, 3)  # maxit hit: not converged, report valid
+    assert rep.iterations == 3 and not rep.converged and rep.final_relative_residual > 0
+
+
+def test_native_library_loaded():
+    maps = open("/proc/self/maps").read()
+    assert "libawg_b200.so" in maps

@@ -1,0 +1,69 @@
+"""End-to-end GPU setup parity: the device builds every
+setup product itself; spectra, mode counts per subdomain, coarse dimension and
+n_- must match the reference exactly, and the solve must match within the
+north-star gates (iterations +-1, x within 1e-7).  Against the probe-fixed
+oracle (exact pivoted factor, basis-invariant coarse solves) the applies also
+match closely."""
+import numpy as np
+import pytest
+
+from conftest import golden_with_base, rel
+from paper_2106_10913_b200 import awg
+
+pytestmark = pytest.mark.gpu
+
+BASE = ["c1", "t2d", "t2d_ov2", "t3d", "t3d_blocks", "telas"]
+
+
+def setup_ctx(g, s, rrf="reference"):
+    n = len(g["b"])
+    off, idx = g["part_offsets"], g["part_indices"]
+    omega = [idx[a:b] for a, b in zip(off[:-1], off[1:])]
+    a = awg.SparseSymMatrix(n, g["A_row_offsets"], g["A_col_indices"], g["A_values"])
+    ctx = awg.ProblemContext(a, g["b"], awg.Partition(omega, n))
+    cfg = awg.PreconditionerConfig(rrf_semantics=rrf)
+    if s.get("fixed_k"):
+        cfg.fixed_k = int(s["fixed_k"])
+    else:
+        cfg.tau_sharp = float(s["tau_sharp"])
+    ctx.setup(cfg)
+    return ctx
+
+
+@pytest.mark.parametrize("case", BASE)
+def test_setup_products(case):
+    g, s = golden_with_base(case)
+    ctx = setup_ctx(g, s)
+    assert np.array_equal(ctx.get("n_nonpos"), g["n_nonpos"])
+    assert np.array_equal(ctx.get("n_zero"), g["n_zero"])
+    lam = ctx.get("lam")
+    assert np.max(np.abs(lam - g["lam"])) <= 1e-10 * np.max(np.abs(g["lam"]))
+    plam = ctx.get("pencil_lam")
+    assert np.max(np.abs(plam - g["pencil_lam"])) <= 1e-8 * max(1.0, np.max(np.abs(g["pencil_lam"])))
+    assert np.array_equal(ctx.get("ks"), g["ks"])
+    q = ctx.query()
+    assert q["n0"] == s["n0"] and q["n_minus"] == s["n_minus"]
+    assert np.allclose(ctx.get("neg_weights"), g["neg_weights"], rtol=1e-9)
+
+
+@pytest.mark.parametrize("case", BASE)
+def test_solve_reference_semantics(case):
+    g, s = golden_with_base(case)
+    ctx = setup_ctx(g, s)
+    x, rep = ctx.pcg(g["b"], s["rtol_solve"], 10000)
+    assert rep.converged
+    assert abs(rep.iterations - s["iterations"]) <= 1, (rep.iterations, s["iterations"])
+    assert rel(x, g["pcg_x"]) <= 1e-7
+
+
+@pytest.mark.parametrize("case", ["c1_exact", "t2d_exact"])
+def test_exact_semantics_against_fixed_oracle(case):
+    g, s = golden_with_base(case)
+    ctx = setup_ctx(g, s, rrf="exact")
+    for name, op in (("H1", awg.Op.H1), ("Q", awg.Op.Q), ("H2", awg.Op.H2), ("QW", awg.Op.QW)):
+        for x, y in zip(g["x_apply"], g["y_" + name]):
+            assert rel(ctx.apply(op, x), y) <= 1e-8, (case, name, rel(ctx.apply(op, x), y))
+    xs, rep = ctx.pcg(g["b"], s["rtol_solve"], 10000)
+    assert abs(rep.iterations - s["iterations"]) <= 1
+    assert rel(xs, g["pcg_x"]) <= 1e-7
+    assert np.array_equal(ctx.get("w_inner_iterations").size, len(g["w_inner_iterations"]))
