@@ -1,0 +1,351 @@
+#!/usr/bin/env python
+"""Benchmark of the AWG-PCG hot path on B200 (BASELINE.json metric).
+
+A "step" is one full PCG solve (x0 = 0, rtol 1e-8) of the configuration's
+system with the reference-default preconditioner H3,ad over NN-hybrid
+(preconditioner.hpp:21-31), on data resident in HBM.  `value` is the number of
+H3 preconditioner applies per second over the K timed solves (device time,
+CUDA events on the library stream, max over ranks); `e2e` is the same metric
+through the public C-ABI call with HOST buffers (H2D of b and D2H of x inside
+the timed region).  The setup runs on the GPU once, before timing, and its
+time is reported separately.
+
+Multi-GPU (torchrun, N ranks): every rank solves its own independent
+right-hand sides of the same system (independent units, no collective:
+weak scaling, SURVEY.md §8e is the later sharded design).
+
+  python bench.py [--config c5] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+REF_DRIVER = os.path.join(ROOT, "oracle", "_ref", "ref_driver")
+METRIC = "AWG-PCG preconditioner applies/s (H3,ad over NN-hybrid, fp64, full PCG solves to rtol 1e-8)"
+DEFAULT_CONFIG = "c2"
+
+# Sizes the reference arm needs for its bounded-sample extrapolation when it
+# cannot run the setup itself (n0, n_minus, mean n_nonpos): measured by this
+# repo's GPU setup on the same generated problems.
+SAMPLE_SIZES = {"c1": (20, 4, 1), "c2": (160, 270, 20), "c3": (880, 2200, 30), "c4": (320, 600, 20),
+                "c5": (2200, 3000, 14)}
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS_PATH) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, device):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._proc = None
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self._proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                           "-lms", "200", "-i", str(self.device)], stdout=subprocess.PIPE,
+                                          stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self._proc = None
+        return self
+
+    def _read(self):
+        for line in self._proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 8:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self._proc:
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=2)
+            except Exception:
+                self._proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def iteration_bytes(q, n, nnz):
+    """Algorithmic bytes of one PCG iteration (SURVEY.md §8d formula, this
+    implementation's factor form: V^s is read twice over the columns k >= m_s,
+    Z block-sparse, W dense)."""
+    b_spmv = 12 * nnz + 4 * (n + 1) + 16 * n
+    b_h1 = 8 * 2 * (q["sum_ns2"] - q["sum_ns_ms"]) + 8 * 3 * q["sum_ns"] + 8 * n
+    b_q = 16 * q["sum_ns_ks"] + 8 * q["r0"] ** 2 + 16 * n
+    b_am = 8 * q["sum_ns_qs"] + 16 * q["sum_ns"]
+    b_w = 16 * n * q["n_minus"] + 8 * q["rw"] ** 2 + 16 * n
+    b_vec = 8 * 16 * n
+    return 3 * b_spmv + b_h1 + 2 * b_q + 2 * b_am + b_w + b_vec
+
+
+def run_reference_sample(p, config, budget_s=15.0, sizes=None):
+    """Bounded sample of the reference CPU implementation (oracle/_ref), 1 core."""
+    if not os.path.exists(REF_DRIVER):
+        return None
+    n0, nm, m_avg = sizes or SAMPLE_SIZES.get(config, (0, 0, 0))
+    with tempfile.TemporaryDirectory() as td:
+        prefix = os.path.join(td, config)
+        p.write(prefix)
+        out = os.path.join(td, "out")
+        t0 = time.time()
+        subprocess.run([REF_DRIVER, "--sample", prefix, out, str(budget_s), str(n0), str(nm), str(m_avg)],
+                       check=True, stdout=subprocess.DEVNULL)
+        with open(os.path.join(out, "sample.json")) as fh:
+            s = json.load(fh)
+        s["wall_s"] = time.time() - t0
+    return s
+
+
+def run_reference_full(p, config):
+    """The reference end to end (setup + solve) where it is feasible (c1)."""
+    if not os.path.exists(REF_DRIVER):
+        return None
+    with tempfile.TemporaryDirectory() as td:
+        prefix = os.path.join(td, config)
+        p.write(prefix)
+        out = os.path.join(td, "out")
+        args = [REF_DRIVER, prefix, out, "--n-apply", "0", "--export-factors", "0", "--apply-reps", "50"]
+        args += ["--fixed-k", str(p.fixed_k)] if p.fixed_k else ["--tau", repr(p.tau_sharp)]
+        subprocess.run(args, check=True, stdout=subprocess.DEVNULL)
+        with open(os.path.join(out, "summary.json")) as fh:
+            return json.load(fh)
+
+
+def cpu_baseline(p, config, sizes=None):
+    if config == "c1":
+        s = run_reference_full(p, config)
+        if s is None:
+            return None
+        return {"value": 1.0 / s["t_h3_apply"], "unit": "applies/s", "cores": 1, "kind": "reference",
+                "sample": f"reference (oracle/_ref) full c1 run: setup {s['t_splitting'] + s['t_coarse'] + s['t_w']:.2f} s, "
+                          f"solve {s['t_solve'] * 1e3:.2f} ms / {s['iterations']} it, H3 apply loop of 50"}
+    s = run_reference_sample(p, config, sizes=sizes)
+    if s is None:
+        return None
+    return {"value": 1.0 / s["t_h3_apply_s"], "unit": "applies/s", "cores": 1, "kind": "reference",
+            "sample": (f"reference kernels (oracle/_ref, 1 thread) timed on {config} shapes: spmv full, "
+                       f"one-level on {s['sampled_subdomains']}/{s['n_sub']} subdomains, dense Z/W pairs on 8 "
+                       f"columns, scaled to n0={s['n0']}, n_minus={s['n_minus']}; extrapolated H3 apply "
+                       f"{s['t_h3_apply_s']:.2f} s (setup infeasible on CPU, SURVEY.md §0.9)")}
+
+
+def aggregate(dev_ms, applies, e2e_s, e2e_applies, dist=None, device=None):
+    """Whole-job numbers across ranks: time = max over ranks, work = sum over
+    ranks (independent right-hand sides per rank, no data-path collective).
+    Returns (dev_ms_max, applies_total, e2e_s_max, e2e_applies_total)."""
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return dev_ms, float(applies), e2e_s, float(e2e_applies)
+    import torch
+
+    t = torch.tensor([dev_ms, e2e_s], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    w = torch.tensor([float(applies), float(e2e_applies)], dtype=torch.float64, device=device)
+    dist.all_reduce(w)
+    return float(t[0]), float(w[0]), float(t[1]), float(w[1])
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default=os.environ.get("AWG_BENCH_CONFIG", DEFAULT_CONFIG))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    ws, rank, local = dist_env()
+
+    from paper_2106_10913_b200 import problems
+
+    p = problems.make(args.config)
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        vals = []
+        t0 = time.time()
+        for _ in range(args.steps):
+            cb = cpu_baseline(p, args.config)
+            if cb is None:
+                print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (needs /root/reference)"}))
+                return
+            vals.append(cb["value"])
+        v = statistics.median(vals)
+        cb["value"] = v
+        print(json.dumps({"impl": "reference", "metric": METRIC, "value": v, "unit": "applies/s",
+                          "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                          "ms_per_step": 1e3 / v if v else None, "higher_is_better": True, "scaling": "weak",
+                          "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator)",
+                          "config": {"workload": args.config, "problem": p.meta, "n": p.n, "n_sub": p.n_sub},
+                          "cpu_baseline": cb, "e2e": {"value": v, "unit": "applies/s", "h2d_bytes_per_step": 0,
+                                                       "d2h_bytes_per_step": 0},
+                          "wall_s": time.time() - t0}))
+        return
+
+    import torch
+
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    from paper_2106_10913_b200 import awg
+
+    ctx = awg.context_from_problem(p, device=local)
+    cfg = awg.config_for(p)
+    torch.cuda.synchronize()
+    t0 = time.time()
+    ctx.setup(cfg)
+    setup_s = time.time() - t0
+    q = ctx.query()
+    rtol = p.rtol
+
+    # RHS set: rank r solves b_r (independent units); resident in HBM
+    rng = np.random.default_rng(1000 + rank)
+    b_host = p.b if rank == 0 else rng.uniform(-1.0, 1.0, p.n)
+    b_dev = torch.tensor(b_host, dtype=torch.float64, device="cuda")
+    x_dev = torch.empty_like(b_dev)
+
+    def solve_device():
+        rep = awg._Report()
+        ctx._check(ctx._lib.awg_pcg(ctx._h, ctypes_ptr(b_dev), ctypes_ptr(x_dev), rtol, 10000, 1, ctypes_byref(rep)))
+        return rep
+
+    for _ in range(args.warmup):
+        solve_device()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = ctx.launch_count()
+    dev_ms, applies, its = 0.0, 0, []
+    with Clocks(local) as clk:
+        for _ in range(args.steps):
+            rep = solve_device()
+            dev_ms += rep.solve_ms
+            applies += rep.iterations  # z = H r at start + after every iteration but the last
+            its.append(rep.iterations)
+    torch.cuda.synchronize()
+    launches = ctx.launch_count() - launches0
+    if ws > 1:
+        dist.barrier()
+
+    # e2e through the public API with host buffers (pinned b, result read back)
+    b_pin = torch.tensor(b_host, dtype=torch.float64).pin_memory()
+    x_pin = torch.empty_like(b_pin).pin_memory()
+    e2e_applies, e2e_s = 0, 0.0
+    for _ in range(args.steps):
+        rep = awg._Report()
+        t1 = time.perf_counter()
+        ctx._check(ctx._lib.awg_pcg(ctx._h, ctypes_ptr(b_pin), ctypes_ptr(x_pin), rtol, 10000, 0, ctypes_byref(rep)))
+        e2e_s += time.perf_counter() - t1
+        e2e_applies += rep.iterations
+    dev_ms_max, applies_all, e2e_s, e2e_total = aggregate(
+        dev_ms, applies, e2e_s, e2e_applies, dist=(dist if ws > 1 else None), device="cuda")
+    value = applies_all / (dev_ms_max / 1e3)
+    e2e_value = e2e_total / e2e_s
+
+    # roofline of the dominant kernel pair (batched NN local solve), live
+    peak, peak_kind = hbm_peak()
+    kt = {k: ctx.time_kernel(k, reps=5) for k in ("nn_gemvT", "nn_gemv", "spmv")}
+    if q["n_minus"] > 0:
+        kt.update({k: ctx.time_kernel(k, reps=5) for k in ("w_gemvT", "w_gemv")})
+    dom = max(kt, key=lambda k: kt[k][0])
+    ms_k, bytes_k = kt[dom]
+    achieved = bytes_k / (ms_k / 1e3) / 1e9
+    it_mean = float(np.mean(its))
+    t_iter_ms = (dev_ms / args.steps) / max(it_mean, 1)
+    b_iter = iteration_bytes(q, p.n, p.nnz)
+
+    if rank != 0:
+        return
+    cb = None
+    if not args.no_cpu_baseline and ws == 1:
+        try:
+            cb = cpu_baseline(p, args.config, sizes=(q["n0"], q["n_minus"],
+                                                     max(1, int(round(q["sum_ns_ms"] / max(q["sum_ns"], 1))))))
+        except Exception as e:  # noqa: BLE001
+            cb = {"value": None, "unit": "applies/s", "cores": 1, "kind": "reference", "sample": f"failed: {e}"}
+    out = {
+        "metric": METRIC, "value": value, "unit": "applies/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dev_ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator, problems.py)",
+        "config": {"workload": args.config, "problem": p.meta, "n": p.n, "nnz": p.nnz, "n_sub": p.n_sub,
+                   "selection": ({"fixed_k": p.fixed_k} if p.fixed_k else {"tau_sharp": p.tau_sharp}),
+                   "rtol": rtol, "preconditioner": "H3,ad + NN-hybrid (reference default)",
+                   "l2": "inputs larger than L2" if q["sum_ns2"] * 8 > 126e6 else "inputs fit in L2 (no flush)"},
+        "solve": {"iterations": its, "solve_ms_mean": dev_ms / args.steps, "t_iter_ms": t_iter_ms,
+                  "n0": q["n0"], "r0": q["r0"], "n_minus": q["n_minus"], "rw": q["rw"]},
+        "setup_s": setup_s, "setup_phase_ms": q["t_setup_ms"][:6],
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                     "bytes_per_launch": bytes_k, "ms_per_launch": ms_k,
+                     "kernels": {k: {"ms": v[0], "GBps": v[1] / (v[0] / 1e3) / 1e9} for k, v in kt.items()},
+                     "iteration": {"bytes": b_iter, "ms": t_iter_ms,
+                                   "GBps": b_iter / (t_iter_ms / 1e3) / 1e9,
+                                   "frac": b_iter / (t_iter_ms / 1e3) / 1e9 / peak}},
+        "e2e": {"value": e2e_value, "unit": "applies/s", "h2d_bytes_per_step": 8 * p.n,
+                "d2h_bytes_per_step": 8 * p.n},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "cpu_baseline": cb,
+    }
+    print(json.dumps(out))
+
+
+def ctypes_ptr(t):
+    import ctypes
+
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def ctypes_byref(o):
+    import ctypes
+
+    return ctypes.byref(o)
+
+
+if __name__ == "__main__":
+    main()

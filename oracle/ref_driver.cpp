@@ -208,9 +208,125 @@ CoarseSpace fixed_k_coarse(GeneoContext& ctx, int k, std::vector<int>& ks) {
   return cs;
 }
 
+// --- bounded-sample CPU baseline -------------------------------------------
+// For configurations whose reference setup is infeasible on a CPU (SURVEY.md
+// §0.9: c2..c5 take hours to hundreds of hours), time the reference's own
+// apply kernels on data of the configuration's exact shapes and extrapolate
+// the cost of one H3,ad apply (AwgPreconditioner::apply, preconditioner.cpp:185-198):
+//   second_correct  = W^T x + rank_revealing_solve(KW) + W c          (dense n x n_-)
+//   TwoLevel hybrid = 3 coarse_correct (dense Z, n x n0) + 2 apply_Aplus + OneLevel
+//   OneLevel        = per subdomain restrict, D, V^T, mask, V, D, prolong
+// Matrix entries are random (timing only): the operation sequence is the
+// reference's.  Subdomains / columns are sampled and scaled linearly.
+int sample_mode(const std::string& prefix, double budget_s, int n0, int n_minus, int m_avg, const std::string& out) {
+  SparseSymMatrix a = read_matrix_market(prefix + ".mtx");
+  Partition part = read_partition(prefix + ".part", a.n);
+  PartitionOfUnity pou = build_pou(part);
+  const int n = a.n, N = part.count();
+  std::vector<double> x = uniform_vec(5, n, -1.0, 1.0), y(n);
+  auto timeit = [&](auto&& fn, double min_s) {
+    fn();
+    int reps = 0;
+    double t0 = now_s(), t = 0;
+    do {
+      fn();
+      ++reps;
+      t = now_s() - t0;
+    } while (t < min_s);
+    return t / reps;
+  };
+  const double slot = budget_s / 5.0;
+  // spmv (sparse.cpp:49-56), full size
+  const double t_spmv = timeit([&] { spmv(a, x.data(), y.data()); }, std::min(slot, 1.0));
+  // OneLevel NN on a sample of subdomains (local_Aplus_pinv_apply, splitting.cpp:211-218)
+  double t_local_sum = 0.0;
+  int sampled = 0;
+  double t_start = now_s();
+  for (int s = 0; s < N && (now_s() - t_start) < slot; ++s) {
+    const int ns = part.size_of(s);
+    DenseMatrix v(ns, ns);
+    std::vector<double> r = uniform_vec(100 + s, ns * 1, -1.0, 1.0);
+    for (size_t i = 0; i < v.a.size(); ++i) v.a[i] = r[i % ns] * 0.5 + double(i % 7) * 1e-3;
+    std::vector<double> xs(ns), u(ns), w(ns), lam(ns, 1.0);
+    const auto& om = part.omega[s];
+    const auto& ds = pou.ds[s];
+    t_local_sum += timeit(
+        [&] {
+          for (int k = 0; k < ns; ++k) xs[k] = x[om[k]] * ds[k];
+          matvec_transpose(v, xs.data(), u.data());
+          for (int k = 0; k < ns; ++k) u[k] = (k < m_avg) ? 0.0 : u[k] / lam[k];
+          matvec(v, u.data(), w.data());
+          for (int k = 0; k < ns; ++k) y[om[k]] += w[k] * ds[k];
+        },
+        0.0);
+    ++sampled;
+  }
+  const double t_h1 = t_local_sum / sampled * N;
+  // dense tall-skinny pairs: W (n x n_minus) and Z (n x n0), column-sampled
+  auto pair_time = [&](int cols) {
+    const int sc = std::max(1, std::min(cols, 8));
+    DenseMatrix m(n, sc);
+    for (size_t i = 0; i < m.a.size(); ++i) m.a[i] = double(i % 13) * 1e-2;
+    std::vector<double> c(sc), out(n);
+    const double t = timeit(
+        [&] {
+          matvec_transpose(m, x.data(), c.data());
+          matvec(m, c.data(), out.data());
+        },
+        std::min(slot, 2.0));
+    return t * double(cols) / sc;
+  };
+  const double t_w = n_minus > 0 ? pair_time(n_minus) : 0.0;
+  const double t_z = n0 > 0 ? pair_time(n0) : 0.0;
+  // rank_revealing_solve on an r x r factor (dense.cpp:348-366)
+  auto rrs_time = [&](int r) {
+    if (r <= 0) return 0.0;
+    RankRevealingFactor f;
+    f.original_dim = r;
+    f.l11 = DenseMatrix(r, r);
+    for (int j = 0; j < r; ++j)
+      for (int i = j; i < r; ++i) f.l11(i, j) = (i == j) ? 1.0 : 1e-3;
+    f.retained.resize(r);
+    for (int i = 0; i < r; ++i) f.retained[i] = i;
+    std::vector<double> b(r, 1.0), xx(r);
+    return timeit([&] { rank_revealing_solve(f, b.data(), xx.data()); }, std::min(slot, 0.5));
+  };
+  const double t_k0 = rrs_time(n0), t_kw = rrs_time(n_minus);
+  // A- x: per subdomain q_s ~ m_avg dot+axpy pairs over n_s (splitting.cpp:119-140)
+  double sum_ns = 0;
+  for (int s = 0; s < N; ++s) sum_ns += part.size_of(s);
+  const double t_vec_elem = t_spmv / std::max(1, a.nnz());  // per fused element, as a lower bound
+  const double t_aminus = 4.0 * m_avg * sum_ns * t_vec_elem;
+  const double t_q = t_z + t_k0;
+  const double t_h2 = 3.0 * t_q + 2.0 * (t_aminus + t_spmv) + t_h1;
+  const double t_h3 = t_h2 + t_w + t_kw;
+  const double t_iter = t_h3 + t_spmv;
+  FILE* js = std::fopen((out + "/sample.json").c_str(), "w");
+  std::fprintf(js,
+               "{\"t_h3_apply_s\": %.9g, \"t_iter_s\": %.9g, \"t_spmv_s\": %.9g, \"t_h1_s\": %.9g, "
+               "\"t_z_pair_s\": %.9g, \"t_w_pair_s\": %.9g, \"t_k0_solve_s\": %.9g, \"t_kw_solve_s\": %.9g, "
+               "\"sampled_subdomains\": %d, \"n_sub\": %d, \"n\": %d, \"n0\": %d, \"n_minus\": %d, "
+               "\"elapsed_s\": %.3f}\n",
+               t_h3, t_iter, t_spmv, t_h1, t_z, t_w, t_k0, t_kw, sampled, N, n, n0, n_minus,
+               now_s() - t_start);
+  std::fclose(js);
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
+  if (argc >= 3 && std::string(argv[1]) == "--sample") {
+    // ref_driver --sample <prefix> <outdir> <budget_s> <n0> <n_minus> <m_avg>
+    if (argc < 8) {
+      std::fprintf(stderr, "usage: ref_driver --sample <prefix> <outdir> <budget_s> <n0> <n_minus> <m_avg>\n");
+      return 2;
+    }
+    std::string cmd = "mkdir -p '" + std::string(argv[3]) + "'";
+    if (std::system(cmd.c_str()) != 0) return 2;
+    return sample_mode(argv[2], std::stod(argv[4]), std::stoi(argv[5]), std::stoi(argv[6]), std::stoi(argv[7]),
+                       argv[3]);
+  }
   const Args args = parse(argc, argv);
   std::string cmd = "mkdir -p '" + args.out + "'";
   if (std::system(cmd.c_str()) != 0) return 2;

@@ -164,12 +164,28 @@ void finalize_factors(Ctx& c) {
   // NN task lists
   std::vector<GemvTTask> tT;
   std::vector<GemvTask> t;
+  std::vector<int> nkc(N, 0);
+  int kcmax = 1;
   for (int s = 0; s < N; ++s) {
     for (int j0 = c.h_m[s]; j0 < c.h_ns[s]; j0 += 64) tT.push_back({s, j0, std::min(j0 + 64, c.h_ns[s]), 0});
-    for (int i0 = 0; i0 < c.h_ns[s]; i0 += c.rows_per_gemv) t.push_back({s, i0});
+    // split-K over column chunks of gemv_cols (the last chunk takes the remainder)
+    const int cols = c.h_ns[s] - c.h_m[s];
+    const int kcs = std::max(1, cols / c.gemv_cols);
+    nkc[s] = kcs;
+    kcmax = std::max(kcmax, kcs);
+    for (int kc = 0; kc < kcs; ++kc) {
+      const int j0 = c.h_m[s] + int((long long)cols * kc / kcs);
+      const int j1 = c.h_m[s] + int((long long)cols * (kc + 1) / kcs);
+      for (int i0 = 0; i0 < c.h_ns[s]; i0 += c.rows_per_gemv) t.push_back({s, i0, j0, j1, kc, 0});
+    }
   }
   c.t_gemvT.upload(tT, c.stream);
   c.t_gemv.upload(t, c.stream);
+  c.nkc.upload(nkc, c.stream);
+  c.wpart_nn.alloc(size_t(kcmax) * std::max<long long>(c.P, 1));
+  c.wpart_nn.zero(c.stream);
+  c.gemv_cols_max = 0;
+  for (const auto& tk : t) c.gemv_cols_max = std::max(c.gemv_cols_max, tk.j1 - tk.j0);
   // A- modes: k < n_nonpos with lambda != 0 (splitting.cpp:129-131), ascending (s, k)
   std::vector<int> ns_, nk_, noff(N + 1, 0);
   std::vector<double> nw_;
@@ -511,13 +527,13 @@ int awg_time_kernel(awg_ctx* ctx, int which, int reps, double* ms, double* bytes
     }
     std::function<void()> launch;
     switch (which) {
-      case 0:  // V^T reads + xs read + uh written (columns >= m)
-        b = 8.0 * vcols + 8.0 * P + 8.0 * P;
-        launch = [&] { k::nn_gemvT(c, c.xs.p, nullptr); };
+      case 0:  // V^T reads + x gathered (x, idx, D) + uh written (columns >= m)
+        b = 8.0 * vcols + 20.0 * P + 8.0 * P;
+        launch = [&] { k::nn_gemvT(c, c.pb.p, nullptr); };
         break;
-      case 1:  // V reads + uh, D read + w written
-        b = 8.0 * vcols + 8.0 * P * 3;
-        launch = [&] { k::nn_gemv(c, c.wl.p, nullptr); };
+      case 1:  // V reads + uh read + partials written
+        b = 8.0 * vcols + 8.0 * P * 2;
+        launch = [&] { k::nn_gemv(c, nullptr); };
         break;
       case 2:  // values + col indices + row offsets + x + y
         b = 12.0 * c.nnz + 4.0 * (c.n + 1) + 16.0 * c.n;

@@ -91,8 +91,8 @@ inline int round_up(int v, int m) { return (v + m - 1) / m * m; }
 struct GemvTTask {  // columns [j0, j1) of V^s
   int s, j0, j1, pad;
 };
-struct GemvTask {  // rows [i0, i0 + rows) of V^s
-  int s, i0;
+struct GemvTask {  // rows [i0, i0 + rows) x columns [j0, j1) of V^s, partial slot kc
+  int s, i0, j0, j1, kc, pad;
 };
 
 // Triangular coarse factor with retained pivots (RankRevealingFactor,
@@ -129,9 +129,10 @@ namespace k {
 void spmv(Ctx& c, const double* x, double* y, int mode, const double* add, const double* sub, const int* gate);
 void gather(Ctx& c, const double* x, const double* scale, double* xs, const int* gate);
 void prolong(Ctx& c, const double* w, double* y, const int* gate);
-void nn_local(Ctx& c, const double* xs, double* w, const int* gate);  // w = D V mask(1/lam) V^T xs
-void nn_gemvT(Ctx& c, const double* xs, const int* gate);              // uh = mask(1/lam) V^T xs
-void nn_gemv(Ctx& c, double* w, const int* gate);                      // w = D V uh
+void h1(Ctx& c, const double* x, double* y, const int* gate);         // one-level NN
+void nn_gemvT(Ctx& c, const double* x, const int* gate);               // uh = mask(1/lam) V^T D R x
+void nn_gemv(Ctx& c, const int* gate);                                 // part = V uh (column chunks)
+void nn_prolong(Ctx& c, double* y, const int* gate);                   // y = sum_s R^T D sum_kc part
 void aminus(Ctx& c, const double* x, double* y, const int* gate);     // y = A- x
 void coarse_q(Ctx& c, const double* x, double* y, const int* gate);   // y = Z K0+ Z^T x
 void second_q(Ctx& c, const double* x, double* y, const int* gate);   // y = W KW+ W^T x
@@ -142,6 +143,7 @@ void tri_inverse(Ctx& c, const double* l, int r, double* linv);
 void zT(Ctx& c, const double* x, double* out, const int* gate);  // out = Z^T x (n0)
 void wT(Ctx& c, const double* x, double* out, const int* gate);  // out = W^T x (n_minus)
 void w_apply_public(Ctx& c, const double* coef, double* y, const int* gate);  // y = W coef
+void scatter_col(Ctx& c, int s, const double* col, double* z);  // z[Omega^s] = col (z pre-zeroed)
 }  // namespace k
 
 // ---- the context --------------------------------------------------------------
@@ -178,6 +180,10 @@ struct Ctx {
   DArr<GemvTTask> t_gemvT;
   DArr<GemvTask> t_gemv;
   int rows_per_gemv = 512;
+  int gemv_cols = 1024;  // column chunk of the split GEMV
+  int gemv_cols_max = 0;
+  DArr<int> nkc;         // column chunks per subdomain
+  DArr<double> wpart_nn; // nkc_max x P partial sums
 
   // A- modes
   int nneg = 0;
@@ -243,6 +249,9 @@ void run_pcg(Ctx& c, const double* b_dev, double rtol, int maxit, awg_solve_repo
 void finalize_factors(Ctx& c);  // task lists, A- modes, inverses, work buffers
 void build_core(Ctx& c);        // INEX core LU
 void run_setup(Ctx& c, const awg_config& cfg);  // setup.cu
+// wbuild.cu: batched inner PCGs for W (modes = (s, k) list, ascending)
+void build_w_batched(Ctx& c, struct cublasContext* h, const std::vector<std::pair<int, int>>& modes, int maxit,
+                     double rtol, std::vector<int>& iters, int max_block);
 
 }  // namespace awgb
 

@@ -90,22 +90,25 @@ __global__ void k_prolong(const int* __restrict__ gate, int n, const int* __rest
 }
 
 // ---------------------------------------------------------------------------
-// Batched NN local solve, first half (local_Aplus_pinv_apply, splitting.cpp:211-218):
-//   uh[p_s + j] = (V^s(:, j) . xs_s) / lambda_j   for j >= n_nonpos(s)
-// One CTA per (s, column chunk); xs_s staged once in shared memory; one warp per
-// column, 16-byte coalesced loads down the column, 4 loads in flight per lane.
+// Batched NN local solve, first half (local_Aplus_pinv_apply, splitting.cpp:211-218,
+// with OneLevel's restriction and D^s scaling, preconditioner.cpp:41-49, fused):
+//   uh[p_s + j] = (V^s(:, j) . (D^s x[Omega^s])) / lambda_j   for j >= n_nonpos(s)
+// One CTA per (s, column chunk); the scaled restriction is staged once in shared
+// memory; one warp per column, 16-byte coalesced loads down the column, 4 loads
+// in flight per lane.
 template <int NW>
 __global__ void __launch_bounds__(NW * 32) k_nn_gemvT(const int* __restrict__ gate, const GemvTTask* __restrict__ tasks,
                                                    const double* __restrict__ V, const long long* __restrict__ voff,
                                                    const int* __restrict__ ns, const int* __restrict__ ld,
-                                                   const long long* __restrict__ poff, const double* __restrict__ xs,
+                                                   const long long* __restrict__ poff, const int* __restrict__ pidx,
+                                                   const double* __restrict__ ds, const double* __restrict__ x,
                                                    const double* __restrict__ lam, double* __restrict__ uh) {
   if (gated(gate)) return;
   extern __shared__ double sx[];
   const GemvTTask t = tasks[blockIdx.x];
   const int s = t.s, n = ns[s], L = ld[s];
   const long long p0 = poff[s];
-  for (int i = threadIdx.x; i < L; i += blockDim.x) sx[i] = (i < n) ? xs[p0 + i] : 0.0;
+  for (int i = threadIdx.x; i < L; i += blockDim.x) sx[i] = (i < n) ? __ldg(x + pidx[p0 + i]) * ds[p0 + i] : 0.0;
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double* Vs = V + voff[s];
@@ -134,49 +137,71 @@ __global__ void __launch_bounds__(NW * 32) k_nn_gemvT(const int* __restrict__ ga
   }
 }
 
-// Second half: w[p_s + i] = D^s_i * sum_{j >= n_nonpos(s)} V^s(i, j) uh[p_s + j]
-// One CTA per (s, 2*blockDim row panel); each thread owns two adjacent rows
-// (16-byte loads, a warp reads 512 contiguous bytes of a column per step),
-// 8 column loads in flight per thread; uh_s staged in shared memory.
+// Second half, split over column chunks: part[kc * P + p_s + i] =
+//   sum_{j in chunk kc, j >= n_nonpos(s)} V^s(i, j) uh[p_s + j]
+// One CTA per (s, 2*blockDim row panel, column chunk); each thread owns two
+// adjacent rows (16-byte loads, a warp reads 512 contiguous bytes of a column
+// per step), 8 column loads in flight per thread; the chunk of uh_s is staged
+// in shared memory.  D^s and the chunk sum are applied by k_prolong_nn.
 __global__ void __launch_bounds__(kThreads) k_nn_gemv(const int* __restrict__ gate, const GemvTask* __restrict__ tasks,
                                                    const double* __restrict__ V, const long long* __restrict__ voff,
                                                    const int* __restrict__ ns, const int* __restrict__ ld,
-                                                   const int* __restrict__ msz, const long long* __restrict__ poff,
-                                                   const double* __restrict__ uh, const double* __restrict__ ds,
-                                                   double* __restrict__ w) {
+                                                   const long long* __restrict__ poff, long long P,
+                                                   const double* __restrict__ uh, double* __restrict__ part) {
   if (gated(gate)) return;
   extern __shared__ double su[];
   const GemvTask t = tasks[blockIdx.x];
-  const int s = t.s, n = ns[s], L = ld[s], m = msz[s];
+  const int s = t.s, n = ns[s], L = ld[s];
+  const int j0 = t.j0, j1 = t.j1;
   const long long p0 = poff[s];
-  for (int j = m + threadIdx.x; j < n; j += blockDim.x) su[j] = uh[p0 + j];
+  for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x) su[j - j0] = uh[p0 + j];
   __syncthreads();
   const int i = t.i0 + 2 * threadIdx.x;
   if (i >= n) return;
   const double* Vs = V + voff[s] + i;
   double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
-  int j = m;
-  for (; j + 8 <= n; j += 8) {
+  int j = j0;
+  for (; j + 8 <= j1; j += 8) {
     double2 v[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) v[u] = __ldcs(reinterpret_cast<const double2*>(Vs + (size_t)(j + u) * L));
 #pragma unroll
     for (int u = 0; u < 8; u += 2) {
-      const double c0 = su[j + u], c1 = su[j + u + 1];
+      const double c0 = su[j + u - j0], c1 = su[j + u + 1 - j0];
       a0 = fma(v[u].x, c0, a0);
       a1 = fma(v[u].y, c0, a1);
       b0 = fma(v[u + 1].x, c1, b0);
       b1 = fma(v[u + 1].y, c1, b1);
     }
   }
-  for (; j < n; ++j) {
+  for (; j < j1; ++j) {
     const double2 v0 = __ldcs(reinterpret_cast<const double2*>(Vs + (size_t)j * L));
-    const double c0 = su[j];
+    const double c0 = su[j - j0];
     a0 = fma(v0.x, c0, a0);
     a1 = fma(v0.y, c0, a1);
   }
-  w[p0 + i] = (a0 + b0) * ds[p0 + i];
-  if (i + 1 < n) w[p0 + i + 1] = (a1 + b1) * ds[p0 + i + 1];
+  double* out = part + (size_t)t.kc * P + p0;
+  out[i] = a0 + b0;
+  if (i + 1 < n) out[i + 1] = a1 + b1;
+}
+
+// y[i] = sum over s containing i (ascending s) of D^s_i * (sum_kc part[kc][p(s,i)])
+__global__ void k_prolong_nn(const int* __restrict__ gate, int n, const int* __restrict__ own_off,
+                             const int* __restrict__ own_pos, const int* __restrict__ psub,
+                             const int* __restrict__ nkc, long long P, const double* __restrict__ part,
+                             const double* __restrict__ ds, double* __restrict__ y) {
+  if (gated(gate)) return;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int q = own_off[i]; q < own_off[i + 1]; ++q) {
+      const int p = own_pos[q];
+      const int kcs = nkc[psub[p]];
+      double w = 0.0;
+      for (int kc = 0; kc < kcs; ++kc) w += part[(size_t)kc * P + p];
+      acc += w * ds[p];
+    }
+    y[i] = acc;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -281,6 +306,11 @@ __global__ void k_tri_upperT(const int* __restrict__ gate, int r, const double* 
   for (int i = k + lane; i < r; i += 32) acc = fma(col[i], t[i], acc);
   acc = warp_sum(acc);
   if (lane == 0) x[ret[k]] = acc;
+}
+
+__global__ void k_scatter(int n, const int* __restrict__ om, const double* __restrict__ y, double* __restrict__ z) {
+  const int l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l < n) z[om[l]] = y[l];
 }
 
 __global__ void k_zero(const int* __restrict__ gate, int n, double* __restrict__ y) {
@@ -455,32 +485,39 @@ static size_t nn_smem(Ctx& c) {
   static size_t configured = 0;
   if (smem > configured) {
     AWG_CUDA(cudaFuncSetAttribute(k_nn_gemvT<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    AWG_CUDA(cudaFuncSetAttribute(k_nn_gemv, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     configured = smem;
   }
   return smem;
 }
 
-void nn_gemvT(Ctx& c, const double* xs, const int* gate) {
+void nn_gemvT(Ctx& c, const double* x, const int* gate) {
   const size_t smem = nn_smem(c);
   if (!c.t_gemvT.n) return;
   k_nn_gemvT<8><<<int(c.t_gemvT.n), 256, smem, c.stream>>>(gate, c.t_gemvT.p, c.V.p, c.voff.p, c.ns.p, c.ld.p,
-                                                           c.poff.p, xs, c.lam.p, c.uh.p);
+                                                           c.poff.p, c.pidx.p, c.ds.p, x, c.lam.p, c.uh.p);
   ++c.launches;
   check_launch("nn_gemvT");
 }
 
-void nn_gemv(Ctx& c, double* w, const int* gate) {
-  const size_t smem = nn_smem(c);
-  k_nn_gemv<<<int(c.t_gemv.n), kThreads, smem, c.stream>>>(gate, c.t_gemv.p, c.V.p, c.voff.p, c.ns.p, c.ld.p,
-                                                           c.msz.p, c.poff.p, c.uh.p, c.ds.p, w);
+void nn_gemv(Ctx& c, const int* gate) {
+  if (!c.t_gemv.n) return;
+  k_nn_gemv<<<int(c.t_gemv.n), kThreads, size_t(c.gemv_cols_max) * sizeof(double), c.stream>>>(
+      gate, c.t_gemv.p, c.V.p, c.voff.p, c.ns.p, c.ld.p, c.poff.p, c.P, c.uh.p, c.wpart_nn.p);
   ++c.launches;
   check_launch("nn_gemv");
 }
 
-void nn_local(Ctx& c, const double* xs, double* w, const int* gate) {
-  nn_gemvT(c, xs, gate);
-  nn_gemv(c, w, gate);
+void nn_prolong(Ctx& c, double* y, const int* gate) {
+  k_prolong_nn<<<grid_for(c, c.n), kThreads, 0, c.stream>>>(gate, c.n, c.own_off.p, c.own_pos.p, c.psub.p,
+                                                           c.nkc.p, c.P, c.wpart_nn.p, c.ds.p, y);
+  ++c.launches;
+  check_launch("prolong_nn");
+}
+
+void h1(Ctx& c, const double* x, double* y, const int* gate) {
+  nn_gemvT(c, x, gate);
+  nn_gemv(c, gate);
+  nn_prolong(c, y, gate);
 }
 
 void aminus(Ctx& c, const double* x, double* y, const int* gate) {
@@ -574,6 +611,13 @@ static void w_apply(Ctx& c, const double* coef, double* y, const int* gate) {
 }
 
 void wT(Ctx& c, const double* x, double* out, const int* gate) { w_transpose_apply(c, x, out, gate); }
+
+void scatter_col(Ctx& c, int s, const double* col, double* z) {
+  const int n = c.h_ns[s];
+  k_scatter<<<(n + kThreads - 1) / kThreads, kThreads, 0, c.stream>>>(n, c.pidx.p + c.h_poff[s], col, z);
+  ++c.launches;
+  check_launch("scatter");
+}
 void w_apply_public(Ctx& c, const double* coef, double* y, const int* gate) { w_apply(c, coef, y, gate); }
 
 void second_q(Ctx& c, const double* x, double* y, const int* gate) {

@@ -262,11 +262,7 @@ void Ctx::alloc_work() {
   for (DArr<double>* b : {&px, &pr, &pz, &pp, &pq, &pb, &pt}) b->alloc(nn);
 }
 
-static void h1(Ctx& c, const double* x, double* y, const int* gate) {
-  k::gather(c, x, c.ds.p, c.xs.p, gate);
-  k::nn_local(c, c.xs.p, c.wl.p, gate);
-  k::prolong(c, c.wl.p, y, gate);
-}
+static void h1(Ctx& c, const double* x, double* y, const int* gate) { k::h1(c, x, y, gate); }
 
 static void aplus(Ctx& c, const double* x, double* y, const int* gate) {
   k::aminus(c, x, y, gate);

@@ -626,30 +626,27 @@ void run_setup(Ctx& c, const awg_config& cfg) {
   if (nm > 0) {
     c.W.alloc(size_t(c.ldw) * nm);
     c.W.zero(c.stream);
-    DArr<double> rhs;
-    rhs.alloc(c.n);
-    int col = 0;
-    for (int s = 0; s < N; ++s) {
+    std::vector<std::pair<int, int>> modes;
+    for (int s = 0; s < N; ++s)
       for (int k = 0; k < c.h_m[s]; ++k) {
         const double lam = c.h_lam[c.h_poff[s] + k];
-        if (lam == 0.0) continue;
-        AWG_CUDA(cudaMemsetAsync(rhs.p, 0, sizeof(double) * c.n, c.stream));
-        k_scatter_col<<<(c.h_ns[s] + kThreads - 1) / kThreads, kThreads, 0, c.stream>>>(
-            c.h_ns[s], c.pidx.p + c.h_poff[s], c.V.p + c.h_voff[s] + size_t(k) * c.h_ld[s], rhs.p);
-        ++c.launches;
+        if (lam == 0.0) continue;  // kernel columns of B^s are dropped (preconditioner.cpp:103)
+        modes.push_back({s, k});
         c.h_neg_weights.push_back(-lam);
-        awg_solve_report rep{};
-        const long long maxit = (long long)std::max(1, cfg.w_maxit_factor) * c.n;
-        run_pcg(c, rhs.p, cfg.w_rtol, int(std::min<long long>(maxit, 1 << 30)), &rep, AWG_OP_APLUS, AWG_OP_H2);
-        if (!rep.converged)
-          c.fail(AWG_E_NO_CONVERGENCE, "build_w: inner PCG for a W column did not converge");
-        AWG_CUDA(cudaMemcpyAsync(c.W.p + size_t(col) * c.ldw, c.px.p, sizeof(double) * c.n, cudaMemcpyDeviceToDevice,
-                                 c.stream));
-        c.h_w_inner.push_back(rep.iterations);
-        ++col;
       }
+    cublasHandle_t hb = nullptr;
+    AWG_BLAS(cublasCreate(&hb));
+    c.w_batches = 0;
+    const long long maxit = (long long)std::max(1, cfg.w_maxit_factor) * c.n;
+    try {
+      build_w_batched(c, hb, modes, int(std::min<long long>(maxit, 1 << 30)), cfg.w_rtol, c.h_w_inner, 512);
+    } catch (...) {
+      cublasDestroy(hb);
+      throw;
     }
-    c.w_batches = col;
+    cublasDestroy(hb);
+    const int col = int(modes.size());
+    (void)col;
     c.neg_weights.upload(c.h_neg_weights, c.stream);
     c.t_setup_ms[3] = now_ms() - t0;
     // W^T A W (preconditioner.cpp:119-126)

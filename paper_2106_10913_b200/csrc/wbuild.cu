@@ -1,0 +1,590 @@
+// Batched construction of the second coarse space W (build_w,
+// preconditioner.cpp:84-128).
+//
+// The reference runs one PCG per strictly negative mode, sequentially:
+//   W(:, col) = pcg(A+, H2, R^s^T v_k, w_rtol, 10 n)          (:99-116)
+// Here B columns run at once as B independent PCGs: every column keeps its own
+// alpha, beta, rho, iteration count and stopping decision (the same recursive +
+// true residual rule, krylov.cpp:93-102), so per-column semantics are the
+// reference's; only the operators are applied to the n x B block at once.  The
+// one-level NN solve of a block is two DGEMMs per subdomain (V^s^T X_s and
+// V^s U_s, FP64 tensor-core tiles via cuBLAS), so the V^s stream is amortized
+// over B right-hand sides.
+#include <cublas_v2.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "awg_internal.cuh"
+
+namespace awgb {
+namespace {
+
+#define AWG_BLAS(x)                                                                                  \
+  do {                                                                                               \
+    cublasStatus_t st_ = (x);                                                                        \
+    if (st_ != CUBLAS_STATUS_SUCCESS)                                                                \
+      throw AwgError(AWG_E_CUDA, std::string(#x) + ": cublas status " + std::to_string(int(st_)));   \
+  } while (0)
+
+constexpr int kT = 256;
+
+struct ColState {
+  double bnorm, rz, pq, alpha, beta, relres, alpha_prev, beta_prev, true_rel;
+  int it, done, converged, past_rtol, need_true, error, pad0, pad1;
+};
+
+__device__ __forceinline__ double wsum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ bool col_off(const int* done, int b) { return done != nullptr && done[b] != 0; }
+
+// Y(:,b) = A X(:,b) (+ epilogues as k_spmv): mode 0 plain, 1 add + AX, 2 sub - (add + AX), 3 sub - AX
+__global__ void kb_spmv(int n, int ld, const int* __restrict__ rp, const int* __restrict__ ci,
+                        const double* __restrict__ va, const double* __restrict__ X, double* __restrict__ Y, int mode,
+                        const double* __restrict__ add, const double* __restrict__ sub, const int* __restrict__ done) {
+  const int b = blockIdx.y;
+  if (col_off(done, b)) return;
+  const size_t o = (size_t)b * ld;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int k = rp[i]; k < rp[i + 1]; ++k) acc = __dadd_rn(acc, __dmul_rn(va[k], __ldg(X + o + ci[k])));
+    double out;
+    if (mode == 0) out = acc;
+    else if (mode == 1) out = add[o + i] + acc;
+    else if (mode == 2) out = sub[o + i] - (add[o + i] + acc);
+    else out = sub[o + i] - acc;
+    Y[o + i] = out;
+  }
+}
+
+// block-P layout: subdomain s, column b at boff[s] + b * ld_s
+__global__ void kb_gather(long long P, const int* __restrict__ psub, const long long* __restrict__ poff,
+                          const int* __restrict__ pidx, const int* __restrict__ lds,
+                          const long long* __restrict__ boff, const double* __restrict__ ds, int ldx,
+                          const double* __restrict__ X, double* __restrict__ XS, const int* __restrict__ done) {
+  const int b = blockIdx.y;
+  if (col_off(done, b)) return;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < P; p += (long long)gridDim.x * blockDim.x) {
+    const int s = psub[p];
+    const int i = int(p - poff[s]);
+    double v = X[(size_t)b * ldx + pidx[p]];
+    if (ds) v *= ds[p];
+    XS[boff[s] + (size_t)b * lds[s] + i] = v;
+  }
+}
+
+// U(j, b) = 0 for j < n_nonpos(s), U(j, b) / lambda_j otherwise
+__global__ void kb_mask(long long P, const int* __restrict__ psub, const long long* __restrict__ poff,
+                        const int* __restrict__ lds, const long long* __restrict__ boff, const int* __restrict__ msz,
+                        const double* __restrict__ lam, int B, double* __restrict__ U) {
+  const int b = blockIdx.y;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < P; p += (long long)gridDim.x * blockDim.x) {
+    const int s = psub[p];
+    const int j = int(p - poff[s]);
+    double* u = U + boff[s] + (size_t)b * lds[s] + j;
+    *u = (j < msz[s]) ? 0.0 : *u / lam[p];
+  }
+}
+
+// Y(i,b) = sum over s containing i (ascending) of (ds) * WS(s, loc, b)
+__global__ void kb_prolong(int n, int ldx, const int* __restrict__ own_off, const int* __restrict__ own_pos,
+                           const int* __restrict__ psub, const long long* __restrict__ poff,
+                           const int* __restrict__ lds, const long long* __restrict__ boff,
+                           const double* __restrict__ ds, const double* __restrict__ WS, double* __restrict__ Y,
+                           const int* __restrict__ done) {
+  const int b = blockIdx.y;
+  if (col_off(done, b)) return;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int q = own_off[i]; q < own_off[i + 1]; ++q) {
+      const int p = own_pos[q];
+      const int s = psub[p];
+      double w = WS[boff[s] + (size_t)b * lds[s] + (p - poff[s])];
+      if (ds) w *= ds[p];
+      acc += w;
+    }
+    Y[(size_t)b * ldx + i] = acc;
+  }
+}
+
+// C(j, b) = w_j * (V^s(:, k_j) . X(Omega^s, b)) — warp per (mode, column)
+__global__ void kb_neg_dot(int nneg, int B, const int* __restrict__ neg_s, const int* __restrict__ neg_k,
+                           const double* __restrict__ neg_w, const double* __restrict__ V,
+                           const long long* __restrict__ voff, const int* __restrict__ ns, const int* __restrict__ ld,
+                           const long long* __restrict__ poff, const int* __restrict__ pidx, int ldx,
+                           const double* __restrict__ X, double* __restrict__ C, const int* __restrict__ done) {
+  const int lane = threadIdx.x & 31;
+  const long long w = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (w >= (long long)nneg * B) return;
+  const int j = int(w % nneg), b = int(w / nneg);
+  if (col_off(done, b)) return;
+  const int s = neg_s[j], n = ns[s];
+  const double* v = V + voff[s] + (size_t)neg_k[j] * ld[s];
+  const int* idx = pidx + poff[s];
+  const double* x = X + (size_t)b * ldx;
+  double acc = 0.0;
+  for (int i = lane; i < n; i += 32) acc = fma(v[i], __ldg(x + idx[i]), acc);
+  acc = wsum(acc);
+  if (lane == 0) C[(size_t)b * nneg + j] = neg_w[j] * acc;
+}
+
+// WS(s, i, b) = sum_q coef(q, b) M_s(i, col(q))  for the q of subdomain s
+__global__ void kb_combine(long long P, const int* __restrict__ psub, const long long* __restrict__ poff,
+                           const int* __restrict__ coff, const int* __restrict__ ccol, const double* __restrict__ M,
+                           const long long* __restrict__ moff, const int* __restrict__ ld, int ncoef,
+                           const double* __restrict__ coef, const int* __restrict__ lds,
+                           const long long* __restrict__ boff, double* __restrict__ WS, const int* __restrict__ done) {
+  const int b = blockIdx.y;
+  if (col_off(done, b)) return;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < P; p += (long long)gridDim.x * blockDim.x) {
+    const int s = psub[p];
+    const int i = int(p - poff[s]);
+    const double* Ms = M + moff[s] + i;
+    const int L = ld[s];
+    double acc = 0.0;
+    for (int q = coff[s]; q < coff[s + 1]; ++q) {
+      const int col = ccol ? ccol[q] : (q - coff[s]);
+      acc = fma(coef[(size_t)b * ncoef + q], Ms[(size_t)col * L], acc);
+    }
+    WS[boff[s] + (size_t)b * lds[s] + i] = acc;
+  }
+}
+
+// ZX(j, b) = Y_s(:, c_j) . X(Omega^s, b)
+__global__ void kb_zT(int n0, int B, const int* __restrict__ zcol_s, const int* __restrict__ zcol_loc,
+                      const double* __restrict__ Y, const long long* __restrict__ yoff, const int* __restrict__ ns,
+                      const int* __restrict__ ld, const long long* __restrict__ poff, const int* __restrict__ pidx,
+                      int ldx, const double* __restrict__ X, double* __restrict__ ZX, const int* __restrict__ done) {
+  const int lane = threadIdx.x & 31;
+  const long long w = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (w >= (long long)n0 * B) return;
+  const int j = int(w % n0), b = int(w / n0);
+  if (col_off(done, b)) return;
+  const int s = zcol_s[j], n = ns[s];
+  const double* y = Y + yoff[s] + (size_t)zcol_loc[j] * ld[s];
+  const int* idx = pidx + poff[s];
+  const double* x = X + (size_t)b * ldx;
+  double acc = 0.0;
+  for (int i = lane; i < n; i += 32) acc = fma(y[i], __ldg(x + idx[i]), acc);
+  acc = wsum(acc);
+  if (lane == 0) ZX[(size_t)b * n0 + j] = acc;
+}
+
+__global__ void kb_take(int r, int n0, int B, const int* __restrict__ ret, const double* __restrict__ src,
+                        double* __restrict__ dst) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= (long long)r * B) return;
+  const int k = int(t % r), b = int(t / r);
+  dst[t] = src[(size_t)b * n0 + ret[k]];
+}
+
+__global__ void kb_put(int r, int n0, int B, const int* __restrict__ ret, const double* __restrict__ src,
+                       double* __restrict__ dst) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= (long long)r * B) return;
+  const int k = int(t % r), b = int(t / r);
+  dst[(size_t)b * n0 + ret[k]] = src[t];
+}
+
+// Y = (A - Bm) + D | A + Bm | A - Bm, column-gated
+__global__ void kb_axpby(int n, int ld, const double* __restrict__ a, const double* __restrict__ bm,
+                         const double* __restrict__ d, double* __restrict__ y, int mode, const int* __restrict__ done) {
+  const int b = blockIdx.y;
+  if (col_off(done, b)) return;
+  const size_t o = (size_t)b * ld;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double v;
+    if (mode == 0) v = (a[o + i] - bm[o + i]) + d[o + i];
+    else if (mode == 1) v = a[o + i] + bm[o + i];
+    else v = a[o + i] - bm[o + i];
+    y[o + i] = v;
+  }
+}
+
+// per-column partial dot products: part[b * G + g]
+__global__ void kb_dot(int n, int ld, const double* __restrict__ x, const double* __restrict__ y,
+                       double* __restrict__ part, int mode, const double* __restrict__ bm) {
+  // mode 0: <x, y>;  mode 1: ||bm - y||^2 (true residual);  x unused in mode 1
+  __shared__ double sred[32];
+  const int b = blockIdx.y;
+  const size_t o = (size_t)b * ld;
+  double acc = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    if (mode == 0) acc = fma(x[o + i], y[o + i], acc);
+    else {
+      const double d = bm[o + i] - y[o + i];
+      acc = fma(d, d, acc);
+    }
+  }
+  acc = wsum(acc);
+  if ((threadIdx.x & 31) == 0) sred[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += sred[w];
+    part[(size_t)b * gridDim.x + blockIdx.x] = s;
+  }
+}
+
+__device__ double sum_parts(const double* part, int G, int b) {
+  double s = 0.0;
+  for (int g = 0; g < G; ++g) s += part[(size_t)b * G + g];
+  return s;
+}
+
+// ---- per-column PCG scalar steps (the k_pcg_* logic of ops.cu, per column) --------
+__global__ void kc_init(int B, ColState* st, const double* part, int G, int* done) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  ColState c{};
+  const double s = sum_parts(part, G, b);
+  c.bnorm = sqrt(s);
+  c.done = (s == 0.0);
+  c.converged = (s == 0.0);
+  st[b] = c;
+  done[b] = c.done;
+}
+
+__global__ void kc_rz(int B, ColState* st, const double* part, int G, int* done, int initial) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  ColState& c = st[b];
+  if (c.done) return;
+  const double rz = sum_parts(part, G, b);
+  if (initial) {
+    if (rz <= 0.0) {
+      c.error = PCG_BAD_PRECOND;
+      c.done = 1;
+    }
+    c.rz = rz;
+    c.beta = 0.0;
+  } else if (rz <= 0.0) {
+    if (!c.past_rtol) c.error = PCG_BAD_PRECOND;
+    c.done = 1;
+  } else {
+    const double beta = rz / c.rz;
+    c.beta = beta;
+    c.rz = rz;
+    c.beta_prev = beta;
+    c.alpha_prev = c.alpha;
+  }
+  done[b] = c.done;
+}
+
+__global__ void kc_alpha(int B, ColState* st, const double* part, int G, int* done) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  ColState& c = st[b];
+  if (c.done) return;
+  const double pq = sum_parts(part, G, b);
+  c.pq = pq;
+  if (pq <= 0.0) {
+    if (!c.past_rtol) c.error = PCG_BAD_OPERATOR;
+    c.done = 1;
+  } else {
+    c.alpha = c.rz / pq;
+  }
+  done[b] = c.done;
+}
+
+// X += alpha P; R -= alpha Q (gated per column); partial ||R||^2
+__global__ void kb_update(int n, int ld, const ColState* st, double* __restrict__ X, double* __restrict__ R,
+                          const double* __restrict__ P, const double* __restrict__ Q, double* __restrict__ part) {
+  __shared__ double sred[32];
+  const int b = blockIdx.y;
+  const size_t o = (size_t)b * ld;
+  const bool active = !st[b].done;
+  const double alpha = st[b].alpha;
+  double acc = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double ri = R[o + i];
+    if (active) {
+      X[o + i] = fma(alpha, P[o + i], X[o + i]);
+      ri = fma(-alpha, Q[o + i], ri);
+      R[o + i] = ri;
+    }
+    acc = fma(ri, ri, acc);
+  }
+  acc = wsum(acc);
+  if ((threadIdx.x & 31) == 0) sred[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += sred[w];
+    part[(size_t)b * gridDim.x + blockIdx.x] = s;
+  }
+}
+
+__global__ void kc_relres(int B, ColState* st, const double* part, int G, double rtol, int maxit, int* done,
+                          int* any_true) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  ColState& c = st[b];
+  if (c.done) {
+    c.need_true = 0;
+    return;
+  }
+  const double relres = sqrt(sum_parts(part, G, b)) / c.bnorm;
+  c.it += 1;
+  c.relres = relres;
+  c.need_true = (relres <= rtol);
+  if (c.need_true) {
+    c.past_rtol = 1;
+    atomicOr(any_true, 1);
+  }
+  if (!c.need_true && c.it == maxit) c.done = 1;
+  done[b] = c.done;
+}
+
+__global__ void kc_true(int B, ColState* st, const double* part, int G, double rtol, int maxit, int* done) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  ColState& c = st[b];
+  if (c.done || !c.need_true) return;
+  const double tr = sqrt(sum_parts(part, G, b)) / c.bnorm;
+  c.true_rel = tr;
+  if (tr <= rtol || fabs(tr - c.relres) <= 1e-8) {
+    c.converged = 1;
+    c.done = 1;
+  } else if (c.it == maxit) {
+    c.done = 1;
+  }
+  done[b] = c.done;
+}
+
+__global__ void kb_p(int n, int ld, const ColState* st, const double* __restrict__ Z, double* __restrict__ P,
+                     int initial) {
+  const int b = blockIdx.y;
+  if (st[b].done) return;
+  const double beta = st[b].beta;
+  const size_t o = (size_t)b * ld;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    P[o + i] = initial ? Z[o + i] : fma(beta, P[o + i], Z[o + i]);
+}
+
+// ---------------------------------------------------------------------------
+struct Block {
+  int B = 0, ld = 0, G = 0;
+  DArr<double> X, R, Z, Pm, Q, Bm, T, C0, C1, C2, C3, C4, C5;
+  DArr<double> XS, WS;  // block-P layout
+  DArr<double> zx, zr, zt, zc, negc, part;
+  DArr<ColState> st;
+  DArr<int> done, any_true;
+  DArr<long long> boff;
+  std::vector<long long> h_boff;
+};
+
+struct BlockOps {
+  Ctx& c;
+  Block& k;
+  cublasHandle_t h;
+  const CoarseFactor& k0;
+
+  dim3 grid_n() const { return dim3(std::max(1, std::min((c.n + kT - 1) / kT, 148 * 2)), k.B); }
+  dim3 grid_p() const {
+    return dim3(std::max(1, int(std::min<long long>((c.P + kT - 1) / kT, 148 * 2))), k.B);
+  }
+
+  void spmv(const double* X, double* Y, int mode, const double* add, const double* sub, const int* done) {
+    kb_spmv<<<grid_n(), kT, 0, c.stream>>>(c.n, k.ld, c.rp.p, c.ci.p, c.va.p, X, Y, mode, add, sub, done);
+    ++c.launches;
+  }
+  void aminus(const double* X, double* Y, const int* done) {
+    if (c.nneg == 0) {
+      AWG_CUDA(cudaMemsetAsync(Y, 0, sizeof(double) * k.ld * k.B, c.stream));
+      return;
+    }
+    const long long warps = (long long)c.nneg * k.B;
+    kb_neg_dot<<<int((warps + 7) / 8), 256, 0, c.stream>>>(c.nneg, k.B, c.neg_s.p, c.neg_k.p, c.neg_w.p, c.V.p,
+                                                           c.voff.p, c.ns.p, c.ld.p, c.poff.p, c.pidx.p, k.ld, X,
+                                                           k.negc.p, done);
+    kb_combine<<<grid_p(), kT, 0, c.stream>>>(c.P, c.psub.p, c.poff.p, c.negoff.p, c.neg_k.p, c.V.p, c.voff.p,
+                                              c.ld.p, c.nneg, k.negc.p, c.ld.p, k.boff.p, k.WS.p, done);
+    kb_prolong<<<grid_n(), kT, 0, c.stream>>>(c.n, k.ld, c.own_off.p, c.own_pos.p, c.psub.p, c.poff.p, c.ld.p,
+                                              k.boff.p, nullptr, k.WS.p, Y, done);
+    c.launches += 3;
+  }
+  void aplus(const double* X, double* Y, const int* done) {
+    aminus(X, Y, done);
+    spmv(X, Y, 1, Y, nullptr, done);
+  }
+  void q(const double* X, double* Y, const int* done) {
+    const int n0 = c.n0, r = k0.rank, B = k.B;
+    const long long warps = (long long)n0 * B;
+    kb_zT<<<int((warps + 7) / 8), 256, 0, c.stream>>>(n0, B, c.zcol_s.p, c.zcol_loc.p, c.Y.p, c.yoff.p, c.ns.p,
+                                                     c.ld.p, c.poff.p, c.pidx.p, k.ld, X, k.zx.p, done);
+    AWG_CUDA(cudaMemsetAsync(k.zc.p, 0, sizeof(double) * n0 * B, c.stream));
+    if (r > 0) {
+      kb_take<<<int(((long long)r * B + kT - 1) / kT), kT, 0, c.stream>>>(r, n0, B, k0.retained.p, k.zx.p, k.zr.p);
+      const double one = 1.0, zero = 0.0;
+      // t = L^-1 b_r, y = L^-T t  (rank_revealing_solve, dense.cpp:348-366)
+      AWG_BLAS(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, r, B, r, &one, k0.linv.p, r, k.zr.p, r, &zero, k.zt.p, r));
+      AWG_BLAS(cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, r, B, r, &one, k0.linv.p, r, k.zt.p, r, &zero, k.zr.p, r));
+      kb_put<<<int(((long long)r * B + kT - 1) / kT), kT, 0, c.stream>>>(r, n0, B, k0.retained.p, k.zr.p, k.zc.p);
+      c.launches += 2;
+    }
+    kb_combine<<<grid_p(), kT, 0, c.stream>>>(c.P, c.psub.p, c.poff.p, c.koff.p, nullptr, c.Y.p, c.yoff.p, c.ld.p,
+                                              n0, k.zc.p, c.ld.p, k.boff.p, k.WS.p, done);
+    kb_prolong<<<grid_n(), kT, 0, c.stream>>>(c.n, k.ld, c.own_off.p, c.own_pos.p, c.psub.p, c.poff.p, c.ld.p,
+                                              k.boff.p, nullptr, k.WS.p, Y, done);
+    c.launches += 3;
+  }
+  void h1(const double* X, double* Y, const int* done) {
+    kb_gather<<<grid_p(), kT, 0, c.stream>>>(c.P, c.psub.p, c.poff.p, c.pidx.p, c.ld.p, k.boff.p, c.ds.p, k.ld, X,
+                                             k.XS.p, done);
+    const double one = 1.0, zero = 0.0;
+    for (int s = 0; s < c.N; ++s) {
+      const int n = c.h_ns[s], L = c.h_ld[s];
+      const double* Vs = c.V.p + c.h_voff[s];
+      AWG_BLAS(cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, n, k.B, n, &one, Vs, L, k.XS.p + k.h_boff[s], L, &zero,
+                           k.WS.p + k.h_boff[s], L));
+    }
+    kb_mask<<<grid_p(), kT, 0, c.stream>>>(c.P, c.psub.p, c.poff.p, c.ld.p, k.boff.p, c.msz.p, c.lam.p, k.B, k.WS.p);
+    for (int s = 0; s < c.N; ++s) {
+      const int n = c.h_ns[s], L = c.h_ld[s];
+      const double* Vs = c.V.p + c.h_voff[s];
+      AWG_BLAS(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, n, k.B, n, &one, Vs, L, k.WS.p + k.h_boff[s], L, &zero,
+                           k.XS.p + k.h_boff[s], L));
+    }
+    kb_prolong<<<grid_n(), kT, 0, c.stream>>>(c.n, k.ld, c.own_off.p, c.own_pos.p, c.psub.p, c.poff.p, c.ld.p,
+                                              k.boff.p, c.ds.p, k.XS.p, Y, done);
+    c.launches += 3;
+  }
+  // TwoLevel::apply (preconditioner.cpp:64-82)
+  void h2(const double* X, double* Y, const int* done) {
+    if (c.n0 == 0) {
+      h1(X, Y, done);
+      return;
+    }
+    q(X, k.C0.p, done);
+    if (c.cfg.composition == 0) {
+      h1(X, k.C1.p, done);
+      axpby(k.C1.p, k.C0.p, nullptr, Y, 1, done);
+      return;
+    }
+    aminus(k.C0.p, k.C1.p, done);
+    spmv(k.C0.p, k.C2.p, 2, k.C1.p, X, done);
+    h1(k.C2.p, k.C3.p, done);
+    aplus(k.C3.p, k.C4.p, done);
+    q(k.C4.p, k.C5.p, done);
+    axpby(k.C3.p, k.C5.p, k.C0.p, Y, 0, done);
+  }
+  void axpby(const double* a, const double* b, const double* d, double* y, int mode, const int* done) {
+    kb_axpby<<<grid_n(), kT, 0, c.stream>>>(c.n, k.ld, a, b, d, y, mode, done);
+    ++c.launches;
+  }
+  void dot(const double* x, const double* y, int mode, const double* bm) {
+    kb_dot<<<dim3(k.G, k.B), kT, 0, c.stream>>>(c.n, k.ld, x, y, k.part.p, mode, bm);
+    ++c.launches;
+  }
+};
+
+}  // namespace
+
+// Solve A+ W(:, j) = R^s^T v_k for the given columns (block of rhs already in
+// k.Bm), H2 preconditioned; returns per-column iteration counts.
+void build_w_batched(Ctx& c, cublasHandle_t h, const std::vector<std::pair<int, int>>& modes, int maxit,
+                     double rtol, std::vector<int>& iters, int max_block) {
+  const int total = int(modes.size());
+  iters.assign(total, 0);
+  if (total == 0) return;
+  size_t free_b = 0, tot_b = 0;
+  AWG_CUDA(cudaMemGetInfo(&free_b, &tot_b));
+  // bytes per batched column: 13 n-blocks, 2 restricted blocks, coarse and mode scratch
+  const size_t per_col =
+      sizeof(double) * (size_t(c.ldw) * 13 + size_t(c.P + 4 * c.N) * 2 + size_t(c.n0) * 4 + c.nneg + 256);
+  int B = int(std::min<size_t>(size_t(max_block), (free_b * 7 / 10) / std::max<size_t>(per_col, 1)));
+  B = std::max(1, std::min(B, total));
+  Block k;
+  k.B = B;
+  k.ld = c.ldw;
+  k.G = std::max(1, std::min((c.n + kT - 1) / kT, 148));
+  for (DArr<double>* m : {&k.X, &k.R, &k.Z, &k.Pm, &k.Q, &k.Bm, &k.T, &k.C0, &k.C1, &k.C2, &k.C3, &k.C4, &k.C5})
+    m->alloc(size_t(k.ld) * B);
+  k.h_boff.assign(c.N + 1, 0);
+  for (int s = 0; s < c.N; ++s) k.h_boff[s + 1] = k.h_boff[s] + (long long)c.h_ld[s] * B;
+  k.boff.upload(k.h_boff, c.stream);
+  k.XS.alloc(size_t(k.h_boff[c.N]));
+  k.WS.alloc(size_t(k.h_boff[c.N]));
+  k.XS.zero(c.stream);
+  k.WS.zero(c.stream);
+  k.zx.alloc(size_t(std::max(c.n0, 1)) * B);
+  k.zc.alloc(size_t(std::max(c.n0, 1)) * B);
+  k.zr.alloc(size_t(std::max(c.k0.rank, 1)) * B);
+  k.zt.alloc(size_t(std::max(c.k0.rank, 1)) * B);
+  k.negc.alloc(size_t(std::max(c.nneg, 1)) * B);
+  k.part.alloc(size_t(k.G) * B);
+  k.st.alloc(B);
+  k.done.alloc(B);
+  k.any_true.alloc(1);
+  AWG_BLAS(cublasSetStream(h, c.stream));
+  BlockOps ops{c, k, h, c.k0};
+  const int cb = (B + 127) / 128;
+  std::vector<ColState> hs(B);
+  for (int c0 = 0; c0 < total; c0 += B) {
+    const int nb = std::min(B, total - c0);
+    // right-hand sides R^s^T v_k for the batch (unused columns: zero -> done at init)
+    k.Bm.zero(c.stream);
+    for (int j = 0; j < nb; ++j) {
+      const int s = modes[c0 + j].first, kk = modes[c0 + j].second;
+      k::scatter_col(c, s, c.V.p + c.h_voff[s] + size_t(kk) * c.h_ld[s], k.Bm.p + size_t(j) * k.ld);
+    }
+    const dim3 gn = ops.grid_n();
+    // init: X = 0, R = B, bnorm
+    k.X.zero(c.stream);
+    AWG_CUDA(cudaMemcpyAsync(k.R.p, k.Bm.p, sizeof(double) * k.ld * B, cudaMemcpyDeviceToDevice, c.stream));
+    ops.dot(k.R.p, k.R.p, 0, nullptr);
+    kc_init<<<cb, 128, 0, c.stream>>>(B, k.st.p, k.part.p, k.G, k.done.p);
+    ops.h2(k.R.p, k.Z.p, k.done.p);
+    ops.dot(k.R.p, k.Z.p, 0, nullptr);
+    kc_rz<<<cb, 128, 0, c.stream>>>(B, k.st.p, k.part.p, k.G, k.done.p, 1);
+    kb_p<<<gn, kT, 0, c.stream>>>(c.n, k.ld, k.st.p, k.Z.p, k.Pm.p, 1);
+    c.launches += 3;
+    for (int it = 0; it < maxit; ++it) {
+      ops.aplus(k.Pm.p, k.Q.p, k.done.p);
+      ops.dot(k.Pm.p, k.Q.p, 0, nullptr);
+      kc_alpha<<<cb, 128, 0, c.stream>>>(B, k.st.p, k.part.p, k.G, k.done.p);
+      kb_update<<<dim3(k.G, B), kT, 0, c.stream>>>(c.n, k.ld, k.st.p, k.X.p, k.R.p, k.Pm.p, k.Q.p, k.part.p);
+      AWG_CUDA(cudaMemsetAsync(k.any_true.p, 0, sizeof(int), c.stream));
+      kc_relres<<<cb, 128, 0, c.stream>>>(B, k.st.p, k.part.p, k.G, rtol, maxit, k.done.p, k.any_true.p);
+      c.launches += 3;
+      int any = 0;
+      AWG_CUDA(cudaMemcpyAsync(&any, k.any_true.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+      AWG_CUDA(cudaStreamSynchronize(c.stream));
+      if (any) {  // true residual b - A+ x for the columns that reached rtol
+        ops.aplus(k.X.p, k.T.p, k.done.p);
+        ops.dot(nullptr, k.T.p, 1, k.Bm.p);
+        kc_true<<<cb, 128, 0, c.stream>>>(B, k.st.p, k.part.p, k.G, rtol, maxit, k.done.p);
+        ++c.launches;
+      }
+      ops.h2(k.R.p, k.Z.p, k.done.p);
+      ops.dot(k.R.p, k.Z.p, 0, nullptr);
+      kc_rz<<<cb, 128, 0, c.stream>>>(B, k.st.p, k.part.p, k.G, k.done.p, 0);
+      kb_p<<<gn, kT, 0, c.stream>>>(c.n, k.ld, k.st.p, k.Z.p, k.Pm.p, 0);
+      c.launches += 2;
+      AWG_CUDA(cudaMemcpyAsync(hs.data(), k.st.p, sizeof(ColState) * B, cudaMemcpyDeviceToHost, c.stream));
+      AWG_CUDA(cudaStreamSynchronize(c.stream));
+      bool all = true;
+      for (int j = 0; j < nb; ++j) all = all && hs[j].done;
+      if (all) break;
+    }
+    AWG_CUDA(cudaMemcpyAsync(hs.data(), k.st.p, sizeof(ColState) * B, cudaMemcpyDeviceToHost, c.stream));
+    AWG_CUDA(cudaStreamSynchronize(c.stream));
+    for (int j = 0; j < nb; ++j) {
+      if (hs[j].error) c.fail(AWG_E_BREAKDOWN, "build_w: inner PCG breakdown");
+      if (!hs[j].converged) c.fail(AWG_E_NO_CONVERGENCE, "build_w: inner PCG for a W column did not converge");
+      iters[c0 + j] = hs[j].it;
+      AWG_CUDA(cudaMemcpyAsync(c.W.p + size_t(c0 + j) * c.ldw, k.X.p + size_t(j) * k.ld, sizeof(double) * c.n,
+                               cudaMemcpyDeviceToDevice, c.stream));
+    }
+    ++c.w_batches;
+  }
+  AWG_CUDA(cudaStreamSynchronize(c.stream));
+}
+
+}  // namespace awgb
