@@ -195,6 +195,8 @@ def main():
     ap.add_argument("--config", default=os.environ.get("AWG_BENCH_CONFIG", DEFAULT_CONFIG))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--rrf", default="reference", choices=["reference", "exact"],
+                    help="pivoted-factor semantics: the reference's (default) or the exact one")
     args = ap.parse_args()
     ws, rank, local = dist_env()
 
@@ -235,7 +237,7 @@ def main():
     from paper_2106_10913_b200 import awg
 
     ctx = awg.context_from_problem(p, device=local)
-    cfg = awg.config_for(p)
+    cfg = awg.config_for(p, rrf_semantics=args.rrf)
     torch.cuda.synchronize()
     t0 = time.time()
     ctx.setup(cfg)
@@ -315,6 +317,7 @@ def main():
         "config": {"workload": args.config, "problem": p.meta, "n": p.n, "nnz": p.nnz, "n_sub": p.n_sub,
                    "selection": ({"fixed_k": p.fixed_k} if p.fixed_k else {"tau_sharp": p.tau_sharp}),
                    "rtol": rtol, "preconditioner": "H3,ad + NN-hybrid (reference default)",
+                   "pivoted_factor": args.rrf,
                    "l2": "inputs larger than L2" if q["sum_ns2"] * 8 > 126e6 else "inputs fit in L2 (no flush)"},
         "solve": {"iterations": its, "solve_ms_mean": dev_ms / args.steps, "t_iter_ms": t_iter_ms,
                   "n0": q["n0"], "r0": q["r0"], "n_minus": q["n_minus"], "rw": q["rw"]},

@@ -87,6 +87,9 @@ struct DArr {
 
 inline int round_up(int v, int m) { return (v + m - 1) / m * m; }
 
+struct Ctx;
+int w_chunks(const Ctx& c);  // column chunks of the W c GEMV (enough CTAs for small n)
+
 // Work items of the batched NN local solve.
 struct GemvTTask {  // columns [j0, j1) of V^s
   int s, j0, j1, pad;
@@ -219,6 +222,7 @@ struct Ctx {
   DArr<double> t0, t1, t2, t3, t4, t5, t6, t7, t8;  // n each
   DArr<double> cz, cz2;                             // max(n0, nm) each
   DArr<double> wpart;                               // split-K partials of W^T x
+  DArr<double> wpart2;                              // column-chunk partials of W c
   DArr<double> red;                                 // reduction partials
   DArr<unsigned> red_count;
 

@@ -347,23 +347,42 @@ __global__ void k_transpose(int r, const double* __restrict__ a, double* __restr
 
 // ---------------------------------------------------------------------------
 // Tall-skinny W (n x nm, column-major, ld): split-K W^T x, then W c.
-__global__ void k_dense_gemvT_part(const int* __restrict__ gate, int n, int nm, int ldw, int chunk,
-                                   const double* __restrict__ W, const double* __restrict__ x,
-                                   double* __restrict__ part) {
+// CTA per (row chunk of kWChunk rows, group of 32 columns): the x chunk is staged
+// in shared memory (zero past n), one warp per column, 16-byte loads, 4 in flight
+// per lane; part[chunk * nm + j] holds the chunk's partial dot.
+constexpr int kWChunk = 4096;
+__global__ void __launch_bounds__(kThreads) k_dense_gemvT_part(const int* __restrict__ gate, int n, int nm, int ldw,
+                                                            const double* __restrict__ W, const double* __restrict__ x,
+                                                            double* __restrict__ part) {
   if (gated(gate)) return;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int r0 = blockIdx.y * chunk;
-  const int r1 = min(n, r0 + chunk);
-  for (int j = blockIdx.x * nw + warp; j < nm; j += gridDim.x * nw) {
-    const double* col = W + (size_t)j * ldw;
-    double a0 = 0.0, a1 = 0.0;
-    int i = r0 + lane;
-    for (; i + 32 < r1; i += 64) {
-      a0 = fma(__ldcs(col + i), __ldg(x + i), a0);
-      a1 = fma(__ldcs(col + i + 32), __ldg(x + i + 32), a1);
+  __shared__ double2 sx2[kWChunk / 2];
+  double* sx = reinterpret_cast<double*>(sx2);
+  const int r0 = blockIdx.y * kWChunk;
+  const int rows = min(kWChunk, ldw - r0);  // ldw is a multiple of 4: pad rows of W are zero
+  for (int i = threadIdx.x; i < kWChunk; i += blockDim.x) sx[i] = (r0 + i < n) ? x[r0 + i] : 0.0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int npair = rows >> 1;
+  const int jend = min(nm, (int)(blockIdx.x + 1) * 32);
+  for (int j = blockIdx.x * 32 + warp; j < jend; j += 8) {
+    const double2* col = reinterpret_cast<const double2*>(W + (size_t)j * ldw + r0);
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int q = lane;
+    for (; q + 96 < npair; q += 128) {
+      const double2 v0 = __ldcs(col + q), v1 = __ldcs(col + q + 32), v2 = __ldcs(col + q + 64),
+                    v3 = __ldcs(col + q + 96);
+      const double2 x0 = sx2[q], x1 = sx2[q + 32], x2 = sx2[q + 64], x3 = sx2[q + 96];
+      a0 = fma(v0.x, x0.x, a0); a0 = fma(v0.y, x0.y, a0);
+      a1 = fma(v1.x, x1.x, a1); a1 = fma(v1.y, x1.y, a1);
+      a2 = fma(v2.x, x2.x, a2); a2 = fma(v2.y, x2.y, a2);
+      a3 = fma(v3.x, x3.x, a3); a3 = fma(v3.y, x3.y, a3);
     }
-    for (; i < r1; i += 32) a0 = fma(__ldcs(col + i), __ldg(x + i), a0);
-    const double sum = warp_sum(a0 + a1);
+    for (; q < npair; q += 32) {
+      const double2 v0 = __ldcs(col + q);
+      const double2 x0 = sx2[q];
+      a0 = fma(v0.x, x0.x, a0); a0 = fma(v0.y, x0.y, a0);
+    }
+    const double sum = warp_sum((a0 + a1) + (a2 + a3));
     if (lane == 0) part[(size_t)blockIdx.y * nm + j] = sum;
   }
 }
@@ -378,24 +397,55 @@ __global__ void k_colsum(const int* __restrict__ gate, int nm, int nchunks, cons
   out[j] = acc;
 }
 
-__global__ void __launch_bounds__(kThreads) k_dense_gemv(const int* __restrict__ gate, int n, int nm, int ldw,
+// y = W c, CTA per (512-row panel, column chunk kc of nkc): two rows per thread
+// (16-byte loads), 8 columns in flight; with nkc > 1 the chunk results go to
+// part[kc * ldw + i] and k_chunk_sum adds them in fixed order.
+__global__ void __launch_bounds__(kThreads) k_dense_gemv(const int* __restrict__ gate, int n, int nm, int ldw, int nkc,
                                                       const double* __restrict__ W, const double* __restrict__ c,
-                                                      double* __restrict__ y) {
+                                                      double* __restrict__ y, double* __restrict__ part) {
   if (gated(gate)) return;
   extern __shared__ double scoef[];
-  for (int j = threadIdx.x; j < nm; j += blockDim.x) scoef[j] = c[j];
+  const int kc = blockIdx.y;
+  const int j0 = int((long long)nm * kc / nkc), j1 = int((long long)nm * (kc + 1) / nkc);
+  for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x) scoef[j - j0] = c[j];
   __syncthreads();
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) * 2;
   if (i >= n) return;
   const double* w = W + i;
-  double a0 = 0.0, a1 = 0.0;
-  int j = 0;
-  for (; j + 2 <= nm; j += 2) {
-    a0 = fma(__ldcs(w + (size_t)j * ldw), scoef[j], a0);
-    a1 = fma(__ldcs(w + (size_t)(j + 1) * ldw), scoef[j + 1], a1);
+  double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+  int j = j0;
+  for (; j + 8 <= j1; j += 8) {
+    double2 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __ldcs(reinterpret_cast<const double2*>(w + (size_t)(j + u) * ldw));
+#pragma unroll
+    for (int u = 0; u < 8; u += 2) {
+      const double c0 = scoef[j + u - j0], c1 = scoef[j + u + 1 - j0];
+      a0 = fma(v[u].x, c0, a0);
+      a1 = fma(v[u].y, c0, a1);
+      b0 = fma(v[u + 1].x, c1, b0);
+      b1 = fma(v[u + 1].y, c1, b1);
+    }
   }
-  if (j < nm) a0 = fma(__ldcs(w + (size_t)j * ldw), scoef[j], a0);
-  y[i] = a0 + a1;
+  for (; j < j1; ++j) {
+    const double2 v0 = __ldcs(reinterpret_cast<const double2*>(w + (size_t)j * ldw));
+    const double c0 = scoef[j - j0];
+    a0 = fma(v0.x, c0, a0);
+    a1 = fma(v0.y, c0, a1);
+  }
+  double* out = (nkc == 1) ? y : part + (size_t)kc * ldw;
+  out[i] = a0 + b0;
+  if (i + 1 < n) out[i + 1] = a1 + b1;
+}
+
+__global__ void k_chunk_sum(const int* __restrict__ gate, int n, int ldw, int nkc, const double* __restrict__ part,
+                            double* __restrict__ y) {
+  if (gated(gate)) return;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int kc = 0; kc < nkc; ++kc) acc += part[(size_t)kc * ldw + i];
+    y[i] = acc;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -585,11 +635,9 @@ void zT(Ctx& c, const double* x, double* out, const int* gate) {
 }
 
 static void w_transpose_apply(Ctx& c, const double* x, double* out, const int* gate) {
-  const int chunk = 4096;
-  const int nch = (c.n + chunk - 1) / chunk;
-  const int wpb = kThreads / 32;
-  dim3 grid((c.nm + wpb - 1) / wpb, nch);
-  k_dense_gemvT_part<<<grid, kThreads, 0, c.stream>>>(gate, c.n, c.nm, c.ldw, chunk, c.W.p, x, c.wpart.p);
+  const int nch = (c.ldw + kWChunk - 1) / kWChunk;
+  dim3 grid((c.nm + 31) / 32, nch);
+  k_dense_gemvT_part<<<grid, kThreads, 0, c.stream>>>(gate, c.n, c.nm, c.ldw, c.W.p, x, c.wpart.p);
   ++c.launches;
   check_launch("dense_gemvT_part");
   k_colsum<<<(c.nm + kThreads - 1) / kThreads, kThreads, 0, c.stream>>>(gate, c.nm, nch, c.wpart.p, out);
@@ -598,16 +646,23 @@ static void w_transpose_apply(Ctx& c, const double* x, double* out, const int* g
 }
 
 static void w_apply(Ctx& c, const double* coef, double* y, const int* gate) {
-  const size_t smem = size_t(c.nm) * sizeof(double);
+  const int nkc = w_chunks(c);
+  const int chunk = (c.nm + nkc - 1) / nkc + 1;
+  const size_t smem = size_t(chunk) * sizeof(double);
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
     AWG_CUDA(cudaFuncSetAttribute(k_dense_gemv, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     configured = smem;
   }
-  k_dense_gemv<<<(c.n + kThreads - 1) / kThreads, kThreads, smem, c.stream>>>(gate, c.n, c.nm, c.ldw, c.W.p, coef,
-                                                                              y);
+  dim3 grid((c.n + 2 * kThreads - 1) / (2 * kThreads), nkc);
+  k_dense_gemv<<<grid, kThreads, smem, c.stream>>>(gate, c.n, c.nm, c.ldw, nkc, c.W.p, coef, y, c.wpart2.p);
   ++c.launches;
   check_launch("dense_gemv");
+  if (nkc > 1) {
+    k_chunk_sum<<<grid_for(c, c.n), kThreads, 0, c.stream>>>(gate, c.n, c.ldw, nkc, c.wpart2.p, y);
+    ++c.launches;
+    check_launch("chunk_sum");
+  }
 }
 
 void wT(Ctx& c, const double* x, double* out, const int* gate) { w_transpose_apply(c, x, out, gate); }

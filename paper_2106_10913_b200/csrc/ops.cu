@@ -243,6 +243,14 @@ double tridiag_eig(const std::vector<double>& d, const std::vector<double>& e, i
 }  // namespace
 
 // ---------------------------------------------------------------------------
+int w_chunks(const Ctx& c) {
+  // 512-row panels; split the n_minus columns until ~4 CTAs per SM exist,
+  // keeping at least 128 columns per chunk
+  const int panels = (c.n + 511) / 512;
+  const int want = (4 * c.sm_count + panels - 1) / panels;
+  return std::max(1, std::min(want, c.nm / 128));
+}
+
 void Ctx::alloc_work() {
   invalidate_graphs();
   const size_t nn = size_t(n);
@@ -253,8 +261,9 @@ void Ctx::alloc_work() {
   const size_t cdim = size_t(std::max(n0, nm)) * 2 + 2;
   cz.alloc(cdim);
   cz2.alloc(cdim);
-  const int nch = (n + 4095) / 4096;
+  const int nch = (round_up(n, 4) + 4095) / 4096;
   wpart.alloc(size_t(std::max(nm, 1)) * nch);
+  wpart2.alloc(size_t(w_chunks(*this)) * round_up(n, 4));
   red.alloc(size_t(sm_count) * 16);
   red_count.alloc(1);
   red_count.zero(stream);
