@@ -112,6 +112,8 @@ struct Args {
   int fixed_k = -1;
   std::string awg = "ad";
   std::string comp = "hybrid";
+  std::string one_level = "NN";
+  double tau_flat = 10.0;
   double rtol = 1e-8;
   double w_rtol = 1e-10;
   int maxit = 10000;
@@ -146,6 +148,8 @@ Args parse(int argc, char** argv) {
     else if (k == "--fixed-k") a.fixed_k = std::stoi(next());
     else if (k == "--awg") a.awg = next();
     else if (k == "--comp") a.comp = next();
+    else if (k == "--one-level") a.one_level = next();
+    else if (k == "--tau-flat") a.tau_flat = std::stod(next());
     else if (k == "--rtol") a.rtol = std::stod(next());
     else if (k == "--w-rtol") a.w_rtol = std::stod(next());
     else if (k == "--maxit") a.maxit = std::stoi(next());
@@ -365,22 +369,46 @@ int main(int argc, char** argv) {
   t0 = now_s();
   std::vector<int> ks;
   CoarseSpace cs;
+  const OneLevelKind kind =
+      args.one_level == "AS" ? OneLevelKind::AS : args.one_level == "AS_PLUS" ? OneLevelKind::AS_PLUS : OneLevelKind::NN;
+  auto count_below = [](const EigenDecomposition& e, double tau) {
+    int m = 0;
+    while (m < int(e.eigenvalues.size()) && e.eigenvalues[m] < tau) ++m;
+    return m;
+  };
+  std::vector<std::vector<double>> ycols(N);  // exported coarse vectors per subdomain, Z column order
   if (args.fixed_k > 0) {
     cs = fixed_k_coarse(geneo, args.fixed_k, ks);
   } else {
     const double tau = args.tau > 0 ? args.tau : 0.1;
-    // build_coarse with ThresholdSpec::nn; ks recovered from the pencils.
+    // build_coarse (coarse.cpp:113-154); per-subdomain counts recovered from the pencils
     for (int s = 0; s < N; ++s) {
-      const auto& e = geneo.pencil_nn(s);
-      int m = 0;
-      while (m < int(e.eigenvalues.size()) && e.eigenvalues[m] < tau) ++m;
-      ks.push_back(m);
+      if (kind == OneLevelKind::NN) {
+        ks.push_back(count_below(geneo.pencil_nn(s), tau));
+      } else if (kind == OneLevelKind::AS_PLUS) {
+        ks.push_back(count_below(geneo.pencil_nn(s), 1.0 / args.tau_flat));
+      } else {
+        const int m1 = count_below(geneo.pencil_as1(s), 1.0 / args.tau_flat);
+        const int m2 = count_below(geneo.pencil_as2(s), tau);
+        ks.push_back(m1 + m2);
+        const auto& e1 = geneo.pencil_as1(s).eigenvectors;
+        const auto& e2 = geneo.pencil_as2(s).eigenvectors;
+        ycols[s].assign(e1.a.begin(), e1.a.begin() + size_t(e1.rows) * m1);
+        ycols[s].insert(ycols[s].end(), e2.a.begin(), e2.a.begin() + size_t(e2.rows) * m2);
+      }
     }
-    cs = build_coarse(ThresholdSpec::nn(tau), geneo);
+    if (kind == OneLevelKind::NN) cs = build_coarse(ThresholdSpec::nn(tau), geneo);
+    else if (kind == OneLevelKind::AS_PLUS) cs = build_coarse(ThresholdSpec::as_plus(args.tau_flat), geneo);
+    else cs = build_coarse(ThresholdSpec::as(tau, args.tau_flat), geneo);
   }
+  for (int s = 0; s < N; ++s)
+    if (kind != OneLevelKind::AS) {
+      const auto& pm = geneo.pencil_nn(s).eigenvectors;
+      ycols[s].assign(pm.a.begin(), pm.a.begin() + size_t(pm.rows) * ks[s]);
+    }
   double t_coarse = now_s() - t0;
   const Composition comp = args.comp == "additive" ? Composition::ADDITIVE : Composition::HYBRID;
-  auto h2 = std::make_shared<TwoLevel>(OneLevel(OneLevelKind::NN, split), cs, comp, split);
+  auto h2 = std::make_shared<TwoLevel>(OneLevel(kind, split), cs, comp, split);
 
   t0 = now_s();
   const AwgMode mode = mode_of(args.awg);
@@ -420,6 +448,17 @@ int main(int argc, char** argv) {
     }
     npy_d(out, "lam", lam);
     npy_d(out, "pencil_lam", plam);
+    if (kind == OneLevelKind::AS) {
+      std::vector<double> a1, a2;
+      for (int s = 0; s < N; ++s) {
+        auto& e1 = geneo.pencil_as1(s).eigenvalues;
+        a1.insert(a1.end(), e1.begin(), e1.end());
+        auto& e2 = geneo.pencil_as2(s).eigenvalues;
+        a2.insert(a2.end(), e2.begin(), e2.end());
+      }
+      npy_d(out, "pencil_as1_lam", a1);
+      npy_d(out, "pencil_as2_lam", a2);
+    }
   }
   npy_i(out, "k0_retained", cs.k0.retained);
   npy_mat(out, "k0_l11", cs.k0.l11);
@@ -456,8 +495,7 @@ int main(int argc, char** argv) {
     for (int s = 0; s < N; ++s) {
       auto& m = split.splits()[s].eig.eigenvectors.a;
       V.insert(V.end(), m.begin(), m.end());
-      auto& pm = geneo.pencil_nn(s).eigenvectors;
-      Y.insert(Y.end(), pm.a.begin(), pm.a.begin() + size_t(pm.rows) * ks[s]);
+      Y.insert(Y.end(), ycols[s].begin(), ycols[s].end());
     }
     npy_d(out, "V", V);
     npy_d(out, "Y", Y);
@@ -491,7 +529,7 @@ int main(int argc, char** argv) {
   // ---- applies on seeded vectors -----------------------------------------
   {
     std::vector<std::vector<double>> X, yA, yAm, yAp, yH1, yQ, yQW, yH2, yAD, yHYB, yINEX, yPI3, yPI3T;
-    OneLevel h1(OneLevelKind::NN, split);
+    OneLevel h1(kind, split);
     for (int m = 0; m < args.n_apply; ++m) {
       std::vector<double> x = uniform_vec(1000 + m, n, -1.0, 1.0), y(n);
       X.push_back(x);
@@ -562,6 +600,7 @@ int main(int argc, char** argv) {
     std::fprintf(js, "  \"ritz_min\": %.17g, \"ritz_max\": %.17g, \"kappa\": %.17g,\n", rep.ritz_min,
                  rep.ritz_max, rep.kappa_estimate);
   }
+  std::fprintf(js, "  \"one_level\": \"%s\", \"tau_flat\": %.17g,\n", args.one_level.c_str(), args.tau_flat);
   std::fprintf(js, "  \"awg\": \"%s\", \"rtol\": %.17g, \"w_rtol\": %.17g, \"tau\": %.17g, \"fixed_k\": %d\n}\n",
                args.awg.c_str(), args.rtol, args.w_rtol, args.tau, args.fixed_k);
   std::fclose(js);

@@ -161,31 +161,43 @@ void finalize_factors(Ctx& c) {
   c.msz.upload(c.h_m, c.stream);
   c.voff.upload(c.h_voff, c.stream);
   c.yoff.upload(c.h_yoff, c.stream);
-  // NN task lists
-  std::vector<GemvTTask> tT;
-  std::vector<GemvTask> t;
-  std::vector<int> nkc(N, 0);
-  int kcmax = 1;
-  for (int s = 0; s < N; ++s) {
-    for (int j0 = c.h_m[s]; j0 < c.h_ns[s]; j0 += 64) tT.push_back({s, j0, std::min(j0 + 64, c.h_ns[s]), 0});
-    // split-K over column chunks of gemv_cols (the last chunk takes the remainder)
-    const int cols = c.h_ns[s] - c.h_m[s];
-    const int kcs = std::max(1, cols / c.gemv_cols);
-    nkc[s] = kcs;
-    kcmax = std::max(kcmax, kcs);
-    for (int kc = 0; kc < kcs; ++kc) {
-      const int j0 = c.h_m[s] + int((long long)cols * kc / kcs);
-      const int j1 = c.h_m[s] + int((long long)cols * (kc + 1) / kcs);
-      for (int i0 = 0; i0 < c.h_ns[s]; i0 += c.rows_per_gemv) t.push_back({s, i0, j0, j1, kc, 0});
+  // local-solve task lists: NN always (V^s columns j >= n_nonpos), AS/AS+ when configured
+  auto build_plan = [&](LocalPlan& pl, bool tri) {
+    std::vector<GemvTTask> tT;
+    std::vector<GemvTask> t;
+    std::vector<int> nkc(N, 0);
+    pl.kcmax = 1;
+    for (int s = 0; s < N; ++s) {
+      const int jstart = tri ? 0 : c.h_m[s];
+      for (int j0 = jstart; j0 < c.h_ns[s]; j0 += 64) tT.push_back({s, j0, std::min(j0 + 64, c.h_ns[s]), 0});
+      // split-K over column chunks of gemv_cols (the last chunk takes the remainder)
+      const int cols = c.h_ns[s] - jstart;
+      const int kcs = std::max(1, cols / c.gemv_cols);
+      nkc[s] = kcs;
+      pl.kcmax = std::max(pl.kcmax, kcs);
+      for (int kc = 0; kc < kcs; ++kc) {
+        const int j0 = jstart + int((long long)cols * kc / kcs);
+        const int j1 = jstart + int((long long)cols * (kc + 1) / kcs);
+        for (int i0 = 0; i0 < c.h_ns[s]; i0 += c.rows_per_gemv) {
+          // upper-triangular U^s: columns j < i0 are zero for the whole panel; an
+          // empty task still writes its (zero) partial slot
+          const int jj0 = tri ? std::max(j0, std::min(i0, j1)) : j0;
+          t.push_back({s, i0, jj0, j1, kc, 0});
+        }
+      }
     }
-  }
-  c.t_gemvT.upload(tT, c.stream);
-  c.t_gemv.upload(t, c.stream);
-  c.nkc.upload(nkc, c.stream);
+    pl.tT.upload(tT, c.stream);
+    pl.t.upload(t, c.stream);
+    pl.nkc.upload(nkc, c.stream);
+    pl.cols_max = 1;
+    for (const auto& tk : t) pl.cols_max = std::max(pl.cols_max, tk.j1 - tk.j0);
+  };
+  c.one_level = c.cfg.one_level;
+  build_plan(c.plan_nn, false);
+  if (c.one_level != 2) build_plan(c.plan_as, true);
+  const int kcmax = std::max(c.plan_nn.kcmax, c.one_level != 2 ? c.plan_as.kcmax : 1);
   c.wpart_nn.alloc(size_t(kcmax) * std::max<long long>(c.P, 1));
   c.wpart_nn.zero(c.stream);
-  c.gemv_cols_max = 0;
-  for (const auto& tk : t) c.gemv_cols_max = std::max(c.gemv_cols_max, tk.j1 - tk.j0);
   // A- modes: k < n_nonpos with lambda != 0 (splitting.cpp:129-131), ascending (s, k)
   std::vector<int> ns_, nk_, noff(N + 1, 0);
   std::vector<double> nw_;
@@ -271,11 +283,16 @@ int guarded(awg_ctx* ctx, F f) {
 }
 
 void check_config(Ctx& c, const awg_config& cfg) {
-  if (cfg.one_level != 2)
-    c.fail(AWG_E_ARG, "one_level: only NN is implemented on the device (AS/AS_PLUS: SURVEY.md §8f)");
+  if (cfg.one_level < 0 || cfg.one_level > 2) c.fail(AWG_E_ARG, "one_level must be 0 (AS), 1 (AS_PLUS) or 2 (NN)");
+  if (cfg.fixed_k > 0 && cfg.one_level != 2) c.fail(AWG_E_ARG, "fixed-k selection is defined for the NN pencil only");
+  // ThresholdSpec ranges (coarse.cpp:9-24)
+  if (cfg.use_coarse && cfg.one_level == 1 && !(cfg.tau_flat > 1.0))
+    c.fail(AWG_E_ARG, "AS_PLUS threshold requires tau_flat > 1");
+  if (cfg.use_coarse && cfg.one_level == 0 && (!(cfg.tau_sharp > 0.0 && cfg.tau_sharp < 1.0) || !(cfg.tau_flat > 1.0)))
+    c.fail(AWG_E_ARG, "AS threshold requires 0 < tau_sharp < 1 and tau_flat > 1");
   if (cfg.composition != 0 && cfg.composition != 1) c.fail(AWG_E_ARG, "composition must be 0 or 1");
   if (cfg.awg_mode < 0 || cfg.awg_mode > 3) c.fail(AWG_E_ARG, "awg_mode must be 0..3");
-  if (cfg.use_coarse && cfg.fixed_k <= 0 && !(cfg.tau_sharp > 0.0 && cfg.tau_sharp < 1.0))
+  if (cfg.use_coarse && cfg.one_level == 2 && cfg.fixed_k <= 0 && !(cfg.tau_sharp > 0.0 && cfg.tau_sharp < 1.0))
     c.fail(AWG_E_ARG, "NN threshold requires 0 < tau_sharp < 1");
 }
 
@@ -463,6 +480,9 @@ int awg_load_factors(awg_ctx* ctx, const awg_config* cfg, const awg_factors* f) 
       if (!f->neg_weights) c.fail(AWG_E_ARG, "load_factors: INEX needs neg_weights");
       build_core(c);
     }
+    // AS / AS+: the local Cholesky factors are computed here from A (and the
+    // loaded V^s for the A+ blocks); Cholesky factors are unique
+    if (c.one_level != 2) build_local_cholesky(c);
     AWG_CUDA(cudaStreamSynchronize(c.stream));
     c.have_factors = true;
   });

@@ -98,6 +98,16 @@ struct GemvTask {  // rows [i0, i0 + rows) x columns [j0, j1) of V^s, partial sl
   int s, i0, j0, j1, kc, pad;
 };
 
+// Work lists of one batched local solve (GEMV^T tasks, split GEMV tasks, column
+// chunks per subdomain).
+struct LocalPlan {
+  DArr<GemvTTask> tT;
+  DArr<GemvTask> t;
+  DArr<int> nkc;
+  int cols_max = 0;
+  int kcmax = 1;
+};
+
 // Triangular coarse factor with retained pivots (RankRevealingFactor,
 // dense.hpp:81-86), stored as the inverse of l11.
 struct CoarseFactor {
@@ -177,16 +187,18 @@ struct Ctx {
   std::vector<int> h_m, h_nzero, h_ks;
   std::vector<long long> h_voff, h_yoff;
   std::vector<double> h_lam, h_eps, h_plam;
+  std::vector<double> h_plam2;  // AS: pencil_as2 spectrum (h_plam holds pencil_as1)
+  std::vector<int> h_ks_as1;    // AS: columns per subdomain taken from pencil_as1
   DArr<int> ns, ld, msz;
   DArr<long long> voff;
   DArr<double> V, lam;
-  DArr<GemvTTask> t_gemvT;
-  DArr<GemvTask> t_gemv;
   int rows_per_gemv = 512;
   int gemv_cols = 1024;  // column chunk of the split GEMV
-  int gemv_cols_max = 0;
-  DArr<int> nkc;         // column chunks per subdomain
-  DArr<double> wpart_nn; // nkc_max x P partial sums
+  int one_level = 2;     // OneLevelKind of the configuration: 0 AS, 1 AS_PLUS, 2 NN
+  LocalPlan plan_nn;     // V^s with the eigenvalue mask (NN)
+  LocalPlan plan_as;     // U^s = L^-T, triangular (AS / AS+)
+  DArr<double> U;        // AS / AS+ local factors, same layout as V
+  DArr<double> wpart_nn; // kcmax x P partial sums
 
   // A- modes
   int nneg = 0;
@@ -253,6 +265,7 @@ void run_pcg(Ctx& c, const double* b_dev, double rtol, int maxit, awg_solve_repo
 void finalize_factors(Ctx& c);  // task lists, A- modes, inverses, work buffers
 void build_core(Ctx& c);        // INEX core LU
 void run_setup(Ctx& c, const awg_config& cfg);  // setup.cu
+void build_local_cholesky(Ctx& c);              // setup.cu: AS / AS+ factors U^s = L^-T
 // wbuild.cu: batched inner PCGs for W (modes = (s, k) list, ascending)
 void build_w_batched(Ctx& c, struct cublasContext* h, const std::vector<std::pair<int, int>>& modes, int maxit,
                      double rtol, std::vector<int>& iters, int max_block);

@@ -96,7 +96,10 @@ __global__ void k_prolong(const int* __restrict__ gate, int n, const int* __rest
 // One CTA per (s, column chunk); the scaled restriction is staged once in shared
 // memory; one warp per column, 16-byte coalesced loads down the column, 4 loads
 // in flight per lane.
-template <int NW>
+// TRI = true: the AS / AS+ one-level (Cholesky factor form, preconditioner.cpp:43-46):
+// V is U^s = L^-T (upper triangular, zeros below the diagonal stored), column j
+// is read over rows 0..j only, no D^s and no eigenvalue division (lam = nullptr).
+template <int NW, bool TRI>
 __global__ void __launch_bounds__(NW * 32) k_nn_gemvT(const int* __restrict__ gate, const GemvTTask* __restrict__ tasks,
                                                    const double* __restrict__ V, const long long* __restrict__ voff,
                                                    const int* __restrict__ ns, const int* __restrict__ ld,
@@ -108,13 +111,14 @@ __global__ void __launch_bounds__(NW * 32) k_nn_gemvT(const int* __restrict__ ga
   const GemvTTask t = tasks[blockIdx.x];
   const int s = t.s, n = ns[s], L = ld[s];
   const long long p0 = poff[s];
-  for (int i = threadIdx.x; i < L; i += blockDim.x) sx[i] = (i < n) ? __ldg(x + pidx[p0 + i]) * ds[p0 + i] : 0.0;
+  for (int i = threadIdx.x; i < L; i += blockDim.x)
+    sx[i] = (i < n) ? (ds ? __ldg(x + pidx[p0 + i]) * ds[p0 + i] : __ldg(x + pidx[p0 + i])) : 0.0;
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double* Vs = V + voff[s];
   const double2* sx2 = reinterpret_cast<const double2*>(sx);
-  const int npair = L >> 1;
   for (int j = t.j0 + warp; j < t.j1; j += NW) {
+    const int npair = TRI ? min(L >> 1, (j >> 1) + 1) : (L >> 1);
     const double2* col = reinterpret_cast<const double2*>(Vs + (size_t)j * L);
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     int q = lane;
@@ -133,7 +137,7 @@ __global__ void __launch_bounds__(NW * 32) k_nn_gemvT(const int* __restrict__ ga
       a0 = fma(v0.x, x0.x, a0); a0 = fma(v0.y, x0.y, a0);
     }
     const double sum = warp_sum((a0 + a1) + (a2 + a3));
-    if (lane == 0) uh[p0 + j] = sum / lam[p0 + j];
+    if (lane == 0) uh[p0 + j] = TRI ? sum : sum / lam[p0 + j];
   }
 }
 
@@ -198,7 +202,7 @@ __global__ void k_prolong_nn(const int* __restrict__ gate, int n, const int* __r
       const int kcs = nkc[psub[p]];
       double w = 0.0;
       for (int kc = 0; kc < kcs; ++kc) w += part[(size_t)kc * P + p];
-      acc += w * ds[p];
+      acc += ds ? w * ds[p] : w;
     }
     y[i] = acc;
   }
@@ -534,32 +538,45 @@ static size_t nn_smem(Ctx& c) {
   const size_t smem = size_t(ldmax) * sizeof(double);
   static size_t configured = 0;
   if (smem > configured) {
-    AWG_CUDA(cudaFuncSetAttribute(k_nn_gemvT<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    AWG_CUDA(cudaFuncSetAttribute(k_nn_gemvT<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    AWG_CUDA(cudaFuncSetAttribute(k_nn_gemvT<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     configured = smem;
   }
   return smem;
 }
 
+// The one-level factor in use: NN (V^s, eigenvalue mask, D^s) or AS/AS+ (U^s = L^-T).
+static const LocalPlan& plan(const Ctx& c) { return c.one_level == 2 ? c.plan_nn : c.plan_as; }
+
 void nn_gemvT(Ctx& c, const double* x, const int* gate) {
   const size_t smem = nn_smem(c);
-  if (!c.t_gemvT.n) return;
-  k_nn_gemvT<8><<<int(c.t_gemvT.n), 256, smem, c.stream>>>(gate, c.t_gemvT.p, c.V.p, c.voff.p, c.ns.p, c.ld.p,
-                                                           c.poff.p, c.pidx.p, c.ds.p, x, c.lam.p, c.uh.p);
+  const LocalPlan& pl = plan(c);
+  if (!pl.tT.n) return;
+  if (c.one_level == 2)
+    k_nn_gemvT<8, false><<<int(pl.tT.n), 256, smem, c.stream>>>(gate, pl.tT.p, c.V.p, c.voff.p, c.ns.p, c.ld.p,
+                                                                c.poff.p, c.pidx.p, c.ds.p, x, c.lam.p, c.uh.p);
+  else
+    k_nn_gemvT<8, true><<<int(pl.tT.n), 256, smem, c.stream>>>(gate, pl.tT.p, c.U.p, c.voff.p, c.ns.p, c.ld.p,
+                                                               c.poff.p, c.pidx.p, nullptr, x, nullptr, c.uh.p);
   ++c.launches;
   check_launch("nn_gemvT");
 }
 
 void nn_gemv(Ctx& c, const int* gate) {
-  if (!c.t_gemv.n) return;
-  k_nn_gemv<<<int(c.t_gemv.n), kThreads, size_t(c.gemv_cols_max) * sizeof(double), c.stream>>>(
-      gate, c.t_gemv.p, c.V.p, c.voff.p, c.ns.p, c.ld.p, c.poff.p, c.P, c.uh.p, c.wpart_nn.p);
+  const LocalPlan& pl = plan(c);
+  if (!pl.t.n) return;
+  k_nn_gemv<<<int(pl.t.n), kThreads, size_t(pl.cols_max) * sizeof(double), c.stream>>>(
+      gate, pl.t.p, c.one_level == 2 ? c.V.p : c.U.p, c.voff.p, c.ns.p, c.ld.p, c.poff.p, c.P, c.uh.p,
+      c.wpart_nn.p);
   ++c.launches;
   check_launch("nn_gemv");
 }
 
 void nn_prolong(Ctx& c, double* y, const int* gate) {
+  const LocalPlan& pl = plan(c);
   k_prolong_nn<<<grid_for(c, c.n), kThreads, 0, c.stream>>>(gate, c.n, c.own_off.p, c.own_pos.p, c.psub.p,
-                                                           c.nkc.p, c.P, c.wpart_nn.p, c.ds.p, y);
+                                                           pl.nkc.p, c.P, c.wpart_nn.p,
+                                                           c.one_level == 2 ? c.ds.p : nullptr, y);
   ++c.launches;
   check_launch("prolong_nn");
 }

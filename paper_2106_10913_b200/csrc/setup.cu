@@ -369,7 +369,161 @@ void pivoted_factor(Ctx& c, DArr<double>& G, int n, int exact, CoarseFactor& f, 
   AWG_CUDA(cudaStreamSynchronize(c.stream));
 }
 
+__global__ void k_identity(int n, int ld, double* __restrict__ M) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= (long long)n * n) return;
+  const int i = int(t % n), j = int(t / n);
+  M[i + (size_t)j * ld] = (i == j) ? 1.0 : 0.0;
+}
+
+// Dense local blocks of subdomain s on stream q (scratch per stream):
+//   a_block      R^s A R^s^T                                      splitting.cpp:161-173
+//   aplus_block  R^s A R^s^T + neighbours' restricted V-|L-|V-^T  splitting.cpp:175-209
+//   weighted     Ds^-1 (B^s + V-|L-|V-^T) Ds^-1, symmetrized       coarse.cpp:69-96
+struct LocalBlocks {
+  Ctx& c;
+  Solvers& sv;
+  std::vector<std::vector<int>> nb;  // neighbours (self included, ascending), splitting.cpp:96-104
+  std::vector<int> q_of;             // strictly negative mode count per subdomain
+  DArr<double> G1[Solvers::S], G2[Solvers::S];
+  std::vector<DArr<int>> d_ct, d_ck;
+  std::vector<DArr<double>> d_cw;
+
+  LocalBlocks(Ctx& cc, Solvers& s) : c(cc), sv(s), d_ct(cc.N), d_ck(cc.N), d_cw(cc.N) {
+    const int N = c.N;
+    nb.assign(N, {});
+    std::vector<std::vector<int>> subs(c.n);
+    for (int t = 0; t < N; ++t)
+      for (long long p = c.h_poff[t]; p < c.h_poff[t + 1]; ++p) subs[c.h_pidx[p]].push_back(t);
+    std::vector<char> touch(size_t(N) * N, 0);
+    for (int i = 0; i < c.n; ++i)
+      for (int a : subs[i])
+        for (int b : subs[i]) touch[size_t(a) * N + b] = 1;
+    for (int a = 0; a < N; ++a)
+      for (int b = 0; b < N; ++b)
+        if (touch[size_t(a) * N + b]) nb[a].push_back(b);
+    q_of.resize(N);
+    for (int t = 0; t < N; ++t) q_of[t] = c.h_m[t] - c.h_nzero[t];
+    int ldmax = 1, qn_max = 1;
+    for (int t = 0; t < N; ++t) {
+      ldmax = std::max(ldmax, c.h_ld[t]);
+      int qn = 0;
+      for (int u : nb[t]) qn += q_of[u];
+      qn_max = std::max(qn_max, qn);
+    }
+    for (int i = 0; i < Solvers::S; ++i) {
+      G1[i].alloc(size_t(ldmax) * qn_max);
+      G2[i].alloc(size_t(ldmax) * qn_max);
+    }
+  }
+
+  void a_block(int s, int q, double* M) {
+    const int n = c.h_ns[s], ld = c.h_ld[s];
+    AWG_CUDA(cudaMemsetAsync(M, 0, sizeof(double) * ld * n, sv.st[q]));
+    k_assemble<<<(n + kThreads - 1) / kThreads, kThreads, 0, sv.st[q]>>>(s, n, ld, c.poff.p, c.pidx.p, c.rp.p,
+                                                                          c.ci.p, c.va.p, c.emult.p, 1, M);
+    ++c.launches;
+  }
+
+  void aplus_block(int s, int q, double* M) {
+    a_block(s, q, M);
+    const int n = c.h_ns[s], ld = c.h_ld[s];
+    std::vector<int> ct, ck;
+    std::vector<double> cw;
+    for (int t : nb[s])
+      for (int k = 0; k < q_of[t]; ++k) {
+        ct.push_back(t);
+        ck.push_back(k);
+        cw.push_back(-c.h_lam[c.h_poff[t] + k]);
+      }
+    const int qn = int(ct.size());
+    if (qn == 0) return;
+    d_ct[s].upload(ct, sv.st[q]);
+    d_ck[s].upload(ck, sv.st[q]);
+    d_cw[s].upload(cw, sv.st[q]);
+    dim3 g((n + kThreads - 1) / kThreads, qn);
+    k_gather_neighbour_modes<<<g, kThreads, 0, sv.st[q]>>>(n, ld, c.pidx.p + c.h_poff[s], qn, d_ct[s].p, d_ck[s].p,
+                                                            d_cw[s].p, c.V.p, c.voff.p, c.ns.p, c.ld.p, c.poff.p,
+                                                            c.pidx.p, G1[q].p, G2[q].p);
+    ++c.launches;
+    const double one = 1.0;
+    AWG_BLAS(cublasDgemm(sv.blas[q], CUBLAS_OP_N, CUBLAS_OP_T, n, n, qn, &one, G2[q].p, ld, G1[q].p, ld, &one, M, ld));
+  }
+
+  void weighted(int s, int q, double* M) {
+    const int n = c.h_ns[s], ld = c.h_ld[s];
+    AWG_CUDA(cudaMemsetAsync(M, 0, sizeof(double) * ld * n, sv.st[q]));
+    k_assemble<<<(n + kThreads - 1) / kThreads, kThreads, 0, sv.st[q]>>>(s, n, ld, c.poff.p, c.pidx.p, c.rp.p,
+                                                                          c.ci.p, c.va.p, c.emult.p, 0, M);
+    ++c.launches;
+    const int qs = q_of[s];
+    const double* Vs = c.V.p + c.h_voff[s];
+    if (qs > 0) {
+      dim3 g((n + kThreads - 1) / kThreads, qs);
+      k_scale_cols<<<g, kThreads, 0, sv.st[q]>>>(n, qs, ld, Vs, c.lam.p + c.h_poff[s], G1[q].p);
+      ++c.launches;
+      const double one = 1.0;
+      AWG_BLAS(cublasDgemm(sv.blas[q], CUBLAS_OP_N, CUBLAS_OP_T, n, n, qs, &one, G1[q].p, ld, Vs, ld, &one, M, ld));
+    }
+    k_weight_sym<<<int(((long long)n * n + kThreads - 1) / kThreads), kThreads, 0, sv.st[q]>>>(
+        n, ld, c.pidx.p + c.h_poff[s], c.mult.p, M);
+    ++c.launches;
+  }
+};
+
+// AS / AS+ one-level factors (OneLevel ctor, preconditioner.cpp:20-30):
+// M^s = R A R^T (AS) or R A+ R^T (AS+), M^s = L L^T (cusolver potrf),
+// U^s = L^-T (triangular solve against the identity), stored in c.U.
+void local_cholesky(Ctx& c, Solvers& sv, LocalBlocks& lb) {
+  const int N = c.N;
+  c.U.alloc(size_t(c.h_voff[N]));
+  c.U.zero(c.stream);
+  AWG_CUDA(cudaStreamSynchronize(c.stream));
+  size_t blk_max = 1;
+  int lw_max = 1;
+  for (int s = 0; s < N; ++s) {
+    blk_max = std::max(blk_max, size_t(c.h_ld[s]) * c.h_ns[s]);
+    int lw = 0;
+    AWG_SOLVER(cusolverDnDpotrf_bufferSize(sv.sol[0], CUBLAS_FILL_MODE_LOWER, c.h_ns[s], nullptr, c.h_ld[s], &lw));
+    lw_max = std::max(lw_max, lw);
+  }
+  std::vector<DArr<double>> T(Solvers::S);
+  for (int i = 0; i < Solvers::S; ++i) {
+    T[i].alloc(blk_max);
+    sv.work[i].alloc(size_t(lw_max) + 1);
+  }
+  sv.info.zero(nullptr);
+  AWG_CUDA(cudaDeviceSynchronize());
+  for (int s = 0; s < N; ++s) {
+    const int q = s % Solvers::S;
+    const int n = c.h_ns[s], ld = c.h_ld[s];
+    if (c.one_level == 0) lb.a_block(s, q, T[q].p);
+    else lb.aplus_block(s, q, T[q].p);
+    AWG_SOLVER(cusolverDnDpotrf(sv.sol[q], CUBLAS_FILL_MODE_LOWER, n, T[q].p, ld, sv.work[q].p, lw_max,
+                                sv.info.p + s));
+    double* Us = c.U.p + c.h_voff[s];
+    k_identity<<<int(((long long)n * n + kThreads - 1) / kThreads), kThreads, 0, sv.st[q]>>>(n, ld, Us);
+    ++c.launches;
+    const double one = 1.0;
+    AWG_BLAS(cublasDtrsm(sv.blas[q], CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, n, n,
+                         &one, T[q].p, ld, Us, ld));
+  }
+  sv.sync();
+  std::vector<int> info(N);
+  AWG_CUDA(cudaMemcpy(info.data(), sv.info.p, sizeof(int) * N, cudaMemcpyDeviceToHost));
+  for (int s = 0; s < N; ++s)
+    if (info[s] > 0)
+      c.fail(AWG_E_NOT_SPD, "matrix not spd: non-positive pivot at index " + std::to_string(info[s] - 1),
+             info[s] - 1);
+}
 }  // namespace
+
+void build_local_cholesky(Ctx& c) {
+  Solvers sv;
+  sv.init(c.N);
+  LocalBlocks lb(c, sv);
+  local_cholesky(c, sv, lb);
+}
 
 void run_setup(Ctx& c, const awg_config& cfg) {
   const double t_start = now_ms();
@@ -443,148 +597,130 @@ void run_setup(Ctx& c, const awg_config& cfg) {
   }
   c.t_setup_ms[0] = now_ms() - t0;
 
-  // ---- 4. NN pencils + 5. selection ---------------------------------------------
+  // ---- 4. pencils + 5. selection (coarse.cpp:98-130) --------------------------------
+  // NN / AS+: pencil_nn = (weighted A+^s, R A+ R^T); AS: pencil_as1 = (weighted A+^s,
+  // R A R^T) below 1/tau_flat and pencil_as2 = (R A R^T, R A+ R^T) below tau_sharp.
   t0 = now_ms();
+  c.one_level = cfg.one_level;
   std::vector<int> ks(N, 0);
-  DArr<double> plam;
-  plam.alloc(c.P);
-  std::vector<DArr<double>> Ycol(N);  // eigenvectors kept until the coarse layout is known
+  LocalBlocks lb(c, sv);
   if (cfg.use_coarse) {
-    // neighbour lists (Splitting ctor, splitting.cpp:96-104): s ~ t when they share a dof
-    std::vector<std::vector<int>> nb(N);
-    {
-      std::vector<std::vector<int>> subs(c.n);
-      for (int s = 0; s < N; ++s)
-        for (long long p = c.h_poff[s]; p < c.h_poff[s + 1]; ++p) subs[c.h_pidx[p]].push_back(s);
-      std::vector<char> touch(size_t(N) * N, 0);
-      for (int i = 0; i < c.n; ++i)
-        for (int a : subs[i])
-          for (int b : subs[i]) touch[size_t(a) * N + b] = 1;
-      for (int s = 0; s < N; ++s)
-        for (int t = 0; t < N; ++t)
-          if (touch[size_t(s) * N + t]) nb[s].push_back(t);
-    }
-    std::vector<int> q_of(N);
-    for (int s = 0; s < N; ++s) q_of[s] = c.h_m[s] - c.h_nzero[s];
-    // per-stream workspaces
-    int lw_max = 0;
+    const bool as = (cfg.one_level == 0);
+    int lw_max = 1;
+    size_t blk_max = 1;
     for (int s = 0; s < N; ++s) {
       int lw = 0;
       AWG_SOLVER(cusolverDnDsygvd_bufferSize(sv.sol[0], CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR,
                                              CUBLAS_FILL_MODE_LOWER, c.h_ns[s], nullptr, c.h_ld[s], nullptr,
                                              c.h_ld[s], nullptr, &lw));
       lw_max = std::max(lw_max, lw);
-    }
-    size_t blk_max = 0;
-    int qn_max = 1;
-    for (int s = 0; s < N; ++s) {
       blk_max = std::max(blk_max, size_t(c.h_ld[s]) * c.h_ns[s]);
-      int qn = 0;
-      for (int t : nb[s]) qn += q_of[t];
-      qn_max = std::max(qn_max, qn);
     }
-    std::vector<DArr<double>> MA(Solvers::S), MB(Solvers::S), G1(Solvers::S), G2(Solvers::S);
-    int nmax_ld = *std::max_element(c.h_ld.begin(), c.h_ld.end());
+    const int nbuf = as ? 4 : 2;
+    std::vector<DArr<double>> buf(Solvers::S * nbuf);
     for (int i = 0; i < Solvers::S; ++i) {
       sv.work[i].alloc(size_t(lw_max) + 1);
-      MA[i].alloc(blk_max);
-      MB[i].alloc(blk_max);
-      G1[i].alloc(size_t(nmax_ld) * qn_max);
-      G2[i].alloc(size_t(nmax_ld) * qn_max);
+      for (int b = 0; b < nbuf; ++b) buf[i * nbuf + b].alloc(blk_max);
     }
-    std::vector<std::vector<int>> ct(N), ck(N);
-    std::vector<std::vector<double>> cw(N);
-    std::vector<DArr<int>> d_ct(N), d_ck(N);
-    std::vector<DArr<double>> d_cw(N);
+    DArr<double> plam, plam2;
+    plam.alloc(c.P);
+    if (as) plam2.alloc(c.P);
+    std::vector<DArr<double>> Ycol(N), Ycol2(N);
+    DArr<int> info2;
+    info2.alloc(N);
+    info2.zero(nullptr);
     sv.info.zero(nullptr);
     AWG_CUDA(cudaDeviceSynchronize());
     for (int s = 0; s < N; ++s) {
       const int q = s % Solvers::S;
       cudaStream_t st = sv.st[q];
       const int n = c.h_ns[s], ld = c.h_ld[s];
-      const double* Vs = c.V.p + c.h_voff[s];
-      // MA = B^s + V- |L-| V-^T, weighted and symmetrized (coarse.cpp:69-96)
-      AWG_CUDA(cudaMemsetAsync(MA[q].p, 0, sizeof(double) * ld * n, st));
-      k_assemble<<<(n + kThreads - 1) / kThreads, kThreads, 0, st>>>(s, n, ld, c.poff.p, c.pidx.p, c.rp.p, c.ci.p,
-                                                                      c.va.p, c.emult.p, 0, MA[q].p);
-      ++c.launches;
-      const int qs = q_of[s];
-      if (qs > 0) {
-        dim3 g((n + kThreads - 1) / kThreads, qs);
-        k_scale_cols<<<g, kThreads, 0, st>>>(n, qs, ld, Vs, c.lam.p + c.h_poff[s], G1[q].p);
-        ++c.launches;
-        const double one = 1.0;
-        AWG_BLAS(cublasDgemm(sv.blas[q], CUBLAS_OP_N, CUBLAS_OP_T, n, n, qs, &one, G1[q].p, ld, Vs, ld, &one,
-                             MA[q].p, ld));
-      }
-      k_weight_sym<<<int(((long long)n * n + kThreads - 1) / kThreads), kThreads, 0, st>>>(
-          n, ld, c.pidx.p + c.h_poff[s], c.mult.p, MA[q].p);
-      ++c.launches;
-      // MB = R A R^T + sum_t shared-row rank-q_t updates (splitting.cpp:175-209)
-      AWG_CUDA(cudaMemsetAsync(MB[q].p, 0, sizeof(double) * ld * n, st));
-      k_assemble<<<(n + kThreads - 1) / kThreads, kThreads, 0, st>>>(s, n, ld, c.poff.p, c.pidx.p, c.rp.p, c.ci.p,
-                                                                      c.va.p, c.emult.p, 1, MB[q].p);
-      ++c.launches;
-      for (int t : nb[s])
-        for (int k = 0; k < q_of[t]; ++k) {
-          ct[s].push_back(t);
-          ck[s].push_back(k);
-          cw[s].push_back(-c.h_lam[c.h_poff[t] + k]);
-        }
-      const int qn = int(ct[s].size());
-      if (qn > 0) {
-        d_ct[s].upload(ct[s], st);
-        d_ck[s].upload(ck[s], st);
-        d_cw[s].upload(cw[s], st);
-        dim3 g((n + kThreads - 1) / kThreads, qn);
-        k_gather_neighbour_modes<<<g, kThreads, 0, st>>>(n, ld, c.pidx.p + c.h_poff[s], qn, d_ct[s].p, d_ck[s].p,
-                                                          d_cw[s].p, c.V.p, c.voff.p, c.ns.p, c.ld.p, c.poff.p,
-                                                          c.pidx.p, G1[q].p, G2[q].p);
-        ++c.launches;
-        const double one = 1.0;
-        AWG_BLAS(cublasDgemm(sv.blas[q], CUBLAS_OP_N, CUBLAS_OP_T, n, n, qn, &one, G2[q].p, ld, G1[q].p, ld, &one,
-                             MB[q].p, ld));
-      }
-      // generalized eigenproblem MA y = lambda MB y  (dense.cpp:211-224)
-      AWG_SOLVER(cusolverDnDsygvd(sv.sol[q], CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n,
-                                  MA[q].p, ld, MB[q].p, ld, plam.p + c.h_poff[s], sv.work[q].p, lw_max,
-                                  sv.info.p + s));
-      // keep the low end of the spectrum's eigenvectors (selection happens after)
+      double* MA = buf[q * nbuf].p;
+      double* MB = buf[q * nbuf + 1].p;
+      lb.weighted(s, q, MA);
       int keep = n;
       if (cfg.fixed_k > 0) keep = std::min(n, std::max(cfg.fixed_k, c.h_m[s]) + 64);
-      Ycol[s].alloc(size_t(ld) * keep);
-      AWG_CUDA(cudaMemcpyAsync(Ycol[s].p, MA[q].p, sizeof(double) * ld * keep, cudaMemcpyDeviceToDevice, st));
-      // MA/MB of this stream are reused by subdomain s + S: stream order protects them
+      if (!as) {
+        lb.aplus_block(s, q, MB);
+        AWG_SOLVER(cusolverDnDsygvd(sv.sol[q], CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER,
+                                    n, MA, ld, MB, ld, plam.p + c.h_poff[s], sv.work[q].p, lw_max, sv.info.p + s));
+        Ycol[s].alloc(size_t(ld) * keep);
+        AWG_CUDA(cudaMemcpyAsync(Ycol[s].p, MA, sizeof(double) * ld * keep, cudaMemcpyDeviceToDevice, st));
+      } else {
+        double* AB = buf[q * nbuf + 2].p;
+        double* AB2 = buf[q * nbuf + 3].p;
+        lb.aplus_block(s, q, MB);
+        lb.a_block(s, q, AB);
+        AWG_CUDA(cudaMemcpyAsync(AB2, AB, sizeof(double) * ld * n, cudaMemcpyDeviceToDevice, st));
+        AWG_SOLVER(cusolverDnDsygvd(sv.sol[q], CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER,
+                                    n, MA, ld, AB, ld, plam.p + c.h_poff[s], sv.work[q].p, lw_max, sv.info.p + s));
+        AWG_SOLVER(cusolverDnDsygvd(sv.sol[q], CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER,
+                                    n, AB2, ld, MB, ld, plam2.p + c.h_poff[s], sv.work[q].p, lw_max,
+                                    info2.p + s));
+        Ycol[s].alloc(size_t(ld) * n);
+        Ycol2[s].alloc(size_t(ld) * n);
+        AWG_CUDA(cudaMemcpyAsync(Ycol[s].p, MA, sizeof(double) * ld * n, cudaMemcpyDeviceToDevice, st));
+        AWG_CUDA(cudaMemcpyAsync(Ycol2[s].p, AB2, sizeof(double) * ld * n, cudaMemcpyDeviceToDevice, st));
+      }
     }
     sv.sync();
-    std::vector<int> info(N);
+    std::vector<int> info(N), i2(N);
     AWG_CUDA(cudaMemcpy(info.data(), sv.info.p, sizeof(int) * N, cudaMemcpyDeviceToHost));
-    for (int s = 0; s < N; ++s) {
-      if (info[s] > c.h_ns[s])
-        c.fail(AWG_E_NOT_SPD, "matrix not spd: non-positive pivot at index " + std::to_string(info[s] - c.h_ns[s] - 1),
-               info[s] - c.h_ns[s] - 1);
-      if (info[s] != 0) c.fail(AWG_E_NO_CONVERGENCE, "generalized_sym_eig: eigensolver failed");
-    }
-    DArr<int> dks;
+    AWG_CUDA(cudaMemcpy(i2.data(), info2.p, sizeof(int) * N, cudaMemcpyDeviceToHost));
+    for (int s = 0; s < N; ++s)
+      for (int v : {info[s], i2[s]}) {
+        if (v > c.h_ns[s])
+          c.fail(AWG_E_NOT_SPD, "matrix not spd: non-positive pivot at index " + std::to_string(v - c.h_ns[s] - 1),
+                 v - c.h_ns[s] - 1);
+        if (v != 0) c.fail(AWG_E_NO_CONVERGENCE, "generalized_sym_eig: eigensolver failed");
+      }
+    DArr<int> dks, dks2;
     dks.alloc(N);
-    k_select<<<(N + 127) / 128, 128, 0, c.stream>>>(N, c.poff.p, plam.p, c.msz.p, cfg.tau_sharp, cfg.fixed_k,
-                                                    dks.p);
-    ++c.launches;
-    ks = dks.download(c.stream);
-    c.h_plam = plam.download(c.stream);
+    if (!as) {
+      const double tau = cfg.one_level == 1 ? 1.0 / cfg.tau_flat : cfg.tau_sharp;
+      k_select<<<(N + 127) / 128, 128, 0, c.stream>>>(N, c.poff.p, plam.p, c.msz.p, tau, cfg.fixed_k, dks.p);
+      ++c.launches;
+      ks = dks.download(c.stream);
+      c.h_plam = plam.download(c.stream);
+    } else {
+      dks2.alloc(N);
+      k_select<<<(N + 127) / 128, 128, 0, c.stream>>>(N, c.poff.p, plam.p, c.msz.p, 1.0 / cfg.tau_flat, 0, dks.p);
+      k_select<<<(N + 127) / 128, 128, 0, c.stream>>>(N, c.poff.p, plam2.p, c.msz.p, cfg.tau_sharp, 0, dks2.p);
+      c.launches += 2;
+      std::vector<int> m1 = dks.download(c.stream), m2 = dks2.download(c.stream);
+      for (int s = 0; s < N; ++s) ks[s] = m1[s] + m2[s];
+      c.h_plam = plam.download(c.stream);
+      c.h_plam2 = plam2.download(c.stream);
+      c.h_ks_as1 = m1;
+    }
+    c.h_ks = ks;
+    // coarse layout, task lists, A- modes, work buffers
+    finalize_factors(c);
+    c.Y.alloc(size_t(std::max<long long>(c.h_yoff[N], 1)));
+    for (int s = 0; s < N; ++s) {
+      if (ks[s] == 0) continue;
+      const size_t ld = c.h_ld[s];
+      if (!as) {
+        if (Ycol[s].n < ld * ks[s]) c.fail(AWG_E_STATE, "setup: fixed-k cluster extension beyond the kept eigenvectors");
+        AWG_CUDA(cudaMemcpyAsync(c.Y.p + c.h_yoff[s], Ycol[s].p, sizeof(double) * ld * ks[s], cudaMemcpyDeviceToDevice,
+                                 c.stream));
+      } else {  // [as1 low modes, as2 low modes] (coarse.cpp:127-130 push order)
+        const int m1 = c.h_ks_as1[s], m2 = ks[s] - m1;
+        if (m1)
+          AWG_CUDA(cudaMemcpyAsync(c.Y.p + c.h_yoff[s], Ycol[s].p, sizeof(double) * ld * m1, cudaMemcpyDeviceToDevice,
+                                   c.stream));
+        if (m2)
+          AWG_CUDA(cudaMemcpyAsync(c.Y.p + c.h_yoff[s] + ld * m1, Ycol2[s].p, sizeof(double) * ld * m2,
+                                   cudaMemcpyDeviceToDevice, c.stream));
+      }
+    }
+    AWG_CUDA(cudaStreamSynchronize(c.stream));
+  } else {
+    c.h_ks = ks;
+    finalize_factors(c);
+    c.Y.alloc(1);
   }
-  c.h_ks = ks;
-  // coarse layout, task lists, A- modes, work buffers
-  finalize_factors(c);
-  c.Y.alloc(size_t(std::max<long long>(c.h_yoff[N], 1)));
-  for (int s = 0; s < N; ++s) {
-    if (ks[s] == 0) continue;
-    if (Ycol[s].n < size_t(c.h_ld[s]) * ks[s])
-      c.fail(AWG_E_STATE, "setup: fixed-k cluster extension beyond the kept eigenvectors");
-    AWG_CUDA(cudaMemcpyAsync(c.Y.p + c.h_yoff[s], Ycol[s].p, sizeof(double) * c.h_ld[s] * ks[s],
-                             cudaMemcpyDeviceToDevice, c.stream));
-  }
-  Ycol.clear();
+  if (cfg.one_level != 2) local_cholesky(c, sv, lb);
   AWG_CUDA(cudaStreamSynchronize(c.stream));
   c.t_setup_ms[1] = now_ms() - t0;
 

@@ -434,26 +434,39 @@ struct BlockOps {
                                               k.boff.p, nullptr, k.WS.p, Y, done);
     c.launches += 3;
   }
+  // OneLevel::apply on the block: NN = R^T D V mask(1/lam) V^T D R, AS/AS+ =
+  // R^T U U^T R with U = L^-T (triangular products as DTRMM)
   void h1(const double* X, double* Y, const int* done) {
-    kb_gather<<<grid_p(), kT, 0, c.stream>>>(c.P, c.psub.p, c.poff.p, c.pidx.p, c.ld.p, k.boff.p, c.ds.p, k.ld, X,
-                                             k.XS.p, done);
+    const bool nn = (c.one_level == 2);
+    kb_gather<<<grid_p(), kT, 0, c.stream>>>(c.P, c.psub.p, c.poff.p, c.pidx.p, c.ld.p, k.boff.p,
+                                             nn ? c.ds.p : nullptr, k.ld, X, k.XS.p, done);
     const double one = 1.0, zero = 0.0;
     for (int s = 0; s < c.N; ++s) {
       const int n = c.h_ns[s], L = c.h_ld[s];
-      const double* Vs = c.V.p + c.h_voff[s];
-      AWG_BLAS(cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, n, k.B, n, &one, Vs, L, k.XS.p + k.h_boff[s], L, &zero,
-                           k.WS.p + k.h_boff[s], L));
+      if (nn) {
+        AWG_BLAS(cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, n, k.B, n, &one, c.V.p + c.h_voff[s], L,
+                             k.XS.p + k.h_boff[s], L, &zero, k.WS.p + k.h_boff[s], L));
+      } else {
+        AWG_BLAS(cublasDtrmm(h, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, n, k.B,
+                             &one, c.U.p + c.h_voff[s], L, k.XS.p + k.h_boff[s], L, k.WS.p + k.h_boff[s], L));
+      }
     }
-    kb_mask<<<grid_p(), kT, 0, c.stream>>>(c.P, c.psub.p, c.poff.p, c.ld.p, k.boff.p, c.msz.p, c.lam.p, k.B, k.WS.p);
+    if (nn)
+      kb_mask<<<grid_p(), kT, 0, c.stream>>>(c.P, c.psub.p, c.poff.p, c.ld.p, k.boff.p, c.msz.p, c.lam.p, k.B,
+                                             k.WS.p);
     for (int s = 0; s < c.N; ++s) {
       const int n = c.h_ns[s], L = c.h_ld[s];
-      const double* Vs = c.V.p + c.h_voff[s];
-      AWG_BLAS(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, n, k.B, n, &one, Vs, L, k.WS.p + k.h_boff[s], L, &zero,
-                           k.XS.p + k.h_boff[s], L));
+      if (nn) {
+        AWG_BLAS(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, n, k.B, n, &one, c.V.p + c.h_voff[s], L,
+                             k.WS.p + k.h_boff[s], L, &zero, k.XS.p + k.h_boff[s], L));
+      } else {
+        AWG_BLAS(cublasDtrmm(h, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, n, k.B,
+                             &one, c.U.p + c.h_voff[s], L, k.WS.p + k.h_boff[s], L, k.XS.p + k.h_boff[s], L));
+      }
     }
     kb_prolong<<<grid_n(), kT, 0, c.stream>>>(c.n, k.ld, c.own_off.p, c.own_pos.p, c.psub.p, c.poff.p, c.ld.p,
-                                              k.boff.p, c.ds.p, k.XS.p, Y, done);
-    c.launches += 3;
+                                              k.boff.p, nn ? c.ds.p : nullptr, k.XS.p, Y, done);
+    c.launches += nn ? 3 : 2;
   }
   // TwoLevel::apply (preconditioner.cpp:64-82)
   void h2(const double* X, double* Y, const int* done) {

@@ -24,14 +24,38 @@ def load_golden(case):
 
 
 def golden_with_base(case):
-    """*_exact fixtures store only what differs from the base case."""
+    """Variant fixtures (*_exact, *_additive, *_none) store only what differs
+    from their base case."""
     g, s = load_golden(case)
     d = {k: g[k] for k in g.files}
-    if case.endswith("_exact"):
-        base, _ = load_golden(case[: -len("_exact")])
-        for k in base.files:
-            d.setdefault(k, base[k])
+    if s.get("base"):
+        base, _ = load_golden(s["base"])
+        for k in ("V", "Y", "lam", "pencil_lam"):  # what make_golden.py drops from variants
+            if k not in d:
+                d[k] = base[k]
     return d, s
+
+
+ALL_CASES = ["c1", "c1_exact", "t2d", "t2d_exact", "t2d_additive", "t2d_ov2", "t3d", "t3d_none", "t3d_blocks",
+             "telas"]
+
+
+def case_options(s):
+    """(composition, awg mode) the fixture was generated with (ref_driver args)."""
+    args = s.get("args") or []
+    comp = args[args.index("--comp") + 1] if "--comp" in args else "hybrid"
+    mode = args[args.index("--awg") + 1] if "--awg" in args else "ad"
+    return comp, mode
+
+
+def one_level_of(s):
+    args = s.get("args") or []
+    return args[args.index("--one-level") + 1] if "--one-level" in args else "NN"
+
+
+def omega_of(g):
+    off, idx = g["part_offsets"], g["part_indices"]
+    return [idx[a:b] for a, b in zip(off[:-1], off[1:])]
 
 
 def rel(a, b):

@@ -27,21 +27,30 @@ from paper_2106_10913_b200 import problems  # noqa: E402
 HERE = os.path.dirname(os.path.abspath(__file__))
 REF = os.path.join(ROOT, "oracle", "_ref")
 
-# case -> (problem, driver binary, extra args, export dense pencil matrices)
+# case -> (problem, driver binary, extra args, export dense pencil matrices, base case)
+# Variants store only what differs from their base case (same problem, same
+# B^s eigenpairs and pencils).
 CASES = {
-    "c1": ("c1", "ref_driver", [], False),
-    "c1_exact": ("c1", "ref_driver_fixed", [], False),
-    "t2d": ("t2d", "ref_driver", [], False),
-    "t2d_exact": ("t2d", "ref_driver_fixed", [], False),
-    "t2d_ov2": ("t2d_ov2", "ref_driver", [], False),
-    "t3d": ("t3d", "ref_driver", [], False),
-    "t3d_blocks": ("t3d_blocks", "ref_driver", [], False),
-    "telas": ("telas", "ref_driver", [], True),
+    "c1": ("c1", "ref_driver", [], False, None),
+    "c1_exact": ("c1", "ref_driver_fixed", [], False, "c1"),
+    "t2d": ("t2d", "ref_driver", [], False, None),
+    "t2d_exact": ("t2d", "ref_driver_fixed", [], False, "t2d"),
+    "t2d_additive": ("t2d", "ref_driver", ["--comp", "additive"], False, "t2d"),
+    "t2d_ov2": ("t2d_ov2", "ref_driver", [], False, None),
+    "t3d": ("t3d", "ref_driver", [], False, None),
+    "t3d_none": ("t3d", "ref_driver", ["--awg", "none"], False, "t3d"),
+    "t3d_blocks": ("t3d_blocks", "ref_driver", [], False, None),
+    "telas": ("telas", "ref_driver", [], True, None),
+    # one-level AS / AS+ (Cholesky factor form, preconditioner.cpp:20-30) with their
+    # coarse spaces (coarse.cpp:122-130): Y comes from other pencils, so it is kept
+    "t2d_as": ("t2d", "ref_driver", ["--one-level", "AS", "--tau-flat", "10"], False, "t2d"),
+    "t2d_asplus": ("t2d", "ref_driver", ["--one-level", "AS_PLUS", "--tau-flat", "10"], False, "t2d"),
+    "telas_as": ("telas", "ref_driver", ["--one-level", "AS", "--tau-flat", "10"], False, "telas"),
 }
 
 
 def run_case(name: str) -> str:
-    prob_name, driver, extra, dense = CASES[name]
+    prob_name, driver, extra, dense, base = CASES[name]
     p = problems.make(prob_name)
     with tempfile.TemporaryDirectory() as td:
         prefix = os.path.join(td, prob_name)
@@ -62,10 +71,10 @@ def run_case(name: str) -> str:
             summary = json.load(fh)
     data.pop("Z", None)  # dense Z is derivable from Y; keep fixtures small
     data.pop("v_minus", None)  # derivable from V and n_nonpos
-    if name.endswith("_exact"):
-        # Only the factorization semantics differ from the base case: keep the
-        # coarse factors, the operators fed to them and everything downstream.
-        for k in ["V", "Y", "lam", "pencil_lam"]:  # W depends on K0 (inner H2 solves): kept
+    if base:
+        # B^s eigenpairs and pencil vectors are those of the base case; the
+        # coarse factors, W (inner H2 solves) and everything downstream are kept.
+        for k in ["V", "lam", "pencil_lam"] + ([] if "--one-level" in extra else ["Y"]):
             data.pop(k, None)
     data["A_row_offsets"] = p.row_offsets
     data["A_col_indices"] = p.col_indices
@@ -73,7 +82,7 @@ def run_case(name: str) -> str:
     data["b"] = p.b
     data["part_offsets"] = p.part_offsets()
     data["part_indices"] = p.part_indices()
-    summary.update({"case": name, "problem": prob_name, "driver": driver,
+    summary.update({"case": name, "problem": prob_name, "driver": driver, "base": base, "args": extra,
                     "tau_sharp": p.tau_sharp, "fixed_k": p.fixed_k, "rtol_solve": p.rtol})
     path = os.path.join(HERE, name + ".npz")
     np.savez_compressed(path, **data)

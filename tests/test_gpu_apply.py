@@ -6,26 +6,29 @@ import os
 import numpy as np
 import pytest
 
-from conftest import golden_with_base, rel
+from conftest import ALL_CASES, case_options, golden_with_base, one_level_of, rel
 from oracle import awg_oracle as O
 from paper_2106_10913_b200 import awg
 
 pytestmark = pytest.mark.gpu
 
-CASES = ["c1", "c1_exact", "t2d", "t2d_exact", "t2d_ov2", "t3d", "t3d_blocks", "telas"]
+CASES = ALL_CASES + ["t2d_as", "t2d_asplus", "telas_as"]
+KINDS = {"NN": awg.OneLevelKind.NN, "AS": awg.OneLevelKind.AS, "AS_PLUS": awg.OneLevelKind.AS_PLUS}
+MODES = {"none": awg.AwgMode.NONE, "ad": awg.AwgMode.AD, "hyb": awg.AwgMode.HYB, "inex": awg.AwgMode.INEX}
+COMPS = {"hybrid": awg.Composition.HYBRID, "additive": awg.Composition.ADDITIVE}
 OPS = {"A": awg.Op.A, "Aminus": awg.Op.AMINUS, "Aplus": awg.Op.APLUS, "H1": awg.Op.H1, "Q": awg.Op.Q,
        "QW": awg.Op.QW, "H2": awg.Op.H2, "PI3": awg.Op.PI3, "PI3T": awg.Op.PI3T}
 # Same bound the oracle restatement meets on these inputs (see test_oracle_golden).
 TOL = {"H3inex": 1e-8, "PI3": 1e-10, "PI3T": 1e-10}
 
 
-def make_ctx(g, mode=awg.AwgMode.AD, composition=awg.Composition.HYBRID, lu="reference"):
+def make_ctx(g, mode=awg.AwgMode.AD, composition=awg.Composition.HYBRID, lu="reference", one_level="NN"):
     n = len(g["b"])
     off, idx = g["part_offsets"], g["part_indices"]
     omega = [idx[a:b] for a, b in zip(off[:-1], off[1:])]
     a = awg.SparseSymMatrix(n, g["A_row_offsets"], g["A_col_indices"], g["A_values"])
     ctx = awg.ProblemContext(a, g["b"], awg.Partition(omega, n))
-    cfg = awg.PreconditionerConfig(awg=mode, composition=composition, lu_semantics=lu)
+    cfg = awg.PreconditionerConfig(awg=mode, composition=composition, lu_semantics=lu, one_level=KINDS[one_level])
     ctx.load_factors(cfg, g)
     return ctx
 
@@ -33,7 +36,9 @@ def make_ctx(g, mode=awg.AwgMode.AD, composition=awg.Composition.HYBRID, lu="ref
 @pytest.mark.parametrize("case", CASES)
 def test_operator_parity(case):
     g, s = golden_with_base(case)
-    ctx = make_ctx(g)
+    comp, mode = case_options(s)
+    kind = one_level_of(s)
+    ctx = make_ctx(g, mode=MODES[mode], composition=COMPS[comp], one_level=kind)
     for name, op in OPS.items():
         if "y_" + name not in g:
             continue
@@ -46,7 +51,7 @@ def test_operator_parity(case):
     for mode, key in ((awg.AwgMode.AD, "H3ad"), (awg.AwgMode.HYB, "H3hyb"), (awg.AwgMode.INEX, "H3inex")):
         if "y_" + key not in g:
             continue
-        c2 = make_ctx(g, mode=mode)
+        c2 = make_ctx(g, mode=mode, composition=COMPS[comp], one_level=kind)
         for x, y in zip(g["x_apply"], g["y_" + key]):
             assert rel(c2.apply(awg.Op.H3, x), y) <= TOL.get(key, 1e-11), (case, key)
 
@@ -54,7 +59,8 @@ def test_operator_parity(case):
 @pytest.mark.parametrize("case", CASES)
 def test_pcg_parity(case):
     g, s = golden_with_base(case)
-    ctx = make_ctx(g)
+    comp, mode = case_options(s)
+    ctx = make_ctx(g, mode=MODES[mode], composition=COMPS[comp], one_level=one_level_of(s))
     x, rep = ctx.pcg(g["b"], s["rtol_solve"], 10000)
     assert rep.converged
     assert abs(rep.iterations - s["iterations"]) <= 1

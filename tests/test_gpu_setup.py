@@ -7,12 +7,17 @@ match closely."""
 import numpy as np
 import pytest
 
-from conftest import golden_with_base, rel
+from conftest import case_options, golden_with_base, one_level_of, rel
 from paper_2106_10913_b200 import awg
 
 pytestmark = pytest.mark.gpu
 
 BASE = ["c1", "t2d", "t2d_ov2", "t3d", "t3d_blocks", "telas"]
+
+
+KINDS = {"NN": awg.OneLevelKind.NN, "AS": awg.OneLevelKind.AS, "AS_PLUS": awg.OneLevelKind.AS_PLUS}
+COMPS = {"hybrid": awg.Composition.HYBRID, "additive": awg.Composition.ADDITIVE}
+MODES = {"none": awg.AwgMode.NONE, "ad": awg.AwgMode.AD}
 
 
 def setup_ctx(g, s, rrf="reference"):
@@ -21,7 +26,9 @@ def setup_ctx(g, s, rrf="reference"):
     omega = [idx[a:b] for a, b in zip(off[:-1], off[1:])]
     a = awg.SparseSymMatrix(n, g["A_row_offsets"], g["A_col_indices"], g["A_values"])
     ctx = awg.ProblemContext(a, g["b"], awg.Partition(omega, n))
-    cfg = awg.PreconditionerConfig(rrf_semantics=rrf)
+    comp, mode = case_options(s)
+    cfg = awg.PreconditionerConfig(rrf_semantics=rrf, one_level=KINDS[one_level_of(s)], composition=COMPS[comp],
+                                   awg=MODES[mode], tau_flat=float(s.get("tau_flat", 10.0)))
     if s.get("fixed_k"):
         cfg.fixed_k = int(s["fixed_k"])
     else:
@@ -46,7 +53,7 @@ def test_setup_products(case):
     assert np.allclose(ctx.get("neg_weights"), g["neg_weights"], rtol=1e-9)
 
 
-@pytest.mark.parametrize("case", BASE)
+@pytest.mark.parametrize("case", BASE + ["t2d_additive", "t3d_none", "t2d_as", "t2d_asplus", "telas_as"])
 def test_solve_reference_semantics(case):
     g, s = golden_with_base(case)
     ctx = setup_ctx(g, s)
@@ -54,6 +61,20 @@ def test_solve_reference_semantics(case):
     assert rep.converged
     assert abs(rep.iterations - s["iterations"]) <= 1, (rep.iterations, s["iterations"])
     assert rel(x, g["pcg_x"]) <= 1e-7
+
+
+@pytest.mark.parametrize("case", ["t2d_as", "t2d_asplus", "telas_as"])
+def test_as_setup_products(case):
+    """AS / AS+ coarse spaces: per-subdomain column counts (two pencils for AS,
+    coarse.cpp:127-130) and the coarse dimension match the reference."""
+    g, s = golden_with_base(case)
+    ctx = setup_ctx(g, s)
+    assert np.array_equal(ctx.get("ks"), g["ks"])
+    q = ctx.query()
+    assert q["n0"] == s["n0"] and q["n_minus"] == s["n_minus"]
+    if "pencil_as1_lam" in g:
+        assert np.max(np.abs(ctx.get("pencil_lam") - g["pencil_as1_lam"])) <= 1e-8 * max(
+            1.0, np.max(np.abs(g["pencil_as1_lam"])))
 
 
 @pytest.mark.parametrize("case", ["c1_exact", "t2d_exact"])

@@ -3,10 +3,10 @@ reference's outputs (tests/golden, made by oracle/_ref/ref_driver)."""
 import numpy as np
 import pytest
 
-from conftest import golden_with_base, rel
+from conftest import ALL_CASES, case_options, golden_with_base, omega_of, one_level_of, rel
 from oracle import awg_oracle as O
 
-CASES = ["c1", "c1_exact", "t2d", "t2d_exact", "t2d_ov2", "t3d", "t3d_blocks", "telas"]
+CASES = ALL_CASES + ["t2d_as", "t2d_asplus", "telas_as"]
 # INEX inherits lu_solve's wrong back substitution (dense.cpp:404-409), which is
 # unstable on the 1e7-contrast elasticity analogue: looser bound there.
 TOL = {"H3inex": 1e-8, "PI3": 1e-10, "PI3T": 1e-10}
@@ -24,8 +24,9 @@ def ops(orc):
 @pytest.mark.parametrize("case", CASES)
 def test_applies_match_reference(case):
     g, s = golden_with_base(case)
-    orc = O.AwgOracle(len(g["b"]), g["A_row_offsets"], g["A_col_indices"], g["A_values"],
-                      [g["part_indices"][a:b] for a, b in zip(g["part_offsets"][:-1], g["part_offsets"][1:])], g)
+    comp, _ = case_options(s)
+    orc = O.AwgOracle(len(g["b"]), g["A_row_offsets"], g["A_col_indices"], g["A_values"], omega_of(g), g,
+                      composition=comp, one_level_kind=one_level_of(s))
     for name, fn in ops(orc).items():
         if "y_" + name not in g:
             continue
@@ -50,8 +51,10 @@ def test_rank_revealing_factor_port(case):
 @pytest.mark.parametrize("case", CASES)
 def test_pcg_matches_reference(case):
     g, s = golden_with_base(case)
-    orc = O.oracle_from_golden(type("G", (), {"files": list(g), "__getitem__": lambda self, k: g[k]})())
-    x, rep = O.pcg(lambda v: O.spmv(orc.a, v), lambda v: orc.h3(v, "ad"), g["b"], s["rtol_solve"], 10000)
+    comp, mode = case_options(s)
+    orc = O.AwgOracle(len(g["b"]), g["A_row_offsets"], g["A_col_indices"], g["A_values"], omega_of(g), g,
+                      composition=comp, one_level_kind=one_level_of(s))
+    x, rep = O.pcg(lambda v: O.spmv(orc.a, v), lambda v: orc.h3(v, mode), g["b"], s["rtol_solve"], 10000)
     assert rep.iterations == s["iterations"]
     assert rep.converged == s["converged"]
     assert rel(x, g["pcg_x"]) <= 1e-7
