@@ -45,6 +45,26 @@ SAMPLE_SIZES = {"c1": (20, 4, 1), "c2": (160, 270, 20), "c3": (880, 2200, 30), "
                 "c5": (2200, 3000, 14)}
 
 
+KERNEL_SYMBOL = {"nn_gemvT": "k_nn_gemvT", "nn_gemv": "k_nn_gemv", "spmv": "k_spmv", "w_gemvT": "k_dense_gemvT_part",
+                 "w_gemv": "k_dense_gemv"}
+
+
+def ncu_traffic(config, kernel):
+    """DRAM bytes (read + write) per launch of `kernel` from the newest committed
+    `ncu --set full` capture of this config (profiles/r*/traffic_<config>.json)."""
+    import glob
+
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", f"traffic_{config}.json")), reverse=True):
+        try:
+            with open(path) as fh:
+                d = json.load(fh)["dram_bytes_per_launch"]
+            if KERNEL_SYMBOL.get(kernel) in d:
+                return d[KERNEL_SYMBOL[kernel]], os.path.relpath(path, ROOT)
+        except Exception:
+            continue
+    return None, None
+
+
 def hbm_peak():
     try:
         with open(PEAKS_PATH) as fh:
@@ -297,6 +317,7 @@ def main():
     dom = max(kt, key=lambda k: kt[k][0])
     ms_k, bytes_k = kt[dom]
     achieved = bytes_k / (ms_k / 1e3) / 1e9
+    traffic, traffic_src = ncu_traffic(args.config, dom)
     it_mean = float(np.mean(its))
     t_iter_ms = (dev_ms / args.steps) / max(it_mean, 1)
     b_iter = iteration_bytes(q, p.n, p.nnz)
@@ -323,7 +344,8 @@ def main():
                   "n0": q["n0"], "r0": q["r0"], "n_minus": q["n_minus"], "rw": q["rw"]},
         "setup_s": setup_s, "setup_phase_ms": q["t_setup_ms"][:6],
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                     "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                     "peak_kind": peak_kind,
                      "bytes_per_launch": bytes_k, "ms_per_launch": ms_k,
                      "kernels": {k: {"ms": v[0], "GBps": v[1] / (v[0] / 1e3) / 1e9} for k, v in kt.items()},
                      "iteration": {"bytes": b_iter, "ms": t_iter_ms,

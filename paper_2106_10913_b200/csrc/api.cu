@@ -136,10 +136,11 @@ void set_factor(Ctx& c, CoarseFactor& f, int dim, int r, const int* ret, const d
   f.h_l11.assign(l11, l11 + size_t(r) * r);
   f.retained.upload(f.h_retained, c.stream);
   f.linv.alloc(size_t(std::max(r, 1)) * std::max(r, 1));
+  f.linvT.alloc(size_t(std::max(r, 1)) * std::max(r, 1));
   if (r) {
     DArr<double> l;
     l.upload(f.h_l11, c.stream);
-    k::tri_inverse(c, l.p, r, f.linv.p);
+    k::tri_inverse(c, l.p, r, f.linv.p, f.linvT.p);
   }
 }
 
@@ -317,6 +318,9 @@ int awg_create(awg_ctx** out, int device) {
   int rc = guarded(ctx, [&](Ctx& cc) {
     AWG_CUDA(cudaSetDevice(device));
     AWG_CUDA(cudaStreamCreateWithFlags(&cc.stream, cudaStreamNonBlocking));
+    AWG_CUDA(cudaStreamCreateWithFlags(&cc.side, cudaStreamNonBlocking));
+    AWG_CUDA(cudaEventCreateWithFlags(&cc.ev_fork, cudaEventDisableTiming));
+    AWG_CUDA(cudaEventCreateWithFlags(&cc.ev_join, cudaEventDisableTiming));
     AWG_CUDA(cudaDeviceGetAttribute(&cc.sm_count, cudaDevAttrMultiProcessorCount, device));
   });
   *out = ctx;
@@ -329,9 +333,13 @@ void awg_destroy(awg_ctx* ctx) {
     cudaSetDevice(ctx->c.device);
     if (ctx->c.stream) cudaStreamSynchronize(ctx->c.stream);
   }
-  cudaStream_t s = ctx->c.stream;
+  cudaStream_t s = ctx->c.stream, side = ctx->c.side;
+  cudaEvent_t e0 = ctx->c.ev_fork, e1 = ctx->c.ev_join;
   delete ctx;
   if (s) cudaStreamDestroy(s);
+  if (side) cudaStreamDestroy(side);
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
 }
 
 const char* awg_last_error(const awg_ctx* ctx) { return ctx ? ctx->c.err.c_str() : "null context"; }
@@ -562,12 +570,12 @@ int awg_time_kernel(awg_ctx* ctx, int which, int reps, double* ms, double* bytes
       case 3:
         if (c.nm == 0) c.fail(AWG_E_STATE, "time_kernel: no W");
         b = 8.0 * c.n * c.nm + 8.0 * c.n + 8.0 * c.nm;
-        launch = [&] { k::wT(c, c.pb.p, c.cz.p, nullptr); };
+        launch = [&] { k::wT(c, c.pb.p, c.cw.p, nullptr); };
         break;
       case 4:
         if (c.nm == 0) c.fail(AWG_E_STATE, "time_kernel: no W");
         b = 8.0 * c.n * c.nm + 8.0 * c.n + 8.0 * c.nm;
-        launch = [&] { k::w_apply_public(c, c.cz.p, c.pz.p, nullptr); };
+        launch = [&] { k::w_apply_public(c, c.cw.p, c.pz.p, nullptr); };
         break;
       default:
         c.fail(AWG_E_ARG, "time_kernel: unknown kernel");

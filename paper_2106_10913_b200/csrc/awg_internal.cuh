@@ -114,13 +114,15 @@ struct CoarseFactor {
   int dim = 0;   // original dimension (n0 or n_minus)
   int rank = 0;  // r
   DArr<int> retained;
-  DArr<double> linv;  // r x r, column-major, lower
+  DArr<double> linv;   // r x r, column-major, lower
+  DArr<double> linvT;  // its transpose (row i of L^-1 contiguous)
   std::vector<int> h_retained;
   std::vector<double> h_l11;  // r x r, as produced (for exports)
   void clear() {
     dim = rank = 0;
     retained.release();
     linv.release();
+    linvT.release();
     h_retained.clear();
     h_l11.clear();
   }
@@ -151,8 +153,8 @@ void coarse_q(Ctx& c, const double* x, double* y, const int* gate);   // y = Z K
 void second_q(Ctx& c, const double* x, double* y, const int* gate);   // y = W KW+ W^T x
 void inex_q(Ctx& c, const double* x, double* y, const int* gate);     // y = W core^-1 W^T x
 void axpby(Ctx& c, int n, const double* a, const double* b, const double* d, double* y, int mode, const int* gate);
-void rr_solve(Ctx& c, const CoarseFactor& f, const double* b, double* x, const int* gate);
-void tri_inverse(Ctx& c, const double* l, int r, double* linv);
+void rr_solve(Ctx& c, const CoarseFactor& f, const double* b, double* x, const int* gate, double* tmp);
+void tri_inverse(Ctx& c, const double* l, int r, double* linv, double* linvT);
 void zT(Ctx& c, const double* x, double* out, const int* gate);  // out = Z^T x (n0)
 void wT(Ctx& c, const double* x, double* out, const int* gate);  // out = W^T x (n_minus)
 void w_apply_public(Ctx& c, const double* coef, double* y, const int* gate);  // y = W coef
@@ -163,6 +165,8 @@ void scatter_col(Ctx& c, int s, const double* col, double* z);  // z[Omega^s] = 
 struct Ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;  // concurrent branch (second coarse correction of H3,ad)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::string err;
   int err_index = -1;
   long long launches = 0;
@@ -232,7 +236,8 @@ struct Ctx {
   // work buffers
   DArr<double> xs, uh, wl;                          // P each
   DArr<double> t0, t1, t2, t3, t4, t5, t6, t7, t8;  // n each
-  DArr<double> cz, cz2;                             // max(n0, nm) each
+  DArr<double> cz, cz2;                             // coarse (K0) scratch
+  DArr<double> cw, cw2;                             // second coarse (KW) scratch (may run concurrently)
   DArr<double> wpart;                               // split-K partials of W^T x
   DArr<double> wpart2;                              // column-chunk partials of W c
   DArr<double> red;                                 // reduction partials

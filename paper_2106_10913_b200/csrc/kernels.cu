@@ -211,6 +211,21 @@ __global__ void k_prolong_nn(const int* __restrict__ gate, int n, const int* __r
 // ---------------------------------------------------------------------------
 // A- x (splitting.cpp:119-140): per strictly negative mode (s,k):
 //   c = (-lambda_k) * (v_k . x[Omega^s]);   u_s = sum_k c_k v_k;   y = sum_s R^s^T u_s
+// CTA-wide sum of one value per thread (fixed tree: deterministic)
+__device__ __forceinline__ double block_sum(double v) {
+  __shared__ double sred[32];
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) sred[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x < 32) {
+    s = (threadIdx.x < (blockDim.x >> 5)) ? sred[threadIdx.x] : 0.0;
+    s = warp_sum(s);
+  }
+  return s;  // valid in thread 0
+}
+
+// one CTA per negative mode: enough loads in flight even when n_- is small
 __global__ void k_neg_dot(const int* __restrict__ gate, int nneg, const int* __restrict__ neg_s,
                           const int* __restrict__ neg_k, const double* __restrict__ neg_w,
                           const double* __restrict__ V, const long long* __restrict__ voff,
@@ -218,16 +233,14 @@ __global__ void k_neg_dot(const int* __restrict__ gate, int nneg, const int* __r
                           const long long* __restrict__ poff, const int* __restrict__ pidx,
                           const double* __restrict__ x, double* __restrict__ cout) {
   if (gated(gate)) return;
-  const int lane = threadIdx.x & 31;
-  const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (j >= nneg) return;
+  const int j = blockIdx.x;
   const int s = neg_s[j], k = neg_k[j], n = ns[s];
   const double* v = V + voff[s] + (size_t)k * ld[s];
   const int* idx = pidx + poff[s];
   double acc = 0.0;
-  for (int i = lane; i < n; i += 32) acc = fma(v[i], __ldg(x + idx[i]), acc);
-  acc = warp_sum(acc);
-  if (lane == 0) cout[j] = neg_w[j] * acc;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) acc = fma(v[i], __ldg(x + idx[i]), acc);
+  acc = block_sum(acc);
+  if (threadIdx.x == 0) cout[j] = neg_w[j] * acc;
 }
 
 // u[p] = sum over the negative modes of s(p), ascending k, of c_k v_k[i]
@@ -254,49 +267,39 @@ __global__ void k_block_combine(const int* __restrict__ gate, long long P, const
 }
 
 // Z^T x with Z block sparse (coarse.cpp:136-141 + matvec_transpose, dense.cpp:47-54):
-// warp per coarse column j of subdomain s: zx[j] = Y_s(:, j - koff[s]) . x[Omega^s]
+// CTA per coarse column j of subdomain s: zx[j] = Y_s(:, j - koff[s]) . x[Omega^s]
 __global__ void k_zT(const int* __restrict__ gate, int n0, const int* __restrict__ zcol_s,
                      const int* __restrict__ zcol_loc, const double* __restrict__ Y,
                      const long long* __restrict__ yoff, const int* __restrict__ ns,
                      const int* __restrict__ ld, const long long* __restrict__ poff,
                      const int* __restrict__ pidx, const double* __restrict__ x, double* __restrict__ zx) {
   if (gated(gate)) return;
-  const int lane = threadIdx.x & 31;
-  const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (j >= n0) return;
+  const int j = blockIdx.x;
   const int s = zcol_s[j], n = ns[s];
   const double* y = Y + yoff[s] + (size_t)zcol_loc[j] * ld[s];
   const int* idx = pidx + poff[s];
   double acc = 0.0;
-  for (int i = lane; i < n; i += 32) acc = fma(y[i], __ldg(x + idx[i]), acc);
-  acc = warp_sum(acc);
-  if (lane == 0) zx[j] = acc;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) acc = fma(y[i], __ldg(x + idx[i]), acc);
+  acc = block_sum(acc);
+  if (threadIdx.x == 0) zx[j] = acc;
 }
 
 // ---------------------------------------------------------------------------
 // rank_revealing_solve (dense.cpp:348-366) with the inverse of l11:
 //   b_r = b[retained]; t = L^-1 b_r; y = L^-T t; x = 0, x[retained] = y
-__global__ void __launch_bounds__(kThreads) k_tri_lower(const int* __restrict__ gate, int r, const double* __restrict__ linv,
-                                                     const double* __restrict__ b, const int* __restrict__ ret,
-                                                     double* __restrict__ t) {
+// t_i = sum_{j <= i} L^-1(i, j) b[ret[j]]: warp per row, reading row i of L^-1
+// as column i of its transpose (linvT, column-major upper) — coalesced
+__global__ void k_tri_lower(const int* __restrict__ gate, int r, const double* __restrict__ linvT,
+                            const double* __restrict__ b, const int* __restrict__ ret, double* __restrict__ t) {
   if (gated(gate)) return;
-  extern __shared__ double sb[];
-  constexpr int CH = 4096;
-  const int i0 = blockIdx.x * blockDim.x;
-  const int i = i0 + threadIdx.x;
-  const int jmax = min(r, i0 + (int)blockDim.x);  // columns j <= i needed
+  const int lane = threadIdx.x & 31;
+  const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (i >= r) return;
+  const double* row = linvT + (size_t)i * r;
   double acc = 0.0;
-  for (int c0 = 0; c0 < jmax; c0 += CH) {
-    const int c1 = min(jmax, c0 + CH);
-    __syncthreads();
-    for (int j = c0 + threadIdx.x; j < c1; j += blockDim.x) sb[j - c0] = b[ret[j]];
-    __syncthreads();
-    if (i < r) {
-      const int jend = min(c1, i + 1);
-      for (int j = c0; j < jend; ++j) acc = fma(linv[i + (size_t)j * r], sb[j - c0], acc);
-    }
-  }
-  if (i < r) t[i] = acc;
+  for (int j = lane; j <= i; j += 32) acc = fma(row[j], __ldg(b + ret[j]), acc);
+  acc = warp_sum(acc);
+  if (lane == 0) t[i] = acc;
 }
 
 __global__ void k_tri_upperT(const int* __restrict__ gate, int r, const double* __restrict__ linv,
@@ -594,10 +597,8 @@ void aminus(Ctx& c, const double* x, double* y, const int* gate) {
     check_launch("zero");
     return;
   }
-  const int wpb = kThreads / 32;
-  k_neg_dot<<<(c.nneg + wpb - 1) / wpb, kThreads, 0, c.stream>>>(gate, c.nneg, c.neg_s.p, c.neg_k.p, c.neg_w.p,
-                                                                c.V.p, c.voff.p, c.ns.p, c.ld.p, c.poff.p, c.pidx.p,
-                                                                x, c.neg_c.p);
+  k_neg_dot<<<c.nneg, kThreads, 0, c.stream>>>(gate, c.nneg, c.neg_s.p, c.neg_k.p, c.neg_w.p, c.V.p, c.voff.p,
+                                               c.ns.p, c.ld.p, c.poff.p, c.pidx.p, x, c.neg_c.p);
   ++c.launches;
   check_launch("neg_dot");
   k_block_combine<<<grid_for(c, c.P), kThreads, 0, c.stream>>>(gate, c.P, c.psub.p, c.poff.p, c.negoff.p, c.neg_k.p,
@@ -607,17 +608,15 @@ void aminus(Ctx& c, const double* x, double* y, const int* gate) {
   prolong(c, c.wl.p, y, gate);
 }
 
-void rr_solve(Ctx& c, const CoarseFactor& f, const double* b, double* x, const int* gate) {
+void rr_solve(Ctx& c, const CoarseFactor& f, const double* b, double* x, const int* gate, double* tmp) {
   k_zero<<<grid_for(c, f.dim), kThreads, 0, c.stream>>>(gate, f.dim, x);
   ++c.launches;
   if (f.rank == 0) return;
-  const size_t smem = size_t(std::min(f.rank, 4096)) * sizeof(double);
-  k_tri_lower<<<(f.rank + kThreads - 1) / kThreads, kThreads, smem, c.stream>>>(gate, f.rank, f.linv.p, b,
-                                                                               f.retained.p, c.cz2.p);
+  const int wpb = kThreads / 32;
+  k_tri_lower<<<(f.rank + wpb - 1) / wpb, kThreads, 0, c.stream>>>(gate, f.rank, f.linvT.p, b, f.retained.p, tmp);
   ++c.launches;
   check_launch("tri_lower");
-  const int wpb = kThreads / 32;
-  k_tri_upperT<<<(f.rank + wpb - 1) / wpb, kThreads, 0, c.stream>>>(gate, f.rank, f.linv.p, c.cz2.p, f.retained.p,
+  k_tri_upperT<<<(f.rank + wpb - 1) / wpb, kThreads, 0, c.stream>>>(gate, f.rank, f.linv.p, tmp, f.retained.p,
                                                                    x);
   ++c.launches;
   check_launch("tri_upperT");
@@ -629,13 +628,12 @@ void coarse_q(Ctx& c, const double* x, double* y, const int* gate) {
     ++c.launches;
     return;
   }
-  const int wpb = kThreads / 32;
-  k_zT<<<(c.n0 + wpb - 1) / wpb, kThreads, 0, c.stream>>>(gate, c.n0, c.zcol_s.p, c.zcol_loc.p, c.Y.p, c.yoff.p,
-                                                         c.ns.p, c.ld.p, c.poff.p, c.pidx.p, x, c.cz.p);
+  k_zT<<<c.n0, kThreads, 0, c.stream>>>(gate, c.n0, c.zcol_s.p, c.zcol_loc.p, c.Y.p, c.yoff.p, c.ns.p, c.ld.p,
+                                        c.poff.p, c.pidx.p, x, c.cz.p);
   ++c.launches;
   check_launch("zT");
   double* coef = c.cz.p + c.n0;  // second half of cz holds the solved coefficients
-  rr_solve(c, c.k0, c.cz.p, coef, gate);
+  rr_solve(c, c.k0, c.cz.p, coef, gate, c.cz2.p);
   k_block_combine<<<grid_for(c, c.P), kThreads, 0, c.stream>>>(gate, c.P, c.psub.p, c.poff.p, c.koff.p, nullptr,
                                                                c.Y.p, c.yoff.p, c.ld.p, coef, c.wl.p);
   ++c.launches;
@@ -644,9 +642,8 @@ void coarse_q(Ctx& c, const double* x, double* y, const int* gate) {
 }
 
 void zT(Ctx& c, const double* x, double* out, const int* gate) {
-  const int wpb = kThreads / 32;
-  k_zT<<<(c.n0 + wpb - 1) / wpb, kThreads, 0, c.stream>>>(gate, c.n0, c.zcol_s.p, c.zcol_loc.p, c.Y.p, c.yoff.p,
-                                                         c.ns.p, c.ld.p, c.poff.p, c.pidx.p, x, out);
+  k_zT<<<c.n0, kThreads, 0, c.stream>>>(gate, c.n0, c.zcol_s.p, c.zcol_loc.p, c.Y.p, c.yoff.p, c.ns.p, c.ld.p,
+                                        c.poff.p, c.pidx.p, x, out);
   ++c.launches;
   check_launch("zT");
 }
@@ -698,16 +695,16 @@ void second_q(Ctx& c, const double* x, double* y, const int* gate) {
     ++c.launches;
     return;
   }
-  double* wx = c.cz.p;
-  double* coef = c.cz.p + c.nm;
+  double* wx = c.cw.p;
+  double* coef = c.cw.p + c.nm;
   w_transpose_apply(c, x, wx, gate);
-  rr_solve(c, c.kw, wx, coef, gate);
+  rr_solve(c, c.kw, wx, coef, gate, c.cw2.p);
   w_apply(c, coef, y, gate);
 }
 
 void inex_q(Ctx& c, const double* x, double* y, const int* gate) {
-  double* wx = c.cz.p;
-  double* coef = c.cz.p + c.nm;
+  double* wx = c.cw.p;
+  double* coef = c.cw.p + c.nm;
   w_transpose_apply(c, x, wx, gate);
   k_lu_solve<<<1, 1024, size_t(c.nm) * sizeof(double), c.stream>>>(gate, c.nm, c.core_lu.p, c.core_perm.p, wx, coef,
                                                                    c.lu_semantics);
@@ -722,15 +719,14 @@ void axpby(Ctx& c, int n, const double* a, const double* b, const double* d, dou
   check_launch("axpby");
 }
 
-void tri_inverse(Ctx& c, const double* l, int r, double* linv) {
+// L^-1 as column-major (linv) and its transpose (linvT = the row-major scratch)
+void tri_inverse(Ctx& c, const double* l, int r, double* linv, double* linvT) {
   if (r == 0) return;
-  DArr<double> scratch;
-  scratch.alloc(size_t(r) * r);
-  k_tri_inverse_rm<<<(r + 127) / 128, 128, 0, c.stream>>>(r, l, scratch.p);
+  k_tri_inverse_rm<<<(r + 127) / 128, 128, 0, c.stream>>>(r, l, linvT);
   ++c.launches;
   check_launch("tri_inverse");
   dim3 grid((r + 31) / 32, (r + 31) / 32);
-  k_transpose<<<grid, dim3(32, 8), 0, c.stream>>>(r, scratch.p, linv);
+  k_transpose<<<grid, dim3(32, 8), 0, c.stream>>>(r, linvT, linv);
   ++c.launches;
   check_launch("transpose");
   AWG_CUDA(cudaStreamSynchronize(c.stream));

@@ -261,6 +261,8 @@ void Ctx::alloc_work() {
   const size_t cdim = size_t(std::max(n0, nm)) * 2 + 2;
   cz.alloc(cdim);
   cz2.alloc(cdim);
+  cw.alloc(cdim);
+  cw2.alloc(cdim);
   const int nch = (round_up(n, 4) + 4095) / 4096;
   wpart.alloc(size_t(std::max(nm, 1)) * nch);
   wpart2.alloc(size_t(w_chunks(*this)) * round_up(n, 4));
@@ -345,9 +347,16 @@ void op_apply(Ctx& c, int op, const double* x, double* y, const int* gate) {
         h2(c, x, y, gate);
         return;
       }
-      if (mode == 1) {  // AD
+      if (mode == 1) {  // AD: W KW^+ W^T x and H2 x are independent — run them concurrently
+        AWG_CUDA(cudaEventRecord(c.ev_fork, c.stream));
+        AWG_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
+        cudaStream_t main = c.stream;
+        c.stream = c.side;
         k::second_q(c, x, c.t6.p, gate);
+        c.stream = main;
+        AWG_CUDA(cudaEventRecord(c.ev_join, c.side));
         h2(c, x, c.t7.p, gate);
+        AWG_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));
         k::axpby(c, c.n, c.t7.p, c.t6.p, nullptr, y, 1, gate);
       } else if (mode == 2) {  // HYB
         k::second_q(c, x, c.t6.p, gate);                 // corr
