@@ -149,6 +149,8 @@ void nn_gemvT(Ctx& c, const double* x, const int* gate);               // uh = m
 void nn_gemv(Ctx& c, const int* gate);                                 // part = V uh (column chunks)
 void nn_prolong(Ctx& c, double* y, const int* gate);                   // y = sum_s R^T D sum_kc part
 void aminus(Ctx& c, const double* x, double* y, const int* gate);     // y = A- x
+// mode 1: y = A+ x;  mode 2: y = sub - A+ x  (A- prolongation fused into the SpMV)
+void aplus(Ctx& c, const double* x, double* y, int mode, const double* sub, const int* gate);
 void coarse_q(Ctx& c, const double* x, double* y, const int* gate);   // y = Z K0+ Z^T x
 void second_q(Ctx& c, const double* x, double* y, const int* gate);   // y = W KW+ W^T x
 void inex_q(Ctx& c, const double* x, double* y, const int* gate);     // y = W core^-1 W^T x

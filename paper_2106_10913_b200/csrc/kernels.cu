@@ -62,6 +62,58 @@ __global__ void k_spmv(const int* __restrict__ gate, int n, const int* __restric
   }
 }
 
+// Prolongation of a block-sparse combination, evaluated at dof i:
+//   sum over subdomains s containing i (ascending) of sum_q coef[q] M_s(loc, col(q))
+// — the k_block_combine + k_prolong pair fused (same association order).
+struct BlockSum {
+  const int* own_off;
+  const int* own_pos;
+  const int* psub;
+  const long long* poff;
+  const int* coff;  // per-subdomain coefficient ranges
+  const int* ccol;  // column of coefficient q (nullptr: q - coff[s])
+  const double* M;
+  const long long* moff;
+  const int* ld;
+  const double* coef;
+  __device__ __forceinline__ double at(int i) const {
+    double acc = 0.0;
+    for (int qo = own_off[i]; qo < own_off[i + 1]; ++qo) {
+      const int p = own_pos[qo];
+      const int s = psub[p];
+      const double* Ms = M + moff[s] + (p - poff[s]);
+      const int L = ld[s];
+      double u = 0.0;
+      for (int q = coff[s]; q < coff[s + 1]; ++q) {
+        const int col = ccol ? ccol[q] : (q - coff[s]);
+        u = fma(coef[q], Ms[(size_t)col * L], u);
+      }
+      acc += u;
+    }
+    return acc;
+  }
+};
+
+// A+ x = A- x + A x with the A- prolongation fused (splitting.cpp:142-147):
+//   mode 1: y = am + A x;  mode 2: y = sub - (am + A x)
+__global__ void k_spmv_aplus(const int* __restrict__ gate, int n, const int* __restrict__ rp,
+                             const int* __restrict__ ci, const double* __restrict__ va,
+                             const double* __restrict__ x, double* __restrict__ y, int mode,
+                             const double* __restrict__ sub, BlockSum am) {
+  if (gated(gate)) return;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int k = rp[i]; k < rp[i + 1]; ++k) acc = __dadd_rn(acc, __dmul_rn(va[k], __ldg(x + ci[k])));
+    const double a = am.at(i) + acc;
+    y[i] = (mode == 1) ? a : sub[i] - a;
+  }
+}
+
+__global__ void k_prolong_sum(const int* __restrict__ gate, int n, BlockSum bs, double* __restrict__ y) {
+  if (gated(gate)) return;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) y[i] = bs.at(i);
+}
+
 // xs[p] = x[pidx[p]] (* scale[p])      restrict_to (splitting.cpp:220-223) and the D^s
 // scaling of OneLevel::apply (preconditioner.cpp:48-49)
 __global__ void k_gather(const int* __restrict__ gate, long long total, const int* __restrict__ pidx,
@@ -608,6 +660,27 @@ void aminus(Ctx& c, const double* x, double* y, const int* gate) {
   prolong(c, c.wl.p, y, gate);
 }
 
+static BlockSum neg_sum(const Ctx& c) {
+  return BlockSum{c.own_off.p, c.own_pos.p, c.psub.p, c.poff.p, c.negoff.p, c.neg_k.p,
+                  c.V.p,       c.voff.p,    c.ld.p,   c.neg_c.p};
+}
+
+// y = A+ x (mode 1) or y = sub - A+ x (mode 2): the A- dots, then one fused
+// SpMV + A- prolongation kernel
+void aplus(Ctx& c, const double* x, double* y, int mode, const double* sub, const int* gate) {
+  if (c.nneg > 0) {
+    k_neg_dot<<<c.nneg, kThreads, 0, c.stream>>>(gate, c.nneg, c.neg_s.p, c.neg_k.p, c.neg_w.p, c.V.p, c.voff.p,
+                                                 c.ns.p, c.ld.p, c.poff.p, c.pidx.p, x, c.neg_c.p);
+    ++c.launches;
+    check_launch("neg_dot");
+  }
+  BlockSum bs = neg_sum(c);
+  if (c.nneg == 0) bs.coff = c.negoff.p;  // empty ranges: all zero
+  k_spmv_aplus<<<grid_for(c, c.n), kThreads, 0, c.stream>>>(gate, c.n, c.rp.p, c.ci.p, c.va.p, x, y, mode, sub, bs);
+  ++c.launches;
+  check_launch("spmv_aplus");
+}
+
 void rr_solve(Ctx& c, const CoarseFactor& f, const double* b, double* x, const int* gate, double* tmp) {
   k_zero<<<grid_for(c, f.dim), kThreads, 0, c.stream>>>(gate, f.dim, x);
   ++c.launches;
@@ -634,11 +707,11 @@ void coarse_q(Ctx& c, const double* x, double* y, const int* gate) {
   check_launch("zT");
   double* coef = c.cz.p + c.n0;  // second half of cz holds the solved coefficients
   rr_solve(c, c.k0, c.cz.p, coef, gate, c.cz2.p);
-  k_block_combine<<<grid_for(c, c.P), kThreads, 0, c.stream>>>(gate, c.P, c.psub.p, c.poff.p, c.koff.p, nullptr,
-                                                               c.Y.p, c.yoff.p, c.ld.p, coef, c.wl.p);
+  // Z c: block-sparse combination fused with the prolongation
+  const BlockSum bs{c.own_off.p, c.own_pos.p, c.psub.p, c.poff.p, c.koff.p, nullptr, c.Y.p, c.yoff.p, c.ld.p, coef};
+  k_prolong_sum<<<grid_for(c, c.n), kThreads, 0, c.stream>>>(gate, c.n, bs, y);
   ++c.launches;
-  check_launch("z_combine");
-  prolong(c, c.wl.p, y, gate);
+  check_launch("z_prolong");
 }
 
 void zT(Ctx& c, const double* x, double* out, const int* gate) {

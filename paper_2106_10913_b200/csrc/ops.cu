@@ -275,10 +275,7 @@ void Ctx::alloc_work() {
 
 static void h1(Ctx& c, const double* x, double* y, const int* gate) { k::h1(c, x, y, gate); }
 
-static void aplus(Ctx& c, const double* x, double* y, const int* gate) {
-  k::aminus(c, x, y, gate);
-  k::spmv(c, x, y, 1, y, nullptr, gate);
-}
+static void aplus(Ctx& c, const double* x, double* y, const int* gate) { k::aplus(c, x, y, 1, nullptr, gate); }
 
 static void h2(Ctx& c, const double* x, double* y, const int* gate) {
   if (c.n0 == 0) {
@@ -291,8 +288,7 @@ static void h2(Ctx& c, const double* x, double* y, const int* gate) {
     k::axpby(c, c.n, c.t1.p, c.t0.p, nullptr, y, 1, gate);
     return;
   }
-  k::aminus(c, c.t0.p, c.t1.p, gate);
-  k::spmv(c, c.t0.p, c.t2.p, 2, c.t1.p, x, gate);  // pt = x - A+ corr
+  k::aplus(c, c.t0.p, c.t2.p, 2, x, gate);         // pt = x - A+ corr
   h1(c, c.t2.p, c.t3.p, gate);                     // hp
   aplus(c, c.t3.p, c.t4.p, gate);                  // A+ hp
   k::coarse_q(c, c.t4.p, c.t5.p, gate);            // Q A+ hp

@@ -121,3 +121,17 @@ def test_error_paths():
 def test_native_library_loaded():
     maps = open("/proc/self/maps").read()
     assert "libawg_b200.so" in maps
+
+
+@pytest.mark.parametrize("case", ["c1", "t2d", "t3d"])
+def test_inex_exact_lu_matches_restatement(case):
+    """INEX with the exact LU back substitution (lu_semantics='exact'): the
+    reference only ships the bug-2 version (dense.cpp:404-409), so the checker
+    is the restatement with lu_exact=True."""
+    g, s = golden_with_base(case)
+    ctx = make_ctx(g, mode=awg.AwgMode.INEX, lu="exact")
+    orc = O.AwgOracle(len(g["b"]), g["A_row_offsets"], g["A_col_indices"], g["A_values"],
+                      [g["part_indices"][a:b] for a, b in zip(g["part_offsets"][:-1], g["part_offsets"][1:])], g,
+                      lu_exact=True)
+    for x in g["x_apply"]:
+        assert rel(ctx.apply(awg.Op.H3, x), orc.h3(x, "inex")) <= 1e-10
