@@ -112,67 +112,10 @@ __global__ void kb_prolong(int n, int ldx, const int* __restrict__ own_off, cons
   }
 }
 
-// C(j, b) = w_j * (V^s(:, k_j) . X(Omega^s, b)) — warp per (mode, column)
-__global__ void kb_neg_dot(int nneg, int B, const int* __restrict__ neg_s, const int* __restrict__ neg_k,
-                           const double* __restrict__ neg_w, const double* __restrict__ V,
-                           const long long* __restrict__ voff, const int* __restrict__ ns, const int* __restrict__ ld,
-                           const long long* __restrict__ poff, const int* __restrict__ pidx, int ldx,
-                           const double* __restrict__ X, double* __restrict__ C, const int* __restrict__ done) {
-  const int lane = threadIdx.x & 31;
-  const long long w = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (w >= (long long)nneg * B) return;
-  const int j = int(w % nneg), b = int(w / nneg);
-  if (col_off(done, b)) return;
-  const int s = neg_s[j], n = ns[s];
-  const double* v = V + voff[s] + (size_t)neg_k[j] * ld[s];
-  const int* idx = pidx + poff[s];
-  const double* x = X + (size_t)b * ldx;
-  double acc = 0.0;
-  for (int i = lane; i < n; i += 32) acc = fma(v[i], __ldg(x + idx[i]), acc);
-  acc = wsum(acc);
-  if (lane == 0) C[(size_t)b * nneg + j] = neg_w[j] * acc;
-}
-
-// WS(s, i, b) = sum_q coef(q, b) M_s(i, col(q))  for the q of subdomain s
-__global__ void kb_combine(long long P, const int* __restrict__ psub, const long long* __restrict__ poff,
-                           const int* __restrict__ coff, const int* __restrict__ ccol, const double* __restrict__ M,
-                           const long long* __restrict__ moff, const int* __restrict__ ld, int ncoef,
-                           const double* __restrict__ coef, const int* __restrict__ lds,
-                           const long long* __restrict__ boff, double* __restrict__ WS, const int* __restrict__ done) {
-  const int b = blockIdx.y;
-  if (col_off(done, b)) return;
-  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < P; p += (long long)gridDim.x * blockDim.x) {
-    const int s = psub[p];
-    const int i = int(p - poff[s]);
-    const double* Ms = M + moff[s] + i;
-    const int L = ld[s];
-    double acc = 0.0;
-    for (int q = coff[s]; q < coff[s + 1]; ++q) {
-      const int col = ccol ? ccol[q] : (q - coff[s]);
-      acc = fma(coef[(size_t)b * ncoef + q], Ms[(size_t)col * L], acc);
-    }
-    WS[boff[s] + (size_t)b * lds[s] + i] = acc;
-  }
-}
-
-// ZX(j, b) = Y_s(:, c_j) . X(Omega^s, b)
-__global__ void kb_zT(int n0, int B, const int* __restrict__ zcol_s, const int* __restrict__ zcol_loc,
-                      const double* __restrict__ Y, const long long* __restrict__ yoff, const int* __restrict__ ns,
-                      const int* __restrict__ ld, const long long* __restrict__ poff, const int* __restrict__ pidx,
-                      int ldx, const double* __restrict__ X, double* __restrict__ ZX, const int* __restrict__ done) {
-  const int lane = threadIdx.x & 31;
-  const long long w = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (w >= (long long)n0 * B) return;
-  const int j = int(w % n0), b = int(w / n0);
-  if (col_off(done, b)) return;
-  const int s = zcol_s[j], n = ns[s];
-  const double* y = Y + yoff[s] + (size_t)zcol_loc[j] * ld[s];
-  const int* idx = pidx + poff[s];
-  const double* x = X + (size_t)b * ldx;
-  double acc = 0.0;
-  for (int i = lane; i < n; i += 32) acc = fma(y[i], __ldg(x + idx[i]), acc);
-  acc = wsum(acc);
-  if (lane == 0) ZX[(size_t)b * n0 + j] = acc;
+// C(j, b) *= w_j  (the -lambda weights of the negative modes)
+__global__ void kb_scale_rows(int m, const double* __restrict__ w, double* __restrict__ C) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < m) C[(size_t)blockIdx.y * m + j] *= w[j];
 }
 
 __global__ void kb_take(int r, int n0, int B, const int* __restrict__ ret, const double* __restrict__ src,
@@ -384,6 +327,18 @@ struct BlockOps {
   Block& k;
   cublasHandle_t h;
   const CoarseFactor& k0;
+  std::vector<int> qs, negoff, koff;  // per subdomain: negative modes, their offset, coarse column offset
+
+  BlockOps(Ctx& cc, Block& kk, cublasHandle_t hh, const CoarseFactor& f) : c(cc), k(kk), h(hh), k0(f) {
+    qs.resize(c.N);
+    negoff.assign(c.N + 1, 0);
+    koff.assign(c.N + 1, 0);
+    for (int s = 0; s < c.N; ++s) {
+      qs[s] = c.h_m[s] - c.h_nzero[s];
+      negoff[s + 1] = negoff[s] + qs[s];
+      koff[s + 1] = koff[s] + c.h_ks[s];
+    }
+  }
 
   dim3 grid_n() const { return dim3(std::max(1, std::min((c.n + kT - 1) / kT, 148 * 2)), k.B); }
   dim3 grid_p() const {
@@ -394,17 +349,31 @@ struct BlockOps {
     kb_spmv<<<grid_n(), kT, 0, c.stream>>>(c.n, k.ld, c.rp.p, c.ci.p, c.va.p, X, Y, mode, add, sub, done);
     ++c.launches;
   }
+  // A- X = sum_s R^s^T V-^s |L-^s| V-^s^T R^s X: the strictly negative modes of s are
+  // the first q_s columns of V^s (ascending spectrum, splitting.cpp:129-137), so both
+  // products are per-subdomain DGEMMs on the gathered block (V-^s read once per batch)
   void aminus(const double* X, double* Y, const int* done) {
     if (c.nneg == 0) {
       AWG_CUDA(cudaMemsetAsync(Y, 0, sizeof(double) * k.ld * k.B, c.stream));
       return;
     }
-    const long long warps = (long long)c.nneg * k.B;
-    kb_neg_dot<<<int((warps + 7) / 8), 256, 0, c.stream>>>(c.nneg, k.B, c.neg_s.p, c.neg_k.p, c.neg_w.p, c.V.p,
-                                                           c.voff.p, c.ns.p, c.ld.p, c.poff.p, c.pidx.p, k.ld, X,
-                                                           k.negc.p, done);
-    kb_combine<<<grid_p(), kT, 0, c.stream>>>(c.P, c.psub.p, c.poff.p, c.negoff.p, c.neg_k.p, c.V.p, c.voff.p,
-                                              c.ld.p, c.nneg, k.negc.p, c.ld.p, k.boff.p, k.WS.p, done);
+    kb_gather<<<grid_p(), kT, 0, c.stream>>>(c.P, c.psub.p, c.poff.p, c.pidx.p, c.ld.p, k.boff.p, nullptr, k.ld, X,
+                                             k.XS.p, done);
+    AWG_CUDA(cudaMemsetAsync(k.WS.p, 0, sizeof(double) * k.WS.n, c.stream));
+    const double one = 1.0, zero = 0.0;
+    for (int s = 0; s < c.N; ++s) {
+      const int q = qs[s];
+      if (q == 0) continue;
+      AWG_BLAS(cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, q, k.B, c.h_ns[s], &one, c.V.p + c.h_voff[s], c.h_ld[s],
+                           k.XS.p + k.h_boff[s], c.h_ld[s], &zero, k.negc.p + negoff[s], c.nneg));
+    }
+    kb_scale_rows<<<dim3((c.nneg + kT - 1) / kT, k.B), kT, 0, c.stream>>>(c.nneg, c.neg_w.p, k.negc.p);
+    for (int s = 0; s < c.N; ++s) {
+      const int q = qs[s];
+      if (q == 0) continue;
+      AWG_BLAS(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, c.h_ns[s], k.B, q, &one, c.V.p + c.h_voff[s], c.h_ld[s],
+                           k.negc.p + negoff[s], c.nneg, &zero, k.WS.p + k.h_boff[s], c.h_ld[s]));
+    }
     kb_prolong<<<grid_n(), kT, 0, c.stream>>>(c.n, k.ld, c.own_off.p, c.own_pos.p, c.psub.p, c.poff.p, c.ld.p,
                                               k.boff.p, nullptr, k.WS.p, Y, done);
     c.launches += 3;
@@ -413,11 +382,21 @@ struct BlockOps {
     aminus(X, Y, done);
     spmv(X, Y, 1, Y, nullptr, done);
   }
+  // coarse_correct on the block: Z^T X and Z C as per-subdomain DGEMMs with Y_s
   void q(const double* X, double* Y, const int* done) {
     const int n0 = c.n0, r = k0.rank, B = k.B;
-    const long long warps = (long long)n0 * B;
-    kb_zT<<<int((warps + 7) / 8), 256, 0, c.stream>>>(n0, B, c.zcol_s.p, c.zcol_loc.p, c.Y.p, c.yoff.p, c.ns.p,
-                                                     c.ld.p, c.poff.p, c.pidx.p, k.ld, X, k.zx.p, done);
+    kb_gather<<<grid_p(), kT, 0, c.stream>>>(c.P, c.psub.p, c.poff.p, c.pidx.p, c.ld.p, k.boff.p, nullptr, k.ld, X,
+                                             k.XS.p, done);
+    ++c.launches;
+    {
+      const double one = 1.0, zero = 0.0;
+      for (int s = 0; s < c.N; ++s) {
+        const int ks = c.h_ks[s];
+        if (ks == 0) continue;
+        AWG_BLAS(cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, ks, B, c.h_ns[s], &one, c.Y.p + c.h_yoff[s], c.h_ld[s],
+                             k.XS.p + k.h_boff[s], c.h_ld[s], &zero, k.zx.p + koff[s], n0));
+      }
+    }
     AWG_CUDA(cudaMemsetAsync(k.zc.p, 0, sizeof(double) * n0 * B, c.stream));
     if (r > 0) {
       kb_take<<<int(((long long)r * B + kT - 1) / kT), kT, 0, c.stream>>>(r, n0, B, k0.retained.p, k.zx.p, k.zr.p);
@@ -428,8 +407,16 @@ struct BlockOps {
       kb_put<<<int(((long long)r * B + kT - 1) / kT), kT, 0, c.stream>>>(r, n0, B, k0.retained.p, k.zr.p, k.zc.p);
       c.launches += 2;
     }
-    kb_combine<<<grid_p(), kT, 0, c.stream>>>(c.P, c.psub.p, c.poff.p, c.koff.p, nullptr, c.Y.p, c.yoff.p, c.ld.p,
-                                              n0, k.zc.p, c.ld.p, k.boff.p, k.WS.p, done);
+    AWG_CUDA(cudaMemsetAsync(k.WS.p, 0, sizeof(double) * k.WS.n, c.stream));
+    {
+      const double one = 1.0, zero = 0.0;
+      for (int s = 0; s < c.N; ++s) {
+        const int ks = c.h_ks[s];
+        if (ks == 0) continue;
+        AWG_BLAS(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, c.h_ns[s], B, ks, &one, c.Y.p + c.h_yoff[s], c.h_ld[s],
+                             k.zc.p + koff[s], n0, &zero, k.WS.p + k.h_boff[s], c.h_ld[s]));
+      }
+    }
     kb_prolong<<<grid_n(), kT, 0, c.stream>>>(c.n, k.ld, c.own_off.p, c.own_pos.p, c.psub.p, c.poff.p, c.ld.p,
                                               k.boff.p, nullptr, k.WS.p, Y, done);
     c.launches += 3;
@@ -536,7 +523,7 @@ void build_w_batched(Ctx& c, cublasHandle_t h, const std::vector<std::pair<int, 
   k.done.alloc(B);
   k.any_true.alloc(1);
   AWG_BLAS(cublasSetStream(h, c.stream));
-  BlockOps ops{c, k, h, c.k0};
+  BlockOps ops(c, k, h, c.k0);
   const int cb = (B + 127) / 128;
   std::vector<ColState> hs(B);
   for (int c0 = 0; c0 < total; c0 += B) {
