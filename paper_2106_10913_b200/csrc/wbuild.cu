@@ -112,6 +112,14 @@ __global__ void kb_prolong(int n, int ldx, const int* __restrict__ own_off, cons
   }
 }
 
+// T(:, j) = V(:, j) / lambda_j  (columns j >= n_nonpos, shifted to start at 0)
+__global__ void kb_scale_inv(int n, int ld, const double* __restrict__ V, const double* __restrict__ lam,
+                             double* __restrict__ T) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y;
+  if (i < ld) T[i + (size_t)j * ld] = (i < n) ? V[i + (size_t)j * ld] / lam[j] : 0.0;
+}
+
 // C(j, b) *= w_j  (the -lambda weights of the negative modes)
 __global__ void kb_scale_rows(int m, const double* __restrict__ w, double* __restrict__ C) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -315,6 +323,7 @@ struct Block {
   int B = 0, ld = 0, G = 0;
   DArr<double> X, R, Z, Pm, Q, Bm, T, C0, C1, C2, C3, C4, C5;
   DArr<double> XS, WS;  // block-P layout
+  DArr<double> Pinv;    // optional P^s = V+ L+^-1 V+^T (NN), V layout
   DArr<double> zx, zr, zt, zc, negc, part;
   DArr<ColState> st;
   DArr<int> done, any_true;
@@ -428,6 +437,17 @@ struct BlockOps {
     kb_gather<<<grid_p(), kT, 0, c.stream>>>(c.P, c.psub.p, c.poff.p, c.pidx.p, c.ld.p, k.boff.p,
                                              nn ? c.ds.p : nullptr, k.ld, X, k.XS.p, done);
     const double one = 1.0, zero = 0.0;
+    if (nn && k.Pinv.p) {  // one DGEMM per subdomain with P^s = V+ L+^-1 V+^T
+      for (int s = 0; s < c.N; ++s) {
+        const int n = c.h_ns[s], L = c.h_ld[s];
+        AWG_BLAS(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, n, k.B, n, &one, k.Pinv.p + c.h_voff[s], L,
+                             k.XS.p + k.h_boff[s], L, &zero, k.WS.p + k.h_boff[s], L));
+      }
+      kb_prolong<<<grid_n(), kT, 0, c.stream>>>(c.n, k.ld, c.own_off.p, c.own_pos.p, c.psub.p, c.poff.p, c.ld.p,
+                                                k.boff.p, c.ds.p, k.WS.p, Y, done);
+      c.launches += 2;
+      return;
+    }
     for (int s = 0; s < c.N; ++s) {
       const int n = c.h_ns[s], L = c.h_ld[s];
       if (nn) {
@@ -498,9 +518,36 @@ void build_w_batched(Ctx& c, cublasHandle_t h, const std::vector<std::pair<int, 
   // bytes per batched column: 13 n-blocks, 2 restricted blocks, coarse and mode scratch
   const size_t per_col =
       sizeof(double) * (size_t(c.ldw) * 13 + size_t(c.P + 4 * c.N) * 2 + size_t(c.n0) * 4 + c.nneg + 256);
+  Block k;
+  // NN: precompute P^s = V+^s (L+^s)^-1 V+^s^T when it fits next to a block of
+  // >= 256 columns — halves the DGEMM work of every block one-level solve
+  const size_t pinv_bytes = sizeof(double) * size_t(c.h_voff[c.N]);
+  if (c.one_level == 2 && free_b > pinv_bytes + 256 * per_col * 10 / 7 + (size_t(2) << 30)) {
+    k.Pinv.alloc(size_t(c.h_voff[c.N]));
+    size_t tmax = 1;
+    for (int s = 0; s < c.N; ++s) tmax = std::max(tmax, size_t(c.h_ld[s]) * c.h_ns[s]);
+    DArr<double> T;
+    T.alloc(tmax);
+    AWG_BLAS(cublasSetStream(h, c.stream));
+    const double one = 1.0, zero = 0.0;
+    for (int s = 0; s < c.N; ++s) {
+      const int n = c.h_ns[s], L = c.h_ld[s], m = c.h_m[s];
+      const double* Vs = c.V.p + c.h_voff[s];
+      if (n - m > 0) {
+        kb_scale_inv<<<dim3((n + kT - 1) / kT, n - m), kT, 0, c.stream>>>(n, L, Vs + size_t(m) * L,
+                                                                          c.lam.p + c.h_poff[s] + m, T.p);
+        AWG_BLAS(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, n, n, n - m, &one, T.p, L, Vs + size_t(m) * L, L, &zero,
+                             k.Pinv.p + c.h_voff[s], L));
+        ++c.launches;
+      } else {
+        AWG_CUDA(cudaMemsetAsync(k.Pinv.p + c.h_voff[s], 0, sizeof(double) * L * n, c.stream));
+      }
+    }
+    AWG_CUDA(cudaStreamSynchronize(c.stream));
+    AWG_CUDA(cudaMemGetInfo(&free_b, &tot_b));
+  }
   int B = int(std::min<size_t>(size_t(max_block), (free_b * 7 / 10) / std::max<size_t>(per_col, 1)));
   B = std::max(1, std::min(B, total));
-  Block k;
   k.B = B;
   k.ld = c.ldw;
   k.G = std::max(1, std::min((c.n + kT - 1) / kT, 148));
