@@ -46,7 +46,7 @@ SAMPLE_SIZES = {"c1": (20, 4, 1), "c2": (160, 270, 20), "c3": (880, 2200, 30), "
 
 
 KERNEL_SYMBOL = {"nn_gemvT": "k_nn_gemvT", "nn_gemv": "k_nn_gemv", "spmv": "k_spmv", "w_gemvT": "k_dense_gemvT_part",
-                 "w_gemv": "k_dense_gemv"}
+                 "w_gemv": "k_dense_gemv", "nn_fused": "k_nn_fused"}
 
 
 def ncu_traffic(config, kernel):
@@ -122,11 +122,13 @@ class Clocks:
 
 
 def iteration_bytes(q, n, nnz):
-    """Algorithmic bytes of one PCG iteration (SURVEY.md §8d formula, this
-    implementation's factor form: V^s is read twice over the columns k >= m_s,
-    Z block-sparse, W dense)."""
+    """Algorithmic bytes of one PCG iteration (SURVEY.md §8d formula with this
+    implementation's factor form: the V^s columns k >= m_s are streamed once per
+    apply by the single-pass local solve (twice by the two-pass path), Z
+    block-sparse, W dense)."""
     b_spmv = 12 * nnz + 4 * (n + 1) + 16 * n
-    b_h1 = 8 * 2 * (q["sum_ns2"] - q["sum_ns_ms"]) + 8 * 3 * q["sum_ns"] + 8 * n
+    passes = 1 if q.get("nn_single_pass") else 2
+    b_h1 = 8 * passes * (q["sum_ns2"] - q["sum_ns_ms"]) + 8 * 3 * q["sum_ns"] + 8 * n
     b_q = 16 * q["sum_ns_ks"] + 8 * q["r0"] ** 2 + 16 * n
     b_am = 8 * q["sum_ns_qs"] + 16 * q["sum_ns"]
     b_w = 16 * n * q["n_minus"] + 8 * q["rw"] ** 2 + 16 * n
@@ -311,7 +313,8 @@ def main():
 
     # roofline of the dominant kernel pair (batched NN local solve), live
     peak, peak_kind = hbm_peak()
-    kt = {k: ctx.time_kernel(k, reps=5) for k in ("nn_gemvT", "nn_gemv", "spmv")}
+    names = ("nn_fused", "spmv") if q.get("nn_single_pass") else ("nn_gemvT", "nn_gemv", "spmv")
+    kt = {k: ctx.time_kernel(k, reps=5) for k in names}
     if q["n_minus"] > 0:
         kt.update({k: ctx.time_kernel(k, reps=5) for k in ("w_gemvT", "w_gemv")})
     dom = max(kt, key=lambda k: kt[k][0])

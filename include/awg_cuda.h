@@ -132,6 +132,7 @@ typedef struct awg_stats {
   double t_setup_ms[8]; /* splitting, pencils, coarse, w, misc... (see awg_setup) */
   int w_inner_total;    /* sum of inner PCG iterations of build_w */
   int w_batches;
+  int nn_single_pass;   /* 1: the NN local solve streams V^s once per apply (k_nn_fused) */
 } awg_stats;
 
 int awg_create(struct awg_ctx** ctx, int device);
@@ -169,7 +170,8 @@ long long awg_launch_count(const struct awg_ctx* ctx);
 int awg_time_apply(struct awg_ctx* ctx, int op, int reps, double* ms_per_apply);
 /* Device time (ms per launch, CUDA events on the context stream) of one hot
  * kernel launched `reps` times back to back: 0 batched NN GEMV^T (V^s^T x),
- * 1 batched NN GEMV (V^s u), 2 CSR SpMV, 3 W^T x, 4 W c.  Also returns the
+ * 1 batched NN GEMV (V^s u), 2 CSR SpMV, 3 W^T x, 4 W c, 5 single-pass NN
+ * local solve (V^s streamed once).  Also returns the
  * algorithmic bytes one launch must move (operands read once, results written). */
 int awg_time_kernel(struct awg_ctx* ctx, int which, int reps, double* ms_per_launch, double* bytes_per_launch);
 

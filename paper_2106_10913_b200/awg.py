@@ -156,6 +156,7 @@ class _Stats(ctypes.Structure):
         ("sum_ns", ctypes.c_longlong), ("sum_ns2", ctypes.c_longlong), ("sum_ns_ks", ctypes.c_longlong),
         ("sum_ns_ms", ctypes.c_longlong), ("sum_ns_qs", ctypes.c_longlong),
         ("t_setup_ms", ctypes.c_double * 8), ("w_inner_total", ctypes.c_int), ("w_batches", ctypes.c_int),
+        ("nn_single_pass", ctypes.c_int),
     ]
 
 
@@ -373,7 +374,7 @@ class ProblemContext:
         self._check(self._lib.awg_time_apply(self._h, int(op), reps, ctypes.byref(ms)))
         return ms.value
 
-    KERNELS = {"nn_gemvT": 0, "nn_gemv": 1, "spmv": 2, "w_gemvT": 3, "w_gemv": 4}
+    KERNELS = {"nn_gemvT": 0, "nn_gemv": 1, "spmv": 2, "w_gemvT": 3, "w_gemv": 4, "nn_fused": 5}
 
     def time_kernel(self, name: str, reps: int = 10) -> Tuple[float, float]:
         """(ms per launch, algorithmic bytes per launch) of one hot kernel."""

@@ -192,11 +192,41 @@ void finalize_factors(Ctx& c) {
     pl.nkc.upload(nkc, c.stream);
     pl.cols_max = 1;
     for (const auto& tk : t) pl.cols_max = std::max(pl.cols_max, tk.j1 - tk.j0);
+    // single-pass plan (NN): column ranges sized for >= 4 CTAs per SM in total
+    int ldmax = 0;
+    long long cols_total = 0;
+    for (int s = 0; s < N; ++s) {
+      ldmax = std::max(ldmax, c.h_ld[s]);
+      cols_total += c.h_ns[s] - (tri ? 0 : c.h_m[s]);
+    }
+    pl.fused = !tri && ldmax <= 6144 && c.use_fused;
+    if (pl.fused) {
+      const long long target = std::max<long long>(4LL * c.sm_count, N);
+      const int cs = int(std::max<long long>(64, (cols_total + target - 1) / target));
+      std::vector<GemvTask> tf;
+      std::vector<int> nkf(N, 0);
+      pl.kcmax_f = 1;
+      for (int s = 0; s < N; ++s) {
+        const int jstart = c.h_m[s];
+        const int cols = c.h_ns[s] - jstart;
+        const int kcs = std::max(1, (cols + cs / 2) / cs);
+        nkf[s] = kcs;
+        pl.kcmax_f = std::max(pl.kcmax_f, kcs);
+        for (int kc = 0; kc < kcs; ++kc) {
+          const int j0 = jstart + int((long long)cols * kc / kcs);
+          const int j1 = jstart + int((long long)cols * (kc + 1) / kcs);
+          tf.push_back({s, 0, j0, j1, kc, 0});
+        }
+      }
+      pl.tf.upload(tf, c.stream);
+      pl.nkc_f.upload(nkf, c.stream);
+    }
   };
   c.one_level = c.cfg.one_level;
   build_plan(c.plan_nn, false);
   if (c.one_level != 2) build_plan(c.plan_as, true);
-  const int kcmax = std::max(c.plan_nn.kcmax, c.one_level != 2 ? c.plan_as.kcmax : 1);
+  const int kcmax = std::max({c.plan_nn.kcmax, c.plan_nn.fused ? c.plan_nn.kcmax_f : 1,
+                              c.one_level != 2 ? c.plan_as.kcmax : 1});
   c.wpart_nn.alloc(size_t(kcmax) * std::max<long long>(c.P, 1));
   c.wpart_nn.zero(c.stream);
   // A- modes: k < n_nonpos with lambda != 0 (splitting.cpp:129-131), ascending (s, k)
@@ -322,6 +352,8 @@ int awg_create(awg_ctx** out, int device) {
     AWG_CUDA(cudaEventCreateWithFlags(&cc.ev_fork, cudaEventDisableTiming));
     AWG_CUDA(cudaEventCreateWithFlags(&cc.ev_join, cudaEventDisableTiming));
     AWG_CUDA(cudaDeviceGetAttribute(&cc.sm_count, cudaDevAttrMultiProcessorCount, device));
+    const char* two_pass = std::getenv("AWG_NN_TWO_PASS");
+    cc.use_fused = !(two_pass && two_pass[0] == '1');
   });
   *out = ctx;
   return rc;
@@ -577,6 +609,11 @@ int awg_time_kernel(awg_ctx* ctx, int which, int reps, double* ms, double* bytes
         b = 8.0 * c.n * c.nm + 8.0 * c.n + 8.0 * c.nm;
         launch = [&] { k::w_apply_public(c, c.cw.p, c.pz.p, nullptr); };
         break;
+      case 5:  // single-pass NN: V once + x gathered + partial slots written
+        if (!c.plan_nn.fused) c.fail(AWG_E_STATE, "time_kernel: single-pass local solve not available");
+        b = 8.0 * vcols + 20.0 * P + 8.0 * P * c.plan_nn.kcmax_f;
+        launch = [&] { k::nn_fused(c, c.pb.p, nullptr); };
+        break;
       default:
         c.fail(AWG_E_ARG, "time_kernel: unknown kernel");
     }
@@ -637,6 +674,7 @@ int awg_query(awg_ctx* ctx, awg_stats* st) {
     for (int i = 0; i < 8; ++i) st->t_setup_ms[i] = c.t_setup_ms[i];
     for (int v : c.h_w_inner) st->w_inner_total += v;
     st->w_batches = c.w_batches;
+    st->nn_single_pass = (c.one_level == 2 && c.plan_nn.fused) ? 1 : 0;
   });
 }
 

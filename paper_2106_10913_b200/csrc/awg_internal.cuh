@@ -106,6 +106,11 @@ struct LocalPlan {
   DArr<int> nkc;
   int cols_max = 0;
   int kcmax = 1;
+  // single-pass variant (k_nn_fused): column ranges per CTA, their chunk counts
+  bool fused = false;
+  DArr<GemvTask> tf;
+  DArr<int> nkc_f;
+  int kcmax_f = 1;
 };
 
 // Triangular coarse factor with retained pivots (RankRevealingFactor,
@@ -148,6 +153,7 @@ void h1(Ctx& c, const double* x, double* y, const int* gate);         // one-lev
 void nn_gemvT(Ctx& c, const double* x, const int* gate);               // uh = mask(1/lam) V^T D R x
 void nn_gemv(Ctx& c, const int* gate);                                 // part = V uh (column chunks)
 void nn_prolong(Ctx& c, double* y, const int* gate);                   // y = sum_s R^T D sum_kc part
+void nn_fused(Ctx& c, const double* x, const int* gate);               // single pass over V^s into part
 void aminus(Ctx& c, const double* x, double* y, const int* gate);     // y = A- x
 // mode 1: y = A+ x;  mode 2: y = sub - A+ x  (A- prolongation fused into the SpMV)
 void aplus(Ctx& c, const double* x, double* y, int mode, const double* sub, const int* gate);
@@ -201,6 +207,7 @@ struct Ctx {
   int rows_per_gemv = 512;
   int gemv_cols = 1024;  // column chunk of the split GEMV
   int one_level = 2;     // OneLevelKind of the configuration: 0 AS, 1 AS_PLUS, 2 NN
+  bool use_fused = true; // single-pass NN local solve (env AWG_NN_TWO_PASS=1 disables)
   LocalPlan plan_nn;     // V^s with the eigenvalue mask (NN)
   LocalPlan plan_as;     // U^s = L^-T, triangular (AS / AS+)
   DArr<double> U;        // AS / AS+ local factors, same layout as V

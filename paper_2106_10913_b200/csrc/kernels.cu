@@ -241,6 +241,146 @@ __global__ void __launch_bounds__(kThreads) k_nn_gemv(const int* __restrict__ ga
   if (i + 1 < n) out[i + 1] = a1 + b1;
 }
 
+// ---------------------------------------------------------------------------
+// Single-pass local solve: y_s = sum_j V(:, j) (V(:, j) . xs) / lambda_j over the
+// CTA's column range — the same V mask(1/lam) V^T product as gemvT + gemv, but
+// each column pair is brought into shared memory ONCE by a TMA bulk copy
+// (cp.async.bulk + mbarrier, double-buffered) and used for both the dot and
+// the rank-1 update, so V^s is streamed from HBM once per apply instead of
+// twice.  The restriction (D^s R^s x) and the partial y live in registers
+// (rows tid + kFusedT * k).  Partials land in the split-K layout of
+// k_nn_gemv; k_prolong_nn sums them in fixed order.
+// TRI: the AS / AS+ factor U^s = L^-T (no eigenvalue division, no D^s).
+constexpr int kFusedT = 512;
+constexpr int kFusedRows = 12;  // rows per thread: ld <= 6144
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arm(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+template <bool TRI>
+__global__ void __launch_bounds__(kFusedT, 1) k_nn_fused(const int* __restrict__ gate, const GemvTask* __restrict__ tasks,
+                                                         const double* __restrict__ V, const long long* __restrict__ voff,
+                                                         const int* __restrict__ ns, const int* __restrict__ ld,
+                                                         const long long* __restrict__ poff,
+                                                         const int* __restrict__ pidx, const double* __restrict__ ds,
+                                                         const double* __restrict__ x, const double* __restrict__ lam,
+                                                         long long P, double* __restrict__ part) {
+  if (gated(gate)) return;
+  extern __shared__ __align__(128) double fsm[];
+  __shared__ __align__(8) unsigned long long bar[2];
+  __shared__ double red[2][kFusedT / 32];
+  __shared__ double coef[2];
+  const GemvTask t = tasks[blockIdx.x];
+  const int s = t.s, n = ns[s], L = ld[s];
+  const long long p0 = poff[s];
+  const double* Vs = V + voff[s];
+  const int npair = (t.j1 - t.j0 + 1) >> 1;
+  const size_t bstride = 2 * (size_t)L;  // buffer b starts at fsm + b * bstride
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int p) {
+    const int j = t.j0 + 2 * p;
+    const int cols = min(2, t.j1 - j);
+    const unsigned bytes = unsigned(cols) * unsigned(L) * 8u;
+    mbar_arm(&bar[p & 1], bytes);
+    bulk_load(fsm + (p & 1) * bstride, Vs + (size_t)j * L, bytes, &bar[p & 1]);
+  };
+  if (tid == 0) {
+    if (npair > 0) issue(0);
+    if (npair > 1) issue(1);
+  }
+  double xr[kFusedRows], yr[kFusedRows];
+#pragma unroll
+  for (int k = 0; k < kFusedRows; ++k) {
+    const int i = tid + k * kFusedT;
+    double v = 0.0;
+    if (i < n) v = TRI ? __ldg(x + pidx[p0 + i]) : __ldg(x + pidx[p0 + i]) * ds[p0 + i];
+    xr[k] = v;
+    yr[k] = 0.0;
+  }
+  for (int p = 0; p < npair; ++p) {
+    const int j = t.j0 + 2 * p;
+    const bool two = (j + 1 < t.j1);
+    mbar_wait(&bar[p & 1], (p >> 1) & 1);
+    const double* c0 = fsm + (p & 1) * bstride;
+    const double* c1 = c0 + L;
+    double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+    for (int k = 0; k < kFusedRows; ++k) {
+      const int i = tid + k * kFusedT;
+      if (i < L) {
+        d0 = fma(c0[i], xr[k], d0);
+        if (two) d1 = fma(c1[i], xr[k], d1);
+      }
+    }
+    d0 = warp_sum(d0);
+    d1 = warp_sum(d1);
+    if (lane == 0) {
+      red[0][warp] = d0;
+      red[1][warp] = d1;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      double a = (lane < kFusedT / 32) ? red[0][lane] : 0.0;
+      double b = (lane < kFusedT / 32) ? red[1][lane] : 0.0;
+      a = warp_sum(a);
+      b = warp_sum(b);
+      if (lane == 0) {
+        coef[0] = TRI ? a : a / lam[p0 + j];
+        coef[1] = two ? (TRI ? b : b / lam[p0 + j + 1]) : 0.0;
+      }
+    }
+    __syncthreads();
+    const double u0 = coef[0], u1 = coef[1];
+#pragma unroll
+    for (int k = 0; k < kFusedRows; ++k) {
+      const int i = tid + k * kFusedT;
+      if (i < L) {
+        yr[k] = fma(c0[i], u0, yr[k]);
+        if (two) yr[k] = fma(c1[i], u1, yr[k]);
+      }
+    }
+    __syncthreads();  // buffer p & 1 is free again
+    if (tid == 0 && p + 2 < npair) issue(p + 2);
+  }
+  double* out = part + (size_t)t.kc * P + p0;
+#pragma unroll
+  for (int k = 0; k < kFusedRows; ++k) {
+    const int i = tid + k * kFusedT;
+    if (i < n) out[i] = yr[k];
+  }
+}
+
 // y[i] = sum over s containing i (ascending s) of D^s_i * (sum_kc part[kc][p(s,i)])
 __global__ void k_prolong_nn(const int* __restrict__ gate, int n, const int* __restrict__ own_off,
                              const int* __restrict__ own_pos, const int* __restrict__ psub,
@@ -636,7 +776,34 @@ void nn_prolong(Ctx& c, double* y, const int* gate) {
   check_launch("prolong_nn");
 }
 
+// single-pass NN local solve into the split-K partials (see k_nn_fused)
+void nn_fused(Ctx& c, const double* x, const int* gate) {
+  const LocalPlan& pl = c.plan_nn;
+  int ldmax = 0;
+  for (int v : c.h_ld) ldmax = std::max(ldmax, v);
+  const size_t smem = size_t(4) * ldmax * sizeof(double);
+  static size_t configured = 0;
+  if (smem > configured) {
+    AWG_CUDA(cudaFuncSetAttribute(k_nn_fused<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    configured = smem;
+  }
+  if (!pl.tf.n) return;
+  k_nn_fused<false><<<int(pl.tf.n), kFusedT, smem, c.stream>>>(gate, pl.tf.p, c.V.p, c.voff.p, c.ns.p, c.ld.p,
+                                                               c.poff.p, c.pidx.p, c.ds.p, x, c.lam.p, c.P,
+                                                               c.wpart_nn.p);
+  ++c.launches;
+  check_launch("nn_fused");
+}
+
 void h1(Ctx& c, const double* x, double* y, const int* gate) {
+  if (c.one_level == 2 && c.plan_nn.fused) {
+    nn_fused(c, x, gate);
+    k_prolong_nn<<<grid_for(c, c.n), kThreads, 0, c.stream>>>(gate, c.n, c.own_off.p, c.own_pos.p, c.psub.p,
+                                                             c.plan_nn.nkc_f.p, c.P, c.wpart_nn.p, c.ds.p, y);
+    ++c.launches;
+    check_launch("prolong_nn");
+    return;
+  }
   nn_gemvT(c, x, gate);
   nn_gemv(c, gate);
   nn_prolong(c, y, gate);

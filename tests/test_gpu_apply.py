@@ -135,3 +135,21 @@ def test_inex_exact_lu_matches_restatement(case):
                       lu_exact=True)
     for x in g["x_apply"]:
         assert rel(ctx.apply(awg.Op.H3, x), orc.h3(x, "inex")) <= 1e-10
+
+
+def test_single_pass_matches_two_pass():
+    """The single-pass local solve (k_nn_fused, V^s streamed once) and the
+    two-pass GEMV^T/GEMV path compute the same V mask(1/lam) V^T product."""
+    g, s = golden_with_base("t2d")
+    ctx1 = make_ctx(g)
+    assert ctx1.query()["nn_single_pass"] == 1
+    os.environ["AWG_NN_TWO_PASS"] = "1"
+    try:
+        ctx2 = make_ctx(g)
+    finally:
+        del os.environ["AWG_NN_TWO_PASS"]
+    assert ctx2.query()["nn_single_pass"] == 0
+    for x in g["x_apply"]:
+        y1, y2 = ctx1.apply(awg.Op.H1, x), ctx2.apply(awg.Op.H1, x)
+        assert rel(y1, y2) <= 1e-13
+        assert rel(y1, g["y_H1"][0] if x is g["x_apply"][0] else y1) <= 1e-11
