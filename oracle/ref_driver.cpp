@@ -426,6 +426,9 @@ int main(int argc, char** argv) {
   double t_h3 = now_s() - t0;
 
   std::fprintf(js, "  \"n\": %d, \"nnz\": %d, \"n_sub\": %d,\n", n, a.nnz(), N);
+  // report-only quantities of run_with_context (harness.cpp:172-174)
+  std::fprintf(js, "  \"coloring_A\": %d, \"coloring_Aplus\": %d,\n", coloring_constant(a, part).n_colors,
+               coloring_constant_aplus(a, part, split.has_negative_modes()).n_colors);
   std::fprintf(js, "  \"n0\": %d, \"r0\": %d, \"n_minus\": %d, \"rw\": %d,\n", cs.dim(), cs.retained_rank(),
                sc ? sc->n_minus() : 0, sc ? sc->kw.rank() : 0);
   std::fprintf(js, "  \"t_read\": %.6f, \"t_splitting\": %.6f, \"t_coarse\": %.6f, \"t_w\": %.6f, \"t_h3\": %.6f,\n",

@@ -299,7 +299,9 @@ __global__ void k_extract_l11(int n, int r, const double* __restrict__ w, double
 
 // --------------------------------------------------------------------------
 struct Solvers {
-  static constexpr int S = 4;
+  // concurrent eigensolves: syevd/sygvd of one subdomain leave most SMs idle
+  // in their tridiagonalization phase, so several run side by side
+  static constexpr int S = 8;
   cudaStream_t st[S] = {};
   cusolverDnHandle_t sol[S] = {};
   cublasHandle_t blas[S] = {};

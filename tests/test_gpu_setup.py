@@ -88,3 +88,23 @@ def test_exact_semantics_against_fixed_oracle(case):
     assert abs(rep.iterations - s["iterations"]) <= 1
     assert rel(xs, g["pcg_x"]) <= 1e-7
     assert np.array_equal(ctx.get("w_inner_iterations").size, len(g["w_inner_iterations"]))
+
+
+def test_report_outputs(tmp_path):
+    """run_with_context's report files (harness.cpp:151-224) from a GPU solve."""
+    import json
+
+    from paper_2106_10913_b200 import report
+
+    g, s = golden_with_base("t2d")
+    ctx = setup_ctx(g, s)
+    x, rep = ctx.pcg(g["b"], s["rtol_solve"], 10000)
+    r = report.write_outputs(str(tmp_path), "t2d run", ctx, ctx.cfg, rep, s["rtol_solve"], 10000)
+    assert r["problem"]["coloring_A"] == s["coloring_A"]
+    assert r["preconditioner"]["coarse_dim"] == s["n0"]
+    assert r["solve"]["iterations"] == rep.iterations
+    j = json.load(open(tmp_path / "t2d_run_report.json"))
+    assert j["preconditioner"]["n_minus"] == s["n_minus"]
+    lines = open(tmp_path / "rows.csv").read().splitlines()
+    assert lines[0] == "label,kappa,it,lambda_min,lambda_max,v0,n_minus" and len(lines) == 2
+    assert len(open(tmp_path / "t2d_run_residuals.csv").read().splitlines()) == rep.iterations + 1
