@@ -345,7 +345,9 @@ def main():
                    "l2": "inputs larger than L2" if q["sum_ns2"] * 8 > 126e6 else "inputs fit in L2 (no flush)"},
         "solve": {"iterations": its, "solve_ms_mean": dev_ms / args.steps, "t_iter_ms": t_iter_ms,
                   "n0": q["n0"], "r0": q["r0"], "n_minus": q["n_minus"], "rw": q["rw"]},
-        "setup_s": setup_s, "setup_phase_ms": q["t_setup_ms"][:6],
+        "setup_s": setup_s,
+        "setup_phase_ms": dict(zip(["splitting_Bs_eig", "pencils_selection", "coarse_G_factor", "w_inner_pcgs",
+                                    "wtaw_kw", "total"], q["t_setup_ms"][:6])),
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                      "peak_kind": peak_kind,

@@ -199,22 +199,25 @@ void finalize_factors(Ctx& c) {
       ldmax = std::max(ldmax, c.h_ld[s]);
       cols_total += c.h_ns[s] - (tri ? 0 : c.h_m[s]);
     }
-    pl.fused = !tri && ldmax <= 6144 && c.use_fused;
+    pl.fused = ldmax <= 6144 && c.use_fused;
     if (pl.fused) {
-      const long long target = std::max<long long>(4LL * c.sm_count, N);
+      const long long target = std::max<long long>(8LL * c.sm_count, N);  // queue granularity
       const int cs = int(std::max<long long>(64, (cols_total + target - 1) / target));
       std::vector<GemvTask> tf;
       std::vector<int> nkf(N, 0);
       pl.kcmax_f = 1;
       for (int s = 0; s < N; ++s) {
-        const int jstart = c.h_m[s];
+        const int jstart = tri ? 0 : c.h_m[s];
         const int cols = c.h_ns[s] - jstart;
         const int kcs = std::max(1, (cols + cs / 2) / cs);
         nkf[s] = kcs;
         pl.kcmax_f = std::max(pl.kcmax_f, kcs);
         for (int kc = 0; kc < kcs; ++kc) {
-          const int j0 = jstart + int((long long)cols * kc / kcs);
-          const int j1 = jstart + int((long long)cols * (kc + 1) / kcs);
+          // triangular factor: equal-area chunks (column j costs j + 1 rows)
+          const double f0 = tri ? std::sqrt(double(kc) / kcs) : double(kc) / kcs;
+          const double f1 = tri ? std::sqrt(double(kc + 1) / kcs) : double(kc + 1) / kcs;
+          const int j0 = jstart + int(cols * f0);
+          const int j1 = kc + 1 == kcs ? jstart + cols : jstart + int(cols * f1);
           tf.push_back({s, 0, j0, j1, kc, 0});
         }
       }
@@ -226,7 +229,8 @@ void finalize_factors(Ctx& c) {
   build_plan(c.plan_nn, false);
   if (c.one_level != 2) build_plan(c.plan_as, true);
   const int kcmax = std::max({c.plan_nn.kcmax, c.plan_nn.fused ? c.plan_nn.kcmax_f : 1,
-                              c.one_level != 2 ? c.plan_as.kcmax : 1});
+                              c.one_level != 2 ? c.plan_as.kcmax : 1,
+                              (c.one_level != 2 && c.plan_as.fused) ? c.plan_as.kcmax_f : 1});
   c.wpart_nn.alloc(size_t(kcmax) * std::max<long long>(c.P, 1));
   c.wpart_nn.zero(c.stream);
   // A- modes: k < n_nonpos with lambda != 0 (splitting.cpp:129-131), ascending (s, k)
@@ -610,7 +614,8 @@ int awg_time_kernel(awg_ctx* ctx, int which, int reps, double* ms, double* bytes
         launch = [&] { k::w_apply_public(c, c.cw.p, c.pz.p, nullptr); };
         break;
       case 5:  // single-pass NN: V once + x gathered + partial slots written
-        if (!c.plan_nn.fused) c.fail(AWG_E_STATE, "time_kernel: single-pass local solve not available");
+        if (!(c.one_level == 2 ? c.plan_nn.fused : c.plan_as.fused))
+          c.fail(AWG_E_STATE, "time_kernel: single-pass local solve not available");
         b = 8.0 * vcols + 20.0 * P + 8.0 * P * c.plan_nn.kcmax_f;
         launch = [&] { k::nn_fused(c, c.pb.p, nullptr); };
         break;
@@ -674,7 +679,7 @@ int awg_query(awg_ctx* ctx, awg_stats* st) {
     for (int i = 0; i < 8; ++i) st->t_setup_ms[i] = c.t_setup_ms[i];
     for (int v : c.h_w_inner) st->w_inner_total += v;
     st->w_batches = c.w_batches;
-    st->nn_single_pass = (c.one_level == 2 && c.plan_nn.fused) ? 1 : 0;
+    st->nn_single_pass = ((c.one_level == 2 && c.plan_nn.fused) || (c.one_level != 2 && c.plan_as.fused)) ? 1 : 0;
   });
 }
 

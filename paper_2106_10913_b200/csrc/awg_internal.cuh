@@ -212,6 +212,7 @@ struct Ctx {
   LocalPlan plan_as;     // U^s = L^-T, triangular (AS / AS+)
   DArr<double> U;        // AS / AS+ local factors, same layout as V
   DArr<double> wpart_nn; // kcmax x P partial sums
+  DArr<int> fused_queue; // work counter of the persistent single-pass kernel
 
   // A- modes
   int nneg = 0;

@@ -289,31 +289,52 @@ __global__ void __launch_bounds__(kFusedT, 1) k_nn_fused(const int* __restrict__
                                                          const long long* __restrict__ poff,
                                                          const int* __restrict__ pidx, const double* __restrict__ ds,
                                                          const double* __restrict__ x, const double* __restrict__ lam,
-                                                         long long P, double* __restrict__ part) {
+                                                         long long P, double* __restrict__ part, int ntasks,
+                                                         int* __restrict__ queue) {
   if (gated(gate)) return;
   extern __shared__ __align__(128) double fsm[];
   __shared__ __align__(8) unsigned long long bar[2];
   __shared__ double red[2][kFusedT / 32];
   __shared__ double coef[2];
-  const GemvTask t = tasks[blockIdx.x];
-  const int s = t.s, n = ns[s], L = ld[s];
-  const long long p0 = poff[s];
-  const double* Vs = V + voff[s];
-  const int npair = (t.j1 - t.j0 + 1) >> 1;
-  const size_t bstride = 2 * (size_t)L;  // buffer b starts at fsm + b * bstride
+  __shared__ int s_task;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  // Persistent CTAs (one per SM) pull column chunks from an atomic queue; the
+  // chunk -> partial-slot map is fixed by the task list, so the result does not
+  // depend on which CTA ran which chunk.  g counts the column pairs this CTA
+  // has consumed: buffer g & 1, mbarrier parity (g >> 1) & 1.
+  unsigned g = 0;
+  for (;;) {
   __syncthreads();
+  if (tid == 0) s_task = atomicAdd(queue, 1);
+  __syncthreads();
+  if (s_task >= ntasks) break;
+  const GemvTask t = tasks[s_task];
+  const int s = t.s, n = ns[s], L = ld[s];
+  const long long p0 = poff[s];
+  const double* Vs = V + voff[s];
+  const int npair = (t.j1 - t.j0 + 1) >> 1;
+  const size_t bstride = 2 * (size_t)L;  // buffer b starts at fsm + b * bstride
   auto issue = [&](int p) {
     const int j = t.j0 + 2 * p;
     const int cols = min(2, t.j1 - j);
-    const unsigned bytes = unsigned(cols) * unsigned(L) * 8u;
-    mbar_arm(&bar[p & 1], bytes);
-    bulk_load(fsm + (p & 1) * bstride, Vs + (size_t)j * L, bytes, &bar[p & 1]);
+    const unsigned b = (g + p) & 1;
+    if (!TRI) {
+      const unsigned bytes = unsigned(cols) * unsigned(L) * 8u;
+      mbar_arm(&bar[b], bytes);
+      bulk_load(fsm + b * bstride, Vs + (size_t)j * L, bytes, &bar[b]);
+    } else {
+      // upper-triangular U^s: column c holds rows 0..c; copy an even row count
+      const unsigned r0 = unsigned(min(L, (j + 2) & ~1));
+      const unsigned r1 = cols > 1 ? unsigned(min(L, (j + 3) & ~1)) : 0u;
+      mbar_arm(&bar[b], (r0 + r1) * 8u);
+      bulk_load(fsm + b * bstride, Vs + (size_t)j * L, r0 * 8u, &bar[b]);
+      if (cols > 1) bulk_load(fsm + b * bstride + L, Vs + (size_t)(j + 1) * L, r1 * 8u, &bar[b]);
+    }
   };
   if (tid == 0) {
     if (npair > 0) issue(0);
@@ -331,17 +352,18 @@ __global__ void __launch_bounds__(kFusedT, 1) k_nn_fused(const int* __restrict__
   for (int p = 0; p < npair; ++p) {
     const int j = t.j0 + 2 * p;
     const bool two = (j + 1 < t.j1);
-    mbar_wait(&bar[p & 1], (p >> 1) & 1);
-    const double* c0 = fsm + (p & 1) * bstride;
+    const unsigned gp = g + p;
+    mbar_wait(&bar[gp & 1], (gp >> 1) & 1);
+    const double* c0 = fsm + (gp & 1) * bstride;
     const double* c1 = c0 + L;
+    // TRI: only rows <= j (column j) and <= j + 1 (column j + 1) were copied
+    const int lim0 = TRI ? j + 1 : L, lim1 = TRI ? j + 2 : L;
     double d0 = 0.0, d1 = 0.0;
 #pragma unroll
     for (int k = 0; k < kFusedRows; ++k) {
       const int i = tid + k * kFusedT;
-      if (i < L) {
-        d0 = fma(c0[i], xr[k], d0);
-        if (two) d1 = fma(c1[i], xr[k], d1);
-      }
+      if (i < lim0) d0 = fma(c0[i], xr[k], d0);
+      if (two && i < lim1) d1 = fma(c1[i], xr[k], d1);
     }
     d0 = warp_sum(d0);
     d1 = warp_sum(d1);
@@ -365,12 +387,10 @@ __global__ void __launch_bounds__(kFusedT, 1) k_nn_fused(const int* __restrict__
 #pragma unroll
     for (int k = 0; k < kFusedRows; ++k) {
       const int i = tid + k * kFusedT;
-      if (i < L) {
-        yr[k] = fma(c0[i], u0, yr[k]);
-        if (two) yr[k] = fma(c1[i], u1, yr[k]);
-      }
+      if (i < lim0) yr[k] = fma(c0[i], u0, yr[k]);
+      if (two && i < lim1) yr[k] = fma(c1[i], u1, yr[k]);
     }
-    __syncthreads();  // buffer p & 1 is free again
+    __syncthreads();  // buffer gp & 1 is free again
     if (tid == 0 && p + 2 < npair) issue(p + 2);
   }
   double* out = part + (size_t)t.kc * P + p0;
@@ -378,6 +398,8 @@ __global__ void __launch_bounds__(kFusedT, 1) k_nn_fused(const int* __restrict__
   for (int k = 0; k < kFusedRows; ++k) {
     const int i = tid + k * kFusedT;
     if (i < n) out[i] = yr[k];
+  }
+  g += npair;
   }
 }
 
@@ -778,28 +800,41 @@ void nn_prolong(Ctx& c, double* y, const int* gate) {
 
 // single-pass NN local solve into the split-K partials (see k_nn_fused)
 void nn_fused(Ctx& c, const double* x, const int* gate) {
-  const LocalPlan& pl = c.plan_nn;
+  const bool nn = (c.one_level == 2);
+  const LocalPlan& pl = plan(c);
   int ldmax = 0;
   for (int v : c.h_ld) ldmax = std::max(ldmax, v);
   const size_t smem = size_t(4) * ldmax * sizeof(double);
   static size_t configured = 0;
   if (smem > configured) {
     AWG_CUDA(cudaFuncSetAttribute(k_nn_fused<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    AWG_CUDA(cudaFuncSetAttribute(k_nn_fused<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     configured = smem;
   }
   if (!pl.tf.n) return;
-  k_nn_fused<false><<<int(pl.tf.n), kFusedT, smem, c.stream>>>(gate, pl.tf.p, c.V.p, c.voff.p, c.ns.p, c.ld.p,
-                                                               c.poff.p, c.pidx.p, c.ds.p, x, c.lam.p, c.P,
-                                                               c.wpart_nn.p);
+  if (!c.fused_queue.p) c.fused_queue.alloc(1);
+  AWG_CUDA(cudaMemsetAsync(c.fused_queue.p, 0, sizeof(int), c.stream));
+  const int ntasks = int(pl.tf.n);
+  const int grid = std::min(ntasks, c.sm_count);
+  if (nn)
+    k_nn_fused<false><<<grid, kFusedT, smem, c.stream>>>(gate, pl.tf.p, c.V.p, c.voff.p, c.ns.p, c.ld.p, c.poff.p,
+                                                         c.pidx.p, c.ds.p, x, c.lam.p, c.P, c.wpart_nn.p, ntasks,
+                                                         c.fused_queue.p);
+  else
+    k_nn_fused<true><<<grid, kFusedT, smem, c.stream>>>(gate, pl.tf.p, c.U.p, c.voff.p, c.ns.p, c.ld.p, c.poff.p,
+                                                        c.pidx.p, nullptr, x, nullptr, c.P, c.wpart_nn.p, ntasks,
+                                                        c.fused_queue.p);
   ++c.launches;
   check_launch("nn_fused");
 }
 
 void h1(Ctx& c, const double* x, double* y, const int* gate) {
-  if (c.one_level == 2 && c.plan_nn.fused) {
+  const LocalPlan& pl = plan(c);
+  if (pl.fused) {
     nn_fused(c, x, gate);
     k_prolong_nn<<<grid_for(c, c.n), kThreads, 0, c.stream>>>(gate, c.n, c.own_off.p, c.own_pos.p, c.psub.p,
-                                                             c.plan_nn.nkc_f.p, c.P, c.wpart_nn.p, c.ds.p, y);
+                                                             pl.nkc_f.p, c.P, c.wpart_nn.p,
+                                                             c.one_level == 2 ? c.ds.p : nullptr, y);
     ++c.launches;
     check_launch("prolong_nn");
     return;
