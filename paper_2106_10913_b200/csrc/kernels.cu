@@ -253,6 +253,7 @@ __global__ void __launch_bounds__(kThreads) k_nn_gemv(const int* __restrict__ ga
 // TRI: the AS / AS+ factor U^s = L^-T (no eigenvalue division, no D^s).
 constexpr int kFusedT = 512;
 constexpr int kFusedRows = 12;  // rows per thread: ld <= 6144
+constexpr int kFusedMaxBuf = 6;  // deepest copy pipeline
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
@@ -282,7 +283,7 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
       : "memory");
 }
 
-template <bool TRI>
+template <bool TRI, int CPB>
 __global__ void __launch_bounds__(kFusedT, 1) k_nn_fused(const int* __restrict__ gate, const GemvTask* __restrict__ tasks,
                                                          const double* __restrict__ V, const long long* __restrict__ voff,
                                                          const int* __restrict__ ns, const int* __restrict__ ld,
@@ -290,23 +291,22 @@ __global__ void __launch_bounds__(kFusedT, 1) k_nn_fused(const int* __restrict__
                                                          const int* __restrict__ pidx, const double* __restrict__ ds,
                                                          const double* __restrict__ x, const double* __restrict__ lam,
                                                          long long P, double* __restrict__ part, int ntasks,
-                                                         int* __restrict__ queue) {
+                                                         int* __restrict__ queue, int nbuf) {
   if (gated(gate)) return;
   extern __shared__ __align__(128) double fsm[];
-  __shared__ __align__(8) unsigned long long bar[2];
-  __shared__ double red[2][kFusedT / 32];
-  __shared__ double coef[2];
+  __shared__ __align__(8) unsigned long long bar[kFusedMaxBuf];
+  __shared__ double red[CPB][kFusedT / 32];
   __shared__ int s_task;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+    for (int b = 0; b < nbuf; ++b) mbar_init(&bar[b], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   // Persistent CTAs (one per SM) pull column chunks from an atomic queue; the
   // chunk -> partial-slot map is fixed by the task list, so the result does not
-  // depend on which CTA ran which chunk.  g counts the column pairs this CTA
-  // has consumed: buffer g & 1, mbarrier parity (g >> 1) & 1.
+  // depend on which CTA ran which chunk.  A step covers CPB columns; g counts
+  // the steps this CTA has consumed: buffer g % nbuf, mbarrier parity
+  // (g / nbuf) & 1.  nbuf - 1 bulk copies stay in flight during every step.
   unsigned g = 0;
   for (;;) {
   __syncthreads();
@@ -317,29 +317,32 @@ __global__ void __launch_bounds__(kFusedT, 1) k_nn_fused(const int* __restrict__
   const int s = t.s, n = ns[s], L = ld[s];
   const long long p0 = poff[s];
   const double* Vs = V + voff[s];
-  const int npair = (t.j1 - t.j0 + 1) >> 1;
-  const size_t bstride = 2 * (size_t)L;  // buffer b starts at fsm + b * bstride
+  const int nstep = (t.j1 - t.j0 + CPB - 1) / CPB;
+  const size_t bstride = (size_t)CPB * L;  // buffer b starts at fsm + b * bstride
   auto issue = [&](int p) {
-    const int j = t.j0 + 2 * p;
-    const int cols = min(2, t.j1 - j);
-    const unsigned b = (g + p) & 1;
+    const int j = t.j0 + CPB * p;
+    const int cols = min(CPB, t.j1 - j);
+    const unsigned b = (g + p) % nbuf;
     if (!TRI) {
       const unsigned bytes = unsigned(cols) * unsigned(L) * 8u;
       mbar_arm(&bar[b], bytes);
       bulk_load(fsm + b * bstride, Vs + (size_t)j * L, bytes, &bar[b]);
     } else {
       // upper-triangular U^s: column c holds rows 0..c; copy an even row count
-      const unsigned r0 = unsigned(min(L, (j + 2) & ~1));
-      const unsigned r1 = cols > 1 ? unsigned(min(L, (j + 3) & ~1)) : 0u;
-      mbar_arm(&bar[b], (r0 + r1) * 8u);
-      bulk_load(fsm + b * bstride, Vs + (size_t)j * L, r0 * 8u, &bar[b]);
-      if (cols > 1) bulk_load(fsm + b * bstride + L, Vs + (size_t)(j + 1) * L, r1 * 8u, &bar[b]);
+      unsigned rows[CPB], total = 0;
+#pragma unroll
+      for (int c = 0; c < CPB; ++c) {
+        rows[c] = c < cols ? unsigned(min(L, (j + c + 2) & ~1)) : 0u;
+        total += rows[c];
+      }
+      mbar_arm(&bar[b], total * 8u);
+#pragma unroll
+      for (int c = 0; c < CPB; ++c)
+        if (rows[c]) bulk_load(fsm + b * bstride + (size_t)c * L, Vs + (size_t)(j + c) * L, rows[c] * 8u, &bar[b]);
     }
   };
-  if (tid == 0) {
-    if (npair > 0) issue(0);
-    if (npair > 1) issue(1);
-  }
+  if (tid == 0)
+    for (int p = 0; p < nbuf && p < nstep; ++p) issue(p);
   double xr[kFusedRows], yr[kFusedRows];
 #pragma unroll
   for (int k = 0; k < kFusedRows; ++k) {
@@ -349,49 +352,46 @@ __global__ void __launch_bounds__(kFusedT, 1) k_nn_fused(const int* __restrict__
     xr[k] = v;
     yr[k] = 0.0;
   }
-  for (int p = 0; p < npair; ++p) {
-    const int j = t.j0 + 2 * p;
-    const bool two = (j + 1 < t.j1);
+  for (int p = 0; p < nstep; ++p) {
+    const int j = t.j0 + CPB * p;
     const unsigned gp = g + p;
-    mbar_wait(&bar[gp & 1], (gp >> 1) & 1);
-    const double* c0 = fsm + (gp & 1) * bstride;
-    const double* c1 = c0 + L;
-    // TRI: only rows <= j (column j) and <= j + 1 (column j + 1) were copied
-    const int lim0 = TRI ? j + 1 : L, lim1 = TRI ? j + 2 : L;
-    double d0 = 0.0, d1 = 0.0;
+    mbar_wait(&bar[gp % nbuf], (gp / nbuf) & 1);
+    const double* cb = fsm + (gp % nbuf) * bstride;
+    double d[CPB];
 #pragma unroll
-    for (int k = 0; k < kFusedRows; ++k) {
-      const int i = tid + k * kFusedT;
-      if (i < lim0) d0 = fma(c0[i], xr[k], d0);
-      if (two && i < lim1) d1 = fma(c1[i], xr[k], d1);
-    }
-    d0 = warp_sum(d0);
-    d1 = warp_sum(d1);
-    if (lane == 0) {
-      red[0][warp] = d0;
-      red[1][warp] = d1;
+    for (int c = 0; c < CPB; ++c) {
+      // TRI: only rows <= j + c were copied for column j + c
+      const int lim = (j + c < t.j1) ? (TRI ? j + c + 1 : L) : 0;
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < kFusedRows; ++k) {
+        const int i = tid + k * kFusedT;
+        if (i < lim) acc = fma(cb[(size_t)c * L + i], xr[k], acc);
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) red[c][warp] = acc;
     }
     __syncthreads();
-    if (warp == 0) {
-      double a = (lane < kFusedT / 32) ? red[0][lane] : 0.0;
-      double b = (lane < kFusedT / 32) ? red[1][lane] : 0.0;
-      a = warp_sum(a);
-      b = warp_sum(b);
-      if (lane == 0) {
-        coef[0] = TRI ? a : a / lam[p0 + j];
-        coef[1] = two ? (TRI ? b : b / lam[p0 + j + 1]) : 0.0;
+    // every warp finishes the reduction itself (same fixed order everywhere)
+#pragma unroll
+    for (int c = 0; c < CPB; ++c) {
+      double a = 0.0;
+#pragma unroll
+      for (int w = 0; w < kFusedT / 32; ++w) a += red[c][w];
+      const bool live = (j + c < t.j1);
+      d[c] = live ? (TRI ? a : a / lam[p0 + j + c]) : 0.0;
+    }
+#pragma unroll
+    for (int c = 0; c < CPB; ++c) {
+      const int lim = (j + c < t.j1) ? (TRI ? j + c + 1 : L) : 0;
+#pragma unroll
+      for (int k = 0; k < kFusedRows; ++k) {
+        const int i = tid + k * kFusedT;
+        if (i < lim) yr[k] = fma(cb[(size_t)c * L + i], d[c], yr[k]);
       }
     }
-    __syncthreads();
-    const double u0 = coef[0], u1 = coef[1];
-#pragma unroll
-    for (int k = 0; k < kFusedRows; ++k) {
-      const int i = tid + k * kFusedT;
-      if (i < lim0) yr[k] = fma(c0[i], u0, yr[k]);
-      if (two && i < lim1) yr[k] = fma(c1[i], u1, yr[k]);
-    }
-    __syncthreads();  // buffer gp & 1 is free again
-    if (tid == 0 && p + 2 < npair) issue(p + 2);
+    __syncthreads();  // buffer gp % nbuf and red are free again
+    if (tid == 0 && p + nbuf < nstep) issue(p + nbuf);
   }
   double* out = part + (size_t)t.kc * P + p0;
 #pragma unroll
@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(kFusedT, 1) k_nn_fused(const int* __restrict__
     const int i = tid + k * kFusedT;
     if (i < n) out[i] = yr[k];
   }
-  g += npair;
+  g += nstep;
   }
 }
 
@@ -804,26 +804,45 @@ void nn_fused(Ctx& c, const double* x, const int* gate) {
   const LocalPlan& pl = plan(c);
   int ldmax = 0;
   for (int v : c.h_ld) ldmax = std::max(ldmax, v);
-  const size_t smem = size_t(4) * ldmax * sizeof(double);
+  // copy pipeline: 2-column steps when >= 3 of them fit in shared memory,
+  // otherwise 1-column steps; as many buffers as fit (<= kFusedMaxBuf)
+  const size_t cap = size_t(224) * 1024;
+  const size_t col_bytes = size_t(ldmax) * sizeof(double);
+  const int cpb = (cap / (2 * col_bytes) >= 3) ? 2 : 1;
+  const int nbuf = int(std::min<size_t>(kFusedMaxBuf, cap / (cpb * col_bytes)));
+  const size_t smem = size_t(nbuf) * cpb * col_bytes;
   static size_t configured = 0;
   if (smem > configured) {
-    AWG_CUDA(cudaFuncSetAttribute(k_nn_fused<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    AWG_CUDA(cudaFuncSetAttribute(k_nn_fused<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    configured = smem;
+    AWG_CUDA(cudaFuncSetAttribute(k_nn_fused<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(cap)));
+    AWG_CUDA(cudaFuncSetAttribute(k_nn_fused<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(cap)));
+    AWG_CUDA(cudaFuncSetAttribute(k_nn_fused<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(cap)));
+    AWG_CUDA(cudaFuncSetAttribute(k_nn_fused<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(cap)));
+    configured = cap;
   }
   if (!pl.tf.n) return;
   if (!c.fused_queue.p) c.fused_queue.alloc(1);
   AWG_CUDA(cudaMemsetAsync(c.fused_queue.p, 0, sizeof(int), c.stream));
   const int ntasks = int(pl.tf.n);
   const int grid = std::min(ntasks, c.sm_count);
-  if (nn)
-    k_nn_fused<false><<<grid, kFusedT, smem, c.stream>>>(gate, pl.tf.p, c.V.p, c.voff.p, c.ns.p, c.ld.p, c.poff.p,
-                                                         c.pidx.p, c.ds.p, x, c.lam.p, c.P, c.wpart_nn.p, ntasks,
-                                                         c.fused_queue.p);
+  const double* F = nn ? c.V.p : c.U.p;
+  const double* D = nn ? c.ds.p : nullptr;
+  const double* lam = nn ? c.lam.p : nullptr;
+  if (nn && cpb == 2)
+    k_nn_fused<false, 2><<<grid, kFusedT, smem, c.stream>>>(gate, pl.tf.p, F, c.voff.p, c.ns.p, c.ld.p, c.poff.p,
+                                                            c.pidx.p, D, x, lam, c.P, c.wpart_nn.p, ntasks,
+                                                            c.fused_queue.p, nbuf);
+  else if (nn)
+    k_nn_fused<false, 1><<<grid, kFusedT, smem, c.stream>>>(gate, pl.tf.p, F, c.voff.p, c.ns.p, c.ld.p, c.poff.p,
+                                                            c.pidx.p, D, x, lam, c.P, c.wpart_nn.p, ntasks,
+                                                            c.fused_queue.p, nbuf);
+  else if (cpb == 2)
+    k_nn_fused<true, 2><<<grid, kFusedT, smem, c.stream>>>(gate, pl.tf.p, F, c.voff.p, c.ns.p, c.ld.p, c.poff.p,
+                                                           c.pidx.p, D, x, lam, c.P, c.wpart_nn.p, ntasks,
+                                                           c.fused_queue.p, nbuf);
   else
-    k_nn_fused<true><<<grid, kFusedT, smem, c.stream>>>(gate, pl.tf.p, c.U.p, c.voff.p, c.ns.p, c.ld.p, c.poff.p,
-                                                        c.pidx.p, nullptr, x, nullptr, c.P, c.wpart_nn.p, ntasks,
-                                                        c.fused_queue.p);
+    k_nn_fused<true, 1><<<grid, kFusedT, smem, c.stream>>>(gate, pl.tf.p, F, c.voff.p, c.ns.p, c.ld.p, c.poff.p,
+                                                           c.pidx.p, D, x, lam, c.P, c.wpart_nn.p, ntasks,
+                                                           c.fused_queue.p, nbuf);
   ++c.launches;
   check_launch("nn_fused");
 }

@@ -51,6 +51,13 @@ double now_ms() {
   return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
+// progress trace on stderr when AWG_VERBOSE=1
+void trace(const Ctx& c, const std::string& what, double ms) {
+  (void)c;
+  const char* v = std::getenv("AWG_VERBOSE");
+  if (v && v[0] == '1') std::fprintf(stderr, "[awg setup] %s: %.1f s\n", what.c_str(), ms / 1e3);
+}
+
 // --------------------------------------------------------------------------
 // 1. dense local blocks from the CSR.  mode 0: B^s (A_ij / M_mu(ij)), mode 1: R A R^T.
 __global__ void k_assemble(int s, int n, int ld, const long long* __restrict__ poff, const int* __restrict__ pidx,
@@ -599,6 +606,7 @@ void run_setup(Ctx& c, const awg_config& cfg) {
     c.msz.upload(c.h_m, c.stream);
   }
   c.t_setup_ms[0] = now_ms() - t0;
+  trace(c, "splitting (B^s + eig)", c.t_setup_ms[0]);
 
   // ---- 4. pencils + 5. selection (coarse.cpp:98-130) --------------------------------
   // NN / AS+: pencil_nn = (weighted A+^s, R A+ R^T); AS: pencil_as1 = (weighted A+^s,
@@ -726,6 +734,7 @@ void run_setup(Ctx& c, const awg_config& cfg) {
   if (cfg.one_level != 2) local_cholesky(c, sv, lb);
   AWG_CUDA(cudaStreamSynchronize(c.stream));
   c.t_setup_ms[1] = now_ms() - t0;
+  trace(c, "pencils + selection (n0 = " + std::to_string(c.n0) + ")", c.t_setup_ms[1]);
 
   // ---- 6. coarse operator G = Z^T A+ Z and its pivoted factor ---------------------------
   t0 = now_ms();
@@ -751,6 +760,7 @@ void run_setup(Ctx& c, const awg_config& cfg) {
     pivoted_factor(c, G, c.n0, cfg.rrf_semantics, c.k0, c.n0);
   }
   c.t_setup_ms[2] = now_ms() - t0;
+  trace(c, "coarse operator + pivoted factor (r0 = " + std::to_string(c.k0.rank) + ")", c.t_setup_ms[2]);
 
   // ---- 7. second coarse space W (preconditioner.cpp:84-128) ------------------------------
   t0 = now_ms();
@@ -788,6 +798,7 @@ void run_setup(Ctx& c, const awg_config& cfg) {
     (void)col;
     c.neg_weights.upload(c.h_neg_weights, c.stream);
     c.t_setup_ms[3] = now_ms() - t0;
+    trace(c, "W inner PCGs (n_minus = " + std::to_string(nm) + ")", c.t_setup_ms[3]);
     // W^T A W (preconditioner.cpp:119-126)
     t0 = now_ms();
     c.nm = nm;

@@ -617,7 +617,16 @@ void build_w_batched(Ctx& c, cublasHandle_t h, const std::vector<std::pair<int, 
       AWG_CUDA(cudaMemcpyAsync(hs.data(), k.st.p, sizeof(ColState) * B, cudaMemcpyDeviceToHost, c.stream));
       AWG_CUDA(cudaStreamSynchronize(c.stream));
       bool all = true;
-      for (int j = 0; j < nb; ++j) all = all && hs[j].done;
+      int ndone = 0;
+      for (int j = 0; j < nb; ++j) {
+        all = all && hs[j].done;
+        ndone += hs[j].done ? 1 : 0;
+      }
+      if (it % 250 == 249) {
+        const char* v = std::getenv("AWG_VERBOSE");
+        if (v && v[0] == '1')
+          std::fprintf(stderr, "[awg setup]   W batch at iteration %d: %d of %d columns done\n", it + 1, ndone, nb);
+      }
       if (all) break;
     }
     AWG_CUDA(cudaMemcpyAsync(hs.data(), k.st.p, sizeof(ColState) * B, cudaMemcpyDeviceToHost, c.stream));
@@ -630,6 +639,15 @@ void build_w_batched(Ctx& c, cublasHandle_t h, const std::vector<std::pair<int, 
                                cudaMemcpyDeviceToDevice, c.stream));
     }
     ++c.w_batches;
+    {
+      const char* v = std::getenv("AWG_VERBOSE");
+      if (v && v[0] == '1') {
+        int itmax = 0;
+        for (int j = 0; j < nb; ++j) itmax = std::max(itmax, hs[j].it);
+        std::fprintf(stderr, "[awg setup] W batch %d: columns %d..%d (B = %d), max inner iterations %d\n",
+                     c.w_batches, c0, c0 + nb - 1, B, itmax);
+      }
+    }
   }
   AWG_CUDA(cudaStreamSynchronize(c.stream));
 }
