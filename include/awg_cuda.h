@@ -174,6 +174,10 @@ int awg_time_apply(struct awg_ctx* ctx, int op, int reps, double* ms_per_apply);
  * local solve (V^s streamed once).  Also returns the
  * algorithmic bytes one launch must move (operands read once, results written). */
 int awg_time_kernel(struct awg_ctx* ctx, int which, int reps, double* ms_per_launch, double* bytes_per_launch);
+/* Benchmark hook: synthetic local factors (V^s filled on the device with
+ * pseudo-random values, n_nonpos = m_per_sub zero modes, no coarse spaces) so
+ * the local-solve kernels can be timed at full scale without the setup. */
+int awg_synthetic_factors(struct awg_ctx* ctx, int m_per_sub, unsigned long long seed);
 
 #ifdef __cplusplus
 }

@@ -164,6 +164,7 @@ EXPORTED_SYMBOLS = [
     "awg_create", "awg_destroy", "awg_last_error", "awg_last_error_index", "awg_set_matrix",
     "awg_set_partition", "awg_setup", "awg_load_factors", "awg_apply", "awg_pcg", "awg_query",
     "awg_get_history", "awg_get_array", "awg_launch_count", "awg_time_apply", "awg_time_kernel",
+    "awg_synthetic_factors",
 ]
 
 _lib = None
@@ -198,6 +199,7 @@ def load_library(path: str = LIB_PATH):
     lib.awg_time_apply.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
     lib.awg_time_kernel.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
                                     ctypes.POINTER(ctypes.c_double)]
+    lib.awg_synthetic_factors.argtypes = [vp, ctypes.c_int, ctypes.c_ulonglong]
     _lib = lib
     return lib
 
@@ -419,6 +421,10 @@ class ProblemContext:
         self._check(self._lib.awg_get_array(self._h, which, arr.ctypes.data_as(ctypes.c_void_p), cnt.value,
                                              ctypes.byref(cnt)))
         return arr[:cnt.value]
+
+    def synthetic_factors(self, m_per_sub: int = 0, seed: int = 1):
+        """Benchmark hook: random local factors at full scale (no setup)."""
+        self._check(self._lib.awg_synthetic_factors(self._h, int(m_per_sub), int(seed)))
 
     def launch_count(self) -> int:
         return int(self._lib.awg_launch_count(self._h))

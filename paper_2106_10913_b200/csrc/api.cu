@@ -73,6 +73,17 @@ __global__ void k_core(int nm, const int* __restrict__ neg_s, const int* __restr
   if (lane == 0) core[i + (size_t)j * nm] = -acc + (i == j ? 1.0 / negw[j] : 0.0);
 }
 
+// synthetic factor values for kernel timing (awg_synthetic_factors)
+__global__ void k_fill_hash(size_t count, unsigned long long seed, double* __restrict__ v) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x) {
+    unsigned long long z = seed + 0x9E3779B97F4A7C15ull * (i + 1);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    v[i] = double(z >> 11) * 0x1.0p-53 - 0.5;
+  }
+}
+
 // lu_factor (dense.cpp:368-393): partial pivoting, first maximum, full row
 // swaps; single CTA (n_minus is small).
 __global__ void k_lu_factor(int m, double* __restrict__ a, int* __restrict__ perm, int* __restrict__ singular) {
@@ -201,7 +212,7 @@ void finalize_factors(Ctx& c) {
     }
     pl.fused = ldmax <= 6144 && c.use_fused;
     if (pl.fused) {
-      const long long target = std::max<long long>(8LL * c.sm_count, N);  // queue granularity
+      const long long target = std::max<long long>((long long)c.fused_chunks_per_sm * c.sm_count, N);  // queue granularity
       const int cs = int(std::max<long long>(64, (cols_total + target - 1) / target));
       std::vector<GemvTask> tf;
       std::vector<int> nkf(N, 0);
@@ -358,6 +369,13 @@ int awg_create(awg_ctx** out, int device) {
     AWG_CUDA(cudaDeviceGetAttribute(&cc.sm_count, cudaDevAttrMultiProcessorCount, device));
     const char* two_pass = std::getenv("AWG_NN_TWO_PASS");
     cc.use_fused = !(two_pass && two_pass[0] == '1');
+    auto env_int = [](const char* k, int dflt) {
+      const char* v = std::getenv(k);
+      return v ? std::atoi(v) : dflt;
+    };
+    cc.fused_cpb = env_int("AWG_FUSED_CPB", 0);
+    cc.fused_nbuf = env_int("AWG_FUSED_NBUF", 0);
+    cc.fused_chunks_per_sm = std::max(1, env_int("AWG_FUSED_CHUNKS", 4));
   });
   *out = ctx;
   return rc;
@@ -527,6 +545,44 @@ int awg_load_factors(awg_ctx* ctx, const awg_config* cfg, const awg_factors* f) 
     // AS / AS+: the local Cholesky factors are computed here from A (and the
     // loaded V^s for the A+ blocks); Cholesky factors are unique
     if (c.one_level != 2) build_local_cholesky(c);
+    AWG_CUDA(cudaStreamSynchronize(c.stream));
+    c.have_factors = true;
+  });
+}
+
+int awg_synthetic_factors(awg_ctx* ctx, int m_per_sub, unsigned long long seed) {
+  return guarded(ctx, [&](Ctx& c) {
+    if (c.N == 0) c.fail(AWG_E_STATE, "synthetic_factors: set matrix and partition first");
+    awg_config cfg{};
+    cfg.one_level = 2;
+    cfg.composition = 1;
+    cfg.use_coarse = 0;
+    cfg.awg_mode = 0;
+    cfg.tau_sharp = 0.1;
+    cfg.tau_flat = 10.0;
+    cfg.w_rtol = 1e-10;
+    c.cfg = cfg;
+    const int N = c.N;
+    c.h_m.assign(N, 0);
+    c.h_nzero.assign(N, 0);
+    c.h_ks.assign(N, 0);
+    c.h_lam.assign(c.P, 1.0);
+    for (int s = 0; s < N; ++s) {
+      c.h_m[s] = c.h_nzero[s] = std::max(0, std::min(m_per_sub, c.h_ns[s]));
+      for (int j = 0; j < c.h_ns[s]; ++j) c.h_lam[c.h_poff[s] + j] = j < c.h_m[s] ? 0.0 : 1.0 + 1e-3 * j;
+    }
+    c.h_eps.assign(N, 0.0);
+    c.lam.upload(c.h_lam, c.stream);
+    finalize_factors(c);
+    c.V.alloc(size_t(c.h_voff[N]));
+    k_fill_hash<<<c.sm_count * 8, 256, 0, c.stream>>>(c.V.n, seed, c.V.p);
+    ++c.launches;
+    check_launch("fill_hash");
+    c.Y.alloc(1);
+    c.k0.clear();
+    c.kw.clear();
+    c.nm = 0;
+    c.alloc_work();
     AWG_CUDA(cudaStreamSynchronize(c.stream));
     c.have_factors = true;
   });

@@ -208,6 +208,8 @@ struct Ctx {
   int gemv_cols = 1024;  // column chunk of the split GEMV
   int one_level = 2;     // OneLevelKind of the configuration: 0 AS, 1 AS_PLUS, 2 NN
   bool use_fused = true; // single-pass NN local solve (env AWG_NN_TWO_PASS=1 disables)
+  // single-pass tuning (env AWG_FUSED_CPB / AWG_FUSED_NBUF / AWG_FUSED_CHUNKS; 0 = automatic)
+  int fused_cpb = 0, fused_nbuf = 0, fused_chunks_per_sm = 4;
   LocalPlan plan_nn;     // V^s with the eigenvalue mask (NN)
   LocalPlan plan_as;     // U^s = L^-T, triangular (AS / AS+)
   DArr<double> U;        // AS / AS+ local factors, same layout as V

@@ -808,8 +808,11 @@ void nn_fused(Ctx& c, const double* x, const int* gate) {
   // otherwise 1-column steps; as many buffers as fit (<= kFusedMaxBuf)
   const size_t cap = size_t(224) * 1024;
   const size_t col_bytes = size_t(ldmax) * sizeof(double);
-  const int cpb = (cap / (2 * col_bytes) >= 3) ? 2 : 1;
-  const int nbuf = int(std::min<size_t>(kFusedMaxBuf, cap / (cpb * col_bytes)));
+  int cpb = (cap / (2 * col_bytes) >= 3) ? 2 : 1;
+  if (c.fused_cpb > 0) cpb = std::min(2, c.fused_cpb);
+  int nbuf = int(std::min<size_t>(kFusedMaxBuf, cap / (cpb * col_bytes)));
+  if (c.fused_nbuf > 0) nbuf = std::min(nbuf, c.fused_nbuf);
+  if (nbuf < 2) c.fail(AWG_E_STATE, "single-pass local solve: subdomain too large for the copy pipeline");
   const size_t smem = size_t(nbuf) * cpb * col_bytes;
   static size_t configured = 0;
   if (smem > configured) {

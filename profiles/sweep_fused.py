@@ -1,0 +1,38 @@
+"""Time the local-solve kernels on synthetic factors at full scale for several
+single-pass pipeline settings (env knobs read at context creation).
+    python profiles/sweep_fused.py c2 c5"""
+import itertools
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2106_10913_b200 import awg, problems  # noqa: E402
+
+for cfg in sys.argv[1:] or ["c2"]:
+    p = problems.make(cfg)
+    rows = []
+    settings = [("two-pass", {"AWG_NN_TWO_PASS": "1"})]
+    for cpb, nbuf, chunks in itertools.product([1, 2], [2, 3, 4, 6], [1, 2, 4, 8]):
+        settings.append((f"cpb{cpb}_nbuf{nbuf}_chunks{chunks}",
+                         {"AWG_FUSED_CPB": str(cpb), "AWG_FUSED_NBUF": str(nbuf), "AWG_FUSED_CHUNKS": str(chunks)}))
+    for name, env in settings:
+        for k in ("AWG_NN_TWO_PASS", "AWG_FUSED_CPB", "AWG_FUSED_NBUF", "AWG_FUSED_CHUNKS"):
+            os.environ.pop(k, None)
+        os.environ.update(env)
+        try:
+            ctx = awg.context_from_problem(p)
+            ctx.synthetic_factors(m_per_sub=8)
+            if name == "two-pass":
+                a = ctx.time_kernel("nn_gemvT", reps=5)
+                b = ctx.time_kernel("nn_gemv", reps=5)
+                ms, by = a[0] + b[0], a[1] + b[1]
+            else:
+                ms, by = ctx.time_kernel("nn_fused", reps=5)
+            h1 = ctx.time_apply(awg.Op.H1, reps=5)
+            rows.append({"setting": name, "kernel_ms": ms, "GBps": by / ms / 1e6, "h1_ms": h1})
+            ctx.close()
+        except Exception as e:  # noqa: BLE001
+            rows.append({"setting": name, "error": str(e)[:120]})
+    rows.sort(key=lambda r: r.get("h1_ms", 1e9))
+    print(json.dumps({"config": cfg, "results": rows}))
