@@ -417,8 +417,10 @@ def make(name: str) -> Problem:
         return fd_problem("t3d_blocks", (8, 8, 8), block_powers((8, 8, 8), 4), (2, 2, 2), 1, fixed_k=3)
     if name == "telas":  # c4 analogue
         return elasticity_problem("telas", 16, 8, 2, [(1e7, 0.45), (1.0, 0.3)], (2, 1), 1, tau_sharp=0.1)
+    if name == "telas8":  # c4 analogue with c4's 8-element layers and 2x2 nodal boxes
+        return elasticity_problem("telas8", 32, 16, 8, [(1e7, 0.45), (1.0, 0.3)], (2, 2), 1, tau_sharp=0.1)
     raise KeyError(name)
 
 
 CONFIGS = ["c1", "c2", "c3", "c4", "c5"]
-ANALOGUES = ["t2d", "t2d_ov2", "t3d", "t3d_blocks", "telas"]
+ANALOGUES = ["t2d", "t2d_ov2", "t3d", "t3d_blocks", "telas", "telas8"]

@@ -41,6 +41,7 @@ CASES = {
     "t3d_none": ("t3d", "ref_driver", ["--awg", "none"], False, "t3d"),
     "t3d_blocks": ("t3d_blocks", "ref_driver", [], False, None),
     "telas": ("telas", "ref_driver", [], True, None),
+    "telas8": ("telas8", "ref_driver", [], False, None),
     # one-level AS / AS+ (Cholesky factor form, preconditioner.cpp:20-30) with their
     # coarse spaces (coarse.cpp:122-130): Y comes from other pencils, so it is kept
     "t2d_as": ("t2d", "ref_driver", ["--one-level", "AS", "--tau-flat", "10"], False, "t2d"),

@@ -12,7 +12,7 @@ from paper_2106_10913_b200 import awg
 
 pytestmark = pytest.mark.gpu
 
-BASE = ["c1", "t2d", "t2d_ov2", "t3d", "t3d_blocks", "telas"]
+BASE = ["c1", "t2d", "t2d_ov2", "t3d", "t3d_blocks", "telas", "telas8"]
 
 
 KINDS = {"NN": awg.OneLevelKind.NN, "AS": awg.OneLevelKind.AS, "AS_PLUS": awg.OneLevelKind.AS_PLUS}
@@ -87,7 +87,11 @@ def test_exact_semantics_against_fixed_oracle(case):
     xs, rep = ctx.pcg(g["b"], s["rtol_solve"], 10000)
     assert abs(rep.iterations - s["iterations"]) <= 1
     assert rel(xs, g["pcg_x"]) <= 1e-7
-    assert np.array_equal(ctx.get("w_inner_iterations").size, len(g["w_inner_iterations"]))
+    # the batched W build keeps the per-column PCG semantics of build_w: every
+    # inner solve stops at (nearly) the same iteration as the reference's
+    inner = ctx.get("w_inner_iterations")
+    assert inner.size == len(g["w_inner_iterations"])
+    assert np.max(np.abs(inner - g["w_inner_iterations"])) <= 2, (inner, g["w_inner_iterations"])
 
 
 def test_report_outputs(tmp_path):
