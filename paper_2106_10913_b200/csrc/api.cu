@@ -173,6 +173,12 @@ void finalize_factors(Ctx& c) {
   c.msz.upload(c.h_m, c.stream);
   c.voff.upload(c.h_voff, c.stream);
   c.yoff.upload(c.h_yoff, c.stream);
+  {
+    std::vector<double> rl(c.h_lam.size(), 0.0);
+    for (size_t i = 0; i < rl.size(); ++i)
+      if (c.h_lam[i] > 0.0) rl[i] = 1.0 / c.h_lam[i];
+    c.rlam.upload(rl, c.stream);
+  }
   // local-solve task lists: NN always (V^s columns j >= n_nonpos), AS/AS+ when configured
   auto build_plan = [&](LocalPlan& pl, bool tri) {
     std::vector<GemvTTask> tT;
@@ -213,7 +219,9 @@ void finalize_factors(Ctx& c) {
     pl.fused = ldmax <= 6144 && c.use_fused;
     if (pl.fused) {
       const long long target = std::max<long long>((long long)c.fused_chunks_per_sm * c.sm_count, N);  // queue granularity
-      const int cs = int(std::max<long long>(64, (cols_total + target - 1) / target));
+      // >= 128 columns per task keeps the per-task restriction gather and partial
+      // write (about 3 columns' worth of traffic) below ~3%
+      const int cs = int(std::max<long long>(128, (cols_total + target - 1) / target));
       std::vector<GemvTask> tf;
       std::vector<int> nkf(N, 0);
       pl.kcmax_f = 1;
@@ -375,7 +383,7 @@ int awg_create(awg_ctx** out, int device) {
     };
     cc.fused_cpb = env_int("AWG_FUSED_CPB", 0);
     cc.fused_nbuf = env_int("AWG_FUSED_NBUF", 0);
-    cc.fused_chunks_per_sm = std::max(1, env_int("AWG_FUSED_CHUNKS", 4));
+    cc.fused_chunks_per_sm = std::max(1, env_int("AWG_FUSED_CHUNKS", 8));
   });
   *out = ctx;
   return rc;

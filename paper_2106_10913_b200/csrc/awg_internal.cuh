@@ -204,12 +204,13 @@ struct Ctx {
   DArr<int> ns, ld, msz;
   DArr<long long> voff;
   DArr<double> V, lam;
+  DArr<double> rlam;  // 1 / lambda for lambda > 0 (single-pass local solve), else 0
   int rows_per_gemv = 512;
   int gemv_cols = 1024;  // column chunk of the split GEMV
   int one_level = 2;     // OneLevelKind of the configuration: 0 AS, 1 AS_PLUS, 2 NN
   bool use_fused = true; // single-pass NN local solve (env AWG_NN_TWO_PASS=1 disables)
   // single-pass tuning (env AWG_FUSED_CPB / AWG_FUSED_NBUF / AWG_FUSED_CHUNKS; 0 = automatic)
-  int fused_cpb = 0, fused_nbuf = 0, fused_chunks_per_sm = 4;
+  int fused_cpb = 0, fused_nbuf = 0, fused_chunks_per_sm = 8;  // 0: automatic
   LocalPlan plan_nn;     // V^s with the eigenvalue mask (NN)
   LocalPlan plan_as;     // U^s = L^-T, triangular (AS / AS+)
   DArr<double> U;        // AS / AS+ local factors, same layout as V

@@ -244,16 +244,20 @@ __global__ void __launch_bounds__(kThreads) k_nn_gemv(const int* __restrict__ ga
 // ---------------------------------------------------------------------------
 // Single-pass local solve: y_s = sum_j V(:, j) (V(:, j) . xs) / lambda_j over the
 // CTA's column range — the same V mask(1/lam) V^T product as gemvT + gemv, but
-// each column pair is brought into shared memory ONCE by a TMA bulk copy
-// (cp.async.bulk + mbarrier, double-buffered) and used for both the dot and
-// the rank-1 update, so V^s is streamed from HBM once per apply instead of
-// twice.  The restriction (D^s R^s x) and the partial y live in registers
-// (rows tid + kFusedT * k).  Partials land in the split-K layout of
-// k_nn_gemv; k_prolong_nn sums them in fixed order.
+// each column (or column pair) is brought into shared memory ONCE by a TMA bulk
+// copy (cp.async.bulk + mbarrier, up to kFusedMaxBuf buffers in flight) and
+// used there for both the dot and the rank-1 update, so V^s is streamed from
+// HBM once per apply instead of twice.  The restriction (D^s R^s x) and the
+// partial y live in registers (rows tid + kFusedT * k, k < R).  The loops carry
+// no bounds checks or branches (a branch per row made the first version
+// latency-bound: ~1,900 cycles per column on the dependent chains, see
+// profiles/README.md).  Partials land in the split-K layout of k_nn_gemv;
+// k_prolong_nn sums them in fixed order.
 // TRI: the AS / AS+ factor U^s = L^-T (no eigenvalue division, no D^s).
 constexpr int kFusedT = 512;
-constexpr int kFusedRows = 12;  // rows per thread: ld <= 6144
+constexpr int kFusedRowsMax = 12;  // rows per thread: ld <= 6144
 constexpr int kFusedMaxBuf = 6;  // deepest copy pipeline
+constexpr size_t kFusedSmemCap = size_t(224) * 1024;  // dynamic shared memory per CTA
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
@@ -283,123 +287,140 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
       : "memory");
 }
 
-template <bool TRI, int CPB>
+template <bool TRI, int R, int CPB>
 __global__ void __launch_bounds__(kFusedT, 1) k_nn_fused(const int* __restrict__ gate, const GemvTask* __restrict__ tasks,
                                                          const double* __restrict__ V, const long long* __restrict__ voff,
                                                          const int* __restrict__ ns, const int* __restrict__ ld,
                                                          const long long* __restrict__ poff,
                                                          const int* __restrict__ pidx, const double* __restrict__ ds,
-                                                         const double* __restrict__ x, const double* __restrict__ lam,
+                                                         const double* __restrict__ x, const double* __restrict__ rlam,
                                                          long long P, double* __restrict__ part, int ntasks,
-                                                         int* __restrict__ queue, int nbuf) {
+                                                         int* __restrict__ queue, int nbuf, int ldmax, int smem_doubles) {
   if (gated(gate)) return;
   extern __shared__ __align__(128) double fsm[];
   __shared__ __align__(8) unsigned long long bar[kFusedMaxBuf];
-  __shared__ double red[CPB][kFusedT / 32];
+  __shared__ double red[2][CPB][kFusedT / 32];
   __shared__ int s_task;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // Rows are read without bounds checks (no branches in the hot loops): rows
+  // past a column's end read the next column or the zeroed tail, which meet
+  // xr = 0 in the dot and land in rows of yr that are never written out; TRI
+  // masks by value.  So the whole buffer area starts finite.
+  for (int i = tid; i < smem_doubles; i += kFusedT) fsm[i] = 0.0;
   if (tid == 0) {
     for (int b = 0; b < nbuf; ++b) mbar_init(&bar[b], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  // order the zero fill (generic proxy) before the first bulk copies (async proxy)
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  const size_t bstride = (size_t)CPB * ldmax;  // buffer b starts at fsm + b * bstride
   // Persistent CTAs (one per SM) pull column chunks from an atomic queue; the
   // chunk -> partial-slot map is fixed by the task list, so the result does not
   // depend on which CTA ran which chunk.  A step covers CPB columns; g counts
   // the steps this CTA has consumed: buffer g % nbuf, mbarrier parity
-  // (g / nbuf) & 1.  nbuf - 1 bulk copies stay in flight during every step.
+  // (g / nbuf) & 1.  One barrier per step: red is double-buffered, and the
+  // buffer of the previous step is refilled right after the barrier.
   unsigned g = 0;
   for (;;) {
-  __syncthreads();
-  if (tid == 0) s_task = atomicAdd(queue, 1);
-  __syncthreads();
-  if (s_task >= ntasks) break;
-  const GemvTask t = tasks[s_task];
-  const int s = t.s, n = ns[s], L = ld[s];
-  const long long p0 = poff[s];
-  const double* Vs = V + voff[s];
-  const int nstep = (t.j1 - t.j0 + CPB - 1) / CPB;
-  const size_t bstride = (size_t)CPB * L;  // buffer b starts at fsm + b * bstride
-  auto issue = [&](int p) {
-    const int j = t.j0 + CPB * p;
-    const int cols = min(CPB, t.j1 - j);
-    const unsigned b = (g + p) % nbuf;
-    if (!TRI) {
-      const unsigned bytes = unsigned(cols) * unsigned(L) * 8u;
-      mbar_arm(&bar[b], bytes);
-      bulk_load(fsm + b * bstride, Vs + (size_t)j * L, bytes, &bar[b]);
-    } else {
-      // upper-triangular U^s: column c holds rows 0..c; copy an even row count
-      unsigned rows[CPB], total = 0;
+    __syncthreads();
+    if (tid == 0) s_task = atomicAdd(queue, 1);
+    __syncthreads();
+    if (s_task >= ntasks) break;
+    const GemvTask t = tasks[s_task];
+    const int s = t.s, n = ns[s], L = ld[s];
+    const long long p0 = poff[s];
+    const double* Vs = V + voff[s];
+    const int nstep = (t.j1 - t.j0 + CPB - 1) / CPB;
+    auto issue = [&](int p) {
+      const int j = t.j0 + CPB * p;
+      const int cols = min(CPB, t.j1 - j);
+      const unsigned b = (g + p) % nbuf;
+      if (!TRI) {
+        const unsigned bytes = unsigned(cols) * unsigned(L) * 8u;
+        mbar_arm(&bar[b], bytes);
+        bulk_load(fsm + b * bstride, Vs + (size_t)j * L, bytes, &bar[b]);
+      } else {
+        // upper-triangular U^s: column c holds rows 0..c; copy an even row count
+        unsigned rows[CPB], total = 0;
+#pragma unroll
+        for (int c = 0; c < CPB; ++c) {
+          rows[c] = c < cols ? unsigned(min(L, (j + c + 2) & ~1)) : 0u;
+          total += rows[c];
+        }
+        mbar_arm(&bar[b], total * 8u);
+#pragma unroll
+        for (int c = 0; c < CPB; ++c)
+          if (rows[c]) bulk_load(fsm + b * bstride + (size_t)c * L, Vs + (size_t)(j + c) * L, rows[c] * 8u, &bar[b]);
+      }
+    };
+    if (tid == 0)
+      for (int p = 0; p < nbuf && p < nstep; ++p) issue(p);
+    double xr[R], yr[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const int i = tid + k * kFusedT;
+      double v = 0.0;
+      if (i < n) v = TRI ? __ldg(x + pidx[p0 + i]) : __ldg(x + pidx[p0 + i]) * ds[p0 + i];
+      xr[k] = v;
+      yr[k] = 0.0;
+    }
+    for (int p = 0; p < nstep; ++p) {
+      const int j = t.j0 + CPB * p;
+      const unsigned gp = g + p;
+      double rl[CPB];  // issued before the wait: off the post-barrier critical path
+#pragma unroll
+      for (int c = 0; c < CPB; ++c) rl[c] = (!TRI && j + c < t.j1) ? __ldg(rlam + p0 + j + c) : 0.0;
+      mbar_wait(&bar[gp % nbuf], (gp / nbuf) & 1);
+      const double* cb = fsm + (gp % nbuf) * bstride;
+      // dots: two interleaved accumulators per column, fixed order
 #pragma unroll
       for (int c = 0; c < CPB; ++c) {
-        rows[c] = c < cols ? unsigned(min(L, (j + c + 2) & ~1)) : 0u;
-        total += rows[c];
+        const double* col = cb + (size_t)c * L;
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+          double v = col[tid + k * kFusedT];
+          if (TRI) v = (tid + k * kFusedT <= j + c) ? v : 0.0;
+          if (k & 1)
+            a1 = fma(v, xr[k], a1);
+          else
+            a0 = fma(v, xr[k], a0);
+        }
+        const double acc = warp_sum(a0 + a1);
+        if (lane == 0) red[gp & 1][c][warp] = acc;
       }
-      mbar_arm(&bar[b], total * 8u);
+      __syncthreads();
+      // the previous step's buffer is no longer read by anyone
+      if (tid == 0 && p >= 1 && p - 1 + nbuf < nstep) issue(p - 1 + nbuf);
+      double d[CPB];
 #pragma unroll
-      for (int c = 0; c < CPB; ++c)
-        if (rows[c]) bulk_load(fsm + b * bstride + (size_t)c * L, Vs + (size_t)(j + c) * L, rows[c] * 8u, &bar[b]);
-    }
-  };
-  if (tid == 0)
-    for (int p = 0; p < nbuf && p < nstep; ++p) issue(p);
-  double xr[kFusedRows], yr[kFusedRows];
+      for (int c = 0; c < CPB; ++c) {
+        const double* r = red[gp & 1][c];
+        double r8[8];
 #pragma unroll
-  for (int k = 0; k < kFusedRows; ++k) {
-    const int i = tid + k * kFusedT;
-    double v = 0.0;
-    if (i < n) v = TRI ? __ldg(x + pidx[p0 + i]) : __ldg(x + pidx[p0 + i]) * ds[p0 + i];
-    xr[k] = v;
-    yr[k] = 0.0;
-  }
-  for (int p = 0; p < nstep; ++p) {
-    const int j = t.j0 + CPB * p;
-    const unsigned gp = g + p;
-    mbar_wait(&bar[gp % nbuf], (gp / nbuf) & 1);
-    const double* cb = fsm + (gp % nbuf) * bstride;
-    double d[CPB];
-#pragma unroll
-    for (int c = 0; c < CPB; ++c) {
-      // TRI: only rows <= j + c were copied for column j + c
-      const int lim = (j + c < t.j1) ? (TRI ? j + c + 1 : L) : 0;
-      double acc = 0.0;
-#pragma unroll
-      for (int k = 0; k < kFusedRows; ++k) {
-        const int i = tid + k * kFusedT;
-        if (i < lim) acc = fma(cb[(size_t)c * L + i], xr[k], acc);
+        for (int w = 0; w < 8; ++w) r8[w] = r[w] + r[w + 8];
+        const double a = ((r8[0] + r8[4]) + (r8[2] + r8[6])) + ((r8[1] + r8[5]) + (r8[3] + r8[7]));
+        const bool live = (j + c < t.j1);
+        d[c] = live ? (TRI ? a : a * rl[c]) : 0.0;
       }
-      acc = warp_sum(acc);
-      if (lane == 0) red[c][warp] = acc;
-    }
-    __syncthreads();
-    // every warp finishes the reduction itself (same fixed order everywhere)
 #pragma unroll
-    for (int c = 0; c < CPB; ++c) {
-      double a = 0.0;
+      for (int c = 0; c < CPB; ++c) {
+        const double* col = cb + (size_t)c * L;
 #pragma unroll
-      for (int w = 0; w < kFusedT / 32; ++w) a += red[c][w];
-      const bool live = (j + c < t.j1);
-      d[c] = live ? (TRI ? a : a / lam[p0 + j + c]) : 0.0;
-    }
-#pragma unroll
-    for (int c = 0; c < CPB; ++c) {
-      const int lim = (j + c < t.j1) ? (TRI ? j + c + 1 : L) : 0;
-#pragma unroll
-      for (int k = 0; k < kFusedRows; ++k) {
-        const int i = tid + k * kFusedT;
-        if (i < lim) yr[k] = fma(cb[(size_t)c * L + i], d[c], yr[k]);
+        for (int k = 0; k < R; ++k) {
+          double v = col[tid + k * kFusedT];
+          if (TRI) v = (tid + k * kFusedT <= j + c) ? v : 0.0;
+          yr[k] = fma(v, d[c], yr[k]);
+        }
       }
     }
-    __syncthreads();  // buffer gp % nbuf and red are free again
-    if (tid == 0 && p + nbuf < nstep) issue(p + nbuf);
-  }
-  double* out = part + (size_t)t.kc * P + p0;
+    double* out = part + (size_t)t.kc * P + p0;
 #pragma unroll
-  for (int k = 0; k < kFusedRows; ++k) {
-    const int i = tid + k * kFusedT;
-    if (i < n) out[i] = yr[k];
-  }
-  g += nstep;
+    for (int k = 0; k < R; ++k) {
+      const int i = tid + k * kFusedT;
+      if (i < n) out[i] = yr[k];
+    }
+    g += nstep;
   }
 }
 
@@ -799,53 +820,67 @@ void nn_prolong(Ctx& c, double* y, const int* gate) {
 }
 
 // single-pass NN local solve into the split-K partials (see k_nn_fused)
+template <bool TRI, int R, int CPB>
+void launch_fused(Ctx& c, const LocalPlan& pl, const double* F, const double* D, const double* x, const int* gate,
+                  int grid, size_t smem, int nbuf, int ldmax) {
+  static bool configured = false;
+  if (!configured) {
+    AWG_CUDA(cudaFuncSetAttribute(k_nn_fused<TRI, R, CPB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(kFusedSmemCap)));
+    configured = true;
+  }
+  k_nn_fused<TRI, R, CPB><<<grid, kFusedT, smem, c.stream>>>(
+      gate, pl.tf.p, F, c.voff.p, c.ns.p, c.ld.p, c.poff.p, c.pidx.p, D, x, TRI ? nullptr : c.rlam.p, c.P,
+      c.wpart_nn.p, int(pl.tf.n), c.fused_queue.p, nbuf, ldmax, int(smem / sizeof(double)));
+}
+
+template <bool TRI, int CPB>
+void launch_fused_r(Ctx& c, const LocalPlan& pl, const double* F, const double* D, const double* x, const int* gate,
+                    int grid, size_t smem, int nbuf, int ldmax, int R) {
+  switch (R) {
+    case 2: launch_fused<TRI, 2, CPB>(c, pl, F, D, x, gate, grid, smem, nbuf, ldmax); break;
+    case 4: launch_fused<TRI, 4, CPB>(c, pl, F, D, x, gate, grid, smem, nbuf, ldmax); break;
+    case 8: launch_fused<TRI, 8, CPB>(c, pl, F, D, x, gate, grid, smem, nbuf, ldmax); break;
+    case 10: launch_fused<TRI, 10, CPB>(c, pl, F, D, x, gate, grid, smem, nbuf, ldmax); break;
+    case 11: launch_fused<TRI, 11, CPB>(c, pl, F, D, x, gate, grid, smem, nbuf, ldmax); break;
+    default: launch_fused<TRI, 12, CPB>(c, pl, F, D, x, gate, grid, smem, nbuf, ldmax); break;
+  }
+}
+
 void nn_fused(Ctx& c, const double* x, const int* gate) {
   const bool nn = (c.one_level == 2);
   const LocalPlan& pl = plan(c);
   int ldmax = 0;
   for (int v : c.h_ld) ldmax = std::max(ldmax, v);
-  // copy pipeline: 2-column steps when >= 3 of them fit in shared memory,
-  // otherwise 1-column steps; as many buffers as fit (<= kFusedMaxBuf)
-  const size_t cap = size_t(224) * 1024;
-  const size_t col_bytes = size_t(ldmax) * sizeof(double);
-  int cpb = (cap / (2 * col_bytes) >= 3) ? 2 : 1;
-  if (c.fused_cpb > 0) cpb = std::min(2, c.fused_cpb);
-  int nbuf = int(std::min<size_t>(kFusedMaxBuf, cap / (cpb * col_bytes)));
+  // rows per thread: the smallest instantiated R with R * kFusedT >= ldmax
+  const int need = (ldmax + kFusedT - 1) / kFusedT;
+  const int R = need <= 2 ? 2 : need <= 4 ? 4 : need <= 8 ? 8 : need <= 10 ? 10 : need <= 11 ? 11 : 12;
+  // copy pipeline: CPB columns per buffer, as many buffers as fit (<= kFusedMaxBuf),
+  // plus the tail that unchecked rows of the last buffer may reach
+  // (measured, profiles/README.md: two-column steps win while >= 3 two-column
+  // buffers fit — c2, ld 4612 — and lose to 4 one-column buffers at ld 5632, c5)
+  const size_t tail = size_t(std::max(0, R * kFusedT - ldmax)) * sizeof(double);
+  int cpb = (kFusedSmemCap - tail) / (size_t(2) * ldmax * sizeof(double)) >= 3 ? 2 : 1;
+  if (c.fused_cpb == 1 || c.fused_cpb == 2) cpb = c.fused_cpb;
+  const size_t buf_bytes = size_t(cpb) * ldmax * sizeof(double);
+  int nbuf = int(std::min<size_t>(kFusedMaxBuf, (kFusedSmemCap - tail) / buf_bytes));
   if (c.fused_nbuf > 0) nbuf = std::min(nbuf, c.fused_nbuf);
   if (nbuf < 2) c.fail(AWG_E_STATE, "single-pass local solve: subdomain too large for the copy pipeline");
-  const size_t smem = size_t(nbuf) * cpb * col_bytes;
-  static size_t configured = 0;
-  if (smem > configured) {
-    AWG_CUDA(cudaFuncSetAttribute(k_nn_fused<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(cap)));
-    AWG_CUDA(cudaFuncSetAttribute(k_nn_fused<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(cap)));
-    AWG_CUDA(cudaFuncSetAttribute(k_nn_fused<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(cap)));
-    AWG_CUDA(cudaFuncSetAttribute(k_nn_fused<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(cap)));
-    configured = cap;
-  }
+  const size_t smem = size_t(nbuf) * buf_bytes + tail;
   if (!pl.tf.n) return;
   if (!c.fused_queue.p) c.fused_queue.alloc(1);
   AWG_CUDA(cudaMemsetAsync(c.fused_queue.p, 0, sizeof(int), c.stream));
-  const int ntasks = int(pl.tf.n);
-  const int grid = std::min(ntasks, c.sm_count);
+  const int grid = std::min(int(pl.tf.n), c.sm_count);
   const double* F = nn ? c.V.p : c.U.p;
   const double* D = nn ? c.ds.p : nullptr;
-  const double* lam = nn ? c.lam.p : nullptr;
   if (nn && cpb == 2)
-    k_nn_fused<false, 2><<<grid, kFusedT, smem, c.stream>>>(gate, pl.tf.p, F, c.voff.p, c.ns.p, c.ld.p, c.poff.p,
-                                                            c.pidx.p, D, x, lam, c.P, c.wpart_nn.p, ntasks,
-                                                            c.fused_queue.p, nbuf);
+    launch_fused_r<false, 2>(c, pl, F, D, x, gate, grid, smem, nbuf, ldmax, R);
   else if (nn)
-    k_nn_fused<false, 1><<<grid, kFusedT, smem, c.stream>>>(gate, pl.tf.p, F, c.voff.p, c.ns.p, c.ld.p, c.poff.p,
-                                                            c.pidx.p, D, x, lam, c.P, c.wpart_nn.p, ntasks,
-                                                            c.fused_queue.p, nbuf);
+    launch_fused_r<false, 1>(c, pl, F, D, x, gate, grid, smem, nbuf, ldmax, R);
   else if (cpb == 2)
-    k_nn_fused<true, 2><<<grid, kFusedT, smem, c.stream>>>(gate, pl.tf.p, F, c.voff.p, c.ns.p, c.ld.p, c.poff.p,
-                                                           c.pidx.p, D, x, lam, c.P, c.wpart_nn.p, ntasks,
-                                                           c.fused_queue.p, nbuf);
+    launch_fused_r<true, 2>(c, pl, F, D, x, gate, grid, smem, nbuf, ldmax, R);
   else
-    k_nn_fused<true, 1><<<grid, kFusedT, smem, c.stream>>>(gate, pl.tf.p, F, c.voff.p, c.ns.p, c.ld.p, c.poff.p,
-                                                           c.pidx.p, D, x, lam, c.P, c.wpart_nn.p, ntasks,
-                                                           c.fused_queue.p, nbuf);
+    launch_fused_r<true, 1>(c, pl, F, D, x, gate, grid, smem, nbuf, ldmax, R);
   ++c.launches;
   check_launch("nn_fused");
 }

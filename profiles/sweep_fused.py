@@ -13,7 +13,7 @@ for cfg in sys.argv[1:] or ["c2"]:
     p = problems.make(cfg)
     rows = []
     settings = [("two-pass", {"AWG_NN_TWO_PASS": "1"})]
-    for cpb, nbuf, chunks in itertools.product([1, 2], [2, 3, 4, 6], [1, 2, 4, 8]):
+    for cpb, nbuf, chunks in itertools.product([1, 2], [2, 3, 4], [4, 8, 16]):
         settings.append((f"cpb{cpb}_nbuf{nbuf}_chunks{chunks}",
                          {"AWG_FUSED_CPB": str(cpb), "AWG_FUSED_NBUF": str(nbuf), "AWG_FUSED_CHUNKS": str(chunks)}))
     for name, env in settings:
