@@ -122,6 +122,8 @@ struct Args {
   int apply_reps = 0;
   int no_solve = 0;
   int export_dense = 0;
+  int w_probe = 0;          // > 0: run build_w's inner solve for this many W columns, bounded, then exit
+  int w_probe_maxit = 3000;
 };
 
 Args parse(int argc, char** argv) {
@@ -158,6 +160,8 @@ Args parse(int argc, char** argv) {
     else if (k == "--apply-reps") a.apply_reps = std::stoi(next());
     else if (k == "--no-solve") a.no_solve = 1;
     else if (k == "--export-dense") a.export_dense = std::stoi(next());
+    else if (k == "--w-probe") a.w_probe = std::stoi(next());
+    else if (k == "--w-probe-maxit") a.w_probe_maxit = std::stoi(next());
     else {
       std::fprintf(stderr, "unknown flag %s\n", k.c_str());
       std::exit(2);
@@ -409,6 +413,37 @@ int main(int argc, char** argv) {
   double t_coarse = now_s() - t0;
   const Composition comp = args.comp == "additive" ? Composition::ADDITIVE : Composition::HYBRID;
   auto h2 = std::make_shared<TwoLevel>(OneLevel(kind, split), cs, comp, split);
+
+  if (args.w_probe > 0) {
+    // The inner solve of build_w (preconditioner.cpp:97-113) for the first
+    // w_probe strictly negative modes, with maxit bounded: reports how the
+    // reference's own pcg(A+, H2) behaves when build_w would take 10 n iterations.
+    const ApplyFn aplus = [&split](const double* u, double* v) { split.apply_Aplus(u, v); };
+    const ApplyFn happly = [&h2](const double* u, double* v) { h2->apply(u, v); };
+    std::fprintf(js, "  \"n0\": %d, \"r0\": %d, \"n_minus\": %d,\n  \"w_probe\": [", cs.dim(), cs.retained_rank(),
+                 split.n_minus());
+    std::vector<double> rhs(n);
+    int col = 0;
+    for (int s = 0; s < N && col < args.w_probe; ++s) {
+      const LocalSplit& ls = split.splits()[s];
+      for (int k = 0; k < ls.n_nonpos && col < args.w_probe; ++k) {
+        if (ls.eig.eigenvalues[k] == 0.0) continue;
+        std::fill(rhs.begin(), rhs.end(), 0.0);
+        split.prolong_add(s, ls.eig.eigenvectors.col(k), rhs.data());
+        const double tp = now_s();
+        auto res = pcg(aplus, happly, rhs, args.w_rtol, args.w_probe_maxit);
+        const SolveReport& rep = res.second;
+        std::fprintf(js, "%s{\"s\": %d, \"k\": %d, \"iterations\": %d, \"converged\": %d, \"kappa\": %.6e, "
+                     "\"final_relres\": %.6e, \"seconds\": %.3f}", col ? ", " : "", s, k, rep.iterations,
+                     int(rep.converged), rep.kappa_estimate, rep.final_relative_residual, now_s() - tp);
+        std::fflush(js);
+        ++col;
+      }
+    }
+    std::fprintf(js, "],\n  \"t_splitting\": %.3f, \"t_coarse\": %.3f\n}\n", t_split, t_coarse);
+    std::fclose(js);
+    return 0;
+  }
 
   t0 = now_s();
   const AwgMode mode = mode_of(args.awg);

@@ -146,13 +146,9 @@ void set_factor(Ctx& c, CoarseFactor& f, int dim, int r, const int* ret, const d
   f.h_retained.assign(ret, ret + r);
   f.h_l11.assign(l11, l11 + size_t(r) * r);
   f.retained.upload(f.h_retained, c.stream);
-  f.linv.alloc(size_t(std::max(r, 1)) * std::max(r, 1));
-  f.linvT.alloc(size_t(std::max(r, 1)) * std::max(r, 1));
-  if (r) {
-    DArr<double> l;
-    l.upload(f.h_l11, c.stream);
-    k::tri_inverse(c, l.p, r, f.linv.p, f.linvT.p);
-  }
+  DArr<double> l;
+  if (r) l.upload(f.h_l11, c.stream);
+  k::coarse_inverse(c, l.p, f);
 }
 
 }  // namespace
@@ -284,6 +280,28 @@ void finalize_factors(Ctx& c) {
   c.zcol_s.upload(zs, c.stream);
   c.zcol_loc.upload(zl, c.stream);
   c.koff.upload(koff, c.stream);
+  auto build_bs = [&](BsPlan& b, const std::vector<int>& off) {
+    std::vector<int> ts, tc, nch(N, 0);
+    b.maxch = 1;
+    for (int s = 0; s < N; ++s) {
+      if (off[s + 1] == off[s]) continue;
+      nch[s] = (c.h_ns[s] + kBsRows - 1) / kBsRows;
+      b.maxch = std::max(b.maxch, nch[s]);
+      for (int ch = 0; ch < nch[s]; ++ch) {
+        ts.push_back(s);
+        tc.push_back(ch);
+      }
+    }
+    b.ntask = int(ts.size());
+    b.ts.upload(ts, c.stream);
+    b.tc.upload(tc, c.stream);
+    b.nch.upload(nch, c.stream);
+    b.cnt.alloc(N);
+    AWG_CUDA(cudaMemsetAsync(b.cnt.p, 0, sizeof(int) * N, c.stream));
+    b.part.alloc(size_t(std::max(off[N], 1)) * b.maxch);
+  };
+  build_bs(c.bs_neg, noff);
+  build_bs(c.bs_z, koff);
   c.alloc_work();
   AWG_CUDA(cudaStreamSynchronize(c.stream));
 }

@@ -113,6 +113,18 @@ struct LocalPlan {
   int kcmax_f = 1;
 };
 
+// Block-sparse GEMV^T plan (k_bs_gemvT): one CTA per (subdomain, 512-row
+// chunk) over the subdomains that own columns; partials per (column, chunk),
+// summed in chunk order by the last CTA of each subdomain.
+constexpr int kBsRows = 512;  // rows per CTA (256 threads x 2)
+struct BsPlan {
+  DArr<int> ts, tc;  // task -> subdomain, chunk
+  DArr<int> nch;     // chunks per subdomain
+  DArr<int> cnt;     // CTAs finished per subdomain (reset by the last one)
+  DArr<double> part; // columns x maxch
+  int ntask = 0, maxch = 1;
+};
+
 // Triangular coarse factor with retained pivots (RankRevealingFactor,
 // dense.hpp:81-86), stored as the inverse of l11.
 struct CoarseFactor {
@@ -120,14 +132,16 @@ struct CoarseFactor {
   int rank = 0;  // r
   DArr<int> retained;
   DArr<double> linv;   // r x r, column-major, lower
-  DArr<double> linvT;  // its transpose (row i of L^-1 contiguous)
+  DArr<double> kinv;   // L^-T L^-1 (r x r, symmetric): K^+ on the retained pivots
+  DArr<int> pos;       // dim: position among the retained pivots, -1 if dropped
   std::vector<int> h_retained;
   std::vector<double> h_l11;  // r x r, as produced (for exports)
   void clear() {
     dim = rank = 0;
     retained.release();
     linv.release();
-    linvT.release();
+    kinv.release();
+    pos.release();
     h_retained.clear();
     h_l11.clear();
   }
@@ -161,8 +175,9 @@ void coarse_q(Ctx& c, const double* x, double* y, const int* gate);   // y = Z K
 void second_q(Ctx& c, const double* x, double* y, const int* gate);   // y = W KW+ W^T x
 void inex_q(Ctx& c, const double* x, double* y, const int* gate);     // y = W core^-1 W^T x
 void axpby(Ctx& c, int n, const double* a, const double* b, const double* d, double* y, int mode, const int* gate);
-void rr_solve(Ctx& c, const CoarseFactor& f, const double* b, double* x, const int* gate, double* tmp);
-void tri_inverse(Ctx& c, const double* l, int r, double* linv, double* linvT);
+void rr_solve(Ctx& c, const CoarseFactor& f, const double* b, double* x, const int* gate);
+// L^-1 of the r x r lower factor l, K^+ = L^-T L^-1 and the retained positions
+void coarse_inverse(Ctx& c, const double* l, CoarseFactor& f);
 void zT(Ctx& c, const double* x, double* out, const int* gate);  // out = Z^T x (n0)
 void wT(Ctx& c, const double* x, double* out, const int* gate);  // out = W^T x (n_minus)
 void w_apply_public(Ctx& c, const double* coef, double* y, const int* gate);  // y = W coef
@@ -211,6 +226,7 @@ struct Ctx {
   bool use_fused = true; // single-pass NN local solve (env AWG_NN_TWO_PASS=1 disables)
   // single-pass tuning (env AWG_FUSED_CPB / AWG_FUSED_NBUF / AWG_FUSED_CHUNKS; 0 = automatic)
   int fused_cpb = 0, fused_nbuf = 0, fused_chunks_per_sm = 8;  // 0: automatic
+  BsPlan bs_neg, bs_z;   // A- dots (V^s columns k < n_nonpos), Z^T x (Y_s blocks)
   LocalPlan plan_nn;     // V^s with the eigenvalue mask (NN)
   LocalPlan plan_as;     // U^s = L^-T, triangular (AS / AS+)
   DArr<double> U;        // AS / AS+ local factors, same layout as V
@@ -249,8 +265,8 @@ struct Ctx {
   // work buffers
   DArr<double> xs, uh, wl;                          // P each
   DArr<double> t0, t1, t2, t3, t4, t5, t6, t7, t8;  // n each
-  DArr<double> cz, cz2;                             // coarse (K0) scratch
-  DArr<double> cw, cw2;                             // second coarse (KW) scratch (may run concurrently)
+  DArr<double> cz;  // coarse (K0) scratch
+  DArr<double> cw;  // second coarse (KW) scratch (may run concurrently)
   DArr<double> wpart;                               // split-K partials of W^T x
   DArr<double> wpart2;                              // column-chunk partials of W c
   DArr<double> red;                                 // reduction partials

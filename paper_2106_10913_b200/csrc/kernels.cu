@@ -64,7 +64,10 @@ __global__ void k_spmv(const int* __restrict__ gate, int n, const int* __restric
 
 // Prolongation of a block-sparse combination, evaluated at dof i:
 //   sum over subdomains s containing i (ascending) of sum_q coef[q] M_s(loc, col(q))
-// — the k_block_combine + k_prolong pair fused (same association order).
+// — the k_block_combine + k_prolong pair fused.  G lanes share a row: lane t
+// takes q = t, t + G, ... of every owner (G independent load streams instead
+// of one serial chain of up to 4 x 48 loads); the lanes' sums meet in a fixed
+// xor butterfly, so every lane holds the same, run-to-run identical value.
 struct BlockSum {
   const int* own_off;
   const int* own_pos;
@@ -76,42 +79,69 @@ struct BlockSum {
   const long long* moff;
   const int* ld;
   const double* coef;
-  __device__ __forceinline__ double at(int i) const {
+  template <int G>
+  __device__ __forceinline__ double at(int i, int t, bool active) const {
     double acc = 0.0;
-    for (int qo = own_off[i]; qo < own_off[i + 1]; ++qo) {
-      const int p = own_pos[qo];
-      const int s = psub[p];
-      const double* Ms = M + moff[s] + (p - poff[s]);
-      const int L = ld[s];
-      double u = 0.0;
-      for (int q = coff[s]; q < coff[s + 1]; ++q) {
-        const int col = ccol ? ccol[q] : (q - coff[s]);
-        u = fma(coef[q], Ms[(size_t)col * L], u);
+    if (active) {
+      for (int qo = own_off[i]; qo < own_off[i + 1]; ++qo) {
+        const int p = own_pos[qo];
+        const int s = psub[p];
+        const double* Ms = M + moff[s] + (p - poff[s]);
+        const int L = ld[s];
+        const int q0 = coff[s], q1 = coff[s + 1];
+        double u0 = 0.0, u1 = 0.0;
+        int q = q0 + t;
+        for (; q + G < q1; q += 2 * G) {
+          const int c0 = ccol ? ccol[q] : (q - q0);
+          const int c1 = ccol ? ccol[q + G] : (q + G - q0);
+          u0 = fma(coef[q], Ms[(size_t)c0 * L], u0);
+          u1 = fma(coef[q + G], Ms[(size_t)c1 * L], u1);
+        }
+        if (q < q1) u0 = fma(coef[q], Ms[(size_t)(ccol ? ccol[q] : (q - q0)) * L], u0);
+        acc += u0 + u1;
       }
-      acc += u;
     }
+#pragma unroll
+    for (int o = G / 2; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     return acc;
   }
 };
 
 // A+ x = A- x + A x with the A- prolongation fused (splitting.cpp:142-147):
 //   mode 1: y = am + A x;  mode 2: y = sub - (am + A x)
+template <int G>
 __global__ void k_spmv_aplus(const int* __restrict__ gate, int n, const int* __restrict__ rp,
                              const int* __restrict__ ci, const double* __restrict__ va,
                              const double* __restrict__ x, double* __restrict__ y, int mode,
                              const double* __restrict__ sub, BlockSum am) {
   if (gated(gate)) return;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    double acc = 0.0;
-    for (int k = rp[i]; k < rp[i + 1]; ++k) acc = __dadd_rn(acc, __dmul_rn(va[k], __ldg(x + ci[k])));
-    const double a = am.at(i) + acc;
-    y[i] = (mode == 1) ? a : sub[i] - a;
+  // G lanes per row; the loop runs warp-uniformly (the lanes meet in shuffles)
+  const int t = threadIdx.x & (G - 1);
+  const int stride = int((gridDim.x * (long long)blockDim.x) / G);
+  for (int i = int((blockIdx.x * (long long)blockDim.x + threadIdx.x) / G);; i += stride) {
+    const bool active = i < n;
+    if (!__any_sync(0xffffffffu, active)) break;
+    const double m = am.at<G>(i, t, active);
+    if (active && t == 0) {
+      double acc = 0.0;
+      for (int k = rp[i]; k < rp[i + 1]; ++k) acc = __dadd_rn(acc, __dmul_rn(va[k], __ldg(x + ci[k])));
+      const double a = m + acc;
+      y[i] = (mode == 1) ? a : sub[i] - a;
+    }
   }
 }
 
+template <int G>
 __global__ void k_prolong_sum(const int* __restrict__ gate, int n, BlockSum bs, double* __restrict__ y) {
   if (gated(gate)) return;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) y[i] = bs.at(i);
+  const int t = threadIdx.x & (G - 1);
+  const int stride = int((gridDim.x * (long long)blockDim.x) / G);
+  for (int i = int((blockIdx.x * (long long)blockDim.x + threadIdx.x) / G);; i += stride) {
+    const bool active = i < n;
+    if (!__any_sync(0xffffffffu, active)) break;
+    const double v = bs.at<G>(i, t, active);
+    if (active && t == 0) y[i] = v;
+  }
 }
 
 // xs[p] = x[pidx[p]] (* scale[p])      restrict_to (splitting.cpp:220-223) and the D^s
@@ -255,7 +285,6 @@ __global__ void __launch_bounds__(kThreads) k_nn_gemv(const int* __restrict__ ga
 // k_prolong_nn sums them in fixed order.
 // TRI: the AS / AS+ factor U^s = L^-T (no eigenvalue division, no D^s).
 constexpr int kFusedT = 512;
-constexpr int kFusedRowsMax = 12;  // rows per thread: ld <= 6144
 constexpr int kFusedMaxBuf = 6;  // deepest copy pipeline
 constexpr size_t kFusedSmemCap = size_t(224) * 1024;  // dynamic shared memory per CTA
 
@@ -425,59 +454,46 @@ __global__ void __launch_bounds__(kFusedT, 1) k_nn_fused(const int* __restrict__
 }
 
 // y[i] = sum over s containing i (ascending s) of D^s_i * (sum_kc part[kc][p(s,i)])
+template <int G>
 __global__ void k_prolong_nn(const int* __restrict__ gate, int n, const int* __restrict__ own_off,
                              const int* __restrict__ own_pos, const int* __restrict__ psub,
                              const int* __restrict__ nkc, long long P, const double* __restrict__ part,
                              const double* __restrict__ ds, double* __restrict__ y) {
   if (gated(gate)) return;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+  // G lanes per row split the chunk partials (kc = t, t + G, ...); fixed butterfly
+  const int t = threadIdx.x & (G - 1);
+  const int stride = int((gridDim.x * (long long)blockDim.x) / G);
+  for (int i = int((blockIdx.x * (long long)blockDim.x + threadIdx.x) / G);; i += stride) {
+    const bool active = i < n;
+    if (!__any_sync(0xffffffffu, active)) break;
     double acc = 0.0;
-    for (int q = own_off[i]; q < own_off[i + 1]; ++q) {
-      const int p = own_pos[q];
-      const int kcs = nkc[psub[p]];
-      double w = 0.0;
-      for (int kc = 0; kc < kcs; ++kc) w += part[(size_t)kc * P + p];
-      acc += ds ? w * ds[p] : w;
+    if (active) {
+      for (int q = own_off[i]; q < own_off[i + 1]; ++q) {
+        const int p = own_pos[q];
+        const int kcs = nkc[psub[p]];
+        double w0 = 0.0, w1 = 0.0;
+        int kc = t;
+        for (; kc + G < kcs; kc += 2 * G) {
+          w0 += part[(size_t)kc * P + p];
+          w1 += part[(size_t)(kc + G) * P + p];
+        }
+        if (kc < kcs) w0 += part[(size_t)kc * P + p];
+        const double w = w0 + w1;
+        acc += ds ? w * ds[p] : w;
+      }
     }
-    y[i] = acc;
+#pragma unroll
+    for (int o = G / 2; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (active && t == 0) y[i] = acc;
   }
 }
+
+
 
 // ---------------------------------------------------------------------------
 // A- x (splitting.cpp:119-140): per strictly negative mode (s,k):
 //   c = (-lambda_k) * (v_k . x[Omega^s]);   u_s = sum_k c_k v_k;   y = sum_s R^s^T u_s
-// CTA-wide sum of one value per thread (fixed tree: deterministic)
-__device__ __forceinline__ double block_sum(double v) {
-  __shared__ double sred[32];
-  v = warp_sum(v);
-  if ((threadIdx.x & 31) == 0) sred[threadIdx.x >> 5] = v;
-  __syncthreads();
-  double s = 0.0;
-  if (threadIdx.x < 32) {
-    s = (threadIdx.x < (blockDim.x >> 5)) ? sred[threadIdx.x] : 0.0;
-    s = warp_sum(s);
-  }
-  return s;  // valid in thread 0
-}
-
-// one CTA per negative mode: enough loads in flight even when n_- is small
-__global__ void k_neg_dot(const int* __restrict__ gate, int nneg, const int* __restrict__ neg_s,
-                          const int* __restrict__ neg_k, const double* __restrict__ neg_w,
-                          const double* __restrict__ V, const long long* __restrict__ voff,
-                          const int* __restrict__ ns, const int* __restrict__ ld,
-                          const long long* __restrict__ poff, const int* __restrict__ pidx,
-                          const double* __restrict__ x, double* __restrict__ cout) {
-  if (gated(gate)) return;
-  const int j = blockIdx.x;
-  const int s = neg_s[j], k = neg_k[j], n = ns[s];
-  const double* v = V + voff[s] + (size_t)k * ld[s];
-  const int* idx = pidx + poff[s];
-  double acc = 0.0;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) acc = fma(v[i], __ldg(x + idx[i]), acc);
-  acc = block_sum(acc);
-  if (threadIdx.x == 0) cout[j] = neg_w[j] * acc;
-}
-
+// (the dots are k_bs_gemvT below; the combination is fused into the consumer)
 // u[p] = sum over the negative modes of s(p), ascending k, of c_k v_k[i]
 // (Y-combine for Z c uses the same kernel on the Y blocks).
 __global__ void k_block_combine(const int* __restrict__ gate, long long P, const int* __restrict__ psub,
@@ -501,54 +517,142 @@ __global__ void k_block_combine(const int* __restrict__ gate, long long P, const
   }
 }
 
-// Z^T x with Z block sparse (coarse.cpp:136-141 + matvec_transpose, dense.cpp:47-54):
-// CTA per coarse column j of subdomain s: zx[j] = Y_s(:, j - koff[s]) . x[Omega^s]
-__global__ void k_zT(const int* __restrict__ gate, int n0, const int* __restrict__ zcol_s,
-                     const int* __restrict__ zcol_loc, const double* __restrict__ Y,
-                     const long long* __restrict__ yoff, const int* __restrict__ ns,
-                     const int* __restrict__ ld, const long long* __restrict__ poff,
-                     const int* __restrict__ pidx, const double* __restrict__ x, double* __restrict__ zx) {
+
+// Block-sparse GEMV^T: out[q] = w[q] * sum_i M_s(i, col(q)) x[pidx_s[i]] for the
+// columns q in [coff[s], coff[s+1]) of every subdomain s — Z^T x (Y_s blocks,
+// coarse.cpp:136-141 + matvec_transpose) and the A- dots (V^s columns
+// k < n_nonpos, splitting.cpp:124-132).  One CTA per (s, 512-row chunk): the
+// gathered x rows stay in registers while the CTA sweeps all of s's columns
+// (independent loads per column instead of one serial chain per column);
+// per-warp sums go to shared memory, per-chunk partials to `part`, and the
+// last CTA of s sums the chunks in chunk order (run-to-run identical).
+__global__ void __launch_bounds__(256) k_bs_gemvT(const int* __restrict__ gate, const int* __restrict__ task_s,
+                                                  const int* __restrict__ task_c, const int* __restrict__ nch,
+                                                  int maxch, const int* __restrict__ coff,
+                                                  const int* __restrict__ ccol, const double* __restrict__ M,
+                                                  const long long* __restrict__ moff, const int* __restrict__ ns,
+                                                  const int* __restrict__ ld, const long long* __restrict__ poff,
+                                                  const int* __restrict__ pidx, const double* __restrict__ x,
+                                                  const double* __restrict__ w, double* __restrict__ part,
+                                                  int* __restrict__ cnt, double* __restrict__ out) {
   if (gated(gate)) return;
-  const int j = blockIdx.x;
-  const int s = zcol_s[j], n = ns[s];
-  const double* y = Y + yoff[s] + (size_t)zcol_loc[j] * ld[s];
-  const int* idx = pidx + poff[s];
-  double acc = 0.0;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) acc = fma(y[i], __ldg(x + idx[i]), acc);
-  acc = block_sum(acc);
-  if (threadIdx.x == 0) zx[j] = acc;
+  constexpr int kCols = 64;
+  __shared__ double red[8][kCols];
+  __shared__ bool s_last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int s = task_s[blockIdx.x], ch = task_c[blockIdx.x];
+  const int n = ns[s], L = ld[s];
+  const int ia = ch * kBsRows + tid, ib = ia + 256;
+  const long long p0 = poff[s];
+  const double xa = ia < n ? __ldg(x + pidx[p0 + ia]) : 0.0;
+  const double xb = ib < n ? __ldg(x + pidx[p0 + ib]) : 0.0;
+  const double* Ms = M + moff[s];
+  const int q0 = coff[s], nc = coff[s + 1] - q0;
+  for (int cb = 0; cb < nc; cb += kCols) {
+    const int ncb = min(kCols, nc - cb);
+    // batches of 8 columns: all 16 loads issued before the first reduction
+    for (int c0 = 0; c0 < ncb; c0 += 8) {
+      double va[8], vb[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int c = c0 + u;
+        const bool ok = c < ncb;
+        const int col = ok ? (ccol ? ccol[q0 + cb + c] : cb + c) : 0;
+        const double* m = Ms + (size_t)col * L;
+        va[u] = (ok && ia < n) ? m[ia] : 0.0;
+        vb[u] = (ok && ib < n) ? m[ib] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const double a = warp_sum(fma(vb[u], xb, va[u] * xa));
+        if (lane == 0 && c0 + u < ncb) red[warp][c0 + u] = a;
+      }
+    }
+    __syncthreads();
+    if (tid < ncb) {
+      double a = 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) a += red[k][tid];
+      part[(size_t)(q0 + cb + tid) * maxch + ch] = a;
+    }
+    __syncthreads();
+  }
+  __threadfence();
+  if (tid == 0) s_last = (atomicAdd(cnt + s, 1) == nch[s] - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int kch = nch[s];
+  for (int q = tid; q < nc; q += blockDim.x) {
+    const double* pq = part + (size_t)(q0 + q) * maxch;
+    double a = 0.0;
+    for (int k = 0; k < kch; ++k) a += __ldcg(pq + k);
+    out[q0 + q] = w ? w[q0 + q] * a : a;
+  }
+  if (tid == 0) cnt[s] = 0;
 }
 
 // ---------------------------------------------------------------------------
-// rank_revealing_solve (dense.cpp:348-366) with the inverse of l11:
-//   b_r = b[retained]; t = L^-1 b_r; y = L^-T t; x = 0, x[retained] = y
-// t_i = sum_{j <= i} L^-1(i, j) b[ret[j]]: warp per row, reading row i of L^-1
-// as column i of its transpose (linvT, column-major upper) — coalesced
-__global__ void k_tri_lower(const int* __restrict__ gate, int r, const double* __restrict__ linvT,
-                            const double* __restrict__ b, const int* __restrict__ ret, double* __restrict__ t) {
+// rank_revealing_solve (dense.cpp:348-366): b_r = b[retained]; y = L^-T L^-1 b_r;
+// x = 0, x[retained] = y.  L^-T L^-1 = K^+ is formed once at setup (k_gram), so
+// the solve is ONE symmetric GEMV: warp per output entry, reading row pos[i]
+// of K^+ (coalesced) against the gathered b_r (L1/L2 resident).
+__global__ void k_coarse_solve(const int* __restrict__ gate, int dim, int r, const double* __restrict__ kinv,
+                               const int* __restrict__ pos, const int* __restrict__ ret,
+                               const double* __restrict__ b, double* __restrict__ x) {
   if (gated(gate)) return;
   const int lane = threadIdx.x & 31;
   const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (i >= r) return;
-  const double* row = linvT + (size_t)i * r;
+  if (i >= dim) return;
+  const int k = pos[i];
   double acc = 0.0;
-  for (int j = lane; j <= i; j += 32) acc = fma(row[j], __ldg(b + ret[j]), acc);
-  acc = warp_sum(acc);
-  if (lane == 0) t[i] = acc;
+  if (k >= 0) {
+    const double* row = kinv + (size_t)k * r;
+    double a1 = 0.0;
+    int j = lane;
+    for (; j + 32 < r; j += 64) {
+      acc = fma(row[j], __ldg(b + ret[j]), acc);
+      a1 = fma(row[j + 32], __ldg(b + ret[j + 32]), a1);
+    }
+    if (j < r) acc = fma(row[j], __ldg(b + ret[j]), acc);
+    acc = warp_sum(acc + a1);
+  }
+  if (lane == 0) x[i] = acc;
 }
 
-__global__ void k_tri_upperT(const int* __restrict__ gate, int r, const double* __restrict__ linv,
-                             const double* __restrict__ t, const int* __restrict__ ret, double* __restrict__ x) {
-  if (gated(gate)) return;
-  const int lane = threadIdx.x & 31;
-  const int k = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (k >= r) return;
-  const double* col = linv + (size_t)k * r;
-  double acc = 0.0;
-  for (int i = k + lane; i < r; i += 32) acc = fma(col[i], t[i], acc);
-  acc = warp_sum(acc);
-  if (lane == 0) x[ret[k]] = acc;
+// g(i, j) = sum_k a(k, i) a(k, j) for a column-major lower r x r (so k >= max(i, j))
+__global__ void k_gram(int r, const double* __restrict__ a, double* __restrict__ g) {
+  __shared__ double as[32][33], bs[32][33];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int k0 = max(i0, j0); k0 < r; k0 += 32) {
+    for (int yy = ty; yy < 32; yy += 8) {
+      const int k = k0 + yy;
+      as[yy][tx] = (k < r && i0 + tx < r) ? a[k + (size_t)(i0 + tx) * r] : 0.0;
+      bs[yy][tx] = (k < r && j0 + tx < r) ? a[k + (size_t)(j0 + tx) * r] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < 32; ++kk) {
+      const double bv = bs[kk][tx];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[q] = fma(as[kk][ty + 8 * q], bv, acc[q]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int i = i0 + ty + 8 * q, j = j0 + tx;
+    if (i < r && j < r) g[i + (size_t)j * r] = acc[q];
+  }
 }
+
+__global__ void k_retained_set(int r, const int* __restrict__ ret, int* __restrict__ pos) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < r) pos[ret[k]] = k;
+}
+
 
 __global__ void k_scatter(int n, const int* __restrict__ om, const double* __restrict__ y, double* __restrict__ z) {
   const int l = blockIdx.x * blockDim.x + threadIdx.x;
@@ -562,6 +666,7 @@ __global__ void k_zero(const int* __restrict__ gate, int n, double* __restrict__
 
 // L^-1 of a lower-triangular r x r column-major l (setup; thread per column,
 // forward substitution against the identity, row-major scratch then transpose).
+
 __global__ void k_tri_inverse_rm(int r, const double* __restrict__ l, double* __restrict__ xrm) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= r) return;
@@ -810,11 +915,25 @@ void nn_gemv(Ctx& c, const int* gate) {
   check_launch("nn_gemv");
 }
 
+
+// split-K partial sum + D^s + prolongation (k_prolong_nn), lanes per row by size
+static void prolong_nn(Ctx& c, const int* nkc, int kcmax, double* y, const int* gate) {
+  const double* ds = c.one_level == 2 ? c.ds.p : nullptr;
+  const int G = c.n > 300000 ? 1 : (kcmax >= 16 ? 8 : 4);
+  if (G == 8)
+    k_prolong_nn<8><<<grid_for(c, 8LL * c.n), kThreads, 0, c.stream>>>(gate, c.n, c.own_off.p, c.own_pos.p, c.psub.p,
+                                                                      nkc, c.P, c.wpart_nn.p, ds, y);
+  else if (G == 4)
+    k_prolong_nn<4><<<grid_for(c, 4LL * c.n), kThreads, 0, c.stream>>>(gate, c.n, c.own_off.p, c.own_pos.p, c.psub.p,
+                                                                      nkc, c.P, c.wpart_nn.p, ds, y);
+  else
+    k_prolong_nn<1><<<grid_for(c, c.n), kThreads, 0, c.stream>>>(gate, c.n, c.own_off.p, c.own_pos.p, c.psub.p,
+                                                                nkc, c.P, c.wpart_nn.p, ds, y);
+}
+
 void nn_prolong(Ctx& c, double* y, const int* gate) {
   const LocalPlan& pl = plan(c);
-  k_prolong_nn<<<grid_for(c, c.n), kThreads, 0, c.stream>>>(gate, c.n, c.own_off.p, c.own_pos.p, c.psub.p,
-                                                           pl.nkc.p, c.P, c.wpart_nn.p,
-                                                           c.one_level == 2 ? c.ds.p : nullptr, y);
+  prolong_nn(c, pl.nkc.p, pl.kcmax, y, gate);
   ++c.launches;
   check_launch("prolong_nn");
 }
@@ -889,9 +1008,7 @@ void h1(Ctx& c, const double* x, double* y, const int* gate) {
   const LocalPlan& pl = plan(c);
   if (pl.fused) {
     nn_fused(c, x, gate);
-    k_prolong_nn<<<grid_for(c, c.n), kThreads, 0, c.stream>>>(gate, c.n, c.own_off.p, c.own_pos.p, c.psub.p,
-                                                             pl.nkc_f.p, c.P, c.wpart_nn.p,
-                                                             c.one_level == 2 ? c.ds.p : nullptr, y);
+    prolong_nn(c, pl.nkc_f.p, pl.kcmax_f, y, gate);
     ++c.launches;
     check_launch("prolong_nn");
     return;
@@ -901,6 +1018,21 @@ void h1(Ctx& c, const double* x, double* y, const int* gate) {
   nn_prolong(c, y, gate);
 }
 
+static void bs_gemvT(Ctx& c, BsPlan& b, const int* coff, const int* ccol, const double* M, const long long* moff,
+                     const double* x, const double* w, double* out, const int* gate) {
+  if (b.ntask == 0) return;
+  k_bs_gemvT<<<b.ntask, 256, 0, c.stream>>>(gate, b.ts.p, b.tc.p, b.nch.p, b.maxch, coff, ccol, M, moff, c.ns.p,
+                                            c.ld.p, c.poff.p, c.pidx.p, x, w, b.part.p, b.cnt.p, out);
+  ++c.launches;
+  check_launch("bs_gemvT");
+}
+
+static void neg_dot(Ctx& c, const double* x, const int* gate) {
+  bs_gemvT(c, c.bs_neg, c.negoff.p, c.neg_k.p, c.V.p, c.voff.p, x, c.neg_w.p, c.neg_c.p, gate);
+}
+
+static int rows_group(const Ctx& c) { return c.n <= 300000 ? 4 : 1; }
+
 void aminus(Ctx& c, const double* x, double* y, const int* gate) {
   if (c.nneg == 0) {
     k_zero<<<grid_for(c, c.n), kThreads, 0, c.stream>>>(gate, c.n, y);
@@ -908,10 +1040,7 @@ void aminus(Ctx& c, const double* x, double* y, const int* gate) {
     check_launch("zero");
     return;
   }
-  k_neg_dot<<<c.nneg, kThreads, 0, c.stream>>>(gate, c.nneg, c.neg_s.p, c.neg_k.p, c.neg_w.p, c.V.p, c.voff.p,
-                                               c.ns.p, c.ld.p, c.poff.p, c.pidx.p, x, c.neg_c.p);
-  ++c.launches;
-  check_launch("neg_dot");
+  neg_dot(c, x, gate);
   k_block_combine<<<grid_for(c, c.P), kThreads, 0, c.stream>>>(gate, c.P, c.psub.p, c.poff.p, c.negoff.p, c.neg_k.p,
                                                                c.V.p, c.voff.p, c.ld.p, c.neg_c.p, c.wl.p);
   ++c.launches;
@@ -927,31 +1056,30 @@ static BlockSum neg_sum(const Ctx& c) {
 // y = A+ x (mode 1) or y = sub - A+ x (mode 2): the A- dots, then one fused
 // SpMV + A- prolongation kernel
 void aplus(Ctx& c, const double* x, double* y, int mode, const double* sub, const int* gate) {
-  if (c.nneg > 0) {
-    k_neg_dot<<<c.nneg, kThreads, 0, c.stream>>>(gate, c.nneg, c.neg_s.p, c.neg_k.p, c.neg_w.p, c.V.p, c.voff.p,
-                                                 c.ns.p, c.ld.p, c.poff.p, c.pidx.p, x, c.neg_c.p);
-    ++c.launches;
-    check_launch("neg_dot");
-  }
+  if (c.nneg > 0) neg_dot(c, x, gate);
   BlockSum bs = neg_sum(c);
   if (c.nneg == 0) bs.coff = c.negoff.p;  // empty ranges: all zero
-  k_spmv_aplus<<<grid_for(c, c.n), kThreads, 0, c.stream>>>(gate, c.n, c.rp.p, c.ci.p, c.va.p, x, y, mode, sub, bs);
+  if (rows_group(c) == 4)
+    k_spmv_aplus<4><<<grid_for(c, 4LL * c.n), kThreads, 0, c.stream>>>(gate, c.n, c.rp.p, c.ci.p, c.va.p, x, y, mode,
+                                                                       sub, bs);
+  else
+    k_spmv_aplus<1><<<grid_for(c, c.n), kThreads, 0, c.stream>>>(gate, c.n, c.rp.p, c.ci.p, c.va.p, x, y, mode, sub,
+                                                                bs);
   ++c.launches;
   check_launch("spmv_aplus");
 }
 
-void rr_solve(Ctx& c, const CoarseFactor& f, const double* b, double* x, const int* gate, double* tmp) {
-  k_zero<<<grid_for(c, f.dim), kThreads, 0, c.stream>>>(gate, f.dim, x);
-  ++c.launches;
-  if (f.rank == 0) return;
+void rr_solve(Ctx& c, const CoarseFactor& f, const double* b, double* x, const int* gate) {
   const int wpb = kThreads / 32;
-  k_tri_lower<<<(f.rank + wpb - 1) / wpb, kThreads, 0, c.stream>>>(gate, f.rank, f.linvT.p, b, f.retained.p, tmp);
+  if (f.rank == 0) {
+    k_zero<<<grid_for(c, f.dim), kThreads, 0, c.stream>>>(gate, f.dim, x);
+    ++c.launches;
+    return;
+  }
+  k_coarse_solve<<<(f.dim + wpb - 1) / wpb, kThreads, 0, c.stream>>>(gate, f.dim, f.rank, f.kinv.p, f.pos.p,
+                                                                     f.retained.p, b, x);
   ++c.launches;
-  check_launch("tri_lower");
-  k_tri_upperT<<<(f.rank + wpb - 1) / wpb, kThreads, 0, c.stream>>>(gate, f.rank, f.linv.p, tmp, f.retained.p,
-                                                                   x);
-  ++c.launches;
-  check_launch("tri_upperT");
+  check_launch("coarse_solve");
 }
 
 void coarse_q(Ctx& c, const double* x, double* y, const int* gate) {
@@ -960,24 +1088,21 @@ void coarse_q(Ctx& c, const double* x, double* y, const int* gate) {
     ++c.launches;
     return;
   }
-  k_zT<<<c.n0, kThreads, 0, c.stream>>>(gate, c.n0, c.zcol_s.p, c.zcol_loc.p, c.Y.p, c.yoff.p, c.ns.p, c.ld.p,
-                                        c.poff.p, c.pidx.p, x, c.cz.p);
-  ++c.launches;
-  check_launch("zT");
+  zT(c, x, c.cz.p, gate);
   double* coef = c.cz.p + c.n0;  // second half of cz holds the solved coefficients
-  rr_solve(c, c.k0, c.cz.p, coef, gate, c.cz2.p);
+  rr_solve(c, c.k0, c.cz.p, coef, gate);
   // Z c: block-sparse combination fused with the prolongation
   const BlockSum bs{c.own_off.p, c.own_pos.p, c.psub.p, c.poff.p, c.koff.p, nullptr, c.Y.p, c.yoff.p, c.ld.p, coef};
-  k_prolong_sum<<<grid_for(c, c.n), kThreads, 0, c.stream>>>(gate, c.n, bs, y);
+  if (rows_group(c) == 4)
+    k_prolong_sum<4><<<grid_for(c, 4LL * c.n), kThreads, 0, c.stream>>>(gate, c.n, bs, y);
+  else
+    k_prolong_sum<1><<<grid_for(c, c.n), kThreads, 0, c.stream>>>(gate, c.n, bs, y);
   ++c.launches;
   check_launch("z_prolong");
 }
 
 void zT(Ctx& c, const double* x, double* out, const int* gate) {
-  k_zT<<<c.n0, kThreads, 0, c.stream>>>(gate, c.n0, c.zcol_s.p, c.zcol_loc.p, c.Y.p, c.yoff.p, c.ns.p, c.ld.p,
-                                        c.poff.p, c.pidx.p, x, out);
-  ++c.launches;
-  check_launch("zT");
+  bs_gemvT(c, c.bs_z, c.koff.p, nullptr, c.Y.p, c.yoff.p, x, nullptr, out, gate);
 }
 
 static void w_transpose_apply(Ctx& c, const double* x, double* out, const int* gate) {
@@ -1030,7 +1155,7 @@ void second_q(Ctx& c, const double* x, double* y, const int* gate) {
   double* wx = c.cw.p;
   double* coef = c.cw.p + c.nm;
   w_transpose_apply(c, x, wx, gate);
-  rr_solve(c, c.kw, wx, coef, gate, c.cw2.p);
+  rr_solve(c, c.kw, wx, coef, gate);
   w_apply(c, coef, y, gate);
 }
 
@@ -1051,16 +1176,33 @@ void axpby(Ctx& c, int n, const double* a, const double* b, const double* d, dou
   check_launch("axpby");
 }
 
-// L^-1 as column-major (linv) and its transpose (linvT = the row-major scratch)
-void tri_inverse(Ctx& c, const double* l, int r, double* linv, double* linvT) {
-  if (r == 0) return;
-  k_tri_inverse_rm<<<(r + 127) / 128, 128, 0, c.stream>>>(r, l, linvT);
+// L^-1 (column-major, linv: the block W build multiplies by it), K^+ = L^-T L^-1
+// (kinv, the apply-time solve) and the retained positions
+void coarse_inverse(Ctx& c, const double* l, CoarseFactor& f) {
+  const int r = f.rank;
+  f.linv.alloc(size_t(std::max(r, 1)) * std::max(r, 1));
+  f.kinv.alloc(size_t(std::max(r, 1)) * std::max(r, 1));
+  f.pos.alloc(std::max(f.dim, 1));
+  AWG_CUDA(cudaMemsetAsync(f.pos.p, 0xff, sizeof(int) * std::max(f.dim, 1), c.stream));  // -1
+  if (r == 0) {
+    AWG_CUDA(cudaStreamSynchronize(c.stream));
+    return;
+  }
+  DArr<double> linvT;  // row-major L^-1 (k_tri_inverse_rm), transposed into linv
+  linvT.alloc(size_t(r) * r);
+  k_tri_inverse_rm<<<(r + 127) / 128, 128, 0, c.stream>>>(r, l, linvT.p);
   ++c.launches;
   check_launch("tri_inverse");
   dim3 grid((r + 31) / 32, (r + 31) / 32);
-  k_transpose<<<grid, dim3(32, 8), 0, c.stream>>>(r, linvT, linv);
+  k_transpose<<<grid, dim3(32, 8), 0, c.stream>>>(r, linvT.p, f.linv.p);
   ++c.launches;
   check_launch("transpose");
+  k_gram<<<grid, dim3(32, 8), 0, c.stream>>>(r, f.linv.p, f.kinv.p);
+  ++c.launches;
+  check_launch("gram");
+  k_retained_set<<<(r + 255) / 256, 256, 0, c.stream>>>(r, f.retained.p, f.pos.p);
+  ++c.launches;
+  check_launch("retained_pos");
   AWG_CUDA(cudaStreamSynchronize(c.stream));
 }
 

@@ -260,9 +260,7 @@ void Ctx::alloc_work() {
   wl.alloc(P);
   const size_t cdim = size_t(std::max(n0, nm)) * 2 + 2;
   cz.alloc(cdim);
-  cz2.alloc(cdim);
   cw.alloc(cdim);
-  cw2.alloc(cdim);
   const int nch = (round_up(n, 4) + 4095) / 4096;
   wpart.alloc(size_t(std::max(nm, 1)) * nch);
   wpart2.alloc(size_t(w_chunks(*this)) * round_up(n, 4));

@@ -372,10 +372,8 @@ void pivoted_factor(Ctx& c, DArr<double>& G, int n, int exact, CoarseFactor& f, 
     ++c.launches;
     f.h_l11.resize(size_t(r) * r);
     AWG_CUDA(cudaMemcpyAsync(f.h_l11.data(), l.p, sizeof(double) * r * r, cudaMemcpyDeviceToHost, c.stream));
-    f.linv.alloc(size_t(r) * r);
-    f.linvT.alloc(size_t(r) * r);
-    k::tri_inverse(c, l.p, r, f.linv.p, f.linvT.p);
   }
+  k::coarse_inverse(c, l.p, f);
   AWG_CUDA(cudaStreamSynchronize(c.stream));
 }
 

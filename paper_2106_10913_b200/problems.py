@@ -421,6 +421,8 @@ def make(name: str) -> Problem:
         return elasticity_problem("telas8", 32, 16, 8, [(1e7, 0.45), (1.0, 0.3)], (2, 2), 1, tau_sharp=0.1)
     if name == "c4mid":  # c4 with c4-sized subdomains (n_s ~ 4,200) but 4 of them: the reference finishes
         return elasticity_problem("c4mid", 128, 64, 8, [(1e7, 0.45), (1.0, 0.3)], (2, 2), 1, tau_sharp=0.1)
+    if name == "c4s":  # between telas8 and c4mid (n_s ~ 2,400, six 8-element layers)
+        return elasticity_problem("c4s", 96, 48, 8, [(1e7, 0.45), (1.0, 0.3)], (2, 2), 1, tau_sharp=0.1)
     raise KeyError(name)
 
 

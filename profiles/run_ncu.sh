@@ -14,6 +14,6 @@ $CMD > $OUT/plain_$CFG.log 2>&1
 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv \
     --log-file $OUT/launches_${CFG}_${TAG}.csv $CMD > $OUT/ncu_launch_$CFG.log 2>&1
 ncu --profile-from-start off --set full --clock-control none --import-source on \
-    -k regex:"k_nn_fused|k_nn_gemvT|k_nn_gemv|k_dense_gemv|k_spmv|k_prolong_nn" -s 8 -c 6 \
+    -k regex:"k_nn_fused|k_nn_gemvT|k_nn_gemv|k_dense_gemv|k_spmv|k_prolong|k_bs_gemvT" -s 10 -c 9 \
     -o $OUT/prof_${CFG}_${TAG} $CMD > $OUT/ncu_full_$CFG.log 2>&1
 echo done

@@ -1,10 +1,11 @@
 """Summarize ncu outputs for profiles/ (run here, on the CPU box):
-    python profiles/summarize.py <launches.csv> [<prof.ncu-rep>] > profiles/<name>.md
+    python profiles/summarize.py <launches.csv> [<prof.ncu-rep> [<traffic.json> <config>]] > profiles/<name>.md
 Launch list: per-kernel count, device time and share of the profiled solve
 (cold-cache, serialised: shares matter, not absolutes).  Full capture: per
 launch duration, DRAM bytes read+write, DRAM throughput % and occupancy."""
 import collections
 import csv
+import os
 import subprocess
 import sys
 
@@ -62,7 +63,34 @@ def full(path):
     print()
 
 
+_SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+
+
+def traffic(path, out_json, config):
+    """DRAM bytes read + written per launch, first capture of each kernel (the
+    roofline.traffic figure bench.py reports)."""
+    import json
+
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    r = list(csv.reader(out.splitlines()))
+    hdr, units = r[0], r[1]
+    ik, ir, iw = hdr.index("Kernel Name"), hdr.index("dram__bytes_read.sum"), hdr.index("dram__bytes_write.sum")
+    d = {}
+    for row in r[2:]:
+        name = row[ik].split("(")[0].replace("(anonymous namespace)::", "").split("::")[-1].split("<")[0].strip()
+        name = name.replace("void ", "")
+        if name in d:
+            continue
+        b = float(row[ir].replace(",", "")) * _SCALE[units[ir]] + float(row[iw].replace(",", "")) * _SCALE[units[iw]]
+        d[name] = b
+    json.dump({"config": config, "source": "ncu --set full --clock-control none, solve-only capture "
+               "(profiles/prof_solve.py): " + os.path.basename(path), "dram_bytes_per_launch": d},
+              open(out_json, "w"), indent=1)
+
+
 if __name__ == "__main__":
     launches(sys.argv[1])
     if len(sys.argv) > 2:
         full(sys.argv[2])
+    if len(sys.argv) > 4:
+        traffic(sys.argv[2], sys.argv[3], sys.argv[4])

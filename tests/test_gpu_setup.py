@@ -112,3 +112,30 @@ def test_report_outputs(tmp_path):
     lines = open(tmp_path / "rows.csv").read().splitlines()
     assert lines[0] == "label,kappa,it,lambda_min,lambda_max,v0,n_minus" and len(lines) == 2
     assert len(open(tmp_path / "t2d_run_residuals.csv").read().splitlines()) == rep.iterations + 1
+
+
+def test_wide_coarse_blocks():
+    """Subdomains with more than 64 coarse columns (k_bs_gemvT sweeps its
+    columns in batches of 64): Q and A- on the device match the restatement
+    evaluated on the factors the device built."""
+    from oracle import awg_oracle as O
+
+    g, s = golden_with_base("t3d")
+    n = len(g["b"])
+    omega = [g["part_indices"][a:b] for a, b in zip(g["part_offsets"][:-1], g["part_offsets"][1:])]
+    a = awg.SparseSymMatrix(n, g["A_row_offsets"], g["A_col_indices"], g["A_values"])
+    ctx = awg.ProblemContext(a, g["b"], awg.Partition(omega, n))
+    cfg = awg.PreconditionerConfig()
+    cfg.fixed_k = 70
+    ctx.setup(cfg)
+    ks = ctx.get("ks")
+    assert ks.min() >= 70
+    f = {k: ctx.get(k) for k in ("lam", "V", "n_nonpos", "n_zero", "ks", "Y", "k0_retained")}
+    r0 = len(f["k0_retained"])
+    f["k0_l11"] = ctx.get("k0_l11").reshape(r0, r0, order="F")  # column-major lower factor
+    orc = O.AwgOracle(n, g["A_row_offsets"], g["A_col_indices"], g["A_values"], omega, f)
+    rng = np.random.default_rng(11)
+    for _ in range(3):
+        x = rng.uniform(-1, 1, n)
+        assert rel(ctx.apply(awg.Op.Q, x), orc.coarse_correct(x)) <= 1e-11
+        assert rel(ctx.apply(awg.Op.AMINUS, x), orc.apply_Aminus(x)) <= 1e-11
