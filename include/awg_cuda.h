@@ -131,7 +131,7 @@ typedef struct awg_stats {
   long long sum_ns_qs;  /* sum n_s * n_neg(s) */
   double t_setup_ms[8]; /* splitting, pencils, coarse, w, misc... (see awg_setup) */
   int w_inner_total;    /* sum of inner PCG iterations of build_w */
-  int w_batches;
+  int w_batches;        /* block passes of the batched W build (continuous batching) */
   int nn_single_pass;   /* 1: the NN local solve streams V^s once per apply (k_nn_fused) */
 } awg_stats;
 

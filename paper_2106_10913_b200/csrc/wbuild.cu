@@ -32,7 +32,9 @@ constexpr int kT = 256;
 
 struct ColState {
   double bnorm, rz, pq, alpha, beta, relres, alpha_prev, beta_prev, true_rel;
-  int it, done, converged, past_rtol, need_true, error, pad0, pad1;
+  int it, done, converged, past_rtol, need_true, error, fresh, pad1;
+  // fresh: the slot was refilled with a new column (R = b, bnorm set); its next
+  // loop pass is that column's PCG initialisation (alpha = 0, then z = H r, p = z)
 };
 
 __device__ __forceinline__ double wsum(double v) {
@@ -189,16 +191,27 @@ __device__ double sum_parts(const double* part, int G, int b) {
 }
 
 // ---- per-column PCG scalar steps (the k_pcg_* logic of ops.cu, per column) --------
-__global__ void kc_init(int B, ColState* st, const double* part, int G, int* done) {
+// slots the host refilled (fresh[b]): ||b|| from the block dot, state reset
+__global__ void kc_fresh(int B, ColState* st, const double* part, int G, int* done, const int* fresh) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= B) return;
+  if (b >= B || !fresh[b]) return;
   ColState c{};
   const double s = sum_parts(part, G, b);
   c.bnorm = sqrt(s);
   c.done = (s == 0.0);
   c.converged = (s == 0.0);
+  c.fresh = !c.done;
   st[b] = c;
   done[b] = c.done;
+}
+
+__global__ void kc_clear(int B, ColState* st, int* done) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  ColState c{};
+  c.done = 1;
+  st[b] = c;
+  done[b] = 1;
 }
 
 __global__ void kc_rz(int B, ColState* st, const double* part, int G, int* done, int initial) {
@@ -207,13 +220,14 @@ __global__ void kc_rz(int B, ColState* st, const double* part, int G, int* done,
   ColState& c = st[b];
   if (c.done) return;
   const double rz = sum_parts(part, G, b);
-  if (initial) {
+  if (initial || c.fresh) {
     if (rz <= 0.0) {
       c.error = PCG_BAD_PRECOND;
       c.done = 1;
     }
     c.rz = rz;
     c.beta = 0.0;
+    c.fresh = 0;
   } else if (rz <= 0.0) {
     if (!c.past_rtol) c.error = PCG_BAD_PRECOND;
     c.done = 1;
@@ -232,6 +246,10 @@ __global__ void kc_alpha(int B, ColState* st, const double* part, int G, int* do
   if (b >= B) return;
   ColState& c = st[b];
   if (c.done) return;
+  if (c.fresh) {  // initialisation pass: x and r stay as set
+    c.alpha = 0.0;
+    return;
+  }
   const double pq = sum_parts(part, G, b);
   c.pq = pq;
   if (pq <= 0.0) {
@@ -276,7 +294,7 @@ __global__ void kc_relres(int B, ColState* st, const double* part, int G, double
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   ColState& c = st[b];
-  if (c.done) {
+  if (c.done || c.fresh) {
     c.need_true = 0;
     return;
   }
@@ -573,82 +591,85 @@ void build_w_batched(Ctx& c, cublasHandle_t h, const std::vector<std::pair<int, 
   BlockOps ops(c, k, h, c.k0);
   const int cb = (B + 127) / 128;
   std::vector<ColState> hs(B);
-  for (int c0 = 0; c0 < total; c0 += B) {
-    const int nb = std::min(B, total - c0);
-    // right-hand sides R^s^T v_k for the batch (unused columns: zero -> done at init)
-    k.Bm.zero(c.stream);
-    for (int j = 0; j < nb; ++j) {
-      const int s = modes[c0 + j].first, kk = modes[c0 + j].second;
-      k::scatter_col(c, s, c.V.p + c.h_voff[s] + size_t(kk) * c.h_ld[s], k.Bm.p + size_t(j) * k.ld);
+  // Continuous batching: B slots, each running one column's PCG with its own
+  // alpha, beta and stopping state; a slot whose column finished is refilled
+  // with the next column at once, so the block DGEMMs never carry finished
+  // columns while work remains (per-column semantics are unchanged: a refilled
+  // slot spends one pass on its initialisation, r = b, z = H2 r, p = z).
+  std::vector<int> slot(B, -1), fresh(B, 0);
+  DArr<int> d_fresh;
+  d_fresh.alloc(B);
+  int next = 0, finished = 0, passes = 0;
+  kc_clear<<<cb, 128, 0, c.stream>>>(B, k.st.p, k.done.p);
+  ++c.launches;
+  auto refill = [&]() {
+    bool any = false;
+    for (int j = 0; j < B; ++j) {
+      fresh[j] = 0;
+      if (slot[j] >= 0 || next >= total) continue;
+      const int s = modes[next].first, kk = modes[next].second;
+      double* bj = k.Bm.p + size_t(j) * k.ld;
+      AWG_CUDA(cudaMemsetAsync(bj, 0, sizeof(double) * k.ld, c.stream));
+      k::scatter_col(c, s, c.V.p + c.h_voff[s] + size_t(kk) * c.h_ld[s], bj);
+      AWG_CUDA(cudaMemsetAsync(k.X.p + size_t(j) * k.ld, 0, sizeof(double) * k.ld, c.stream));
+      AWG_CUDA(cudaMemcpyAsync(k.R.p + size_t(j) * k.ld, bj, sizeof(double) * k.ld, cudaMemcpyDeviceToDevice,
+                               c.stream));
+      slot[j] = next++;
+      fresh[j] = 1;
+      any = true;
     }
-    const dim3 gn = ops.grid_n();
-    // init: X = 0, R = B, bnorm
-    k.X.zero(c.stream);
-    AWG_CUDA(cudaMemcpyAsync(k.R.p, k.Bm.p, sizeof(double) * k.ld * B, cudaMemcpyDeviceToDevice, c.stream));
+    if (!any) return;
+    d_fresh.upload(fresh, c.stream);
     ops.dot(k.R.p, k.R.p, 0, nullptr);
-    kc_init<<<cb, 128, 0, c.stream>>>(B, k.st.p, k.part.p, k.G, k.done.p);
+    kc_fresh<<<cb, 128, 0, c.stream>>>(B, k.st.p, k.part.p, k.G, k.done.p, d_fresh.p);
+    ++c.launches;
+  };
+  refill();
+  const dim3 gn = ops.grid_n();
+  while (finished < total) {
+    ops.aplus(k.Pm.p, k.Q.p, k.done.p);
+    ops.dot(k.Pm.p, k.Q.p, 0, nullptr);
+    kc_alpha<<<cb, 128, 0, c.stream>>>(B, k.st.p, k.part.p, k.G, k.done.p);
+    kb_update<<<dim3(k.G, B), kT, 0, c.stream>>>(c.n, k.ld, k.st.p, k.X.p, k.R.p, k.Pm.p, k.Q.p, k.part.p);
+    AWG_CUDA(cudaMemsetAsync(k.any_true.p, 0, sizeof(int), c.stream));
+    kc_relres<<<cb, 128, 0, c.stream>>>(B, k.st.p, k.part.p, k.G, rtol, maxit, k.done.p, k.any_true.p);
+    c.launches += 3;
+    int any = 0;
+    AWG_CUDA(cudaMemcpyAsync(&any, k.any_true.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    AWG_CUDA(cudaStreamSynchronize(c.stream));
+    if (any) {  // true residual b - A+ x for the columns that reached rtol
+      ops.aplus(k.X.p, k.T.p, k.done.p);
+      ops.dot(nullptr, k.T.p, 1, k.Bm.p);
+      kc_true<<<cb, 128, 0, c.stream>>>(B, k.st.p, k.part.p, k.G, rtol, maxit, k.done.p);
+      ++c.launches;
+    }
     ops.h2(k.R.p, k.Z.p, k.done.p);
     ops.dot(k.R.p, k.Z.p, 0, nullptr);
-    kc_rz<<<cb, 128, 0, c.stream>>>(B, k.st.p, k.part.p, k.G, k.done.p, 1);
-    kb_p<<<gn, kT, 0, c.stream>>>(c.n, k.ld, k.st.p, k.Z.p, k.Pm.p, 1);
-    c.launches += 3;
-    for (int it = 0; it < maxit; ++it) {
-      ops.aplus(k.Pm.p, k.Q.p, k.done.p);
-      ops.dot(k.Pm.p, k.Q.p, 0, nullptr);
-      kc_alpha<<<cb, 128, 0, c.stream>>>(B, k.st.p, k.part.p, k.G, k.done.p);
-      kb_update<<<dim3(k.G, B), kT, 0, c.stream>>>(c.n, k.ld, k.st.p, k.X.p, k.R.p, k.Pm.p, k.Q.p, k.part.p);
-      AWG_CUDA(cudaMemsetAsync(k.any_true.p, 0, sizeof(int), c.stream));
-      kc_relres<<<cb, 128, 0, c.stream>>>(B, k.st.p, k.part.p, k.G, rtol, maxit, k.done.p, k.any_true.p);
-      c.launches += 3;
-      int any = 0;
-      AWG_CUDA(cudaMemcpyAsync(&any, k.any_true.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
-      AWG_CUDA(cudaStreamSynchronize(c.stream));
-      if (any) {  // true residual b - A+ x for the columns that reached rtol
-        ops.aplus(k.X.p, k.T.p, k.done.p);
-        ops.dot(nullptr, k.T.p, 1, k.Bm.p);
-        kc_true<<<cb, 128, 0, c.stream>>>(B, k.st.p, k.part.p, k.G, rtol, maxit, k.done.p);
-        ++c.launches;
-      }
-      ops.h2(k.R.p, k.Z.p, k.done.p);
-      ops.dot(k.R.p, k.Z.p, 0, nullptr);
-      kc_rz<<<cb, 128, 0, c.stream>>>(B, k.st.p, k.part.p, k.G, k.done.p, 0);
-      kb_p<<<gn, kT, 0, c.stream>>>(c.n, k.ld, k.st.p, k.Z.p, k.Pm.p, 0);
-      c.launches += 2;
-      AWG_CUDA(cudaMemcpyAsync(hs.data(), k.st.p, sizeof(ColState) * B, cudaMemcpyDeviceToHost, c.stream));
-      AWG_CUDA(cudaStreamSynchronize(c.stream));
-      bool all = true;
-      int ndone = 0;
-      for (int j = 0; j < nb; ++j) {
-        all = all && hs[j].done;
-        ndone += hs[j].done ? 1 : 0;
-      }
-      if (it % 250 == 249) {
-        const char* v = std::getenv("AWG_VERBOSE");
-        if (v && v[0] == '1')
-          std::fprintf(stderr, "[awg setup]   W batch at iteration %d: %d of %d columns done\n", it + 1, ndone, nb);
-      }
-      if (all) break;
-    }
+    kc_rz<<<cb, 128, 0, c.stream>>>(B, k.st.p, k.part.p, k.G, k.done.p, 0);
+    kb_p<<<gn, kT, 0, c.stream>>>(c.n, k.ld, k.st.p, k.Z.p, k.Pm.p, 0);
+    c.launches += 2;
+    ++passes;
     AWG_CUDA(cudaMemcpyAsync(hs.data(), k.st.p, sizeof(ColState) * B, cudaMemcpyDeviceToHost, c.stream));
     AWG_CUDA(cudaStreamSynchronize(c.stream));
-    for (int j = 0; j < nb; ++j) {
+    for (int j = 0; j < B; ++j) {
+      if (slot[j] < 0 || !hs[j].done) continue;
       if (hs[j].error) c.fail(AWG_E_BREAKDOWN, "build_w: inner PCG breakdown");
       if (!hs[j].converged) c.fail(AWG_E_NO_CONVERGENCE, "build_w: inner PCG for a W column did not converge");
-      iters[c0 + j] = hs[j].it;
-      AWG_CUDA(cudaMemcpyAsync(c.W.p + size_t(c0 + j) * c.ldw, k.X.p + size_t(j) * k.ld, sizeof(double) * c.n,
+      iters[slot[j]] = hs[j].it;
+      AWG_CUDA(cudaMemcpyAsync(c.W.p + size_t(slot[j]) * c.ldw, k.X.p + size_t(j) * k.ld, sizeof(double) * c.n,
                                cudaMemcpyDeviceToDevice, c.stream));
+      slot[j] = -1;
+      ++finished;
     }
-    ++c.w_batches;
-    {
+    refill();
+    if (passes % 250 == 0) {
       const char* v = std::getenv("AWG_VERBOSE");
-      if (v && v[0] == '1') {
-        int itmax = 0;
-        for (int j = 0; j < nb; ++j) itmax = std::max(itmax, hs[j].it);
-        std::fprintf(stderr, "[awg setup] W batch %d: columns %d..%d (B = %d), max inner iterations %d\n",
-                     c.w_batches, c0, c0 + nb - 1, B, itmax);
-      }
+      if (v && v[0] == '1')
+        std::fprintf(stderr, "[awg setup]   W block pass %d: %d of %d columns done (B = %d)\n", passes, finished,
+                     total, B);
     }
   }
+  c.w_batches += passes;
   AWG_CUDA(cudaStreamSynchronize(c.stream));
 }
 
