@@ -388,8 +388,14 @@ int awg_create(awg_ctx** out, int device) {
   }
   int rc = guarded(ctx, [&](Ctx& cc) {
     AWG_CUDA(cudaSetDevice(device));
-    AWG_CUDA(cudaStreamCreateWithFlags(&cc.stream, cudaStreamNonBlocking));
-    AWG_CUDA(cudaStreamCreateWithFlags(&cc.side, cudaStreamNonBlocking));
+    // the solve's critical path (main stream) outranks the concurrent W branch
+    // (side stream); graph kernel nodes keep these priorities (ops.cu)
+    const char* prio = std::getenv("AWG_STREAM_PRIORITY");
+    cc.use_priority = !(prio && prio[0] == '0');
+    int lo = 0, hi = 0;
+    AWG_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    AWG_CUDA(cudaStreamCreateWithPriority(&cc.stream, cudaStreamNonBlocking, cc.use_priority ? hi : 0));
+    AWG_CUDA(cudaStreamCreateWithPriority(&cc.side, cudaStreamNonBlocking, cc.use_priority ? lo : 0));
     AWG_CUDA(cudaEventCreateWithFlags(&cc.ev_fork, cudaEventDisableTiming));
     AWG_CUDA(cudaEventCreateWithFlags(&cc.ev_join, cudaEventDisableTiming));
     AWG_CUDA(cudaDeviceGetAttribute(&cc.sm_count, cudaDevAttrMultiProcessorCount, device));

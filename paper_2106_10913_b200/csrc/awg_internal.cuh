@@ -225,6 +225,7 @@ struct Ctx {
   int one_level = 2;     // OneLevelKind of the configuration: 0 AS, 1 AS_PLUS, 2 NN
   bool use_fused = true; // single-pass NN local solve (env AWG_NN_TWO_PASS=1 disables)
   // single-pass tuning (env AWG_FUSED_CPB / AWG_FUSED_NBUF / AWG_FUSED_CHUNKS; 0 = automatic)
+  bool use_priority = true;  // main stream high priority, W branch low
   int fused_cpb = 0, fused_nbuf = 0, fused_chunks_per_sm = 8;  // 0: automatic
   BsPlan bs_neg, bs_z;   // A- dots (V^s columns k < n_nonpos), Z^T x (Y_s blocks)
   LocalPlan plan_nn;     // V^s with the eigenvalue mask (NN)

@@ -446,7 +446,7 @@ void run_pcg(Ctx& c, const double* b_dev, double rtol, int maxit, awg_solve_repo
     AWG_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
     iteration();
     AWG_CUDA(cudaStreamEndCapture(c.stream, &graph));
-    AWG_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    AWG_CUDA(cudaGraphInstantiate(&exec, graph, c.use_priority ? cudaGraphInstantiateFlagUseNodePriority : 0));
     cudaGraphDestroy(graph);
     c.graphs[key] = exec;
     c.graph_launches[key] = c.launches - before;

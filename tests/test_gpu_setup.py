@@ -51,6 +51,11 @@ def test_setup_products(case):
     q = ctx.query()
     assert q["n0"] == s["n0"] and q["n_minus"] == s["n_minus"]
     assert np.allclose(ctx.get("neg_weights"), g["neg_weights"], rtol=1e-9)
+    # build_w's inner solves (continuously batched on the device) stop where the
+    # reference's per-column pcg calls stop
+    inner = ctx.get("w_inner_iterations")
+    assert inner.size == len(g["w_inner_iterations"])
+    assert np.max(np.abs(inner - g["w_inner_iterations"]), initial=0) <= 2, (inner, g["w_inner_iterations"])
 
 
 @pytest.mark.parametrize("case", BASE + ["t2d_additive", "t3d_none", "t2d_as", "t2d_asplus", "telas_as"])
