@@ -299,11 +299,22 @@ __device__ __forceinline__ void mbar_arm(unsigned long long* bar, unsigned bytes
                : "memory");
 }
 
-__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
+// V^s is streamed once per apply and is far larger than L2: its lines are
+// marked evict-first so the index arrays, coarse blocks and vectors of the
+// small kernels around the local solve stay L2-resident across iterations
+__device__ __forceinline__ unsigned long long l2_evict_first() {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, unsigned long long* bar,
+                                          unsigned long long pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
 }
 
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
@@ -343,6 +354,7 @@ __global__ void __launch_bounds__(kFusedT, 1) k_nn_fused(const int* __restrict__
   // order the zero fill (generic proxy) before the first bulk copies (async proxy)
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   const size_t bstride = (size_t)CPB * ldmax;  // buffer b starts at fsm + b * bstride
+  const unsigned long long pol = l2_evict_first();
   // Persistent CTAs (one per SM) pull column chunks from an atomic queue; the
   // chunk -> partial-slot map is fixed by the task list, so the result does not
   // depend on which CTA ran which chunk.  A step covers CPB columns; g counts
@@ -367,7 +379,7 @@ __global__ void __launch_bounds__(kFusedT, 1) k_nn_fused(const int* __restrict__
       if (!TRI) {
         const unsigned bytes = unsigned(cols) * unsigned(L) * 8u;
         mbar_arm(&bar[b], bytes);
-        bulk_load(fsm + b * bstride, Vs + (size_t)j * L, bytes, &bar[b]);
+        bulk_load(fsm + b * bstride, Vs + (size_t)j * L, bytes, &bar[b], pol);
       } else {
         // upper-triangular U^s: column c holds rows 0..c; copy an even row count
         unsigned rows[CPB], total = 0;
@@ -379,7 +391,8 @@ __global__ void __launch_bounds__(kFusedT, 1) k_nn_fused(const int* __restrict__
         mbar_arm(&bar[b], total * 8u);
 #pragma unroll
         for (int c = 0; c < CPB; ++c)
-          if (rows[c]) bulk_load(fsm + b * bstride + (size_t)c * L, Vs + (size_t)(j + c) * L, rows[c] * 8u, &bar[b]);
+          if (rows[c])
+            bulk_load(fsm + b * bstride + (size_t)c * L, Vs + (size_t)(j + c) * L, rows[c] * 8u, &bar[b], pol);
       }
     };
     if (tid == 0)
