@@ -392,6 +392,8 @@ int awg_create(awg_ctx** out, int device) {
     // (side stream); graph kernel nodes keep these priorities (ops.cu)
     const char* prio = std::getenv("AWG_STREAM_PRIORITY");
     cc.use_priority = !(prio && prio[0] == '0');
+    const char* pdl = std::getenv("AWG_PDL");
+    cc.use_pdl = !(pdl && pdl[0] == '0');
     int lo = 0, hi = 0;
     AWG_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     AWG_CUDA(cudaStreamCreateWithPriority(&cc.stream, cudaStreamNonBlocking, cc.use_priority ? hi : 0));

@@ -21,7 +21,12 @@ namespace {
 
 constexpr int kThreads = 256;
 
-__device__ __forceinline__ bool gated(const int* gate) { return gate != nullptr && *gate != 0; }
+// first statement of every solve-path kernel: wait for the predecessor grid
+// (programmatic dependent launch), then honour the device-side PCG gate
+__device__ __forceinline__ bool gated(const int* gate) {
+  pdl_wait();
+  return gate != nullptr && *gate != 0;
+}
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -871,19 +876,19 @@ __global__ void k_axpby(const int* __restrict__ gate, int n, const double* __res
 namespace k {
 
 void spmv(Ctx& c, const double* x, double* y, int mode, const double* add, const double* sub, const int* gate) {
-  k_spmv<<<grid_for(c, c.n), kThreads, 0, c.stream>>>(gate, c.n, c.rp.p, c.ci.p, c.va.p, x, y, mode, add, sub);
+  launch(c, k_spmv, grid_for(c, c.n), kThreads, 0, gate, c.n, c.rp.p, c.ci.p, c.va.p, x, y, mode, add, sub);
   ++c.launches;
   check_launch("spmv");
 }
 
 void gather(Ctx& c, const double* x, const double* scale, double* xs, const int* gate) {
-  k_gather<<<grid_for(c, c.P), kThreads, 0, c.stream>>>(gate, c.P, c.pidx.p, x, scale, xs);
+  launch(c, k_gather, grid_for(c, c.P), kThreads, 0, gate, c.P, c.pidx.p, x, scale, xs);
   ++c.launches;
   check_launch("gather");
 }
 
 void prolong(Ctx& c, const double* w, double* y, const int* gate) {
-  k_prolong<<<grid_for(c, c.n), kThreads, 0, c.stream>>>(gate, c.n, c.own_off.p, c.own_pos.p, w, y);
+  launch(c, k_prolong, grid_for(c, c.n), kThreads, 0, gate, c.n, c.own_off.p, c.own_pos.p, w, y);
   ++c.launches;
   check_launch("prolong");
 }
@@ -909,10 +914,10 @@ void nn_gemvT(Ctx& c, const double* x, const int* gate) {
   const LocalPlan& pl = plan(c);
   if (!pl.tT.n) return;
   if (c.one_level == 2)
-    k_nn_gemvT<8, false><<<int(pl.tT.n), 256, smem, c.stream>>>(gate, pl.tT.p, c.V.p, c.voff.p, c.ns.p, c.ld.p,
+    launch(c, (k_nn_gemvT<8, false>), int(pl.tT.n), 256, smem, gate, pl.tT.p, c.V.p, c.voff.p, c.ns.p, c.ld.p,
                                                                 c.poff.p, c.pidx.p, c.ds.p, x, c.lam.p, c.uh.p);
   else
-    k_nn_gemvT<8, true><<<int(pl.tT.n), 256, smem, c.stream>>>(gate, pl.tT.p, c.U.p, c.voff.p, c.ns.p, c.ld.p,
+    launch(c, (k_nn_gemvT<8, true>), int(pl.tT.n), 256, smem, gate, pl.tT.p, c.U.p, c.voff.p, c.ns.p, c.ld.p,
                                                                c.poff.p, c.pidx.p, nullptr, x, nullptr, c.uh.p);
   ++c.launches;
   check_launch("nn_gemvT");
@@ -921,7 +926,7 @@ void nn_gemvT(Ctx& c, const double* x, const int* gate) {
 void nn_gemv(Ctx& c, const int* gate) {
   const LocalPlan& pl = plan(c);
   if (!pl.t.n) return;
-  k_nn_gemv<<<int(pl.t.n), kThreads, size_t(pl.cols_max) * sizeof(double), c.stream>>>(
+  launch(c, k_nn_gemv, int(pl.t.n), kThreads, size_t(pl.cols_max) * sizeof(double), 
       gate, pl.t.p, c.one_level == 2 ? c.V.p : c.U.p, c.voff.p, c.ns.p, c.ld.p, c.poff.p, c.P, c.uh.p,
       c.wpart_nn.p);
   ++c.launches;
@@ -934,13 +939,13 @@ static void prolong_nn(Ctx& c, const int* nkc, int kcmax, double* y, const int* 
   const double* ds = c.one_level == 2 ? c.ds.p : nullptr;
   const int G = c.n > 300000 ? 1 : (kcmax >= 16 ? 8 : 4);
   if (G == 8)
-    k_prolong_nn<8><<<grid_for(c, 8LL * c.n), kThreads, 0, c.stream>>>(gate, c.n, c.own_off.p, c.own_pos.p, c.psub.p,
+    launch(c, k_prolong_nn<8>, grid_for(c, 8LL * c.n), kThreads, 0, gate, c.n, c.own_off.p, c.own_pos.p, c.psub.p,
                                                                       nkc, c.P, c.wpart_nn.p, ds, y);
   else if (G == 4)
-    k_prolong_nn<4><<<grid_for(c, 4LL * c.n), kThreads, 0, c.stream>>>(gate, c.n, c.own_off.p, c.own_pos.p, c.psub.p,
+    launch(c, k_prolong_nn<4>, grid_for(c, 4LL * c.n), kThreads, 0, gate, c.n, c.own_off.p, c.own_pos.p, c.psub.p,
                                                                       nkc, c.P, c.wpart_nn.p, ds, y);
   else
-    k_prolong_nn<1><<<grid_for(c, c.n), kThreads, 0, c.stream>>>(gate, c.n, c.own_off.p, c.own_pos.p, c.psub.p,
+    launch(c, k_prolong_nn<1>, grid_for(c, c.n), kThreads, 0, gate, c.n, c.own_off.p, c.own_pos.p, c.psub.p,
                                                                 nkc, c.P, c.wpart_nn.p, ds, y);
 }
 
@@ -961,9 +966,9 @@ void launch_fused(Ctx& c, const LocalPlan& pl, const double* F, const double* D,
                                   int(kFusedSmemCap)));
     configured = true;
   }
-  k_nn_fused<TRI, R, CPB><<<grid, kFusedT, smem, c.stream>>>(
-      gate, pl.tf.p, F, c.voff.p, c.ns.p, c.ld.p, c.poff.p, c.pidx.p, D, x, TRI ? nullptr : c.rlam.p, c.P,
-      c.wpart_nn.p, int(pl.tf.n), c.fused_queue.p, nbuf, ldmax, int(smem / sizeof(double)));
+  launch(c, k_nn_fused<TRI, R, CPB>, grid, kFusedT, smem, gate, pl.tf.p, F, c.voff.p, c.ns.p, c.ld.p, c.poff.p,
+         c.pidx.p, D, x, TRI ? nullptr : c.rlam.p, c.P, c.wpart_nn.p, int(pl.tf.n), c.fused_queue.p, nbuf, ldmax,
+         int(smem / sizeof(double)));
 }
 
 template <bool TRI, int CPB>
@@ -1034,7 +1039,7 @@ void h1(Ctx& c, const double* x, double* y, const int* gate) {
 static void bs_gemvT(Ctx& c, BsPlan& b, const int* coff, const int* ccol, const double* M, const long long* moff,
                      const double* x, const double* w, double* out, const int* gate) {
   if (b.ntask == 0) return;
-  k_bs_gemvT<<<b.ntask, 256, 0, c.stream>>>(gate, b.ts.p, b.tc.p, b.nch.p, b.maxch, coff, ccol, M, moff, c.ns.p,
+  launch(c, k_bs_gemvT, b.ntask, 256, 0, gate, b.ts.p, b.tc.p, b.nch.p, b.maxch, coff, ccol, M, moff, c.ns.p,
                                             c.ld.p, c.poff.p, c.pidx.p, x, w, b.part.p, b.cnt.p, out);
   ++c.launches;
   check_launch("bs_gemvT");
@@ -1048,13 +1053,13 @@ static int rows_group(const Ctx& c) { return c.n <= 300000 ? 4 : 1; }
 
 void aminus(Ctx& c, const double* x, double* y, const int* gate) {
   if (c.nneg == 0) {
-    k_zero<<<grid_for(c, c.n), kThreads, 0, c.stream>>>(gate, c.n, y);
+    launch(c, k_zero, grid_for(c, c.n), kThreads, 0, gate, c.n, y);
     ++c.launches;
     check_launch("zero");
     return;
   }
   neg_dot(c, x, gate);
-  k_block_combine<<<grid_for(c, c.P), kThreads, 0, c.stream>>>(gate, c.P, c.psub.p, c.poff.p, c.negoff.p, c.neg_k.p,
+  launch(c, k_block_combine, grid_for(c, c.P), kThreads, 0, gate, c.P, c.psub.p, c.poff.p, c.negoff.p, c.neg_k.p,
                                                                c.V.p, c.voff.p, c.ld.p, c.neg_c.p, c.wl.p);
   ++c.launches;
   check_launch("neg_combine");
@@ -1073,10 +1078,10 @@ void aplus(Ctx& c, const double* x, double* y, int mode, const double* sub, cons
   BlockSum bs = neg_sum(c);
   if (c.nneg == 0) bs.coff = c.negoff.p;  // empty ranges: all zero
   if (rows_group(c) == 4)
-    k_spmv_aplus<4><<<grid_for(c, 4LL * c.n), kThreads, 0, c.stream>>>(gate, c.n, c.rp.p, c.ci.p, c.va.p, x, y, mode,
+    launch(c, k_spmv_aplus<4>, grid_for(c, 4LL * c.n), kThreads, 0, gate, c.n, c.rp.p, c.ci.p, c.va.p, x, y, mode,
                                                                        sub, bs);
   else
-    k_spmv_aplus<1><<<grid_for(c, c.n), kThreads, 0, c.stream>>>(gate, c.n, c.rp.p, c.ci.p, c.va.p, x, y, mode, sub,
+    launch(c, k_spmv_aplus<1>, grid_for(c, c.n), kThreads, 0, gate, c.n, c.rp.p, c.ci.p, c.va.p, x, y, mode, sub,
                                                                 bs);
   ++c.launches;
   check_launch("spmv_aplus");
@@ -1085,11 +1090,11 @@ void aplus(Ctx& c, const double* x, double* y, int mode, const double* sub, cons
 void rr_solve(Ctx& c, const CoarseFactor& f, const double* b, double* x, const int* gate) {
   const int wpb = kThreads / 32;
   if (f.rank == 0) {
-    k_zero<<<grid_for(c, f.dim), kThreads, 0, c.stream>>>(gate, f.dim, x);
+    launch(c, k_zero, grid_for(c, f.dim), kThreads, 0, gate, f.dim, x);
     ++c.launches;
     return;
   }
-  k_coarse_solve<<<(f.dim + wpb - 1) / wpb, kThreads, 0, c.stream>>>(gate, f.dim, f.rank, f.kinv.p, f.pos.p,
+  launch(c, k_coarse_solve, (f.dim + wpb - 1) / wpb, kThreads, 0, gate, f.dim, f.rank, f.kinv.p, f.pos.p,
                                                                      f.retained.p, b, x);
   ++c.launches;
   check_launch("coarse_solve");
@@ -1097,7 +1102,7 @@ void rr_solve(Ctx& c, const CoarseFactor& f, const double* b, double* x, const i
 
 void coarse_q(Ctx& c, const double* x, double* y, const int* gate) {
   if (c.n0 == 0) {
-    k_zero<<<grid_for(c, c.n), kThreads, 0, c.stream>>>(gate, c.n, y);
+    launch(c, k_zero, grid_for(c, c.n), kThreads, 0, gate, c.n, y);
     ++c.launches;
     return;
   }
@@ -1107,9 +1112,9 @@ void coarse_q(Ctx& c, const double* x, double* y, const int* gate) {
   // Z c: block-sparse combination fused with the prolongation
   const BlockSum bs{c.own_off.p, c.own_pos.p, c.psub.p, c.poff.p, c.koff.p, nullptr, c.Y.p, c.yoff.p, c.ld.p, coef};
   if (rows_group(c) == 4)
-    k_prolong_sum<4><<<grid_for(c, 4LL * c.n), kThreads, 0, c.stream>>>(gate, c.n, bs, y);
+    launch(c, k_prolong_sum<4>, grid_for(c, 4LL * c.n), kThreads, 0, gate, c.n, bs, y);
   else
-    k_prolong_sum<1><<<grid_for(c, c.n), kThreads, 0, c.stream>>>(gate, c.n, bs, y);
+    launch(c, k_prolong_sum<1>, grid_for(c, c.n), kThreads, 0, gate, c.n, bs, y);
   ++c.launches;
   check_launch("z_prolong");
 }
@@ -1121,10 +1126,10 @@ void zT(Ctx& c, const double* x, double* out, const int* gate) {
 static void w_transpose_apply(Ctx& c, const double* x, double* out, const int* gate) {
   const int nch = (c.ldw + kWChunk - 1) / kWChunk;
   dim3 grid((c.nm + 31) / 32, nch);
-  k_dense_gemvT_part<<<grid, kThreads, 0, c.stream>>>(gate, c.n, c.nm, c.ldw, c.W.p, x, c.wpart.p);
+  launch(c, k_dense_gemvT_part, grid, kThreads, 0, gate, c.n, c.nm, c.ldw, c.W.p, x, c.wpart.p);
   ++c.launches;
   check_launch("dense_gemvT_part");
-  k_colsum<<<(c.nm + kThreads - 1) / kThreads, kThreads, 0, c.stream>>>(gate, c.nm, nch, c.wpart.p, out);
+  launch(c, k_colsum, (c.nm + kThreads - 1) / kThreads, kThreads, 0, gate, c.nm, nch, c.wpart.p, out);
   ++c.launches;
   check_launch("colsum");
 }
@@ -1139,11 +1144,11 @@ static void w_apply(Ctx& c, const double* coef, double* y, const int* gate) {
     configured = smem;
   }
   dim3 grid((c.n + 2 * kThreads - 1) / (2 * kThreads), nkc);
-  k_dense_gemv<<<grid, kThreads, smem, c.stream>>>(gate, c.n, c.nm, c.ldw, nkc, c.W.p, coef, y, c.wpart2.p);
+  launch(c, k_dense_gemv, grid, kThreads, smem, gate, c.n, c.nm, c.ldw, nkc, c.W.p, coef, y, c.wpart2.p);
   ++c.launches;
   check_launch("dense_gemv");
   if (nkc > 1) {
-    k_chunk_sum<<<grid_for(c, c.n), kThreads, 0, c.stream>>>(gate, c.n, c.ldw, nkc, c.wpart2.p, y);
+    launch(c, k_chunk_sum, grid_for(c, c.n), kThreads, 0, gate, c.n, c.ldw, nkc, c.wpart2.p, y);
     ++c.launches;
     check_launch("chunk_sum");
   }
@@ -1161,7 +1166,7 @@ void w_apply_public(Ctx& c, const double* coef, double* y, const int* gate) { w_
 
 void second_q(Ctx& c, const double* x, double* y, const int* gate) {
   if (c.nm == 0) {
-    k_zero<<<grid_for(c, c.n), kThreads, 0, c.stream>>>(gate, c.n, y);
+    launch(c, k_zero, grid_for(c, c.n), kThreads, 0, gate, c.n, y);
     ++c.launches;
     return;
   }
@@ -1176,7 +1181,7 @@ void inex_q(Ctx& c, const double* x, double* y, const int* gate) {
   double* wx = c.cw.p;
   double* coef = c.cw.p + c.nm;
   w_transpose_apply(c, x, wx, gate);
-  k_lu_solve<<<1, 1024, size_t(c.nm) * sizeof(double), c.stream>>>(gate, c.nm, c.core_lu.p, c.core_perm.p, wx, coef,
+  launch(c, k_lu_solve, 1, 1024, size_t(c.nm) * sizeof(double), gate, c.nm, c.core_lu.p, c.core_perm.p, wx, coef,
                                                                    c.lu_semantics);
   ++c.launches;
   check_launch("lu_solve");
@@ -1184,7 +1189,7 @@ void inex_q(Ctx& c, const double* x, double* y, const int* gate) {
 }
 
 void axpby(Ctx& c, int n, const double* a, const double* b, const double* d, double* y, int mode, const int* gate) {
-  k_axpby<<<grid_for(c, n), kThreads, 0, c.stream>>>(gate, n, a, b, d, y, mode);
+  launch(c, k_axpby, grid_for(c, n), kThreads, 0, gate, n, a, b, d, y, mode);
   ++c.launches;
   check_launch("axpby");
 }

@@ -58,6 +58,7 @@ __device__ void grid_reduce(double v, double* part, unsigned* count, Fin fin) {
 
 __global__ void k_pcg_init(PcgState* st, int n, const double* __restrict__ b, double* __restrict__ x,
                            double* __restrict__ r, double* part, unsigned* count) {
+  pdl_wait();
   double acc = 0.0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const double bi = b[i];
@@ -79,6 +80,7 @@ __global__ void k_pcg_init(PcgState* st, int n, const double* __restrict__ b, do
 // rz = <r, z>; the initial check (krylov.cpp:51-53) or the beta step (:105-115).
 __global__ void k_pcg_rz(PcgState* st, int n, const double* __restrict__ r, const double* __restrict__ z,
                          double* part, unsigned* count, int initial) {
+  pdl_wait();
   if (st->done) return;
   double acc = 0.0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) acc = fma(r[i], z[i], acc);
@@ -107,6 +109,7 @@ __global__ void k_pcg_rz(PcgState* st, int n, const double* __restrict__ r, cons
 
 // p = z + beta p   (p = z on the first step: beta = 0 and p zeroed)
 __global__ void k_pcg_p(const PcgState* st, int n, const double* __restrict__ z, double* __restrict__ p, int initial) {
+  pdl_wait();
   if (st->done) return;
   const double beta = st->beta;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
@@ -117,6 +120,7 @@ __global__ void k_pcg_p(const PcgState* st, int n, const double* __restrict__ z,
 __global__ void k_pcg_spmv_dot(PcgState* st, int n, const int* __restrict__ rp, const int* __restrict__ ci,
                                const double* __restrict__ va, const double* __restrict__ p, double* __restrict__ q,
                                const double* __restrict__ add, double* part, unsigned* count) {
+  pdl_wait();
   if (st->done) return;
   double acc = 0.0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -142,6 +146,7 @@ __global__ void k_pcg_spmv_dot(PcgState* st, int n, const int* __restrict__ rp, 
 __global__ void k_pcg_update(PcgState* st, int n, double* __restrict__ x, double* __restrict__ r,
                              const double* __restrict__ p, const double* __restrict__ q, double* part,
                              unsigned* count, double* hres, double* hdiag, double* hoff) {
+  pdl_wait();
   if (st->done) return;
   const double alpha = st->alpha;
   double acc = 0.0;
@@ -169,6 +174,7 @@ __global__ void k_pcg_update(PcgState* st, int n, double* __restrict__ x, double
 __global__ void k_pcg_true(PcgState* st, int n, const int* __restrict__ rp, const int* __restrict__ ci,
                            const double* __restrict__ va, const double* __restrict__ x, const double* __restrict__ b,
                            const double* __restrict__ add, double* part, unsigned* count) {
+  pdl_wait();
   const int force = st->force_true;
   if (!force && (st->done || !st->need_true)) return;
   double acc = 0.0;
@@ -197,10 +203,14 @@ __global__ void k_pcg_true(PcgState* st, int n, const int* __restrict__ rp, cons
   });
 }
 
-__global__ void k_set_force(PcgState* st, int v) { st->force_true = v; }
+__global__ void k_set_force(PcgState* st, int v) {
+  pdl_wait();
+  st->force_true = v;
+}
 
 // skip flag for work that only the true-residual check needs
 __global__ void k_true_gate(const PcgState* st, int* flag) {
+  pdl_wait();
   flag[0] = (st->force_true || (!st->done && st->need_true)) ? 0 : 1;
 }
 
@@ -401,32 +411,32 @@ void run_pcg(Ctx& c, const double* b_dev, double rtol, int maxit, awg_solve_repo
   AWG_CUDA(cudaEventCreate(&e1));
   AWG_CUDA(cudaEventRecord(e0, c.stream));
 
-  k_pcg_init<<<g, kThreads, 0, c.stream>>>(st, n, c.pb.p, c.px.p, c.pr.p, c.red.p, c.red_count.p);
+  launch(c, k_pcg_init, g, kThreads, 0, st, n, c.pb.p, c.px.p, c.pr.p, c.red.p, c.red_count.p);
   ++c.launches;
   op_apply(c, op_h, c.pr.p, c.pz.p, gate);
-  k_pcg_rz<<<g, kThreads, 0, c.stream>>>(st, n, c.pr.p, c.pz.p, c.red.p, c.red_count.p, 1);
-  k_pcg_p<<<g, kThreads, 0, c.stream>>>(st, n, c.pz.p, c.pp.p, 1);
+  launch(c, k_pcg_rz, g, kThreads, 0, st, n, c.pr.p, c.pz.p, c.red.p, c.red_count.p, 1);
+  launch(c, k_pcg_p, g, kThreads, 0, st, n, c.pz.p, c.pp.p, 1);
   c.launches += 2;
   check_launch("pcg init");
 
   auto iteration = [&]() {
     if (aplus) k::aminus(c, c.pp.p, am, gate);
-    k_pcg_spmv_dot<<<g, kThreads, 0, c.stream>>>(st, n, c.rp.p, c.ci.p, c.va.p, c.pp.p, c.pq.p,
+    launch(c, k_pcg_spmv_dot, g, kThreads, 0, st, n, c.rp.p, c.ci.p, c.va.p, c.pp.p, c.pq.p,
                                                   aplus ? am : nullptr, c.red.p, c.red_count.p);
-    k_pcg_update<<<g, kThreads, 0, c.stream>>>(st, n, c.px.p, c.pr.p, c.pp.p, c.pq.p, c.red.p, c.red_count.p,
+    launch(c, k_pcg_update, g, kThreads, 0, st, n, c.px.p, c.pr.p, c.pp.p, c.pq.p, c.red.p, c.red_count.p,
                                                c.hist_res.p, c.hist_diag.p, c.hist_off.p);
     c.launches += 2;
     if (aplus) {
-      k_true_gate<<<1, 1, 0, c.stream>>>(st, c.pcg_flag.p);
+      launch(c, k_true_gate, 1, 1, 0, st, c.pcg_flag.p);
       ++c.launches;
       k::aminus(c, c.px.p, am, c.pcg_flag.p);
     }
-    k_pcg_true<<<g, kThreads, 0, c.stream>>>(st, n, c.rp.p, c.ci.p, c.va.p, c.px.p, c.pb.p, aplus ? am : nullptr,
+    launch(c, k_pcg_true, g, kThreads, 0, st, n, c.rp.p, c.ci.p, c.va.p, c.px.p, c.pb.p, aplus ? am : nullptr,
                                              c.red.p, c.red_count.p);
     ++c.launches;
     op_apply(c, op_h, c.pr.p, c.pz.p, gate);
-    k_pcg_rz<<<g, kThreads, 0, c.stream>>>(st, n, c.pr.p, c.pz.p, c.red.p, c.red_count.p, 0);
-    k_pcg_p<<<g, kThreads, 0, c.stream>>>(st, n, c.pz.p, c.pp.p, 0);
+    launch(c, k_pcg_rz, g, kThreads, 0, st, n, c.pr.p, c.pz.p, c.red.p, c.red_count.p, 0);
+    launch(c, k_pcg_p, g, kThreads, 0, st, n, c.pz.p, c.pp.p, 0);
     c.launches += 2;
     check_launch("pcg iteration");
   };
@@ -467,12 +477,12 @@ void run_pcg(Ctx& c, const double* b_dev, double rtol, int maxit, awg_solve_repo
   }
 
   if (!h.converged && h.it > 0 && !h.error) {
-    k_set_force<<<1, 1, 0, c.stream>>>(st, 1);
+    launch(c, k_set_force, 1, 1, 0, st, 1);
     c.launches += 1;
     if (aplus) k::aminus(c, c.px.p, am, nullptr);
-    k_pcg_true<<<g, kThreads, 0, c.stream>>>(st, n, c.rp.p, c.ci.p, c.va.p, c.px.p, c.pb.p, aplus ? am : nullptr,
+    launch(c, k_pcg_true, g, kThreads, 0, st, n, c.rp.p, c.ci.p, c.va.p, c.px.p, c.pb.p, aplus ? am : nullptr,
                                              c.red.p, c.red_count.p);
-    k_set_force<<<1, 1, 0, c.stream>>>(st, 0);
+    launch(c, k_set_force, 1, 1, 0, st, 0);
     c.launches += 2;
     AWG_CUDA(cudaMemcpyAsync(&h, st, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
   }
