@@ -145,6 +145,27 @@ int awg_set_matrix(struct awg_ctx* ctx, int n, const int* row_offsets, const int
 /* offsets: N+1 (int64), indices: sorted, duplicate-free global dofs per subdomain */
 int awg_set_partition(struct awg_ctx* ctx, int n_sub, const long long* offsets, const int* indices);
 
+/* GPU-side problem assembly, an alternative to
+ * awg_set_matrix / awg_set_partition for the benchmark generators:
+ *   awg_assemble_fd         cell-centred 5-point (dims 2) / 7-point (dims 3) diffusion
+ *                           with harmonic face coefficients; shape = cells per
+ *                           axis, cell_coef lexicographic (x fastest), host memory
+ *   awg_assemble_elasticity Q1 plane strain, h = 1 (assemble, src/fem.cpp:99-162, with the
+ *                           element formula of fem.cpp:53-97 and TripletBuilder's summation
+ *                           order, src/sparse.cpp:19-47); element row ey uses material
+ *                           (ey / layer_thickness) % n_materials; load = body force (2);
+ *                           the assembled rhs is awg_get_array(16)
+ *   awg_partition_owner     Omega^s = disjoint owners grown by `overlap` rings of matrix-graph
+ *                           closure (src/partition.cpp:79-90), computed on the device
+ *   awg_partition_boxes     the same with box owners of the assembled grid / mesh nodes
+ * Built on the device, then installed exactly as awg_set_matrix / awg_set_partition
+ * would (same validation, same errors). */
+int awg_assemble_fd(struct awg_ctx* ctx, int dims, const int* shape, const double* cell_coef);
+int awg_assemble_elasticity(struct awg_ctx* ctx, int nodes_x, int nodes_y, int layer_thickness, int n_materials,
+                            const double* young, const double* poisson, const double* load);
+int awg_partition_owner(struct awg_ctx* ctx, const int* owner, int n_sub, int overlap);
+int awg_partition_boxes(struct awg_ctx* ctx, const int* boxes, int overlap);
+
 int awg_setup(struct awg_ctx* ctx, const awg_config* cfg);
 int awg_load_factors(struct awg_ctx* ctx, const awg_config* cfg, const awg_factors* f);
 
@@ -161,7 +182,9 @@ int awg_get_history(struct awg_ctx* ctx, int which /*0 resid,1 diag,2 offdiag*/,
  *  4 pencil eigenvalues (sum n_s)          5 multiplicity (n, int)
  *  6 k0_retained (r0, int)  7 k0_l11 (r0*r0)  8 kw_retained (rw, int)  9 kw_l11 (rw*rw)
  *  10 W (n*n_minus)  11 neg_weights (n_minus)  12 w_inner_iterations (n_minus, int)
- *  13 Y (sum n_s k_s)  14 V (sum n_s^2)  15 eps_zero (N) */
+ *  13 Y (sum n_s k_s)  14 V (sum n_s^2)  15 eps_zero (N)  16 assembled rhs (n)
+ *  17 row_offsets (n+1, int)  18 col_indices (nnz, int)  19 values (nnz)
+ *  20 partition offsets (N+1, int)  21 partition indices (sum n_s, int) */
 int awg_get_array(struct awg_ctx* ctx, int which, void* out, long long cap_elems, long long* n_elems);
 
 /* Kernel launches issued by this context since creation (product kernels only). */

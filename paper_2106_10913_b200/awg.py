@@ -164,7 +164,8 @@ EXPORTED_SYMBOLS = [
     "awg_create", "awg_destroy", "awg_last_error", "awg_last_error_index", "awg_set_matrix",
     "awg_set_partition", "awg_setup", "awg_load_factors", "awg_apply", "awg_pcg", "awg_query",
     "awg_get_history", "awg_get_array", "awg_launch_count", "awg_time_apply", "awg_time_kernel",
-    "awg_synthetic_factors",
+    "awg_synthetic_factors", "awg_assemble_fd", "awg_assemble_elasticity", "awg_partition_owner",
+    "awg_partition_boxes",
 ]
 
 _lib = None
@@ -187,6 +188,10 @@ def load_library(path: str = LIB_PATH):
     lib.awg_last_error_index.argtypes = [vp]
     lib.awg_set_matrix.argtypes = [vp, ctypes.c_int, _ip, _ip, _dp]
     lib.awg_set_partition.argtypes = [vp, ctypes.c_int, ctypes.POINTER(ctypes.c_longlong), _ip]
+    lib.awg_assemble_fd.argtypes = [vp, ctypes.c_int, _ip, _dp]
+    lib.awg_assemble_elasticity.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _dp, _dp, _dp]
+    lib.awg_partition_owner.argtypes = [vp, _ip, ctypes.c_int, ctypes.c_int]
+    lib.awg_partition_boxes.argtypes = [vp, _ip, ctypes.c_int]
     lib.awg_setup.argtypes = [vp, ctypes.POINTER(_Config)]
     lib.awg_load_factors.argtypes = [vp, ctypes.POINTER(_Config), ctypes.POINTER(_Factors)]
     lib.awg_apply.argtypes = [vp, ctypes.c_int, vp, vp, ctypes.c_int]
@@ -251,7 +256,9 @@ class Partition:
 _ARRAYS = {"lam": (0, "f"), "n_nonpos": (1, "i"), "n_zero": (2, "i"), "ks": (3, "i"), "pencil_lam": (4, "f"),
            "multiplicity": (5, "i"), "k0_retained": (6, "i"), "k0_l11": (7, "f"), "kw_retained": (8, "i"),
            "kw_l11": (9, "f"), "W": (10, "f"), "neg_weights": (11, "f"), "w_inner_iterations": (12, "i"),
-           "Y": (13, "f"), "V": (14, "f"), "eps_zero": (15, "f")}
+           "Y": (13, "f"), "V": (14, "f"), "eps_zero": (15, "f"), "assembled_rhs": (16, "f"),
+           "row_offsets": (17, "i"), "col_indices": (18, "i"), "values": (19, "f"), "part_offsets": (20, "i"),
+           "part_indices": (21, "i")}
 
 
 class ProblemContext:
@@ -284,6 +291,61 @@ class ProblemContext:
         self._check(self._lib.awg_set_partition(self._h, partition.count(), _ptr(off, ctypes.c_longlong),
                                                  _ptr(idx, ctypes.c_int)))
         self.cfg: Optional[PreconditionerConfig] = None
+
+    # -- GPU-side assembly -------------------------------------
+    @classmethod
+    def _bare(cls, device: int = 0) -> "ProblemContext":
+        self = cls.__new__(cls)
+        self._lib = load_library()
+        h = ctypes.c_void_p()
+        rc = self._lib.awg_create(ctypes.byref(h), device)
+        self._h = h
+        if rc != AWG_OK:
+            msg = self._lib.awg_last_error(h).decode()
+            self._lib.awg_destroy(h)
+            self._h = None
+            raise AwgCudaError(msg)
+        self.cfg = None
+        self._keep = []
+        return self
+
+    def _adopt(self, b) -> None:
+        """Host views of the device-assembled system (reports, checks)."""
+        n = self.query()["n"]
+        self.a = SparseSymMatrix(n, self.get("row_offsets"), self.get("col_indices"), self.get("values"))
+        off, idx = self.get("part_offsets"), self.get("part_indices")
+        self.partition = Partition([idx[off[s]:off[s + 1]] for s in range(len(off) - 1)], n)
+        self.b = None if b is None else _f64(b)
+
+    @classmethod
+    def assemble_fd(cls, shape, cell_coef, b, boxes, overlap: int, device: int = 0) -> "ProblemContext":
+        """Cell-centred diffusion assembled on the device, box partition with
+        ``overlap`` rings of closure computed on the device."""
+        self = cls._bare(device)
+        sh = _i32(np.asarray(shape))
+        coef = _f64(cell_coef)
+        self._check(self._lib.awg_assemble_fd(self._h, len(sh), _ptr(sh, ctypes.c_int), _ptr(coef, ctypes.c_double)))
+        bx = _i32(np.asarray(boxes))
+        self._check(self._lib.awg_partition_boxes(self._h, _ptr(bx, ctypes.c_int), int(overlap)))
+        self._adopt(b)
+        return self
+
+    @classmethod
+    def assemble_elasticity(cls, nodes_x: int, nodes_y: int, layer_thickness: int, materials, boxes, overlap: int,
+                            load=(0.0, -9.81), device: int = 0) -> "ProblemContext":
+        """Q1 plane strain assembled on the device (fem.cpp:99-162 rules); the
+        body-force rhs comes back from the device."""
+        self = cls._bare(device)
+        e = _f64([m[0] for m in materials])
+        nu = _f64([m[1] for m in materials])
+        ld = _f64(load)
+        self._check(self._lib.awg_assemble_elasticity(self._h, int(nodes_x), int(nodes_y), int(layer_thickness),
+                                                       len(e), _ptr(e, ctypes.c_double), _ptr(nu, ctypes.c_double),
+                                                       _ptr(ld, ctypes.c_double)))
+        bx = _i32(np.asarray(boxes))
+        self._check(self._lib.awg_partition_boxes(self._h, _ptr(bx, ctypes.c_int), int(overlap)))
+        self._adopt(self.get("assembled_rhs"))
+        return self
 
     # -- plumbing ------------------------------------------------------------
     def _check(self, rc: int):
@@ -493,6 +555,18 @@ def context_from_problem(p, device: int = 0) -> ProblemContext:
     """ProblemContext from a problems.Problem."""
     a = SparseSymMatrix(p.n, p.row_offsets, p.col_indices, p.values)
     return ProblemContext(a, p.b, Partition(list(p.omega), p.n), device=device)
+
+
+def context_from_spec(sp: dict, device: int = 0) -> ProblemContext:
+    """ProblemContext assembled on the device from problems.spec(name)."""
+    from . import problems
+
+    if sp["kind"] == "fd":
+        n = int(np.prod(sp["shape"]))
+        b = problems.uniform(0, n, -1.0, 1.0)
+        return ProblemContext.assemble_fd(sp["shape"], sp["coeff"], b, sp["boxes"], sp["overlap"], device=device)
+    return ProblemContext.assemble_elasticity(sp["nodes_x"], sp["nodes_y"], sp["layer_thickness"], sp["materials"],
+                                              sp["boxes"], sp["overlap"], device=device)
 
 
 def config_for(p, **kw) -> PreconditionerConfig:

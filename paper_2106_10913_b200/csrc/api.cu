@@ -396,8 +396,11 @@ int awg_create(awg_ctx** out, int device) {
     cc.use_pdl = !(pdl && pdl[0] == '0');
     int lo = 0, hi = 0;
     AWG_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    AWG_CUDA(cudaStreamCreateWithPriority(&cc.stream, cudaStreamNonBlocking, cc.use_priority ? hi : 0));
-    AWG_CUDA(cudaStreamCreateWithPriority(&cc.side, cudaStreamNonBlocking, cc.use_priority ? lo : 0));
+    const bool side_first = prio && prio[0] == '2';  // experiment: the W branch outranks the main stream
+    AWG_CUDA(cudaStreamCreateWithPriority(&cc.stream, cudaStreamNonBlocking,
+                                          cc.use_priority ? (side_first ? lo : hi) : 0));
+    AWG_CUDA(cudaStreamCreateWithPriority(&cc.side, cudaStreamNonBlocking,
+                                          cc.use_priority ? (side_first ? hi : lo) : 0));
     AWG_CUDA(cudaEventCreateWithFlags(&cc.ev_fork, cudaEventDisableTiming));
     AWG_CUDA(cudaEventCreateWithFlags(&cc.ev_join, cudaEventDisableTiming));
     AWG_CUDA(cudaDeviceGetAttribute(&cc.sm_count, cudaDevAttrMultiProcessorCount, device));
@@ -448,6 +451,8 @@ int awg_set_matrix(awg_ctx* ctx, int n, const int* rp, const int* ci, const doub
     }
     c.n = n;
     c.nnz = rp[n];
+    c.asm_kind = -1;
+    c.h_rhs_asm.clear();
     c.h_rp.assign(rp, rp + n + 1);
     c.h_ci.assign(ci, ci + c.nnz);
     c.h_va.assign(va, va + c.nnz);
@@ -782,6 +787,97 @@ int awg_get_history(awg_ctx* ctx, int which, double* out, int cap) {
   return int(v.size());
 }
 
+int awg_assemble_fd(awg_ctx* ctx, int dims, const int* shape, const double* cell_coef) {
+  std::vector<int> rp, ci;
+  std::vector<double> va;
+  int rc = guarded(ctx, [&](Ctx& c) {
+    if (c.device < 0) c.fail(AWG_E_CUDA, "no CUDA device");
+    assemble_fd(c, dims, shape, cell_coef, rp, ci, va);
+  });
+  if (rc != AWG_OK) return rc;
+  rc = awg_set_matrix(ctx, int(rp.size()) - 1, rp.data(), ci.data(), va.data());
+  if (rc == AWG_OK) {
+    ctx->c.asm_kind = 0;
+    ctx->c.asm_dims = dims;
+    for (int a = 0; a < 3; ++a) ctx->c.asm_shape[a] = a < dims ? shape[a] : 1;
+  }
+  return rc;
+}
+
+int awg_assemble_elasticity(awg_ctx* ctx, int nodes_x, int nodes_y, int layer_thickness, int n_materials,
+                            const double* young, const double* poisson, const double* load) {
+  std::vector<int> rp, ci;
+  std::vector<double> va, b;
+  int rc = guarded(ctx, [&](Ctx& c) {
+    if (c.device < 0) c.fail(AWG_E_CUDA, "no CUDA device");
+    assemble_elasticity(c, nodes_x, nodes_y, layer_thickness, n_materials, young, poisson, load, rp, ci, va, b);
+  });
+  if (rc != AWG_OK) return rc;
+  rc = awg_set_matrix(ctx, int(rp.size()) - 1, rp.data(), ci.data(), va.data());
+  if (rc == AWG_OK) {
+    ctx->c.asm_kind = 1;
+    ctx->c.asm_dims = 2;
+    ctx->c.asm_shape[0] = nodes_x;
+    ctx->c.asm_shape[1] = nodes_y;
+    ctx->c.asm_shape[2] = 1;
+    ctx->c.h_rhs_asm = b;
+  }
+  return rc;
+}
+
+int awg_partition_owner(awg_ctx* ctx, const int* owner, int n_sub, int overlap) {
+  std::vector<long long> off;
+  std::vector<int> idx;
+  int rc = guarded(ctx, [&](Ctx& c) {
+    if (c.n == 0) c.fail(AWG_E_STATE, "partition: set or assemble the matrix first");
+    if (!owner) c.fail(AWG_E_ARG, "partition: bad arguments");
+    partition_closure(c, std::vector<int>(owner, owner + c.n), n_sub, overlap, off, idx);
+  });
+  if (rc != AWG_OK) return rc;
+  return awg_set_partition(ctx, n_sub, off.data(), idx.data());
+}
+
+int awg_partition_boxes(awg_ctx* ctx, const int* boxes, int overlap) {
+  std::vector<int> owner;
+  int nsub = 0;
+  int rc = guarded(ctx, [&](Ctx& c) {
+    if (c.asm_kind < 0) c.fail(AWG_E_STATE, "partition_boxes: the matrix was not assembled on the device");
+    if (!boxes) c.fail(AWG_E_ARG, "partition_boxes: bad arguments");
+    const int dims = c.asm_dims;
+    nsub = 1;
+    for (int a = 0; a < dims; ++a) {
+      if (boxes[a] < 1 || boxes[a] > c.asm_shape[a]) c.fail(AWG_E_ARG, "partition_boxes: bad box counts");
+      nsub *= boxes[a];
+    }
+    owner.resize(c.n);
+    if (c.asm_kind == 0) {
+      // cells lexicographic (x fastest), box index per axis coord // (shape / boxes)
+      const int nx = c.asm_shape[0], ny = c.asm_shape[1];
+      for (int i = 0; i < c.n; ++i) {
+        const int co[3] = {i % nx, (i / nx) % ny, i / (nx * ny)};
+        int o = 0, mult = 1;
+        for (int a = 0; a < dims; ++a) {
+          o += (co[a] / (c.asm_shape[a] / boxes[a])) * mult;
+          mult *= boxes[a];
+        }
+        owner[i] = o;
+      }
+    } else {
+      // nodal boxes of the Q1 mesh; both dofs of a free node follow the node
+      const int nx = c.asm_shape[0], ny = c.asm_shape[1];
+      const int bw = nx / boxes[0], bh = ny / boxes[1];
+      for (int i = 0; i < c.n; ++i) {
+        const int f = i >> 1, ix = f % (nx - 1) + 1, iy = f / (nx - 1);
+        owner[i] = ix / bw + boxes[0] * (iy / bh);
+      }
+    }
+    for (int o : owner)
+      if (o >= nsub) c.fail(AWG_E_ARG, "partition_boxes: grid not divisible by the box counts");
+  });
+  if (rc != AWG_OK) return rc;
+  return awg_partition_owner(ctx, owner.data(), nsub, overlap);
+}
+
 int awg_get_array(awg_ctx* ctx, int which, void* out, long long cap, long long* n_elems) {
   return guarded(ctx, [&](Ctx& c) {
     std::vector<double> dv;
@@ -828,6 +924,15 @@ int awg_get_array(awg_ctx* ctx, int which, void* out, long long cap, long long* 
         break;
       }
       case 15: dv = c.h_eps; break;
+      case 16: dv = c.h_rhs_asm; break;
+      case 17: iv = c.h_rp; is_int = true; break;
+      case 18: iv = c.h_ci; is_int = true; break;
+      case 19: dv = c.h_va; break;
+      case 20:
+        for (long long o : c.h_poff) iv.push_back(int(o));
+        is_int = true;
+        break;
+      case 21: iv = c.h_pidx; is_int = true; break;
       default: c.fail(AWG_E_ARG, "get_array: unknown array");
     }
     const long long cnt = is_int ? (long long)iv.size() : (long long)dv.size();

@@ -228,6 +228,9 @@ struct Ctx {
   // single-pass tuning (env AWG_FUSED_CPB / AWG_FUSED_NBUF / AWG_FUSED_CHUNKS; 0 = automatic)
   bool use_priority = true;  // main stream high priority, W branch low
   bool use_pdl = true;       // programmatic dependent launch on the solve path
+  // GPU-side assembly (assemble.cu): -1 external matrix, 0 cell grid, 1 Q1 mesh
+  int asm_kind = -1, asm_dims = 0, asm_shape[3] = {0, 0, 0};
+  std::vector<double> h_rhs_asm;  // assembled right-hand side (elasticity body force)
   int fused_cpb = 0, fused_nbuf = 0, fused_chunks_per_sm = 8;  // 0: automatic
   BsPlan bs_neg, bs_z;   // A- dots (V^s columns k < n_nonpos), Z^T x (Y_s blocks)
   LocalPlan plan_nn;     // V^s with the eigenvalue mask (NN)
@@ -326,6 +329,14 @@ void op_apply(Ctx& c, int op, const double* x, double* y, const int* gate);
 void run_pcg(Ctx& c, const double* b_dev, double rtol, int maxit, awg_solve_report* rep,
              int op_a = AWG_OP_A, int op_h = AWG_OP_H3);
 void finalize_factors(Ctx& c);  // task lists, A- modes, inverses, work buffers
+// GPU-side problem assembly (assemble.cu)
+void assemble_fd(Ctx& c, int dims, const int* shape, const double* coef, std::vector<int>& rp, std::vector<int>& ci,
+                 std::vector<double>& va);
+void assemble_elasticity(Ctx& c, int nodes_x, int nodes_y, int layer, int nmat, const double* young,
+                         const double* poisson, const double* load, std::vector<int>& rp, std::vector<int>& ci,
+                         std::vector<double>& va, std::vector<double>& b);
+void partition_closure(Ctx& c, const std::vector<int>& owner, int nsub, int rings, std::vector<long long>& off,
+                       std::vector<int>& idx);
 void build_core(Ctx& c);        // INEX core LU
 void run_setup(Ctx& c, const awg_config& cfg);  // setup.cu
 void build_local_cholesky(Ctx& c);              // setup.cu: AS / AS+ factors U^s = L^-T

@@ -393,37 +393,58 @@ def block_powers(shape, block, seed=1, lo=-3.0, hi=3.0):
     return vals[bidx.reshape(-1)]
 
 
-def make(name: str) -> Problem:
-    """BASELINE.json configs (c1..c5) and the small analogues (t*) used for
-    committed parity fixtures."""
+def spec(name: str) -> dict:
+    """Generator arguments of the BASELINE.json configs (c1..c5) and the small
+    analogues used for committed parity fixtures: kind "fd" (cell grid) or
+    "elasticity" (Q1 mesh).  make() builds them on the host, the GPU-side
+    assembly (awg.context_from_spec) on the device."""
+    def fd(shape, coeff, boxes, overlap, **kw):
+        return dict(kind="fd", name=name, shape=shape, coeff=coeff, boxes=boxes, overlap=overlap, **kw)
+
+    def el(nodes_x, nodes_y, layer, materials, boxes, overlap, **kw):
+        return dict(kind="elasticity", name=name, nodes_x=nodes_x, nodes_y=nodes_y, layer_thickness=layer,
+                    materials=materials, boxes=boxes, overlap=overlap, **kw)
+
+    soft_hard = [(1e7, 0.45), (1.0, 0.3)]
     if name == "c1":
-        return fd_problem("c1", (32, 32), np.ones(1024), (2, 2), 1, tau_sharp=0.5)
+        return fd((32, 32), np.ones(1024), (2, 2), 1, tau_sharp=0.5)
     if name == "c2":
-        return fd_problem("c2", (256, 256), c2_channels(256, 256), (4, 4), 2, tau_sharp=0.1)
+        return fd((256, 256), c2_channels(256, 256), (4, 4), 2, tau_sharp=0.1)
     if name == "c3":
-        return fd_problem("c3", (64, 64, 64), lognormal(64 ** 3), (4, 4, 4), 1, fixed_k=10)
+        return fd((64, 64, 64), lognormal(64 ** 3), (4, 4, 4), 1, fixed_k=10)
     if name == "c4":
-        return elasticity_problem("c4", 512, 128, 8, [(1e7, 0.45), (1.0, 0.3)], (8, 4), 1, tau_sharp=0.1)
+        return el(512, 128, 8, soft_hard, (8, 4), 1, tau_sharp=0.1)
     if name == "c5":
-        return fd_problem("c5", (96, 96, 96), block_powers((96, 96, 96), 8), (6, 6, 6), 1, fixed_k=8)
+        return fd((96, 96, 96), block_powers((96, 96, 96), 8), (6, 6, 6), 1, fixed_k=8)
     # small analogues (same generators, fixture-sized)
     if name == "t2d":  # c1 analogue with n- > 0 via channels
-        return fd_problem("t2d", (24, 24), c2_channels(24, 24, band=6, contrast=1e3), (2, 2), 1, tau_sharp=0.2)
+        return fd((24, 24), c2_channels(24, 24, band=6, contrast=1e3), (2, 2), 1, tau_sharp=0.2)
     if name == "t2d_ov2":  # c2 analogue
-        return fd_problem("t2d_ov2", (24, 24), c2_channels(24, 24), (2, 2), 2, tau_sharp=0.1)
+        return fd((24, 24), c2_channels(24, 24), (2, 2), 2, tau_sharp=0.1)
     if name == "t3d":  # c3 analogue (fixed k)
-        return fd_problem("t3d", (8, 8, 8), lognormal(512), (2, 2, 2), 1, fixed_k=4)
+        return fd((8, 8, 8), lognormal(512), (2, 2, 2), 1, fixed_k=4)
     if name == "t3d_blocks":  # c5 analogue (fixed k)
-        return fd_problem("t3d_blocks", (8, 8, 8), block_powers((8, 8, 8), 4), (2, 2, 2), 1, fixed_k=3)
+        return fd((8, 8, 8), block_powers((8, 8, 8), 4), (2, 2, 2), 1, fixed_k=3)
     if name == "telas":  # c4 analogue
-        return elasticity_problem("telas", 16, 8, 2, [(1e7, 0.45), (1.0, 0.3)], (2, 1), 1, tau_sharp=0.1)
+        return el(16, 8, 2, soft_hard, (2, 1), 1, tau_sharp=0.1)
     if name == "telas8":  # c4 analogue with c4's 8-element layers and 2x2 nodal boxes
-        return elasticity_problem("telas8", 32, 16, 8, [(1e7, 0.45), (1.0, 0.3)], (2, 2), 1, tau_sharp=0.1)
-    if name == "c4mid":  # c4 with c4-sized subdomains (n_s ~ 4,200) but 4 of them: the reference finishes
-        return elasticity_problem("c4mid", 128, 64, 8, [(1e7, 0.45), (1.0, 0.3)], (2, 2), 1, tau_sharp=0.1)
+        return el(32, 16, 8, soft_hard, (2, 2), 1, tau_sharp=0.1)
+    if name == "c4mid":  # c4 with c4-sized subdomains (n_s ~ 4,200) but 4 of them
+        return el(128, 64, 8, soft_hard, (2, 2), 1, tau_sharp=0.1)
     if name == "c4s":  # between telas8 and c4mid (n_s ~ 2,400, six 8-element layers)
-        return elasticity_problem("c4s", 96, 48, 8, [(1e7, 0.45), (1.0, 0.3)], (2, 2), 1, tau_sharp=0.1)
+        return el(96, 48, 8, soft_hard, (2, 2), 1, tau_sharp=0.1)
     raise KeyError(name)
+
+
+def make(name: str) -> Problem:
+    """BASELINE.json configs (c1..c5) and the small analogues (t*), built on
+    the host."""
+    sp = dict(spec(name))
+    kind = sp.pop("kind")
+    if kind == "fd":
+        return fd_problem(sp.pop("name"), sp.pop("shape"), sp.pop("coeff"), sp.pop("boxes"), sp.pop("overlap"), **sp)
+    return elasticity_problem(sp.pop("name"), sp.pop("nodes_x"), sp.pop("nodes_y"), sp.pop("layer_thickness"),
+                              sp.pop("materials"), sp.pop("boxes"), sp.pop("overlap"), **sp)
 
 
 CONFIGS = ["c1", "c2", "c3", "c4", "c5"]
