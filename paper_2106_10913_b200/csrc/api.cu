@@ -413,6 +413,7 @@ int awg_create(awg_ctx** out, int device) {
     cc.fused_cpb = env_int("AWG_FUSED_CPB", 0);
     cc.fused_nbuf = env_int("AWG_FUSED_NBUF", 0);
     cc.fused_chunks_per_sm = std::max(1, env_int("AWG_FUSED_CHUNKS", 8));
+    cc.fused_reserve = std::max(0, env_int("AWG_FUSED_RESERVE", 0));
   });
   *out = ctx;
   return rc;

@@ -1007,7 +1007,8 @@ void nn_fused(Ctx& c, const double* x, const int* gate) {
   if (!pl.tf.n) return;
   if (!c.fused_queue.p) c.fused_queue.alloc(1);
   AWG_CUDA(cudaMemsetAsync(c.fused_queue.p, 0, sizeof(int), c.stream));
-  const int grid = std::min(int(pl.tf.n), c.sm_count);
+  // persistent CTAs: one per SM, less the SMs left to the concurrent W branch
+  const int grid = std::min(int(pl.tf.n), std::max(1, c.sm_count - c.fused_reserve));
   const double* F = nn ? c.V.p : c.U.p;
   const double* D = nn ? c.ds.p : nullptr;
   if (nn && cpb == 2)
