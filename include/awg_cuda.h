@@ -197,6 +197,10 @@ int awg_time_apply(struct awg_ctx* ctx, int op, int reps, double* ms_per_apply);
  * local solve (V^s streamed once).  Also returns the
  * algorithmic bytes one launch must move (operands read once, results written). */
 int awg_time_kernel(struct awg_ctx* ctx, int which, int reps, double* ms_per_launch, double* bytes_per_launch);
+/* In-kernel launch timer of the single-pass local solve (%globaltimer, first
+ * CTA start to last CTA end, accumulated over every launch, graphs included):
+ * total ms and launch count since the last reset. */
+int awg_kernel_timer(struct awg_ctx* ctx, int reset, double* ms_total, long long* launches);
 /* Benchmark hook: synthetic local factors (V^s filled on the device with
  * pseudo-random values, n_nonpos = m_per_sub zero modes, no coarse spaces) so
  * the local-solve kernels can be timed at full scale without the setup. */

@@ -164,7 +164,7 @@ EXPORTED_SYMBOLS = [
     "awg_create", "awg_destroy", "awg_last_error", "awg_last_error_index", "awg_set_matrix",
     "awg_set_partition", "awg_setup", "awg_load_factors", "awg_apply", "awg_pcg", "awg_query",
     "awg_get_history", "awg_get_array", "awg_launch_count", "awg_time_apply", "awg_time_kernel",
-    "awg_synthetic_factors", "awg_assemble_fd", "awg_assemble_elasticity", "awg_partition_owner",
+    "awg_synthetic_factors", "awg_kernel_timer", "awg_assemble_fd", "awg_assemble_elasticity", "awg_partition_owner",
     "awg_partition_boxes",
 ]
 
@@ -189,6 +189,8 @@ def load_library(path: str = LIB_PATH):
     lib.awg_set_matrix.argtypes = [vp, ctypes.c_int, _ip, _ip, _dp]
     lib.awg_set_partition.argtypes = [vp, ctypes.c_int, ctypes.POINTER(ctypes.c_longlong), _ip]
     lib.awg_assemble_fd.argtypes = [vp, ctypes.c_int, _ip, _dp]
+    lib.awg_kernel_timer.argtypes = [vp, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
+                                     ctypes.POINTER(ctypes.c_longlong)]
     lib.awg_assemble_elasticity.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _dp, _dp, _dp]
     lib.awg_partition_owner.argtypes = [vp, _ip, ctypes.c_int, ctypes.c_int]
     lib.awg_partition_boxes.argtypes = [vp, _ip, ctypes.c_int]
@@ -439,6 +441,13 @@ class ProblemContext:
         return ms.value
 
     KERNELS = {"nn_gemvT": 0, "nn_gemv": 1, "spmv": 2, "w_gemvT": 3, "w_gemv": 4, "nn_fused": 5}
+
+    def kernel_timer(self, reset: bool = False) -> Tuple[float, int]:
+        """(total ms, launches) of the single-pass local solve measured inside
+        the kernel since the last reset (covers graph-launched solves)."""
+        ms, n = ctypes.c_double(), ctypes.c_longlong()
+        self._check(self._lib.awg_kernel_timer(self._h, int(reset), ctypes.byref(ms), ctypes.byref(n)))
+        return ms.value, n.value
 
     def time_kernel(self, name: str, reps: int = 10) -> Tuple[float, float]:
         """(ms per launch, algorithmic bytes per launch) of one hot kernel."""

@@ -788,6 +788,20 @@ int awg_get_history(awg_ctx* ctx, int which, double* out, int cap) {
   return int(v.size());
 }
 
+int awg_kernel_timer(awg_ctx* ctx, int reset, double* ms_total, long long* launches) {
+  return guarded(ctx, [&](Ctx& c) {
+    unsigned long long h[5] = {~0ull, 0, 0, 0, 0};
+    AWG_CUDA(cudaStreamSynchronize(c.stream));
+    if (c.fused_timer.p) AWG_CUDA(cudaMemcpy(h, c.fused_timer.p, sizeof(h), cudaMemcpyDeviceToHost));
+    if (ms_total) *ms_total = double(h[3]) * 1e-6;
+    if (launches) *launches = (long long)h[4];
+    if (reset && c.fused_timer.p) {
+      const unsigned long long init[5] = {~0ull, 0, 0, 0, 0};
+      AWG_CUDA(cudaMemcpy(c.fused_timer.p, init, sizeof(init), cudaMemcpyHostToDevice));
+    }
+  });
+}
+
 int awg_assemble_fd(awg_ctx* ctx, int dims, const int* shape, const double* cell_coef) {
   std::vector<int> rp, ci;
   std::vector<double> va;

@@ -295,6 +295,31 @@ constexpr size_t kFusedSmemCap = size_t(224) * 1024;  // dynamic shared memory p
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
+// In-kernel launch timer (live inside the timed solve; bench.py's roofline):
+// tmr[0] earliest CTA start, tmr[1] latest CTA end, tmr[2] CTAs done,
+// tmr[3] accumulated ns, tmr[4] launches.  The last CTA folds this launch's
+// span (first CTA start -> last CTA end) into the total and re-arms.
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ void kernel_timer_end(unsigned long long* tmr) {
+  atomicMax(&tmr[1], globaltimer_ns());
+  __threadfence();
+  if (atomicAdd(&tmr[2], 1ull) == gridDim.x - 1) {
+    __threadfence();
+    const unsigned long long t0 = atomicAdd(&tmr[0], 0ull), t1 = atomicAdd(&tmr[1], 0ull);
+    tmr[3] += t1 - t0;
+    tmr[4] += 1;
+    tmr[0] = ~0ull;
+    tmr[1] = 0;
+    tmr[2] = 0;
+    __threadfence();
+  }
+}
+
 __device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
@@ -340,8 +365,10 @@ __global__ void __launch_bounds__(kFusedT, 1) k_nn_fused(const int* __restrict__
                                                          const int* __restrict__ pidx, const double* __restrict__ ds,
                                                          const double* __restrict__ x, const double* __restrict__ rlam,
                                                          long long P, double* __restrict__ part, int ntasks,
-                                                         int* __restrict__ queue, int nbuf, int ldmax, int smem_doubles) {
+                                                         int* __restrict__ queue, int nbuf, int ldmax, int smem_doubles,
+                                                         unsigned long long* __restrict__ tmr) {
   if (gated(gate)) return;
+  if (tmr && threadIdx.x == 0) atomicMin(&tmr[0], globaltimer_ns());
   extern __shared__ __align__(128) double fsm[];
   __shared__ __align__(8) unsigned long long bar[kFusedMaxBuf];
   __shared__ double red[2][CPB][kFusedT / 32];
@@ -469,6 +496,7 @@ __global__ void __launch_bounds__(kFusedT, 1) k_nn_fused(const int* __restrict__
     }
     g += nstep;
   }
+  if (tmr && tid == 0) kernel_timer_end(tmr);
 }
 
 // y[i] = sum over s containing i (ascending s) of D^s_i * (sum_kc part[kc][p(s,i)])
@@ -968,7 +996,7 @@ void launch_fused(Ctx& c, const LocalPlan& pl, const double* F, const double* D,
   }
   launch(c, k_nn_fused<TRI, R, CPB>, grid, kFusedT, smem, gate, pl.tf.p, F, c.voff.p, c.ns.p, c.ld.p, c.poff.p,
          c.pidx.p, D, x, TRI ? nullptr : c.rlam.p, c.P, c.wpart_nn.p, int(pl.tf.n), c.fused_queue.p, nbuf, ldmax,
-         int(smem / sizeof(double)));
+         int(smem / sizeof(double)), c.fused_timer.p);
 }
 
 template <bool TRI, int CPB>
@@ -1006,6 +1034,11 @@ void nn_fused(Ctx& c, const double* x, const int* gate) {
   const size_t smem = size_t(nbuf) * buf_bytes + tail;
   if (!pl.tf.n) return;
   if (!c.fused_queue.p) c.fused_queue.alloc(1);
+  if (!c.fused_timer.p) {
+    static const unsigned long long init[5] = {~0ull, 0, 0, 0, 0};
+    c.fused_timer.alloc(5);
+    AWG_CUDA(cudaMemcpyAsync(c.fused_timer.p, init, sizeof(init), cudaMemcpyHostToDevice, c.stream));
+  }
   AWG_CUDA(cudaMemsetAsync(c.fused_queue.p, 0, sizeof(int), c.stream));
   // persistent CTAs: one per SM, less the SMs left to the concurrent W branch
   const int grid = std::min(int(pl.tf.n), std::max(1, c.sm_count - c.fused_reserve));

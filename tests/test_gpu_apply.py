@@ -157,3 +157,16 @@ def test_single_pass_matches_two_pass():
         y1, y2 = ctx1.apply(awg.Op.H1, x), ctx2.apply(awg.Op.H1, x)
         assert rel(y1, y2) <= 1e-13
         assert rel(y1, ref) <= 1e-11 and rel(y2, ref) <= 1e-11
+
+
+def test_in_kernel_timer_counts_live_launches():
+    """The single-pass kernel's in-kernel timer (bench.py's live roofline
+    timing) counts exactly the local solves a graph-launched PCG performs —
+    iterations enqueued past convergence are gated off and not counted."""
+    g, s = golden_with_base("t2d")
+    ctx = make_ctx(g)
+    ctx.kernel_timer(reset=True)
+    x, rep = ctx.pcg(g["b"], s["rtol_solve"], 10000)
+    ms, launches = ctx.kernel_timer()
+    assert launches == rep.iterations
+    assert 0.0 < ms < rep.solve_ms
