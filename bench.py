@@ -212,7 +212,7 @@ def dist_env():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default=os.environ.get("AWG_BENCH_CONFIG", DEFAULT_CONFIG))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])

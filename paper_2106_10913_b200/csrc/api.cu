@@ -217,16 +217,21 @@ void finalize_factors(Ctx& c) {
       const long long target = std::max<long long>((long long)c.fused_chunks_per_sm * c.sm_count, N);  // queue granularity
       // >= 128 columns per task keeps the per-task restriction gather and partial
       // write (about 3 columns' worth of traffic) below ~3%
-      const int cs = int(std::max<long long>(128, (cols_total + target - 1) / target));
-      std::vector<GemvTask> tf;
+      const int cs = int(std::max<long long>(c.fused_min_cols, (cols_total + target - 1) / target));
+      std::vector<GemvTask> tf, tail;
       std::vector<int> nkf(N, 0);
       pl.kcmax_f = 1;
       for (int s = 0; s < N; ++s) {
         const int jstart = tri ? 0 : c.h_m[s];
-        const int cols = c.h_ns[s] - jstart;
+        int cols = c.h_ns[s] - jstart;
+        // guided tail (NN): the last tail_pct% of each subdomain's columns in
+        // quarter-size tasks, queued after every bulk task, so the persistent
+        // CTAs finish together
+        const int cs_tail = std::max(32, cs / 4);
+        int tcols = (!tri && c.fused_tail_pct > 0) ? (cols * c.fused_tail_pct / 100) / cs_tail * cs_tail : 0;
+        if (tcols >= cols) tcols = 0;
+        cols -= tcols;
         const int kcs = std::max(1, (cols + cs / 2) / cs);
-        nkf[s] = kcs;
-        pl.kcmax_f = std::max(pl.kcmax_f, kcs);
         for (int kc = 0; kc < kcs; ++kc) {
           // triangular factor: equal-area chunks (column j costs j + 1 rows)
           const double f0 = tri ? std::sqrt(double(kc) / kcs) : double(kc) / kcs;
@@ -235,7 +240,13 @@ void finalize_factors(Ctx& c) {
           const int j1 = kc + 1 == kcs ? jstart + cols : jstart + int(cols * f1);
           tf.push_back({s, 0, j0, j1, kc, 0});
         }
+        int kc = kcs;
+        for (int j0 = jstart + cols; j0 < jstart + cols + tcols; j0 += cs_tail, ++kc)
+          tail.push_back({s, 0, j0, j0 + cs_tail, kc, 0});
+        nkf[s] = kc;
+        pl.kcmax_f = std::max(pl.kcmax_f, kc);
       }
+      tf.insert(tf.end(), tail.begin(), tail.end());
       pl.tf.upload(tf, c.stream);
       pl.nkc_f.upload(nkf, c.stream);
     }
@@ -414,6 +425,8 @@ int awg_create(awg_ctx** out, int device) {
     cc.fused_nbuf = env_int("AWG_FUSED_NBUF", 0);
     cc.fused_chunks_per_sm = std::max(1, env_int("AWG_FUSED_CHUNKS", 8));
     cc.fused_reserve = std::max(0, env_int("AWG_FUSED_RESERVE", 0));
+    cc.fused_min_cols = std::max(8, env_int("AWG_FUSED_MINCOLS", 128));
+    cc.fused_tail_pct = std::max(0, std::min(90, env_int("AWG_FUSED_TAIL", 0)));
   });
   *out = ctx;
   return rc;

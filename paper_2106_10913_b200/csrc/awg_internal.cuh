@@ -232,7 +232,8 @@ struct Ctx {
   int asm_kind = -1, asm_dims = 0, asm_shape[3] = {0, 0, 0};
   std::vector<double> h_rhs_asm;  // assembled right-hand side (elasticity body force)
   DArr<unsigned long long> fused_timer;  // k_nn_fused launch timer (see kernels.cu)
-  int fused_reserve = 0;  // SMs the single-pass kernel leaves free (for the concurrent W branch)
+  int fused_reserve = 0;
+  int fused_min_cols = 128, fused_tail_pct = 0;  // single-pass task sizes (columns), guided tail share  // SMs the single-pass kernel leaves free (for the concurrent W branch)
   int fused_cpb = 0, fused_nbuf = 0, fused_chunks_per_sm = 8;  // 0: automatic
   BsPlan bs_neg, bs_z;   // A- dots (V^s columns k < n_nonpos), Z^T x (Y_s blocks)
   LocalPlan plan_nn;     // V^s with the eigenvalue mask (NN)

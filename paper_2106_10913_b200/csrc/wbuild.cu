@@ -16,6 +16,8 @@
 #include <cmath>
 #include <cstring>
 
+#include <string>
+
 #include "awg_internal.cuh"
 
 namespace awgb {
@@ -355,6 +357,30 @@ struct BlockOps {
   cublasHandle_t h;
   const CoarseFactor& k0;
   std::vector<int> qs, negoff, koff;  // per subdomain: negative modes, their offset, coarse column offset
+  // phase profile of one block pass (AWG_VERBOSE=2): events between phases
+  std::vector<std::pair<std::string, cudaEvent_t>> marks;
+  bool prof = false;
+  void mark(const char* name) {
+    if (!prof) return;
+    cudaEvent_t e;
+    AWG_CUDA(cudaEventCreate(&e));
+    AWG_CUDA(cudaEventRecord(e, c.stream));
+    marks.push_back({name, e});
+  }
+  void report() {
+    if (marks.size() < 2) return;
+    AWG_CUDA(cudaEventSynchronize(marks.back().second));
+    std::string line = "[awg setup]   W pass profile (ms):";
+    for (size_t i = 1; i < marks.size(); ++i) {
+      float ms = 0.f;
+      AWG_CUDA(cudaEventElapsedTime(&ms, marks[i - 1].second, marks[i].second));
+      line += " " + marks[i].first + "=" + std::to_string(ms);
+    }
+    std::fprintf(stderr, "%s\n", line.c_str());
+    for (auto& m : marks) cudaEventDestroy(m.second);
+    marks.clear();
+    prof = false;
+  }
 
   BlockOps(Ctx& cc, Block& kk, cublasHandle_t hh, const CoarseFactor& f) : c(cc), k(kk), h(hh), k0(f) {
     qs.resize(c.N);
@@ -500,6 +526,7 @@ struct BlockOps {
       return;
     }
     q(X, k.C0.p, done);
+    mark("h2.q");
     if (c.cfg.composition == 0) {
       h1(X, k.C1.p, done);
       axpby(k.C1.p, k.C0.p, nullptr, Y, 1, done);
@@ -507,10 +534,15 @@ struct BlockOps {
     }
     aminus(k.C0.p, k.C1.p, done);
     spmv(k.C0.p, k.C2.p, 2, k.C1.p, X, done);
+    mark("h2.aplus");
     h1(k.C2.p, k.C3.p, done);
+    mark("h2.h1");
     aplus(k.C3.p, k.C4.p, done);
+    mark("h2.aplus2");
     q(k.C4.p, k.C5.p, done);
+    mark("h2.q2");
     axpby(k.C3.p, k.C5.p, k.C0.p, Y, 0, done);
+    mark("h2.axpby");
   }
   void axpby(const double* a, const double* b, const double* d, double* y, int mode, const int* done) {
     kb_axpby<<<grid_n(), kT, 0, c.stream>>>(c.n, k.ld, a, b, d, y, mode, done);
@@ -626,8 +658,13 @@ void build_w_batched(Ctx& c, cublasHandle_t h, const std::vector<std::pair<int, 
   };
   refill();
   const dim3 gn = ops.grid_n();
+  const char* vb = std::getenv("AWG_VERBOSE");
+  const bool prof_pass = vb && vb[0] == '2';
   while (finished < total) {
+    ops.prof = prof_pass && passes == 5;
+    ops.mark("start");
     ops.aplus(k.Pm.p, k.Q.p, k.done.p);
+    ops.mark("aplus");
     ops.dot(k.Pm.p, k.Q.p, 0, nullptr);
     kc_alpha<<<cb, 128, 0, c.stream>>>(B, k.st.p, k.part.p, k.G, k.done.p);
     kb_update<<<dim3(k.G, B), kT, 0, c.stream>>>(c.n, k.ld, k.st.p, k.X.p, k.R.p, k.Pm.p, k.Q.p, k.part.p);
@@ -643,11 +680,14 @@ void build_w_batched(Ctx& c, cublasHandle_t h, const std::vector<std::pair<int, 
       kc_true<<<cb, 128, 0, c.stream>>>(B, k.st.p, k.part.p, k.G, rtol, maxit, k.done.p);
       ++c.launches;
     }
+    ops.mark("update+relres");
     ops.h2(k.R.p, k.Z.p, k.done.p);
     ops.dot(k.R.p, k.Z.p, 0, nullptr);
     kc_rz<<<cb, 128, 0, c.stream>>>(B, k.st.p, k.part.p, k.G, k.done.p, 0);
     kb_p<<<gn, kT, 0, c.stream>>>(c.n, k.ld, k.st.p, k.Z.p, k.Pm.p, 0);
     c.launches += 2;
+    ops.mark("rz+p");
+    ops.report();
     ++passes;
     AWG_CUDA(cudaMemcpyAsync(hs.data(), k.st.p, sizeof(ColState) * B, cudaMemcpyDeviceToHost, c.stream));
     AWG_CUDA(cudaStreamSynchronize(c.stream));

@@ -13,11 +13,20 @@ for cfg in sys.argv[1:] or ["c2"]:
     p = problems.make(cfg)
     rows = []
     settings = [("two-pass", {"AWG_NN_TWO_PASS": "1"})]
-    for cpb, nbuf, chunks in itertools.product([1, 2], [2, 3, 4], [4, 8, 16]):
-        settings.append((f"cpb{cpb}_nbuf{nbuf}_chunks{chunks}",
-                         {"AWG_FUSED_CPB": str(cpb), "AWG_FUSED_NBUF": str(nbuf), "AWG_FUSED_CHUNKS": str(chunks)}))
+    mode = os.environ.get("SWEEP", "pipeline")
+    if mode == "tasks":  # task granularity and the guided tail, default pipeline
+        for mincols, chunks, tail in itertools.product([32, 64, 128, 256], [8, 16, 32], [0, 10, 20]):
+            settings.append((f"min{mincols}_chunks{chunks}_tail{tail}",
+                             {"AWG_FUSED_MINCOLS": str(mincols), "AWG_FUSED_CHUNKS": str(chunks),
+                              "AWG_FUSED_TAIL": str(tail)}))
+    else:
+        for cpb, nbuf, chunks in itertools.product([1, 2], [2, 3, 4], [4, 8, 16]):
+            settings.append((f"cpb{cpb}_nbuf{nbuf}_chunks{chunks}",
+                             {"AWG_FUSED_CPB": str(cpb), "AWG_FUSED_NBUF": str(nbuf),
+                              "AWG_FUSED_CHUNKS": str(chunks)}))
     for name, env in settings:
-        for k in ("AWG_NN_TWO_PASS", "AWG_FUSED_CPB", "AWG_FUSED_NBUF", "AWG_FUSED_CHUNKS"):
+        for k in ("AWG_NN_TWO_PASS", "AWG_FUSED_CPB", "AWG_FUSED_NBUF", "AWG_FUSED_CHUNKS", "AWG_FUSED_MINCOLS",
+                  "AWG_FUSED_TAIL"):
             os.environ.pop(k, None)
         os.environ.update(env)
         try:
