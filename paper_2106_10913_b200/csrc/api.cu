@@ -313,6 +313,7 @@ void finalize_factors(Ctx& c) {
   };
   build_bs(c.bs_neg, noff);
   build_bs(c.bs_z, koff);
+  k::owner_tables(c);
   c.alloc_work();
   AWG_CUDA(cudaStreamSynchronize(c.stream));
 }

@@ -112,6 +112,18 @@ struct LocalPlan {
   DArr<GemvTask> tf;
   DArr<int> nkc_f;
   int kcmax_f = 1;
+  DArr<int2> own_nkc, own_nkc_f;  // per owner entry: (p, nkc / nkc_f of its subdomain)
+};
+
+// Owner-list entries resolved once per factor load, so the prolongation kernels
+// walk two dependent loads per dof (own_off, entry) instead of five
+// (own_off, own_pos, psub, per-subdomain offsets, data).  OwnEnt: the block of
+// subdomain s = psub[own_pos[q]] seen from that dof (column-major block, its
+// leading dimension and the coefficient range of s); the int2 form for the
+// local-solve partials: (p, chunk count of s).
+struct OwnEnt {
+  long long mbase;  // moff[s] + (p - poff[s])
+  int L, q0, q1, pad;
 };
 
 // Block-sparse GEMV^T plan (k_bs_gemvT): one CTA per (subdomain, 512-row
@@ -173,6 +185,10 @@ void aminus(Ctx& c, const double* x, double* y, const int* gate);     // y = A- 
 // mode 1: y = A+ x;  mode 2: y = sub - A+ x  (A- prolongation fused into the SpMV)
 void aplus(Ctx& c, const double* x, double* y, int mode, const double* sub, const int* gate);
 void coarse_q(Ctx& c, const double* x, double* y, const int* gate);   // y = Z K0+ Z^T x
+// y = ((a - Z K0+ Z^T x) + d) [+ e] in one epilogue (a == nullptr: y = Z K0+ Z^T x);
+// the stream waits on `wait_before_combine` (if set) before the combining kernel
+void coarse_q_combine(Ctx& c, const double* x, double* y, const double* a, const double* d, const double* e,
+                      cudaEvent_t wait_before_combine, const int* gate);
 void second_q(Ctx& c, const double* x, double* y, const int* gate);   // y = W KW+ W^T x
 void inex_q(Ctx& c, const double* x, double* y, const int* gate);     // y = W core^-1 W^T x
 void axpby(Ctx& c, int n, const double* a, const double* b, const double* d, double* y, int mode, const int* gate);
@@ -183,6 +199,7 @@ void zT(Ctx& c, const double* x, double* out, const int* gate);  // out = Z^T x 
 void wT(Ctx& c, const double* x, double* out, const int* gate);  // out = W^T x (n_minus)
 void w_apply_public(Ctx& c, const double* coef, double* y, const int* gate);  // y = W coef
 void scatter_col(Ctx& c, int s, const double* col, double* z);  // z[Omega^s] = col (z pre-zeroed)
+void owner_tables(Ctx& c);  // ent_neg, ent_z and the plans' own_nkc (after the factors and plans)
 }  // namespace k
 
 // ---- the context --------------------------------------------------------------
@@ -236,6 +253,7 @@ struct Ctx {
   int fused_min_cols = 128, fused_tail_pct = 0;  // single-pass task sizes (columns), guided tail share  // SMs the single-pass kernel leaves free (for the concurrent W branch)
   int fused_cpb = 0, fused_nbuf = 0, fused_chunks_per_sm = 8;  // 0: automatic
   BsPlan bs_neg, bs_z;   // A- dots (V^s columns k < n_nonpos), Z^T x (Y_s blocks)
+  DArr<OwnEnt> ent_neg, ent_z;  // owner entries into V^s (A- modes) and Y_s (Z columns)
   LocalPlan plan_nn;     // V^s with the eigenvalue mask (NN)
   LocalPlan plan_as;     // U^s = L^-T, triangular (AS / AS+)
   DArr<double> U;        // AS / AS+ local factors, same layout as V

@@ -20,6 +20,7 @@ namespace awgb {
 namespace {
 
 constexpr int kThreads = 256;
+constexpr int kCoarseStage = 4096;  // retained pivots staged in shared memory by k_coarse_solve (32 KB)
 
 // first statement of every solve-path kernel: wait for the predecessor grid
 // (programmatic dependent launch), then honour the device-side PCG gate
@@ -75,25 +76,19 @@ __global__ void k_spmv(const int* __restrict__ gate, int n, const int* __restric
 // xor butterfly, so every lane holds the same, run-to-run identical value.
 struct BlockSum {
   const int* own_off;
-  const int* own_pos;
-  const int* psub;
-  const long long* poff;
-  const int* coff;  // per-subdomain coefficient ranges
-  const int* ccol;  // column of coefficient q (nullptr: q - coff[s])
+  const OwnEnt* ent;  // owner entries resolved against (M, moff, coff) — owner_tables()
+  const int* ccol;    // column of coefficient q (nullptr: q - coff[s])
   const double* M;
-  const long long* moff;
-  const int* ld;
   const double* coef;
   template <int G>
   __device__ __forceinline__ double at(int i, int t, bool active) const {
     double acc = 0.0;
     if (active) {
       for (int qo = own_off[i]; qo < own_off[i + 1]; ++qo) {
-        const int p = own_pos[qo];
-        const int s = psub[p];
-        const double* Ms = M + moff[s] + (p - poff[s]);
-        const int L = ld[s];
-        const int q0 = coff[s], q1 = coff[s + 1];
+        const OwnEnt e = ent[qo];
+        const double* Ms = M + e.mbase;
+        const int L = e.L;
+        const int q0 = e.q0, q1 = e.q1;
         double u0 = 0.0, u1 = 0.0;
         int q = q0 + t;
         for (; q + G < q1; q += 2 * G) {
@@ -136,8 +131,21 @@ __global__ void k_spmv_aplus(const int* __restrict__ gate, int n, const int* __r
   }
 }
 
+// Z c with the composition that consumes it fused into the epilogue (the
+// k_axpby steps of TwoLevel::apply / AwgPreconditioner::apply, same operation
+// order, so bit-identical to running them separately):
+//   a == nullptr: y = Z c
+//   a != nullptr: y = (a - Z c) + d           hybrid H2 (preconditioner.cpp:79-81)
+//   e != nullptr: y = ((a - Z c) + d) + e     ... + W KW+ W^T x   (AD, :185-192)
+struct Combine {
+  const double* a;
+  const double* d;
+  const double* e;
+};
+
 template <int G>
-__global__ void k_prolong_sum(const int* __restrict__ gate, int n, BlockSum bs, double* __restrict__ y) {
+__global__ void k_prolong_sum(const int* __restrict__ gate, int n, BlockSum bs, double* __restrict__ y,
+                              Combine cb) {
   if (gated(gate)) return;
   const int t = threadIdx.x & (G - 1);
   const int stride = int((gridDim.x * (long long)blockDim.x) / G);
@@ -145,7 +153,14 @@ __global__ void k_prolong_sum(const int* __restrict__ gate, int n, BlockSum bs, 
     const bool active = i < n;
     if (!__any_sync(0xffffffffu, active)) break;
     const double v = bs.at<G>(i, t, active);
-    if (active && t == 0) y[i] = v;
+    if (active && t == 0) {
+      double out = v;
+      if (cb.a) {
+        out = (cb.a[i] - v) + cb.d[i];
+        if (cb.e) out = out + cb.e[i];
+      }
+      y[i] = out;
+    }
   }
 }
 
@@ -496,14 +511,19 @@ __global__ void __launch_bounds__(kFusedT, 1) k_nn_fused(const int* __restrict__
     }
     g += nstep;
   }
+  // the queue resets itself: the last CTA out (queue[1] counts finished CTAs,
+  // each after its last queue[0] access) rewinds both counters for the next launch
+  if (tid == 0 && atomicAdd(queue + 1, 1) == int(gridDim.x) - 1) {
+    atomicExch(queue, 0);
+    atomicExch(queue + 1, 0);
+  }
   if (tmr && tid == 0) kernel_timer_end(tmr);
 }
 
 // y[i] = sum over s containing i (ascending s) of D^s_i * (sum_kc part[kc][p(s,i)])
 template <int G>
 __global__ void k_prolong_nn(const int* __restrict__ gate, int n, const int* __restrict__ own_off,
-                             const int* __restrict__ own_pos, const int* __restrict__ psub,
-                             const int* __restrict__ nkc, long long P, const double* __restrict__ part,
+                             const int2* __restrict__ own_nkc, long long P, const double* __restrict__ part,
                              const double* __restrict__ ds, double* __restrict__ y) {
   if (gated(gate)) return;
   // G lanes per row split the chunk partials (kc = t, t + G, ...); fixed butterfly
@@ -515,8 +535,8 @@ __global__ void k_prolong_nn(const int* __restrict__ gate, int n, const int* __r
     double acc = 0.0;
     if (active) {
       for (int q = own_off[i]; q < own_off[i + 1]; ++q) {
-        const int p = own_pos[q];
-        const int kcs = nkc[psub[p]];
+        const int2 e = own_nkc[q];
+        const int p = e.x, kcs = e.y;
         double w0 = 0.0, w1 = 0.0;
         int kc = t;
         for (; kc + G < kcs; kc += 2 * G) {
@@ -628,11 +648,20 @@ __global__ void __launch_bounds__(256) k_bs_gemvT(const int* __restrict__ gate, 
   __syncthreads();
   if (!s_last) return;
   __threadfence();
+  // chunk sums in chunk order; the loads of 8 chunks are issued together (no
+  // serial chain of kch dependent L2 round trips), the adds stay sequential
   const int kch = nch[s];
   for (int q = tid; q < nc; q += blockDim.x) {
     const double* pq = part + (size_t)(q0 + q) * maxch;
     double a = 0.0;
-    for (int k = 0; k < kch; ++k) a += __ldcg(pq + k);
+    for (int k0 = 0; k0 < kch; k0 += 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = (k0 + u < kch) ? __ldcg(pq + k0 + u) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (k0 + u < kch) a += v[u];
+    }
     out[q0 + q] = w ? w[q0 + q] * a : a;
   }
   if (tid == 0) cnt[s] = 0;
@@ -647,6 +676,14 @@ __global__ void k_coarse_solve(const int* __restrict__ gate, int dim, int r, con
                                const int* __restrict__ pos, const int* __restrict__ ret,
                                const double* __restrict__ b, double* __restrict__ x) {
   if (gated(gate)) return;
+  // b_r = b[retained] staged once per CTA (kCoarseStage doubles of static
+  // shared memory) instead of two dependent loads per element in every warp
+  __shared__ double sb[kCoarseStage];
+  const bool staged = r <= kCoarseStage;
+  if (staged) {
+    for (int j = threadIdx.x; j < r; j += blockDim.x) sb[j] = __ldg(b + ret[j]);
+    __syncthreads();
+  }
   const int lane = threadIdx.x & 31;
   const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (i >= dim) return;
@@ -656,11 +693,19 @@ __global__ void k_coarse_solve(const int* __restrict__ gate, int dim, int r, con
     const double* row = kinv + (size_t)k * r;
     double a1 = 0.0;
     int j = lane;
-    for (; j + 32 < r; j += 64) {
-      acc = fma(row[j], __ldg(b + ret[j]), acc);
-      a1 = fma(row[j + 32], __ldg(b + ret[j + 32]), a1);
+    if (staged) {
+      for (; j + 32 < r; j += 64) {
+        acc = fma(row[j], sb[j], acc);
+        a1 = fma(row[j + 32], sb[j + 32], a1);
+      }
+      if (j < r) acc = fma(row[j], sb[j], acc);
+    } else {
+      for (; j + 32 < r; j += 64) {
+        acc = fma(row[j], __ldg(b + ret[j]), acc);
+        a1 = fma(row[j + 32], __ldg(b + ret[j + 32]), a1);
+      }
+      if (j < r) acc = fma(row[j], __ldg(b + ret[j]), acc);
     }
-    if (j < r) acc = fma(row[j], __ldg(b + ret[j]), acc);
     acc = warp_sum(acc + a1);
   }
   if (lane == 0) x[i] = acc;
@@ -898,10 +943,61 @@ __global__ void k_axpby(const int* __restrict__ gate, int n, const double* __res
   }
 }
 
+
+// owner-entry tables (see OwnEnt): entry q of the owner lists, p = own_pos[q]
+__global__ void k_own_ent(long long P, const int* __restrict__ own_pos, const int* __restrict__ psub,
+                          const long long* __restrict__ poff, const long long* __restrict__ moff,
+                          const int* __restrict__ ld, const int* __restrict__ coff, OwnEnt* __restrict__ ent) {
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < P; q += (long long)gridDim.x * blockDim.x) {
+    const int p = own_pos[q];
+    const int s = psub[p];
+    OwnEnt e;
+    e.mbase = moff[s] + (p - poff[s]);
+    e.L = ld[s];
+    e.q0 = coff[s];
+    e.q1 = coff[s + 1];
+    e.pad = 0;
+    ent[q] = e;
+  }
+}
+
+__global__ void k_own_nkc(long long P, const int* __restrict__ own_pos, const int* __restrict__ psub,
+                          const int* __restrict__ nkc, int2* __restrict__ out) {
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < P; q += (long long)gridDim.x * blockDim.x) {
+    const int p = own_pos[q];
+    out[q] = make_int2(p, nkc[psub[p]]);
+  }
+}
+
 }  // namespace
 
 // ===========================================================================
 namespace k {
+
+void owner_tables(Ctx& c) {
+  const long long P = std::max<long long>(c.P, 1);
+  const int g = grid_for(c, c.P);
+  c.ent_neg.alloc(P);
+  c.ent_z.alloc(P);
+  k_own_ent<<<g, kThreads, 0, c.stream>>>(c.P, c.own_pos.p, c.psub.p, c.poff.p, c.voff.p, c.ld.p, c.negoff.p,
+                                          c.ent_neg.p);
+  k_own_ent<<<g, kThreads, 0, c.stream>>>(c.P, c.own_pos.p, c.psub.p, c.poff.p, c.yoff.p, c.ld.p, c.koff.p,
+                                          c.ent_z.p);
+  c.launches += 2;
+  for (LocalPlan* pl : {&c.plan_nn, &c.plan_as}) {
+    if (pl->nkc.p) {
+      pl->own_nkc.alloc(P);
+      k_own_nkc<<<g, kThreads, 0, c.stream>>>(c.P, c.own_pos.p, c.psub.p, pl->nkc.p, pl->own_nkc.p);
+      ++c.launches;
+    }
+    if (pl->fused && pl->nkc_f.p) {
+      pl->own_nkc_f.alloc(P);
+      k_own_nkc<<<g, kThreads, 0, c.stream>>>(c.P, c.own_pos.p, c.psub.p, pl->nkc_f.p, pl->own_nkc_f.p);
+      ++c.launches;
+    }
+  }
+  check_launch("owner_tables");
+}
 
 void spmv(Ctx& c, const double* x, double* y, int mode, const double* add, const double* sub, const int* gate) {
   launch(c, k_spmv, grid_for(c, c.n), kThreads, 0, gate, c.n, c.rp.p, c.ci.p, c.va.p, x, y, mode, add, sub);
@@ -963,23 +1059,23 @@ void nn_gemv(Ctx& c, const int* gate) {
 
 
 // split-K partial sum + D^s + prolongation (k_prolong_nn), lanes per row by size
-static void prolong_nn(Ctx& c, const int* nkc, int kcmax, double* y, const int* gate) {
+static void prolong_nn(Ctx& c, const int2* own_nkc, int kcmax, double* y, const int* gate) {
   const double* ds = c.one_level == 2 ? c.ds.p : nullptr;
   const int G = c.n > 300000 ? 1 : (kcmax >= 16 ? 8 : 4);
   if (G == 8)
-    launch(c, k_prolong_nn<8>, grid_for(c, 8LL * c.n), kThreads, 0, gate, c.n, c.own_off.p, c.own_pos.p, c.psub.p,
-                                                                      nkc, c.P, c.wpart_nn.p, ds, y);
+    launch(c, k_prolong_nn<8>, grid_for(c, 8LL * c.n), kThreads, 0, gate, c.n, c.own_off.p, own_nkc, c.P,
+           c.wpart_nn.p, ds, y);
   else if (G == 4)
-    launch(c, k_prolong_nn<4>, grid_for(c, 4LL * c.n), kThreads, 0, gate, c.n, c.own_off.p, c.own_pos.p, c.psub.p,
-                                                                      nkc, c.P, c.wpart_nn.p, ds, y);
+    launch(c, k_prolong_nn<4>, grid_for(c, 4LL * c.n), kThreads, 0, gate, c.n, c.own_off.p, own_nkc, c.P,
+           c.wpart_nn.p, ds, y);
   else
-    launch(c, k_prolong_nn<1>, grid_for(c, c.n), kThreads, 0, gate, c.n, c.own_off.p, c.own_pos.p, c.psub.p,
-                                                                nkc, c.P, c.wpart_nn.p, ds, y);
+    launch(c, k_prolong_nn<1>, grid_for(c, c.n), kThreads, 0, gate, c.n, c.own_off.p, own_nkc, c.P, c.wpart_nn.p,
+           ds, y);
 }
 
 void nn_prolong(Ctx& c, double* y, const int* gate) {
   const LocalPlan& pl = plan(c);
-  prolong_nn(c, pl.nkc.p, pl.kcmax, y, gate);
+  prolong_nn(c, pl.own_nkc.p, pl.kcmax, y, gate);
   ++c.launches;
   check_launch("prolong_nn");
 }
@@ -1033,13 +1129,15 @@ void nn_fused(Ctx& c, const double* x, const int* gate) {
   if (nbuf < 2) c.fail(AWG_E_STATE, "single-pass local solve: subdomain too large for the copy pipeline");
   const size_t smem = size_t(nbuf) * buf_bytes + tail;
   if (!pl.tf.n) return;
-  if (!c.fused_queue.p) c.fused_queue.alloc(1);
+  if (!c.fused_queue.p) {
+    c.fused_queue.alloc(2);  // (next task, CTAs finished); reset by the kernel itself
+    c.fused_queue.zero(c.stream);
+  }
   if (!c.fused_timer.p) {
     static const unsigned long long init[5] = {~0ull, 0, 0, 0, 0};
     c.fused_timer.alloc(5);
     AWG_CUDA(cudaMemcpyAsync(c.fused_timer.p, init, sizeof(init), cudaMemcpyHostToDevice, c.stream));
   }
-  AWG_CUDA(cudaMemsetAsync(c.fused_queue.p, 0, sizeof(int), c.stream));
   // persistent CTAs: one per SM, less the SMs left to the concurrent W branch
   const int grid = std::min(int(pl.tf.n), std::max(1, c.sm_count - c.fused_reserve));
   const double* F = nn ? c.V.p : c.U.p;
@@ -1060,7 +1158,7 @@ void h1(Ctx& c, const double* x, double* y, const int* gate) {
   const LocalPlan& pl = plan(c);
   if (pl.fused) {
     nn_fused(c, x, gate);
-    prolong_nn(c, pl.nkc_f.p, pl.kcmax_f, y, gate);
+    prolong_nn(c, pl.own_nkc_f.p, pl.kcmax_f, y, gate);
     ++c.launches;
     check_launch("prolong_nn");
     return;
@@ -1101,8 +1199,7 @@ void aminus(Ctx& c, const double* x, double* y, const int* gate) {
 }
 
 static BlockSum neg_sum(const Ctx& c) {
-  return BlockSum{c.own_off.p, c.own_pos.p, c.psub.p, c.poff.p, c.negoff.p, c.neg_k.p,
-                  c.V.p,       c.voff.p,    c.ld.p,   c.neg_c.p};
+  return BlockSum{c.own_off.p, c.ent_neg.p, c.neg_k.p, c.V.p, c.neg_c.p};
 }
 
 // y = A+ x (mode 1) or y = sub - A+ x (mode 2): the A- dots, then one fused
@@ -1110,7 +1207,6 @@ static BlockSum neg_sum(const Ctx& c) {
 void aplus(Ctx& c, const double* x, double* y, int mode, const double* sub, const int* gate) {
   if (c.nneg > 0) neg_dot(c, x, gate);
   BlockSum bs = neg_sum(c);
-  if (c.nneg == 0) bs.coff = c.negoff.p;  // empty ranges: all zero
   if (rows_group(c) == 4)
     launch(c, k_spmv_aplus<4>, grid_for(c, 4LL * c.n), kThreads, 0, gate, c.n, c.rp.p, c.ci.p, c.va.p, x, y, mode,
                                                                        sub, bs);
@@ -1140,15 +1236,23 @@ void coarse_q(Ctx& c, const double* x, double* y, const int* gate) {
     ++c.launches;
     return;
   }
+  coarse_q_combine(c, x, y, nullptr, nullptr, nullptr, nullptr, gate);
+}
+
+void coarse_q_combine(Ctx& c, const double* x, double* y, const double* a, const double* d, const double* e,
+                      cudaEvent_t wait_before_combine, const int* gate) {
+  if (c.n0 == 0) c.fail(AWG_E_STATE, "coarse_q: empty coarse space");
   zT(c, x, c.cz.p, gate);
   double* coef = c.cz.p + c.n0;  // second half of cz holds the solved coefficients
   rr_solve(c, c.k0, c.cz.p, coef, gate);
-  // Z c: block-sparse combination fused with the prolongation
-  const BlockSum bs{c.own_off.p, c.own_pos.p, c.psub.p, c.poff.p, c.koff.p, nullptr, c.Y.p, c.yoff.p, c.ld.p, coef};
+  if (wait_before_combine) AWG_CUDA(cudaStreamWaitEvent(c.stream, wait_before_combine, 0));
+  // Z c: block-sparse combination fused with the prolongation and the composition
+  const BlockSum bs{c.own_off.p, c.ent_z.p, nullptr, c.Y.p, coef};
+  const Combine cb{a, d, e};
   if (rows_group(c) == 4)
-    launch(c, k_prolong_sum<4>, grid_for(c, 4LL * c.n), kThreads, 0, gate, c.n, bs, y);
+    launch(c, k_prolong_sum<4>, grid_for(c, 4LL * c.n), kThreads, 0, gate, c.n, bs, y, cb);
   else
-    launch(c, k_prolong_sum<1>, grid_for(c, c.n), kThreads, 0, gate, c.n, bs, y);
+    launch(c, k_prolong_sum<1>, grid_for(c, c.n), kThreads, 0, gate, c.n, bs, y, cb);
   ++c.launches;
   check_launch("z_prolong");
 }

@@ -285,22 +285,32 @@ static void h1(Ctx& c, const double* x, double* y, const int* gate) { k::h1(c, x
 
 static void aplus(Ctx& c, const double* x, double* y, const int* gate) { k::aplus(c, x, y, 1, nullptr, gate); }
 
-static void h2(Ctx& c, const double* x, double* y, const int* gate) {
+// H2 x into y.  With `extra` set (the AD branch's W KW+ W^T x, ready once
+// `extra_ready` has fired) the hybrid composition's last kernel also adds it:
+// y = ((hp - Q A+ hp) + corr) + extra, the reference's two sums in order.
+static void h2(Ctx& c, const double* x, double* y, const int* gate, const double* extra = nullptr,
+               cudaEvent_t extra_ready = nullptr) {
+  auto add_extra = [&](const double* h2y) {
+    if (extra_ready) AWG_CUDA(cudaStreamWaitEvent(c.stream, extra_ready, 0));
+    k::axpby(c, c.n, h2y, extra, nullptr, y, 1, gate);
+  };
   if (c.n0 == 0) {
-    h1(c, x, y, gate);
+    h1(c, x, extra ? c.t1.p : y, gate);
+    if (extra) add_extra(c.t1.p);
     return;
   }
   k::coarse_q(c, x, c.t0.p, gate);  // corr
   if (c.cfg.composition == 0) {
     h1(c, x, c.t1.p, gate);
-    k::axpby(c, c.n, c.t1.p, c.t0.p, nullptr, y, 1, gate);
+    k::axpby(c, c.n, c.t1.p, c.t0.p, nullptr, extra ? c.t2.p : y, 1, gate);
+    if (extra) add_extra(c.t2.p);
     return;
   }
   k::aplus(c, c.t0.p, c.t2.p, 2, x, gate);         // pt = x - A+ corr
   h1(c, c.t2.p, c.t3.p, gate);                     // hp
   aplus(c, c.t3.p, c.t4.p, gate);                  // A+ hp
-  k::coarse_q(c, c.t4.p, c.t5.p, gate);            // Q A+ hp
-  k::axpby(c, c.n, c.t3.p, c.t5.p, c.t0.p, y, 0, gate);
+  // (hp - Q A+ hp) + corr [+ extra], fused into the Z c prolongation
+  k::coarse_q_combine(c, c.t4.p, y, c.t3.p, c.t0.p, extra, extra_ready, gate);
 }
 
 void op_apply(Ctx& c, int op, const double* x, double* y, const int* gate) {
@@ -359,9 +369,7 @@ void op_apply(Ctx& c, int op, const double* x, double* y, const int* gate) {
         k::second_q(c, x, c.t6.p, gate);
         c.stream = main;
         AWG_CUDA(cudaEventRecord(c.ev_join, c.side));
-        h2(c, x, c.t7.p, gate);
-        AWG_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));
-        k::axpby(c, c.n, c.t7.p, c.t6.p, nullptr, y, 1, gate);
+        h2(c, x, y, gate, c.t6.p, c.ev_join);  // joins the branch before its last kernel
       } else if (mode == 2) {  // HYB
         k::second_q(c, x, c.t6.p, gate);                 // corr
         k::spmv(c, c.t6.p, c.t7.p, 3, nullptr, x, gate);  // pt = x - A corr
