@@ -207,6 +207,8 @@ def load_library(path: str = LIB_PATH):
     lib.awg_time_kernel.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
                                     ctypes.POINTER(ctypes.c_double)]
     lib.awg_synthetic_factors.argtypes = [vp, ctypes.c_int, ctypes.c_ulonglong]
+    lib.awg_bench_dgemm.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                    ctypes.POINTER(ctypes.c_double)]
     _lib = lib
     return lib
 
@@ -454,6 +456,14 @@ class ProblemContext:
         ms, by = ctypes.c_double(), ctypes.c_double()
         self._check(self._lib.awg_time_kernel(self._h, self.KERNELS[name], reps, ctypes.byref(ms), ctypes.byref(by)))
         return ms.value, by.value
+
+    def bench_dgemm(self, m: int, n: int, k: int, count: int = 1, reps: int = 5) -> dict:
+        """Grouped FP64 tensor-core GEMM (the W build's block one-level products)
+        against cuBLAS on seeded operands: relative max error, ms, TFLOP/s."""
+        out = (ctypes.c_double * 5)()
+        self._check(self._lib.awg_bench_dgemm(self._h, m, n, k, count, reps, out))
+        return {"rel_err": out[0], "ms_grouped": out[1], "ms_cublas": out[2], "tflops_grouped": out[3],
+                "tflops_cublas": out[4]}
 
     def pcg(self, b=None, rtol: float = 1e-10, maxit: int = 10000) -> Tuple[np.ndarray, SolveReport]:
         """pcg(spmv, H3.apply, b, rtol, maxit) — krylov.cpp:36-124, on device."""

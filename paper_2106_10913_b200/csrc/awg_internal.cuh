@@ -126,6 +126,27 @@ struct OwnEnt {
   int L, q0, q1, pad;
 };
 
+// Grouped FP64 tensor-core GEMM (dgemm.cu): C = A B for a list of column-major
+// problems in one launch (one CTA per 128 x 128 output tile of any problem).
+struct GemmDesc {
+  const double* A;
+  const double* B;
+  double* C;
+  int M, N, K, lda, ldb, ldc;
+};
+struct GemmTile {
+  int prob, m0, n0, pad;
+};
+struct Ctx;
+struct GroupedGemm {
+  DArr<GemmDesc> desc;
+  DArr<GemmTile> tiles;
+  int ntiles = 0;
+  double flops = 0.0;
+  void set(Ctx& c, const std::vector<GemmDesc>& probs);  // validates and uploads the tile list
+  void run(Ctx& c) const;                                 // on c.stream
+};
+
 // Block-sparse GEMV^T plan (k_bs_gemvT): one CTA per (subdomain, 512-row
 // chunk) over the subdomains that own columns; partials per (column, chunk),
 // summed in chunk order by the last CTA of each subdomain.
@@ -358,6 +379,8 @@ void assemble_elasticity(Ctx& c, int nodes_x, int nodes_y, int layer, int nmat, 
                          std::vector<double>& va, std::vector<double>& b);
 void partition_closure(Ctx& c, const std::vector<int>& owner, int nsub, int rings, std::vector<long long>& off,
                        std::vector<int>& idx);
+// dgemm.cu: grouped DMMA GEMM vs cuBLAS on seeded operands (awg_bench_dgemm)
+void bench_grouped_dgemm(Ctx& c, int m, int n, int k, int count, int reps, double* out);
 void build_core(Ctx& c);        // INEX core LU
 void run_setup(Ctx& c, const awg_config& cfg);  // setup.cu
 void build_local_cholesky(Ctx& c);              // setup.cu: AS / AS+ factors U^s = L^-T

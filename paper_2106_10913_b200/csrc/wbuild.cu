@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include <string>
@@ -344,6 +345,7 @@ struct Block {
   DArr<double> X, R, Z, Pm, Q, Bm, T, C0, C1, C2, C3, C4, C5;
   DArr<double> XS, WS;  // block-P layout
   DArr<double> Pinv;    // optional P^s = V+ L+^-1 V+^T (NN), V layout
+  GroupedGemm pgemm;    // P^s X^s over all subdomains (empty: per-subdomain cuBLAS, AWG_WBUILD_GEMM=cublas)
   DArr<double> zx, zr, zt, zc, negc, part;
   DArr<ColState> st;
   DArr<int> done, any_true;
@@ -481,11 +483,15 @@ struct BlockOps {
     kb_gather<<<grid_p(), kT, 0, c.stream>>>(c.P, c.psub.p, c.poff.p, c.pidx.p, c.ld.p, k.boff.p,
                                              nn ? c.ds.p : nullptr, k.ld, X, k.XS.p, done);
     const double one = 1.0, zero = 0.0;
-    if (nn && k.Pinv.p) {  // one DGEMM per subdomain with P^s = V+ L+^-1 V+^T
-      for (int s = 0; s < c.N; ++s) {
-        const int n = c.h_ns[s], L = c.h_ld[s];
-        AWG_BLAS(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, n, k.B, n, &one, k.Pinv.p + c.h_voff[s], L,
-                             k.XS.p + k.h_boff[s], L, &zero, k.WS.p + k.h_boff[s], L));
+    if (nn && k.Pinv.p) {  // P^s X^s for every subdomain, P^s = V+ L+^-1 V+^T
+      if (k.pgemm.ntiles) {
+        k.pgemm.run(c);  // one grouped FP64 tensor-core launch (dgemm.cu)
+      } else {
+        for (int s = 0; s < c.N; ++s) {
+          const int n = c.h_ns[s], L = c.h_ld[s];
+          AWG_BLAS(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, n, k.B, n, &one, k.Pinv.p + c.h_voff[s], L,
+                               k.XS.p + k.h_boff[s], L, &zero, k.WS.p + k.h_boff[s], L));
+        }
       }
       kb_prolong<<<grid_n(), kT, 0, c.stream>>>(c.n, k.ld, c.own_off.p, c.own_pos.p, c.psub.p, c.poff.p, c.ld.p,
                                                 k.boff.p, c.ds.p, k.WS.p, Y, done);
@@ -620,6 +626,17 @@ void build_w_batched(Ctx& c, cublasHandle_t h, const std::vector<std::pair<int, 
   k.done.alloc(B);
   k.any_true.alloc(1);
   AWG_BLAS(cublasSetStream(h, c.stream));
+  if (k.Pinv.p) {
+    const char* g = std::getenv("AWG_WBUILD_GEMM");
+    if (!(g && std::string(g) == "cublas")) {
+      std::vector<GemmDesc> pd;
+      for (int s = 0; s < c.N; ++s) {
+        const int n = c.h_ns[s], L = c.h_ld[s];
+        pd.push_back({k.Pinv.p + c.h_voff[s], k.XS.p + k.h_boff[s], k.WS.p + k.h_boff[s], n, B, n, L, L, L});
+      }
+      k.pgemm.set(c, pd);
+    }
+  }
   BlockOps ops(c, k, h, c.k0);
   const int cb = (B + 127) / 128;
   std::vector<ColState> hs(B);
