@@ -165,7 +165,7 @@ EXPORTED_SYMBOLS = [
     "awg_set_partition", "awg_setup", "awg_load_factors", "awg_apply", "awg_pcg", "awg_query",
     "awg_get_history", "awg_get_array", "awg_launch_count", "awg_time_apply", "awg_time_kernel",
     "awg_synthetic_factors", "awg_kernel_timer", "awg_assemble_fd", "awg_assemble_elasticity", "awg_partition_owner",
-    "awg_partition_boxes",
+    "awg_partition_boxes", "awg_bench_dgemm",
 ]
 
 _lib = None

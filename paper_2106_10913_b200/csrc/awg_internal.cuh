@@ -190,6 +190,16 @@ struct PcgState {
 
 enum PcgError { PCG_OK = 0, PCG_BAD_OPERATOR = 1, PCG_BAD_PRECOND = 2 };
 
+// The PCG's <r, z> fused into the last kernel of the preconditioner apply
+// (k_prolong_sum's combine epilogue) when that kernel writes z.
+struct RzFuse {
+  PcgState* st = nullptr;
+  const double* r = nullptr;
+  const double* z = nullptr;
+  double* part = nullptr;
+  unsigned* count = nullptr;
+};
+
 struct Ctx;
 
 // ---- launchers (kernels.cu) -------------------------------------------------
@@ -321,6 +331,9 @@ struct Ctx {
   DArr<unsigned> red_count;
 
   // pcg
+  RzFuse rz_fuse;         // armed by run_pcg around the preconditioner apply it captures
+  bool rz_fused = false;   // set when an apply consumed rz_fuse
+  DArr<double> pp2;        // second search-direction buffer (p formed inside the SpMV)
   DArr<PcgState> pcg;
   DArr<int> pcg_flag;
   std::map<int, cudaGraphExec_t> graphs;  // one PCG iteration per operator pair

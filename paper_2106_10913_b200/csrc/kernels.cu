@@ -15,6 +15,7 @@
 #include <algorithm>
 
 #include "awg_internal.cuh"
+#include "pcg_device.cuh"
 
 namespace awgb {
 namespace {
@@ -141,6 +142,7 @@ struct Combine {
   const double* a;
   const double* d;
   const double* e;
+  RzFuse rz;  // rz.st != nullptr: also <r, y> into the PCG state (the PCG's beta step)
 };
 
 template <int G>
@@ -149,6 +151,7 @@ __global__ void k_prolong_sum(const int* __restrict__ gate, int n, BlockSum bs, 
   if (gated(gate)) return;
   const int t = threadIdx.x & (G - 1);
   const int stride = int((gridDim.x * (long long)blockDim.x) / G);
+  double rz = 0.0;
   for (int i = int((blockIdx.x * (long long)blockDim.x + threadIdx.x) / G);; i += stride) {
     const bool active = i < n;
     if (!__any_sync(0xffffffffu, active)) break;
@@ -160,8 +163,12 @@ __global__ void k_prolong_sum(const int* __restrict__ gate, int n, BlockSum bs, 
         if (cb.e) out = out + cb.e[i];
       }
       y[i] = out;
+      if (cb.rz.st) rz = fma(cb.rz.r[i], out, rz);
     }
   }
+  // rz = <r, z> and the beta step (krylov.cpp:105-115), fused: k_pcg_rz's work
+  if (cb.rz.st)
+    pcgdev::grid_reduce(rz, cb.rz.part, cb.rz.count, [&](double v) { pcgdev::rz_finish(cb.rz.st, v, 0); });
 }
 
 // xs[p] = x[pidx[p]] (* scale[p])      restrict_to (splitting.cpp:220-223) and the D^s
@@ -1248,7 +1255,11 @@ void coarse_q_combine(Ctx& c, const double* x, double* y, const double* a, const
   if (wait_before_combine) AWG_CUDA(cudaStreamWaitEvent(c.stream, wait_before_combine, 0));
   // Z c: block-sparse combination fused with the prolongation and the composition
   const BlockSum bs{c.own_off.p, c.ent_z.p, nullptr, c.Y.p, coef};
-  const Combine cb{a, d, e};
+  Combine cb{a, d, e, RzFuse{}};
+  if (c.rz_fuse.st && a && y == c.rz_fuse.z) {  // the last kernel of the PCG's preconditioner apply
+    cb.rz = c.rz_fuse;
+    c.rz_fused = true;
+  }
   if (rows_group(c) == 4)
     launch(c, k_prolong_sum<4>, grid_for(c, 4LL * c.n), kThreads, 0, gate, c.n, bs, y, cb);
   else

@@ -12,6 +12,7 @@
 #include <cstring>
 
 #include "awg_internal.cuh"
+#include "pcg_device.cuh"
 
 namespace awgb {
 
@@ -19,42 +20,7 @@ namespace {
 
 constexpr int kThreads = 256;
 
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
-// Block partial -> fixed slot; the last block to arrive sums the slots in a
-// fixed order (deterministic single-pass grid reduction) and runs `fin`.
-template <class Fin>
-__device__ void grid_reduce(double v, double* part, unsigned* count, Fin fin) {
-  __shared__ double sred[32];
-  __shared__ int is_last;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  v = warp_sum(v);
-  if (lane == 0) sred[warp] = v;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double acc = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) acc += sred[w];
-    part[blockIdx.x] = acc;
-    __threadfence();
-    const unsigned t = atomicAdd(count, 1u);
-    is_last = (t == gridDim.x - 1);
-  }
-  __syncthreads();
-  if (is_last && warp == 0) {
-    __threadfence();
-    double acc = 0.0;
-    for (int b = lane; b < (int)gridDim.x; b += 32) acc += __ldcg(part + b);
-    acc = warp_sum(acc);
-    if (lane == 0) {
-      fin(acc);
-      *count = 0;
-    }
-  }
-}
+using pcgdev::grid_reduce;
 
 __global__ void k_pcg_init(PcgState* st, int n, const double* __restrict__ b, double* __restrict__ x,
                            double* __restrict__ r, double* part, unsigned* count) {
@@ -84,27 +50,7 @@ __global__ void k_pcg_rz(PcgState* st, int n, const double* __restrict__ r, cons
   if (st->done) return;
   double acc = 0.0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) acc = fma(r[i], z[i], acc);
-  grid_reduce(acc, part, count, [&](double rz) {
-    if (initial) {
-      if (rz <= 0.0) {
-        st->error = PCG_BAD_PRECOND;
-        st->done = 1;
-      }
-      st->rz = rz;
-      st->beta = 0.0;
-      return;
-    }
-    if (rz <= 0.0) {
-      if (!st->past_rtol) st->error = PCG_BAD_PRECOND;
-      st->done = 1;
-      return;
-    }
-    const double beta = rz / st->rz;
-    st->beta = beta;
-    st->rz = rz;
-    st->beta_prev = beta;
-    st->alpha_prev = st->alpha;
-  });
+  grid_reduce(acc, part, count, [&](double rz) { pcgdev::rz_finish(st, rz, initial); });
 }
 
 // p = z + beta p   (p = z on the first step: beta = 0 and p zeroed)
@@ -129,6 +75,41 @@ __global__ void k_pcg_spmv_dot(PcgState* st, int n, const int* __restrict__ rp, 
     if (add) s = add[i] + s;
     q[i] = s;
     acc = fma(p[i], s, acc);
+  }
+  grid_reduce(acc, part, count, [&](double pq) {
+    st->pq = pq;
+    if (pq <= 0.0) {
+      if (!st->past_rtol) st->error = PCG_BAD_OPERATOR;
+      st->done = 1;
+      return;
+    }
+    st->alpha = st->rz / pq;
+  });
+}
+
+// p = z + beta p_old formed inside the SpMV (the k_pcg_p step fused): every
+// row evaluates fma(beta, p_old[j], z[j]) for its columns — bit for bit the
+// p that k_pcg_p would have stored — and writes its own p_new[i]; then
+// q = A p_new and <p_new, q> (krylov.cpp:77-83, 111-115).  p_old / p_new
+// alternate between two buffers across iterations.
+__global__ void k_pcg_spmv_dot_p(PcgState* st, int n, const int* __restrict__ rp, const int* __restrict__ ci,
+                                 const double* __restrict__ va, const double* __restrict__ z,
+                                 const double* __restrict__ pold, double* __restrict__ pnew,
+                                 double* __restrict__ q, double* part, unsigned* count) {
+  pdl_wait();
+  if (st->done) return;
+  const double beta = st->beta;
+  double acc = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int k = rp[i]; k < rp[i + 1]; ++k) {
+      const int j = ci[k];
+      s = __dadd_rn(s, __dmul_rn(va[k], fma(beta, __ldg(pold + j), __ldg(z + j))));
+    }
+    const double pi = fma(beta, pold[i], z[i]);
+    pnew[i] = pi;
+    q[i] = s;
+    acc = fma(pi, s, acc);
   }
   grid_reduce(acc, part, count, [&](double pq) {
     st->pq = pq;
@@ -278,7 +259,7 @@ void Ctx::alloc_work() {
   red_count.alloc(1);
   red_count.zero(stream);
   pcg.alloc(1);
-  for (DArr<double>* b : {&px, &pr, &pz, &pp, &pq, &pb, &pt}) b->alloc(nn);
+  for (DArr<double>* b : {&px, &pr, &pz, &pp, &pp2, &pq, &pb, &pt}) b->alloc(nn);
 }
 
 static void h1(Ctx& c, const double* x, double* y, const int* gate) { k::h1(c, x, y, gate); }
@@ -419,19 +400,36 @@ void run_pcg(Ctx& c, const double* b_dev, double rtol, int maxit, awg_solve_repo
   AWG_CUDA(cudaEventCreate(&e1));
   AWG_CUDA(cudaEventRecord(e0, c.stream));
 
+  // Fused form (A operator): p = z + beta p is formed inside the next SpMV
+  // (two alternating p buffers, zero before the first step so p_1 = z), and
+  // <r, z> is folded into the preconditioner's last kernel when it can take it.
+  // With A+ the A- product needs p first, so p and rz stay separate kernels.
+  const bool fuse = !aplus;
   launch(c, k_pcg_init, g, kThreads, 0, st, n, c.pb.p, c.px.p, c.pr.p, c.red.p, c.red_count.p);
   ++c.launches;
   op_apply(c, op_h, c.pr.p, c.pz.p, gate);
   launch(c, k_pcg_rz, g, kThreads, 0, st, n, c.pr.p, c.pz.p, c.red.p, c.red_count.p, 1);
-  launch(c, k_pcg_p, g, kThreads, 0, st, n, c.pz.p, c.pp.p, 1);
-  c.launches += 2;
+  ++c.launches;
+  if (fuse) {
+    AWG_CUDA(cudaMemsetAsync(c.pp.p, 0, sizeof(double) * n, c.stream));
+    AWG_CUDA(cudaMemsetAsync(c.pp2.p, 0, sizeof(double) * n, c.stream));
+  } else {
+    launch(c, k_pcg_p, g, kThreads, 0, st, n, c.pz.p, c.pp.p, 1);
+    ++c.launches;
+  }
   check_launch("pcg init");
 
-  auto iteration = [&]() {
-    if (aplus) k::aminus(c, c.pp.p, am, gate);
-    launch(c, k_pcg_spmv_dot, g, kThreads, 0, st, n, c.rp.p, c.ci.p, c.va.p, c.pp.p, c.pq.p,
-                                                  aplus ? am : nullptr, c.red.p, c.red_count.p);
-    launch(c, k_pcg_update, g, kThreads, 0, st, n, c.px.p, c.pr.p, c.pp.p, c.pq.p, c.red.p, c.red_count.p,
+  auto iteration = [&](double* pold, double* pnew) {
+    if (fuse) {
+      launch(c, k_pcg_spmv_dot_p, g, kThreads, 0, st, n, c.rp.p, c.ci.p, c.va.p, c.pz.p, pold, pnew, c.pq.p,
+             c.red.p, c.red_count.p);
+    } else {
+      k::aminus(c, c.pp.p, am, gate);
+      launch(c, k_pcg_spmv_dot, g, kThreads, 0, st, n, c.rp.p, c.ci.p, c.va.p, c.pp.p, c.pq.p, am, c.red.p,
+             c.red_count.p);
+      pnew = c.pp.p;
+    }
+    launch(c, k_pcg_update, g, kThreads, 0, st, n, c.px.p, c.pr.p, pnew, c.pq.p, c.red.p, c.red_count.p,
                                                c.hist_res.p, c.hist_diag.p, c.hist_off.p);
     c.launches += 2;
     if (aplus) {
@@ -442,18 +440,30 @@ void run_pcg(Ctx& c, const double* b_dev, double rtol, int maxit, awg_solve_repo
     launch(c, k_pcg_true, g, kThreads, 0, st, n, c.rp.p, c.ci.p, c.va.p, c.px.p, c.pb.p, aplus ? am : nullptr,
                                              c.red.p, c.red_count.p);
     ++c.launches;
+    if (fuse) {
+      c.rz_fuse = RzFuse{st, c.pr.p, c.pz.p, c.red.p, c.red_count.p};
+      c.rz_fused = false;
+    }
     op_apply(c, op_h, c.pr.p, c.pz.p, gate);
-    launch(c, k_pcg_rz, g, kThreads, 0, st, n, c.pr.p, c.pz.p, c.red.p, c.red_count.p, 0);
-    launch(c, k_pcg_p, g, kThreads, 0, st, n, c.pz.p, c.pp.p, 0);
-    c.launches += 2;
+    c.rz_fuse = RzFuse{};
+    if (!(fuse && c.rz_fused)) {
+      launch(c, k_pcg_rz, g, kThreads, 0, st, n, c.pr.p, c.pz.p, c.red.p, c.red_count.p, 0);
+      ++c.launches;
+    }
+    if (!fuse) {
+      launch(c, k_pcg_p, g, kThreads, 0, st, n, c.pz.p, c.pp.p, 0);
+      ++c.launches;
+    }
     check_launch("pcg iteration");
   };
 
   // Enqueue iterations in batches; the device-side `done` flag turns every
   // kernel after the stopping point into a no-op, so overshooting is free of
-  // side effects.  One CUDA graph holds one iteration; it is cached per
-  // operator pair until buffers or factors change.
+  // side effects.  One CUDA graph holds two iterations (the p buffers swap
+  // roles between them); it is cached per operator pair until buffers or
+  // factors change.
   const int key = op_a * 16 + op_h;
+  constexpr int kItersPerGraph = 2;
   cudaGraphExec_t exec = nullptr;
   auto it_cached = c.graphs.find(key);
   if (it_cached != c.graphs.end()) {
@@ -462,7 +472,8 @@ void run_pcg(Ctx& c, const double* b_dev, double rtol, int maxit, awg_solve_repo
     cudaGraph_t graph = nullptr;
     const long long before = c.launches;
     AWG_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
-    iteration();
+    iteration(c.pp.p, c.pp2.p);
+    iteration(c.pp2.p, c.pp.p);
     AWG_CUDA(cudaStreamEndCapture(c.stream, &graph));
     AWG_CUDA(cudaGraphInstantiate(&exec, graph, c.use_priority ? cudaGraphInstantiateFlagUseNodePriority : 0));
     cudaGraphDestroy(graph);
@@ -470,13 +481,13 @@ void run_pcg(Ctx& c, const double* b_dev, double rtol, int maxit, awg_solve_repo
     c.graph_launches[key] = c.launches - before;
     c.launches = before;
   }
-  const long long per_iter = c.graph_launches[key];
-  int batch = 2;
+  const long long per_graph = c.graph_launches[key];
+  int batch = 2;  // iterations enqueued before the next host check
   int issued = 0;
   while (true) {
-    for (int b = 0; b < batch && issued < maxit; ++b, ++issued) {
+    for (int b = 0; b < batch && issued < maxit; b += kItersPerGraph, issued += kItersPerGraph) {
       AWG_CUDA(cudaGraphLaunch(exec, c.stream));
-      c.launches += per_iter;
+      c.launches += per_graph;
     }
     AWG_CUDA(cudaMemcpyAsync(&h, st, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
     AWG_CUDA(cudaStreamSynchronize(c.stream));
