@@ -207,12 +207,13 @@ int awg_kernel_timer(struct awg_ctx* ctx, int reset, double* ms_total, long long
 int awg_synthetic_factors(struct awg_ctx* ctx, int m_per_sub, unsigned long long seed);
 /* Benchmark / check hook of the setup's grouped FP64 tensor-core GEMM
  * (dgemm.cu; the W build's block one-level P^s X^s, preconditioner.cpp:97-113):
- * `count` column-major products C = A B (A m x k, B k x n, seeded pseudo-random
- * values) in one grouped launch, timed over `reps` launches and checked against
+ * `count` column-major products C = A B (A m x k, B k x n; with transpose_a,
+ * C = A^T B with A stored k x m — the W^T A W assembly), seeded pseudo-random
+ * values, in one grouped launch, timed over `reps` launches and checked against
  * cuBLAS DGEMM on the same operands.  out[0] max |C - C_cublas| / max |C_cublas|,
  * out[1] ms per grouped launch, out[2] ms for the same products as `count`
  * cuBLAS calls, out[3] grouped TFLOP/s, out[4] cuBLAS TFLOP/s. */
-int awg_bench_dgemm(struct awg_ctx* ctx, int m, int n, int k, int count, int reps, double* out);
+int awg_bench_dgemm(struct awg_ctx* ctx, int m, int n, int k, int count, int transpose_a, int reps, double* out);
 
 #ifdef __cplusplus
 }

@@ -208,7 +208,7 @@ def load_library(path: str = LIB_PATH):
                                     ctypes.POINTER(ctypes.c_double)]
     lib.awg_synthetic_factors.argtypes = [vp, ctypes.c_int, ctypes.c_ulonglong]
     lib.awg_bench_dgemm.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
-                                    ctypes.POINTER(ctypes.c_double)]
+                                    ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
     _lib = lib
     return lib
 
@@ -457,11 +457,11 @@ class ProblemContext:
         self._check(self._lib.awg_time_kernel(self._h, self.KERNELS[name], reps, ctypes.byref(ms), ctypes.byref(by)))
         return ms.value, by.value
 
-    def bench_dgemm(self, m: int, n: int, k: int, count: int = 1, reps: int = 5) -> dict:
+    def bench_dgemm(self, m: int, n: int, k: int, count: int = 1, reps: int = 5, transpose_a: bool = False) -> dict:
         """Grouped FP64 tensor-core GEMM (the W build's block one-level products)
         against cuBLAS on seeded operands: relative max error, ms, TFLOP/s."""
         out = (ctypes.c_double * 5)()
-        self._check(self._lib.awg_bench_dgemm(self._h, m, n, k, count, reps, out))
+        self._check(self._lib.awg_bench_dgemm(self._h, m, n, k, count, int(transpose_a), reps, out))
         return {"rel_err": out[0], "ms_grouped": out[1], "ms_cublas": out[2], "tflops_grouped": out[3],
                 "tflops_cublas": out[4]}
 

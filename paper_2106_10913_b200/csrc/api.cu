@@ -689,10 +689,10 @@ int awg_time_apply(awg_ctx* ctx, int op, int reps, double* ms) {
   });
 }
 
-int awg_bench_dgemm(awg_ctx* ctx, int m, int n, int k, int count, int reps, double* out) {
+int awg_bench_dgemm(awg_ctx* ctx, int m, int n, int k, int count, int transpose_a, int reps, double* out) {
   return guarded(ctx, [&](Ctx& c) {
     if (m < 1 || n < 1 || k < 1 || count < 1 || reps < 1 || !out) c.fail(AWG_E_ARG, "bench_dgemm: bad arguments");
-    bench_grouped_dgemm(c, m, n, k, count, reps, out);
+    bench_grouped_dgemm(c, m, n, k, count, transpose_a != 0, reps, out);
   });
 }
 

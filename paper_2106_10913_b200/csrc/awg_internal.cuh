@@ -142,8 +142,10 @@ struct GroupedGemm {
   DArr<GemmDesc> desc;
   DArr<GemmTile> tiles;
   int ntiles = 0;
+  bool ta = false;  // C = A^T B (A stored K x M, column-major)
   double flops = 0.0;
-  void set(Ctx& c, const std::vector<GemmDesc>& probs);  // validates and uploads the tile list
+  // validates and uploads the tile list; transpose_a: every problem is C = A^T B
+  void set(Ctx& c, const std::vector<GemmDesc>& probs, bool transpose_a = false);
   void run(Ctx& c) const;                                 // on c.stream
 };
 
@@ -393,7 +395,7 @@ void assemble_elasticity(Ctx& c, int nodes_x, int nodes_y, int layer, int nmat, 
 void partition_closure(Ctx& c, const std::vector<int>& owner, int nsub, int rings, std::vector<long long>& off,
                        std::vector<int>& idx);
 // dgemm.cu: grouped DMMA GEMM vs cuBLAS on seeded operands (awg_bench_dgemm)
-void bench_grouped_dgemm(Ctx& c, int m, int n, int k, int count, int reps, double* out);
+void bench_grouped_dgemm(Ctx& c, int m, int n, int k, int count, bool transpose_a, int reps, double* out);
 void build_core(Ctx& c);        // INEX core LU
 void run_setup(Ctx& c, const awg_config& cfg);  // setup.cu
 void build_local_cholesky(Ctx& c);              // setup.cu: AS / AS+ factors U^s = L^-T

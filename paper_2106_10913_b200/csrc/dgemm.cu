@@ -29,14 +29,16 @@ namespace {
 
 constexpr int kBM = 128;
 
-template <int BN, int BK, int ST, int WM = 64>
+template <int BN, int BK, int ST, int WM = 64, bool TA = false>
 struct GCfg {
   static constexpr int kWM = kBM / WM;          // warps along m
   static constexpr int kWarps = kWM * (BN / 32);  // kWM (m) x BN/32 (n) warps of WM x 32
   static constexpr int kT = 32 * kWarps;
-  static constexpr int kALd = kBM + 4;  // doubles per k row of the A tile (1056 B = 32 B mod 128 B)
+  // A tile: [k][m] with kBM + 4 doubles per k (1056 B = 32 B mod 128 B); for
+  // C = A^T B (TA, A stored K x M) it is [m][k] like the B tile
+  static constexpr int kALd = TA ? BK + 4 : kBM + 4;
   static constexpr int kBLd = BK + 4;   // doubles per n column of the B tile (160 / 288 B = 32 B mod 128 B)
-  static constexpr int kAStage = BK * kALd, kBStage = BN * kBLd;
+  static constexpr int kAStage = (TA ? kBM : BK) * kALd, kBStage = BN * kBLd;
   static constexpr size_t kSmem = size_t(ST) * (kAStage + kBStage) * sizeof(double);
   static constexpr int kAChunks = BK * kBM / 2, kBChunks = BN * BK / 2;  // 16-byte chunks per tile
 };
@@ -59,13 +61,13 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-template <int BN, int BK, int ST, int MINB, int WM>
-__global__ void __launch_bounds__(GCfg<BN, BK, ST, WM>::kT, MINB)
+template <int BN, int BK, int ST, int MINB, int WM, bool TA>
+__global__ void __launch_bounds__(GCfg<BN, BK, ST, WM, TA>::kT, MINB)
     k_dgemm_grouped(const GemmDesc* __restrict__ probs, const GemmTile* __restrict__ tiles) {
-  using C = GCfg<BN, BK, ST, WM>;
+  using C = GCfg<BN, BK, ST, WM, TA>;
   constexpr int MI = WM / 8;  // 8 x 8 fragments along m per warp
   extern __shared__ __align__(128) double gsm[];
-  double* As = gsm;                      // ST x [BK][kALd]
+  double* As = gsm;                      // ST x A tile
   double* Bs = gsm + ST * C::kAStage;    // ST x [BN][kBLd]
   const GemmTile t = tiles[blockIdx.x];
   const GemmDesc pr = probs[t.prob];
@@ -73,30 +75,49 @@ __global__ void __launch_bounds__(GCfg<BN, BK, ST, WM>::kT, MINB)
   const int m0 = t.m0, n0 = t.n0;
   const int KT = (pr.K + BK - 1) / BK;
 
-  // producer addressing, hoisted: every A chunk of a thread has the same rows
-  // (m), columns k0 + kk0 + u * kAStep; every B chunk the same rows (k) and
-  // columns n0 + nn0 + u * kBStep.  Bounds in M and N are fixed per tile; the
-  // K bound only matters on the last K-tile.
-  constexpr int kAStep = C::kT / 64, kBStep = C::kT / (BK / 2);
-  const int mA = m0 + 2 * (tid & 63), kk0 = tid >> 6;
-  const int a_bytes = 8 * max(0, min(2, pr.M - mA));
-  const double* a_ptr = pr.A + (size_t)kk0 * pr.lda + mA;
-  const int kc2 = 2 * (tid % (BK / 2)), nn0 = tid / (BK / 2);
-  const double* b_ptr = pr.B + (size_t)(n0 + nn0) * pr.ldb + kc2;
+  // producer addressing, hoisted.  A (no transpose): every chunk of a thread
+  // has the same rows (m), columns k0 + kk0 + u * kAStep.  A^T and B: the same
+  // rows (k), columns m0 + mm0 + u * step / n0 + nn0 + u * kBStep.  Bounds in
+  // M and N are fixed per tile; the K bound only matters on the last K-tile.
+  constexpr int kAStep = TA ? C::kT / (BK / 2) : C::kT / 64, kBStep = C::kT / (BK / 2);
+  const int kc2 = 2 * (tid % (BK / 2)), row0 = tid / (BK / 2);  // B (and A^T) chunk coordinates
+  const int mA = m0 + 2 * (tid & 63), kk0 = tid >> 6;            // A chunk coordinates
+  int a_bytes = 0;
+  unsigned a_ok = 0;
+  const double* a_ptr;
+  double* a_dst;
+  if constexpr (TA) {
+#pragma unroll
+    for (int u = 0; u < C::kAChunks / C::kT; ++u) a_ok |= (m0 + row0 + u * kAStep < pr.M) ? (1u << u) : 0u;
+    a_ptr = pr.A + (size_t)(m0 + row0) * pr.lda + kc2;
+    a_dst = As + row0 * C::kALd + kc2;
+  } else {
+    a_bytes = 8 * max(0, min(2, pr.M - mA));
+    a_ptr = pr.A + (size_t)kk0 * pr.lda + mA;
+    a_dst = As + kk0 * C::kALd + 2 * (tid & 63);
+  }
+  const double* b_ptr = pr.B + (size_t)(n0 + row0) * pr.ldb + kc2;
   unsigned b_ok = 0;
 #pragma unroll
-  for (int u = 0; u < C::kBChunks / C::kT; ++u) b_ok |= (n0 + nn0 + u * kBStep < pr.N) ? (1u << u) : 0u;
-  double* a_dst = As + kk0 * C::kALd + 2 * (tid & 63);
-  double* b_dst = Bs + nn0 * C::kBLd + kc2;
+  for (int u = 0; u < C::kBChunks / C::kT; ++u) b_ok |= (n0 + row0 + u * kBStep < pr.N) ? (1u << u) : 0u;
+  double* b_dst = Bs + row0 * C::kBLd + kc2;
   auto load = [&](int kt, int stage) {
     const int k0 = kt * BK;
     const bool full = k0 + BK <= pr.K;
 #pragma unroll
     for (int u = 0; u < C::kAChunks / C::kT; ++u) {
-      int bytes = a_bytes;
-      if (!full && k0 + kk0 + u * kAStep >= pr.K) bytes = 0;
-      cp_async16(a_dst + stage * C::kAStage + u * kAStep * C::kALd,
-                 bytes ? a_ptr + (size_t)(k0 + u * kAStep) * pr.lda : pr.A, bytes);
+      int bytes;
+      const double* src;
+      if constexpr (TA) {
+        bytes = ((a_ok >> u) & 1u) ? 16 : 0;
+        if (!full && bytes) bytes = 8 * max(0, min(2, pr.K - (k0 + kc2)));
+        src = a_ptr + (size_t)u * kAStep * pr.lda + k0;
+      } else {
+        bytes = a_bytes;
+        if (!full && k0 + kk0 + u * kAStep >= pr.K) bytes = 0;
+        src = a_ptr + (size_t)(k0 + u * kAStep) * pr.lda;
+      }
+      cp_async16(a_dst + stage * C::kAStage + u * kAStep * C::kALd, bytes ? src : pr.A, bytes);
     }
 #pragma unroll
     for (int u = 0; u < C::kBChunks / C::kT; ++u) {
@@ -125,13 +146,15 @@ __global__ void __launch_bounds__(GCfg<BN, BK, ST, WM>::kT, MINB)
     __syncthreads();
     if (kt + ST - 1 < KT) load(kt + ST - 1, (kt + ST - 1) % ST);
     cp_commit();
-    const double* as = As + (kt % ST) * C::kAStage + fc * C::kALd + wm + fr;
+    // A fragment (m = fr, k = fc) and B fragment (k = fc, n = fr) of each 8x8x4 step
+    const double* as = TA ? As + (kt % ST) * C::kAStage + (wm + fr) * C::kALd + fc
+                          : As + (kt % ST) * C::kAStage + fc * C::kALd + wm + fr;
     const double* bs = Bs + (kt % ST) * C::kBStage + (wn + fr) * C::kBLd + fc;
 #pragma unroll
     for (int k4 = 0; k4 < BK / 4; ++k4) {
       double a[MI], b[4];
 #pragma unroll
-      for (int i = 0; i < MI; ++i) a[i] = as[k4 * 4 * C::kALd + i * 8];
+      for (int i = 0; i < MI; ++i) a[i] = TA ? as[i * 8 * C::kALd + k4 * 4] : as[k4 * 4 * C::kALd + i * 8];
 #pragma unroll
       for (int j = 0; j < 4; ++j) b[j] = bs[j * 8 * C::kBLd + k4 * 4];
 #pragma unroll
@@ -175,21 +198,22 @@ int gemm_bn() {
   return (v == 1 || v == 2 || v == 5) ? 128 : 64;
 }
 
-template <int BN, int BK, int ST, int MINB, int WM = 64>
+template <int BN, int BK, int ST, int MINB, int WM = 64, bool TA = false>
 void launch_gemm(Ctx& c, int ntiles, const GemmDesc* d, const GemmTile* t) {
-  using C = GCfg<BN, BK, ST, WM>;
+  using C = GCfg<BN, BK, ST, WM, TA>;
   static bool configured = false;
   if (!configured) {
-    AWG_CUDA(cudaFuncSetAttribute(k_dgemm_grouped<BN, BK, ST, MINB, WM>,
+    AWG_CUDA(cudaFuncSetAttribute(k_dgemm_grouped<BN, BK, ST, MINB, WM, TA>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::kSmem)));
     configured = true;
   }
-  k_dgemm_grouped<BN, BK, ST, MINB, WM><<<ntiles, C::kT, C::kSmem, c.stream>>>(d, t);
+  k_dgemm_grouped<BN, BK, ST, MINB, WM, TA><<<ntiles, C::kT, C::kSmem, c.stream>>>(d, t);
 }
 
 }  // namespace
 
-void GroupedGemm::set(Ctx& c, const std::vector<GemmDesc>& probs) {
+void GroupedGemm::set(Ctx& c, const std::vector<GemmDesc>& probs, bool transpose_a) {
+  ta = transpose_a;
   std::vector<GemmTile> tl;
   flops = 0.0;
   for (int p = 0; p < int(probs.size()); ++p) {
@@ -201,7 +225,7 @@ void GroupedGemm::set(Ctx& c, const std::vector<GemmDesc>& probs) {
     flops += 2.0 * d.M * d.N * std::max(d.K, 0);
     // n tiles of one A panel are adjacent in launch order: they run together and
     // share the panel through L2 (A is read from HBM once; B^s stays L2-resident)
-    const int bn = gemm_bn();
+    const int bn = ta ? 64 : gemm_bn();
     for (int m0 = 0; m0 < d.M; m0 += kBM)
       for (int n0 = 0; n0 < d.N; n0 += bn) tl.push_back({p, m0, n0, 0});
   }
@@ -212,6 +236,12 @@ void GroupedGemm::set(Ctx& c, const std::vector<GemmDesc>& probs) {
 
 void GroupedGemm::run(Ctx& c) const {
   if (ntiles == 0) return;
+  if (ta) {  // C = A^T B: default tiling only
+    launch_gemm<64, 16, 3, 2, 32, true>(c, ntiles, desc.p, tiles.p);  // 3 stages: two CTAs per SM fit
+    ++c.launches;
+    check_launch("dgemm_grouped_tn");
+    return;
+  }
   switch (gemm_variant()) {
     case 1: launch_gemm<128, 16, 4, 1>(c, ntiles, desc.p, tiles.p); break;
     case 2: launch_gemm<128, 32, 3, 1>(c, ntiles, desc.p, tiles.p); break;
@@ -254,9 +284,10 @@ __global__ void k_maxabs2(size_t n, const double* a, const double* b, unsigned l
 }
 }  // namespace
 
-void bench_grouped_dgemm(Ctx& c, int m, int n, int k, int count, int reps, double* out) {
-  const int lda = round_up(m, 4), ldb = round_up(k, 4), ldc = round_up(m, 4);
-  const size_t sa = size_t(lda) * k, sb = size_t(ldb) * n, sc = size_t(ldc) * n;
+void bench_grouped_dgemm(Ctx& c, int m, int n, int k, int count, bool ta, int reps, double* out) {
+  // A is m x k (lda = round_up(m, 4)) or, with ta, k x m (lda = round_up(k, 4)) and C = A^T B
+  const int lda = ta ? round_up(k, 4) : round_up(m, 4), ldb = round_up(k, 4), ldc = round_up(m, 4);
+  const size_t sa = size_t(lda) * (ta ? m : k), sb = size_t(ldb) * n, sc = size_t(ldc) * n;
   DArr<double> A, B, C1, C2;
   A.alloc(sa * count);
   B.alloc(sb * count);
@@ -270,14 +301,14 @@ void bench_grouped_dgemm(Ctx& c, int m, int n, int k, int count, int reps, doubl
   for (int q = 0; q < count; ++q)
     probs.push_back({A.p + sa * q, B.p + sb * q, C1.p + sc * q, m, n, k, lda, ldb, ldc});
   GroupedGemm g;
-  g.set(c, probs);
+  g.set(c, probs, ta);
   cublasHandle_t h = nullptr;
   if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) c.fail(AWG_E_CUDA, "bench_dgemm: cublasCreate");
   cublasSetStream(h, c.stream);
   const double one = 1.0, zero = 0.0;
   auto lib = [&]() {
     for (int q = 0; q < count; ++q)
-      cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, m, n, k, &one, A.p + sa * q, lda, B.p + sb * q, ldb, &zero,
+      cublasDgemm(h, ta ? CUBLAS_OP_T : CUBLAS_OP_N, CUBLAS_OP_N, m, n, k, &one, A.p + sa * q, lda, B.p + sb * q, ldb, &zero,
                   C2.p + sc * q, ldc);
   };
   cudaEvent_t e0, e1;

@@ -533,6 +533,49 @@ void build_local_cholesky(Ctx& c) {
   local_cholesky(c, sv, lb);
 }
 
+// G = W^T A W (preconditioner.cpp:119-126): A W in blocks of columns (one SpMV
+// per column), then W^T (A W) as a grouped C = A^T B on the FP64 tensor cores
+// (dgemm.cu), split over the n rows so the nm x 512 output still fills every
+// SM; the split partials are summed in slice order.
+__global__ void k_sum_slices(int S, long long len, const double* __restrict__ part, double* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < len; i += (long long)gridDim.x * blockDim.x) {
+    double a = 0.0;
+    for (int s = 0; s < S; ++s) a += part[(size_t)s * len + i];
+    out[i] = a;
+  }
+}
+
+static void wtaw(Ctx& c, int nm, double* G) {
+  const int Bc = std::min(nm, 512);
+  DArr<double> aw;
+  aw.alloc(size_t(c.ldw) * Bc);
+  aw.zero(c.stream);  // padding rows of each column stay zero
+  const int tiles = ((nm + 127) / 128) * ((Bc + 63) / 64);
+  int S = std::max(1, std::min(32, (8 * c.sm_count + tiles - 1) / tiles));
+  const int kslice = round_up((c.n + S - 1) / S, 16);
+  S = (c.n + kslice - 1) / kslice;
+  DArr<double> part;
+  part.alloc(size_t(S) * nm * Bc);
+  GroupedGemm g;
+  for (int j0 = 0; j0 < nm; j0 += Bc) {
+    const int bc = std::min(Bc, nm - j0);
+    for (int j = 0; j < bc; ++j)
+      k::spmv(c, c.W.p + size_t(j0 + j) * c.ldw, aw.p + size_t(j) * c.ldw, 0, nullptr, nullptr, nullptr);
+    std::vector<GemmDesc> pd;
+    for (int sl = 0; sl < S; ++sl) {
+      const int k0 = sl * kslice, kl = std::min(kslice, c.n - k0);
+      pd.push_back({c.W.p + k0, aw.p + k0, part.p + size_t(sl) * nm * bc, nm, bc, kl, c.ldw, c.ldw, nm});
+    }
+    g.set(c, pd, /*transpose_a=*/true);
+    g.run(c);
+    const long long len = (long long)nm * bc;
+    k_sum_slices<<<int(std::min<long long>((len + kThreads - 1) / kThreads, 4096)), kThreads, 0, c.stream>>>(
+        S, len, part.p, G + size_t(j0) * nm);
+    ++c.launches;
+    check_launch("wtaw");
+  }
+}
+
 void run_setup(Ctx& c, const awg_config& cfg) {
   const double t_start = now_ms();
   const int N = c.N;
@@ -801,13 +844,9 @@ void run_setup(Ctx& c, const awg_config& cfg) {
     t0 = now_ms();
     c.nm = nm;
     c.alloc_work();  // W-sized work buffers
-    DArr<double> G, aw;
+    DArr<double> G;
     G.alloc(size_t(nm) * nm);
-    aw.alloc(c.n);
-    for (int j = 0; j < nm; ++j) {
-      k::spmv(c, c.W.p + size_t(j) * c.ldw, aw.p, 0, nullptr, nullptr, nullptr);
-      k::wT(c, aw.p, G.p + size_t(j) * nm, nullptr);
-    }
+    wtaw(c, nm, G.p);
     k_symmetrize<<<int(((long long)nm * nm + kThreads - 1) / kThreads), kThreads, 0, c.stream>>>(nm, G.p);
     ++c.launches;
     pivoted_factor(c, G, nm, cfg.rrf_semantics, c.kw, nm);

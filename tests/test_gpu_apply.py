@@ -172,14 +172,16 @@ def test_in_kernel_timer_counts_live_launches():
     assert 0.0 < ms < rep.solve_ms
 
 
+@pytest.mark.parametrize("ta", [False, True])
 @pytest.mark.parametrize("shape", [(1001, 77, 333, 3), (130, 64, 17, 2), (4612, 130, 4612, 2)])
-def test_grouped_dgemm_matches_cublas(shape):
+def test_grouped_dgemm_matches_cublas(shape, ta):
     """The setup's grouped FP64 tensor-core GEMM (dgemm.cu, the W build's
     P^s X^s) against cuBLAS DGEMM on the same seeded operands: ragged M, N, K
-    (zero-filled partial tiles), several problems per launch."""
+    (zero-filled partial tiles), several problems per launch; C = A B and
+    C = A^T B (the W^T A W assembly)."""
     g, s = golden_with_base("t2d")
     ctx = make_ctx(g)
     m, n, k, cnt = shape
-    r = ctx.bench_dgemm(m, n, k, cnt, reps=1)
+    r = ctx.bench_dgemm(m, n, k, cnt, reps=1, transpose_a=ta)
     assert r["rel_err"] <= 1e-13, r
     assert r["ms_grouped"] > 0.0
