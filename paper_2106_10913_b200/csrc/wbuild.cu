@@ -96,24 +96,88 @@ __global__ void kb_mask(long long P, const int* __restrict__ psub, const long lo
   }
 }
 
-// Y(i,b) = sum over s containing i (ascending) of (ds) * WS(s, loc, b)
-__global__ void kb_prolong(int n, int ldx, const int* __restrict__ own_off, const int* __restrict__ own_pos,
-                           const int* __restrict__ psub, const long long* __restrict__ poff,
-                           const int* __restrict__ lds, const long long* __restrict__ boff,
-                           const double* __restrict__ ds, const double* __restrict__ WS, double* __restrict__ Y,
-                           const int* __restrict__ done) {
-  const int b = blockIdx.y;
-  if (col_off(done, b)) return;
+// Column-blocked forms: thread per (row i, kBB columns of the block), so the
+// CSR row / owner entries are read once for kBB columns (they were re-read per
+// column from L2: 512 x the CSR arrays per block SpMV).  Per column the
+// arithmetic is exactly kb_spmv's / kb_prolong's.
+constexpr int kBB = 8;
+struct BEnt {  // owner entry q of dof i in the block-P layout: WS(s, loc, b) = WS[base + b * ld]
+  long long base;
+  int ld, p;
+};
+__global__ void kb_build_bent(long long P, const int* __restrict__ own_pos, const int* __restrict__ psub,
+                              const long long* __restrict__ poff, const int* __restrict__ lds,
+                              const long long* __restrict__ boff, BEnt* __restrict__ ent) {
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < P; q += (long long)gridDim.x * blockDim.x) {
+    const int p = own_pos[q];
+    const int s = psub[p];
+    ent[q] = BEnt{boff[s] + (p - poff[s]), lds[s], p};
+  }
+}
+
+__device__ __forceinline__ unsigned live_mask(const int* done, int b0, int B) {
+  unsigned m = 0;
+#pragma unroll
+  for (int u = 0; u < kBB; ++u)
+    if (b0 + u < B && !col_off(done, b0 + u)) m |= 1u << u;
+  return m;
+}
+
+__global__ void kb_spmv8(int n, int B, int ld, const int* __restrict__ rp, const int* __restrict__ ci,
+                         const double* __restrict__ va, const double* __restrict__ X, double* __restrict__ Y, int mode,
+                         const double* __restrict__ add, const double* __restrict__ sub, const int* __restrict__ done) {
+  const int b0 = blockIdx.y * kBB;
+  const unsigned live = live_mask(done, b0, B);
+  if (!live) return;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    double acc = 0.0;
-    for (int q = own_off[i]; q < own_off[i + 1]; ++q) {
-      const int p = own_pos[q];
-      const int s = psub[p];
-      double w = WS[boff[s] + (size_t)b * lds[s] + (p - poff[s])];
-      if (ds) w *= ds[p];
-      acc += w;
+    double acc[kBB];
+#pragma unroll
+    for (int u = 0; u < kBB; ++u) acc[u] = 0.0;
+    for (int k = rp[i]; k < rp[i + 1]; ++k) {
+      const double v = va[k];
+      const size_t j = ci[k];
+#pragma unroll
+      for (int u = 0; u < kBB; ++u)
+        if (live >> u & 1u) acc[u] = __dadd_rn(acc[u], __dmul_rn(v, __ldg(X + (size_t)(b0 + u) * ld + j)));
     }
-    Y[(size_t)b * ldx + i] = acc;
+#pragma unroll
+    for (int u = 0; u < kBB; ++u) {
+      if (!(live >> u & 1u)) continue;
+      const size_t o = (size_t)(b0 + u) * ld + i;
+      double out;
+      if (mode == 0) out = acc[u];
+      else if (mode == 1) out = add[o] + acc[u];
+      else if (mode == 2) out = sub[o] - (add[o] + acc[u]);
+      else out = sub[o] - acc[u];
+      Y[o] = out;
+    }
+  }
+}
+
+__global__ void kb_prolong8(int n, int B, int ldx, const int* __restrict__ own_off, const BEnt* __restrict__ ent,
+                            const double* __restrict__ ds, const double* __restrict__ WS, double* __restrict__ Y,
+                            const int* __restrict__ done) {
+  const int b0 = blockIdx.y * kBB;
+  const unsigned live = live_mask(done, b0, B);
+  if (!live) return;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double acc[kBB];
+#pragma unroll
+    for (int u = 0; u < kBB; ++u) acc[u] = 0.0;
+    for (int q = own_off[i]; q < own_off[i + 1]; ++q) {
+      const BEnt e = ent[q];
+      const double d = ds ? ds[e.p] : 1.0;
+#pragma unroll
+      for (int u = 0; u < kBB; ++u) {
+        if (!(live >> u & 1u)) continue;
+        double w = WS[e.base + (size_t)(b0 + u) * e.ld];
+        if (ds) w *= d;
+        acc[u] += w;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kBB; ++u)
+      if (live >> u & 1u) Y[(size_t)(b0 + u) * ldx + i] = acc[u];
   }
 }
 
@@ -351,6 +415,48 @@ struct Block {
   DArr<int> done, any_true;
   DArr<long long> boff;
   std::vector<long long> h_boff;
+  DArr<BEnt> bent;  // owner entries in the block-P layout (kb_prolong8)
+};
+
+// Per-subdomain products of one block operation as ONE cuBLAS grouped-batched
+// DGEMM call (one group per subdomain): the per-call overhead of N separate
+// DGEMMs dominated these skinny products (q_s or k_s <= ~50 columns).
+struct GroupedCall {
+  std::vector<cublasOperation_t> ta, tb;
+  std::vector<int> m, n, k, lda, ldb, ldc, gs;
+  std::vector<double> al, be;
+  std::vector<const double*> ha, hb;
+  std::vector<double*> hc;
+  DArr<const double*> A, B;
+  DArr<double*> C;
+  void add(cublasOperation_t opa, int mm, int nn, int kk, const double* a, int la, const double* b, int lb, double* cc,
+           int lc) {
+    ta.push_back(opa);
+    tb.push_back(CUBLAS_OP_N);
+    m.push_back(mm);
+    n.push_back(nn);
+    k.push_back(kk);
+    lda.push_back(la);
+    ldb.push_back(lb);
+    ldc.push_back(lc);
+    gs.push_back(1);
+    al.push_back(1.0);
+    be.push_back(0.0);
+    ha.push_back(a);
+    hb.push_back(b);
+    hc.push_back(cc);
+  }
+  void upload(cudaStream_t st) {
+    A.upload(ha, st);
+    B.upload(hb, st);
+    C.upload(hc, st);
+  }
+  void run(cublasHandle_t h) const {
+    if (m.empty()) return;
+    AWG_BLAS(cublasDgemmGroupedBatched(h, ta.data(), tb.data(), m.data(), n.data(), k.data(), al.data(), A.p,
+                                       lda.data(), B.p, ldb.data(), be.data(), C.p, ldc.data(), int(m.size()),
+                                       gs.data()));
+  }
 };
 
 struct BlockOps {
@@ -384,6 +490,8 @@ struct BlockOps {
     prof = false;
   }
 
+  GroupedCall g_negdot, g_negcomb, g_zdot, g_zcomb;  // V-^T XS, V- C, Y^T XS, Y C over all subdomains
+  bool any_q0 = false, any_k0 = false;              // subdomains without negative modes / coarse columns
   BlockOps(Ctx& cc, Block& kk, cublasHandle_t hh, const CoarseFactor& f) : c(cc), k(kk), h(hh), k0(f) {
     qs.resize(c.N);
     negoff.assign(c.N + 1, 0);
@@ -393,15 +501,43 @@ struct BlockOps {
       negoff[s + 1] = negoff[s] + qs[s];
       koff[s + 1] = koff[s] + c.h_ks[s];
     }
+    const int B = k.B, n0 = c.n0;
+    for (int s = 0; s < c.N; ++s) {
+      const int ns = c.h_ns[s], L = c.h_ld[s];
+      double* xs = k.XS.p + k.h_boff[s];
+      double* ws = k.WS.p + k.h_boff[s];
+      if (qs[s] > 0) {
+        const double* v = c.V.p + c.h_voff[s];
+        g_negdot.add(CUBLAS_OP_T, qs[s], B, ns, v, L, xs, L, k.negc.p + negoff[s], c.nneg);
+        g_negcomb.add(CUBLAS_OP_N, ns, B, qs[s], v, L, k.negc.p + negoff[s], c.nneg, ws, L);
+      }
+      if (c.h_ks[s] > 0) {
+        const double* y = c.Y.p + c.h_yoff[s];
+        g_zdot.add(CUBLAS_OP_T, c.h_ks[s], B, ns, y, L, xs, L, k.zx.p + koff[s], n0);
+        g_zcomb.add(CUBLAS_OP_N, ns, B, c.h_ks[s], y, L, k.zc.p + koff[s], n0, ws, L);
+      }
+    }
+    for (int s = 0; s < c.N; ++s) {
+      any_q0 |= qs[s] == 0;
+      any_k0 |= c.h_ks[s] == 0;
+    }
+    for (GroupedCall* g : {&g_negdot, &g_negcomb, &g_zdot, &g_zcomb}) g->upload(c.stream);
   }
 
   dim3 grid_n() const { return dim3(std::max(1, std::min((c.n + kT - 1) / kT, 148 * 2)), k.B); }
+  dim3 grid_bb() const {
+    return dim3(std::max(1, std::min((c.n + kT - 1) / kT, 148 * 2)), (k.B + kBB - 1) / kBB);
+  }
+  void prolong(const double* ds, const double* WS, double* Y, const int* done) {
+    kb_prolong8<<<grid_bb(), kT, 0, c.stream>>>(c.n, k.B, k.ld, c.own_off.p, k.bent.p, ds, WS, Y, done);
+    ++c.launches;
+  }
   dim3 grid_p() const {
     return dim3(std::max(1, int(std::min<long long>((c.P + kT - 1) / kT, 148 * 2))), k.B);
   }
 
   void spmv(const double* X, double* Y, int mode, const double* add, const double* sub, const int* done) {
-    kb_spmv<<<grid_n(), kT, 0, c.stream>>>(c.n, k.ld, c.rp.p, c.ci.p, c.va.p, X, Y, mode, add, sub, done);
+    kb_spmv8<<<grid_bb(), kT, 0, c.stream>>>(c.n, k.B, k.ld, c.rp.p, c.ci.p, c.va.p, X, Y, mode, add, sub, done);
     ++c.launches;
   }
   // A- X = sum_s R^s^T V-^s |L-^s| V-^s^T R^s X: the strictly negative modes of s are
@@ -414,23 +550,18 @@ struct BlockOps {
     }
     kb_gather<<<grid_p(), kT, 0, c.stream>>>(c.P, c.psub.p, c.poff.p, c.pidx.p, c.ld.p, k.boff.p, nullptr, k.ld, X,
                                              k.XS.p, done);
-    AWG_CUDA(cudaMemsetAsync(k.WS.p, 0, sizeof(double) * k.WS.n, c.stream));
-    const double one = 1.0, zero = 0.0;
-    for (int s = 0; s < c.N; ++s) {
-      const int q = qs[s];
-      if (q == 0) continue;
-      AWG_BLAS(cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, q, k.B, c.h_ns[s], &one, c.V.p + c.h_voff[s], c.h_ld[s],
-                           k.XS.p + k.h_boff[s], c.h_ld[s], &zero, k.negc.p + negoff[s], c.nneg));
-    }
+    mark("am.gather");
+    // WS is rewritten (beta = 0) on every row the prolongation reads, except
+    // for subdomains without negative modes: zero it only then
+    if (any_q0) AWG_CUDA(cudaMemsetAsync(k.WS.p, 0, sizeof(double) * k.WS.n, c.stream));
+    mark("am.memset");
+    g_negdot.run(h);  // V-^s^T R^s X, every subdomain
+    mark("am.dots");
     kb_scale_rows<<<dim3((c.nneg + kT - 1) / kT, k.B), kT, 0, c.stream>>>(c.nneg, c.neg_w.p, k.negc.p);
-    for (int s = 0; s < c.N; ++s) {
-      const int q = qs[s];
-      if (q == 0) continue;
-      AWG_BLAS(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, c.h_ns[s], k.B, q, &one, c.V.p + c.h_voff[s], c.h_ld[s],
-                           k.negc.p + negoff[s], c.nneg, &zero, k.WS.p + k.h_boff[s], c.h_ld[s]));
-    }
-    kb_prolong<<<grid_n(), kT, 0, c.stream>>>(c.n, k.ld, c.own_off.p, c.own_pos.p, c.psub.p, c.poff.p, c.ld.p,
-                                              k.boff.p, nullptr, k.WS.p, Y, done);
+    g_negcomb.run(h);  // V-^s C_s
+    mark("am.comb");
+    prolong(nullptr, k.WS.p, Y, done);
+    mark("am.prolong");
     c.launches += 3;
   }
   void aplus(const double* X, double* Y, const int* done) {
@@ -443,15 +574,7 @@ struct BlockOps {
     kb_gather<<<grid_p(), kT, 0, c.stream>>>(c.P, c.psub.p, c.poff.p, c.pidx.p, c.ld.p, k.boff.p, nullptr, k.ld, X,
                                              k.XS.p, done);
     ++c.launches;
-    {
-      const double one = 1.0, zero = 0.0;
-      for (int s = 0; s < c.N; ++s) {
-        const int ks = c.h_ks[s];
-        if (ks == 0) continue;
-        AWG_BLAS(cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, ks, B, c.h_ns[s], &one, c.Y.p + c.h_yoff[s], c.h_ld[s],
-                             k.XS.p + k.h_boff[s], c.h_ld[s], &zero, k.zx.p + koff[s], n0));
-      }
-    }
+    g_zdot.run(h);  // Y_s^T R^s X
     AWG_CUDA(cudaMemsetAsync(k.zc.p, 0, sizeof(double) * n0 * B, c.stream));
     if (r > 0) {
       kb_take<<<int(((long long)r * B + kT - 1) / kT), kT, 0, c.stream>>>(r, n0, B, k0.retained.p, k.zx.p, k.zr.p);
@@ -462,18 +585,9 @@ struct BlockOps {
       kb_put<<<int(((long long)r * B + kT - 1) / kT), kT, 0, c.stream>>>(r, n0, B, k0.retained.p, k.zr.p, k.zc.p);
       c.launches += 2;
     }
-    AWG_CUDA(cudaMemsetAsync(k.WS.p, 0, sizeof(double) * k.WS.n, c.stream));
-    {
-      const double one = 1.0, zero = 0.0;
-      for (int s = 0; s < c.N; ++s) {
-        const int ks = c.h_ks[s];
-        if (ks == 0) continue;
-        AWG_BLAS(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, c.h_ns[s], B, ks, &one, c.Y.p + c.h_yoff[s], c.h_ld[s],
-                             k.zc.p + koff[s], n0, &zero, k.WS.p + k.h_boff[s], c.h_ld[s]));
-      }
-    }
-    kb_prolong<<<grid_n(), kT, 0, c.stream>>>(c.n, k.ld, c.own_off.p, c.own_pos.p, c.psub.p, c.poff.p, c.ld.p,
-                                              k.boff.p, nullptr, k.WS.p, Y, done);
+    if (any_k0) AWG_CUDA(cudaMemsetAsync(k.WS.p, 0, sizeof(double) * k.WS.n, c.stream));
+    g_zcomb.run(h);  // Y_s C_s
+    prolong(nullptr, k.WS.p, Y, done);
     c.launches += 3;
   }
   // OneLevel::apply on the block: NN = R^T D V mask(1/lam) V^T D R, AS/AS+ =
@@ -493,8 +607,7 @@ struct BlockOps {
                                k.XS.p + k.h_boff[s], L, &zero, k.WS.p + k.h_boff[s], L));
         }
       }
-      kb_prolong<<<grid_n(), kT, 0, c.stream>>>(c.n, k.ld, c.own_off.p, c.own_pos.p, c.psub.p, c.poff.p, c.ld.p,
-                                                k.boff.p, c.ds.p, k.WS.p, Y, done);
+      prolong(c.ds.p, k.WS.p, Y, done);
       c.launches += 2;
       return;
     }
@@ -521,8 +634,7 @@ struct BlockOps {
                              &one, c.U.p + c.h_voff[s], L, k.WS.p + k.h_boff[s], L, k.XS.p + k.h_boff[s], L));
       }
     }
-    kb_prolong<<<grid_n(), kT, 0, c.stream>>>(c.n, k.ld, c.own_off.p, c.own_pos.p, c.psub.p, c.poff.p, c.ld.p,
-                                              k.boff.p, nn ? c.ds.p : nullptr, k.XS.p, Y, done);
+    prolong(nn ? c.ds.p : nullptr, k.XS.p, Y, done);
     c.launches += nn ? 3 : 2;
   }
   // TwoLevel::apply (preconditioner.cpp:64-82)
@@ -612,6 +724,9 @@ void build_w_batched(Ctx& c, cublasHandle_t h, const std::vector<std::pair<int, 
   k.h_boff.assign(c.N + 1, 0);
   for (int s = 0; s < c.N; ++s) k.h_boff[s + 1] = k.h_boff[s] + (long long)c.h_ld[s] * B;
   k.boff.upload(k.h_boff, c.stream);
+  k.bent.alloc(size_t(std::max<long long>(c.P, 1)));
+  kb_build_bent<<<int(std::min<long long>((c.P + kT - 1) / kT, 4096)), kT, 0, c.stream>>>(
+      c.P, c.own_pos.p, c.psub.p, c.poff.p, c.ld.p, k.boff.p, k.bent.p);
   k.XS.alloc(size_t(k.h_boff[c.N]));
   k.WS.alloc(size_t(k.h_boff[c.N]));
   k.XS.zero(c.stream);
