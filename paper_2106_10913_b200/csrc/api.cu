@@ -304,6 +304,9 @@ void finalize_factors(Ctx& c) {
       }
     }
     b.ntask = int(ts.size());
+    int maxcols = 1;
+    for (int s = 0; s < N; ++s) maxcols = std::max(maxcols, off[s + 1] - off[s]);
+    b.ncg = (maxcols + 7) / 8;
     b.ts.upload(ts, c.stream);
     b.tc.upload(tc, c.stream);
     b.nch.upload(nch, c.stream);

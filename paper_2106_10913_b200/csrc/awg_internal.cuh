@@ -159,6 +159,7 @@ struct BsPlan {
   DArr<int> cnt;     // CTAs finished per subdomain (reset by the last one)
   DArr<double> part; // columns x maxch
   int ntask = 0, maxch = 1;
+  int ncg = 1;       // column groups of 8 (grid.y): the most columns of any subdomain / 8
 };
 
 // Triangular coarse factor with retained pivots (RankRevealingFactor,

@@ -594,11 +594,13 @@ __global__ void k_block_combine(const int* __restrict__ gate, long long P, const
 // Block-sparse GEMV^T: out[q] = w[q] * sum_i M_s(i, col(q)) x[pidx_s[i]] for the
 // columns q in [coff[s], coff[s+1]) of every subdomain s — Z^T x (Y_s blocks,
 // coarse.cpp:136-141 + matvec_transpose) and the A- dots (V^s columns
-// k < n_nonpos, splitting.cpp:124-132).  One CTA per (s, 512-row chunk): the
-// gathered x rows stay in registers while the CTA sweeps all of s's columns
-// (independent loads per column instead of one serial chain per column);
-// per-warp sums go to shared memory, per-chunk partials to `part`, and the
-// last CTA of s sums the chunks in chunk order (run-to-run identical).
+// k < n_nonpos, splitting.cpp:124-132).  One CTA per (s, 512-row chunk,
+// group of 8 columns): the gathered x rows sit in registers, the 16 column
+// loads of a thread are all in flight at once (one memory round trip per CTA),
+// per-warp sums meet in shared memory and per-chunk partials go to `part`; the
+// last CTA of s (of nch[s] x its column groups) sums the chunks in chunk order
+// (run-to-run identical, same order as before the column split).
+constexpr int kBsCols = 8;
 __global__ void __launch_bounds__(256) k_bs_gemvT(const int* __restrict__ gate, const int* __restrict__ task_s,
                                                   const int* __restrict__ task_c, const int* __restrict__ nch,
                                                   int maxch, const int* __restrict__ coff,
@@ -609,49 +611,45 @@ __global__ void __launch_bounds__(256) k_bs_gemvT(const int* __restrict__ gate, 
                                                   const double* __restrict__ w, double* __restrict__ part,
                                                   int* __restrict__ cnt, double* __restrict__ out) {
   if (gated(gate)) return;
-  constexpr int kCols = 64;
-  __shared__ double red[8][kCols];
+  __shared__ double red[8][kBsCols];
   __shared__ bool s_last;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int s = task_s[blockIdx.x], ch = task_c[blockIdx.x];
+  const int q0 = coff[s], nc = coff[s + 1] - q0;
+  const int cb = blockIdx.y * kBsCols;
+  if (cb >= nc) return;  // not counted: the arrival target is nch[s] x ceil(nc / 8)
+  const int ncb = min(kBsCols, nc - cb);
   const int n = ns[s], L = ld[s];
   const int ia = ch * kBsRows + tid, ib = ia + 256;
   const long long p0 = poff[s];
+  const double* Ms = M + moff[s];
+  double va[kBsCols], vb[kBsCols];
+#pragma unroll
+  for (int u = 0; u < kBsCols; ++u) {
+    const bool ok = u < ncb;
+    const int col = ok ? (ccol ? ccol[q0 + cb + u] : cb + u) : 0;
+    const double* m = Ms + (size_t)col * L;
+    va[u] = (ok && ia < n) ? m[ia] : 0.0;
+    vb[u] = (ok && ib < n) ? m[ib] : 0.0;
+  }
   const double xa = ia < n ? __ldg(x + pidx[p0 + ia]) : 0.0;
   const double xb = ib < n ? __ldg(x + pidx[p0 + ib]) : 0.0;
-  const double* Ms = M + moff[s];
-  const int q0 = coff[s], nc = coff[s + 1] - q0;
-  for (int cb = 0; cb < nc; cb += kCols) {
-    const int ncb = min(kCols, nc - cb);
-    // batches of 8 columns: all 16 loads issued before the first reduction
-    for (int c0 = 0; c0 < ncb; c0 += 8) {
-      double va[8], vb[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int c = c0 + u;
-        const bool ok = c < ncb;
-        const int col = ok ? (ccol ? ccol[q0 + cb + c] : cb + c) : 0;
-        const double* m = Ms + (size_t)col * L;
-        va[u] = (ok && ia < n) ? m[ia] : 0.0;
-        vb[u] = (ok && ib < n) ? m[ib] : 0.0;
-      }
+  for (int u = 0; u < kBsCols; ++u) {
+    const double a = warp_sum(fma(vb[u], xb, va[u] * xa));
+    if (lane == 0) red[warp][u] = a;
+  }
+  __syncthreads();
+  if (tid < ncb) {
+    double a = 0.0;
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const double a = warp_sum(fma(vb[u], xb, va[u] * xa));
-        if (lane == 0 && c0 + u < ncb) red[warp][c0 + u] = a;
-      }
-    }
-    __syncthreads();
-    if (tid < ncb) {
-      double a = 0.0;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) a += red[k][tid];
-      part[(size_t)(q0 + cb + tid) * maxch + ch] = a;
-    }
-    __syncthreads();
+    for (int k = 0; k < 8; ++k) a += red[k][tid];
+    part[(size_t)(q0 + cb + tid) * maxch + ch] = a;
   }
   __threadfence();
-  if (tid == 0) s_last = (atomicAdd(cnt + s, 1) == nch[s] - 1);
+  __syncthreads();
+  const int ncg = (nc + kBsCols - 1) / kBsCols;
+  if (tid == 0) s_last = (atomicAdd(cnt + s, 1) == nch[s] * ncg - 1);
   __syncthreads();
   if (!s_last) return;
   __threadfence();
@@ -1178,7 +1176,7 @@ void h1(Ctx& c, const double* x, double* y, const int* gate) {
 static void bs_gemvT(Ctx& c, BsPlan& b, const int* coff, const int* ccol, const double* M, const long long* moff,
                      const double* x, const double* w, double* out, const int* gate) {
   if (b.ntask == 0) return;
-  launch(c, k_bs_gemvT, b.ntask, 256, 0, gate, b.ts.p, b.tc.p, b.nch.p, b.maxch, coff, ccol, M, moff, c.ns.p,
+  launch(c, k_bs_gemvT, dim3(b.ntask, b.ncg), 256, 0, gate, b.ts.p, b.tc.p, b.nch.p, b.maxch, coff, ccol, M, moff, c.ns.p,
                                             c.ld.p, c.poff.p, c.pidx.p, x, w, b.part.p, b.cnt.p, out);
   ++c.launches;
   check_launch("bs_gemvT");
