@@ -426,6 +426,7 @@ int awg_create(awg_ctx** out, int device) {
       return v ? std::atoi(v) : dflt;
     };
     cc.fused_cpb = env_int("AWG_FUSED_CPB", 0);
+    cc.fused_hold = env_int("AWG_FUSED_HOLD", 1) != 0;
     cc.fused_nbuf = env_int("AWG_FUSED_NBUF", 0);
     cc.fused_chunks_per_sm = std::max(1, env_int("AWG_FUSED_CHUNKS", 8));
     cc.fused_reserve = std::max(0, env_int("AWG_FUSED_RESERVE", 0));

@@ -379,7 +379,7 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
       : "memory");
 }
 
-template <bool TRI, int R, int CPB>
+template <bool TRI, int R, int CPB, bool HOLD>
 __global__ void __launch_bounds__(kFusedT, 1) k_nn_fused(const int* __restrict__ gate, const GemvTask* __restrict__ tasks,
                                                          const double* __restrict__ V, const long long* __restrict__ voff,
                                                          const int* __restrict__ ns, const int* __restrict__ ld,
@@ -468,7 +468,11 @@ __global__ void __launch_bounds__(kFusedT, 1) k_nn_fused(const int* __restrict__
       for (int c = 0; c < CPB; ++c) rl[c] = (!TRI && j + c < t.j1) ? __ldg(rlam + p0 + j + c) : 0.0;
       mbar_wait(&bar[gp % nbuf], (gp / nbuf) & 1);
       const double* cb = fsm + (gp % nbuf) * bstride;
-      // dots: two interleaved accumulators per column, fixed order
+      // dots: two interleaved accumulators per column, fixed order.  HOLD: the
+      // column values stay in registers for the update (shared memory is read
+      // once per element instead of twice: the MIO pipe, not HBM, was the
+      // throttle at power-capped SM clocks)
+      double cv[HOLD ? CPB : 1][HOLD ? R : 1];
 #pragma unroll
       for (int c = 0; c < CPB; ++c) {
         const double* col = cb + (size_t)c * L;
@@ -477,6 +481,7 @@ __global__ void __launch_bounds__(kFusedT, 1) k_nn_fused(const int* __restrict__
         for (int k = 0; k < R; ++k) {
           double v = col[tid + k * kFusedT];
           if (TRI) v = (tid + k * kFusedT <= j + c) ? v : 0.0;
+          if (HOLD) cv[HOLD ? c : 0][HOLD ? k : 0] = v;
           if (k & 1)
             a1 = fma(v, xr[k], a1);
           else
@@ -486,8 +491,13 @@ __global__ void __launch_bounds__(kFusedT, 1) k_nn_fused(const int* __restrict__
         if (lane == 0) red[gp & 1][c][warp] = acc;
       }
       __syncthreads();
-      // the previous step's buffer is no longer read by anyone
-      if (tid == 0 && p >= 1 && p - 1 + nbuf < nstep) issue(p - 1 + nbuf);
+      // the previous step's buffer is no longer read by anyone (with HOLD this
+      // step's buffer is already consumed too: refill it now)
+      if (HOLD) {
+        if (tid == 0 && p + nbuf < nstep) issue(p + nbuf);
+      } else {
+        if (tid == 0 && p >= 1 && p - 1 + nbuf < nstep) issue(p - 1 + nbuf);
+      }
       double d[CPB];
 #pragma unroll
       for (int c = 0; c < CPB; ++c) {
@@ -504,8 +514,13 @@ __global__ void __launch_bounds__(kFusedT, 1) k_nn_fused(const int* __restrict__
         const double* col = cb + (size_t)c * L;
 #pragma unroll
         for (int k = 0; k < R; ++k) {
-          double v = col[tid + k * kFusedT];
-          if (TRI) v = (tid + k * kFusedT <= j + c) ? v : 0.0;
+          double v;
+          if (HOLD) {
+            v = cv[HOLD ? c : 0][HOLD ? k : 0];
+          } else {
+            v = col[tid + k * kFusedT];
+            if (TRI) v = (tid + k * kFusedT <= j + c) ? v : 0.0;
+          }
           yr[k] = fma(v, d[c], yr[k]);
         }
       }
@@ -1086,30 +1101,30 @@ void nn_prolong(Ctx& c, double* y, const int* gate) {
 }
 
 // single-pass NN local solve into the split-K partials (see k_nn_fused)
-template <bool TRI, int R, int CPB>
+template <bool TRI, int R, int CPB, bool HOLD>
 void launch_fused(Ctx& c, const LocalPlan& pl, const double* F, const double* D, const double* x, const int* gate,
                   int grid, size_t smem, int nbuf, int ldmax) {
   static bool configured = false;
   if (!configured) {
-    AWG_CUDA(cudaFuncSetAttribute(k_nn_fused<TRI, R, CPB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    AWG_CUDA(cudaFuncSetAttribute(k_nn_fused<TRI, R, CPB, HOLD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(kFusedSmemCap)));
     configured = true;
   }
-  launch(c, k_nn_fused<TRI, R, CPB>, grid, kFusedT, smem, gate, pl.tf.p, F, c.voff.p, c.ns.p, c.ld.p, c.poff.p,
+  launch(c, k_nn_fused<TRI, R, CPB, HOLD>, grid, kFusedT, smem, gate, pl.tf.p, F, c.voff.p, c.ns.p, c.ld.p, c.poff.p,
          c.pidx.p, D, x, TRI ? nullptr : c.rlam.p, c.P, c.wpart_nn.p, int(pl.tf.n), c.fused_queue.p, nbuf, ldmax,
          int(smem / sizeof(double)), c.fused_timer.p);
 }
 
-template <bool TRI, int CPB>
+template <bool TRI, int CPB, bool HOLD>
 void launch_fused_r(Ctx& c, const LocalPlan& pl, const double* F, const double* D, const double* x, const int* gate,
                     int grid, size_t smem, int nbuf, int ldmax, int R) {
   switch (R) {
-    case 2: launch_fused<TRI, 2, CPB>(c, pl, F, D, x, gate, grid, smem, nbuf, ldmax); break;
-    case 4: launch_fused<TRI, 4, CPB>(c, pl, F, D, x, gate, grid, smem, nbuf, ldmax); break;
-    case 8: launch_fused<TRI, 8, CPB>(c, pl, F, D, x, gate, grid, smem, nbuf, ldmax); break;
-    case 10: launch_fused<TRI, 10, CPB>(c, pl, F, D, x, gate, grid, smem, nbuf, ldmax); break;
-    case 11: launch_fused<TRI, 11, CPB>(c, pl, F, D, x, gate, grid, smem, nbuf, ldmax); break;
-    default: launch_fused<TRI, 12, CPB>(c, pl, F, D, x, gate, grid, smem, nbuf, ldmax); break;
+    case 2: launch_fused<TRI, 2, CPB, HOLD>(c, pl, F, D, x, gate, grid, smem, nbuf, ldmax); break;
+    case 4: launch_fused<TRI, 4, CPB, HOLD>(c, pl, F, D, x, gate, grid, smem, nbuf, ldmax); break;
+    case 8: launch_fused<TRI, 8, CPB, HOLD>(c, pl, F, D, x, gate, grid, smem, nbuf, ldmax); break;
+    case 10: launch_fused<TRI, 10, CPB, HOLD>(c, pl, F, D, x, gate, grid, smem, nbuf, ldmax); break;
+    case 11: launch_fused<TRI, 11, CPB, HOLD>(c, pl, F, D, x, gate, grid, smem, nbuf, ldmax); break;
+    default: launch_fused<TRI, 12, CPB, HOLD>(c, pl, F, D, x, gate, grid, smem, nbuf, ldmax); break;
   }
 }
 
@@ -1126,7 +1141,12 @@ void nn_fused(Ctx& c, const double* x, const int* gate) {
   // (measured, profiles/README.md: two-column steps win while >= 3 two-column
   // buffers fit — c2, ld 4612 — and lose to 4 one-column buffers at ld 5632, c5)
   const size_t tail = size_t(std::max(0, R * kFusedT - ldmax)) * sizeof(double);
-  int cpb = (kFusedSmemCap - tail) / (size_t(2) * ldmax * sizeof(double)) >= 3 ? 2 : 1;
+  // with HOLD a buffer is refilled one step earlier, so two 2-column buffers
+  // keep the copy engine busy (profiles/r01b/sweep_hold.json: c5 6.86 ms with
+  // 2 x 2 columns vs 6.93 ms with 4 x 1)
+  const bool hold = c.fused_hold && nn;  // NN only (the triangular AS variant spills with it at R = 12)
+  const size_t need_bufs = hold ? 2 : 3;
+  int cpb = (kFusedSmemCap - tail) / (size_t(2) * ldmax * sizeof(double)) >= need_bufs ? 2 : 1;
   if (c.fused_cpb == 1 || c.fused_cpb == 2) cpb = c.fused_cpb;
   const size_t buf_bytes = size_t(cpb) * ldmax * sizeof(double);
   int nbuf = int(std::min<size_t>(kFusedMaxBuf, (kFusedSmemCap - tail) / buf_bytes));
@@ -1148,13 +1168,17 @@ void nn_fused(Ctx& c, const double* x, const int* gate) {
   const double* F = nn ? c.V.p : c.U.p;
   const double* D = nn ? c.ds.p : nullptr;
   if (nn && cpb == 2)
-    launch_fused_r<false, 2>(c, pl, F, D, x, gate, grid, smem, nbuf, ldmax, R);
+    hold ? launch_fused_r<false, 2, true>(c, pl, F, D, x, gate, grid, smem, nbuf, ldmax, R)
+         : launch_fused_r<false, 2, false>(c, pl, F, D, x, gate, grid, smem, nbuf, ldmax, R);
   else if (nn)
-    launch_fused_r<false, 1>(c, pl, F, D, x, gate, grid, smem, nbuf, ldmax, R);
+    hold ? launch_fused_r<false, 1, true>(c, pl, F, D, x, gate, grid, smem, nbuf, ldmax, R)
+         : launch_fused_r<false, 1, false>(c, pl, F, D, x, gate, grid, smem, nbuf, ldmax, R);
   else if (cpb == 2)
-    launch_fused_r<true, 2>(c, pl, F, D, x, gate, grid, smem, nbuf, ldmax, R);
+    hold ? launch_fused_r<true, 2, true>(c, pl, F, D, x, gate, grid, smem, nbuf, ldmax, R)
+         : launch_fused_r<true, 2, false>(c, pl, F, D, x, gate, grid, smem, nbuf, ldmax, R);
   else
-    launch_fused_r<true, 1>(c, pl, F, D, x, gate, grid, smem, nbuf, ldmax, R);
+    hold ? launch_fused_r<true, 1, true>(c, pl, F, D, x, gate, grid, smem, nbuf, ldmax, R)
+         : launch_fused_r<true, 1, false>(c, pl, F, D, x, gate, grid, smem, nbuf, ldmax, R);
   ++c.launches;
   check_launch("nn_fused");
 }

@@ -19,6 +19,10 @@ for cfg in sys.argv[1:] or ["c2"]:
             settings.append((f"min{mincols}_chunks{chunks}_tail{tail}",
                              {"AWG_FUSED_MINCOLS": str(mincols), "AWG_FUSED_CHUNKS": str(chunks),
                               "AWG_FUSED_TAIL": str(tail)}))
+    elif mode == "hold":  # column values held in registers across the reduction (AWG_FUSED_HOLD)
+        for hold, cpb, nbuf in itertools.product([0, 1], [1, 2], [3, 4, 6]):
+            settings.append((f"hold{hold}_cpb{cpb}_nbuf{nbuf}",
+                             {"AWG_FUSED_HOLD": str(hold), "AWG_FUSED_CPB": str(cpb), "AWG_FUSED_NBUF": str(nbuf)}))
     else:
         for cpb, nbuf, chunks in itertools.product([1, 2], [2, 3, 4], [4, 8, 16]):
             settings.append((f"cpb{cpb}_nbuf{nbuf}_chunks{chunks}",
@@ -26,7 +30,7 @@ for cfg in sys.argv[1:] or ["c2"]:
                               "AWG_FUSED_CHUNKS": str(chunks)}))
     for name, env in settings:
         for k in ("AWG_NN_TWO_PASS", "AWG_FUSED_CPB", "AWG_FUSED_NBUF", "AWG_FUSED_CHUNKS", "AWG_FUSED_MINCOLS",
-                  "AWG_FUSED_TAIL"):
+                  "AWG_FUSED_TAIL", "AWG_FUSED_HOLD"):
             os.environ.pop(k, None)
         os.environ.update(env)
         try:
