@@ -498,14 +498,16 @@ __global__ void __launch_bounds__(kFusedT, 1) k_nn_fused(const int* __restrict__
       } else {
         if (tid == 0 && p >= 1 && p - 1 + nbuf < nstep) issue(p - 1 + nbuf);
       }
+      // the 16 warp partials: lane l reads partial l & 15 (one shared load per
+      // warp instead of 16 broadcast loads per thread), then an xor butterfly
+      // over 16 lanes — the fixed tree ((r0+r8)+(r4+r12)) + ((r2+r10)+(r6+r14))
+      // + ..., identical in every lane and run
       double d[CPB];
 #pragma unroll
       for (int c = 0; c < CPB; ++c) {
-        const double* r = red[gp & 1][c];
-        double r8[8];
+        double a = red[gp & 1][c][lane & 15];
 #pragma unroll
-        for (int w = 0; w < 8; ++w) r8[w] = r[w] + r[w + 8];
-        const double a = ((r8[0] + r8[4]) + (r8[2] + r8[6])) + ((r8[1] + r8[5]) + (r8[3] + r8[7]));
+        for (int o = 8; o >= 1; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
         const bool live = (j + c < t.j1);
         d[c] = live ? (TRI ? a : a * rl[c]) : 0.0;
       }
@@ -1137,19 +1139,28 @@ void nn_fused(Ctx& c, const double* x, const int* gate) {
   const int need = (ldmax + kFusedT - 1) / kFusedT;
   const int R = need <= 2 ? 2 : need <= 4 ? 4 : need <= 8 ? 8 : need <= 10 ? 10 : need <= 11 ? 11 : 12;
   // copy pipeline: CPB columns per buffer, as many buffers as fit (<= kFusedMaxBuf),
-  // plus the tail that unchecked rows of the last buffer may reach
-  // (measured, profiles/README.md: two-column steps win while >= 3 two-column
-  // buffers fit — c2, ld 4612 — and lose to 4 one-column buffers at ld 5632, c5)
+  // plus the tail that unchecked rows of the last buffer may reach.  Without
+  // HOLD (profiles/README.md): two-column steps win while >= 3 two-column
+  // buffers fit (c2, ld 4612) and lose to 4 one-column buffers at ld 5632 (c5).
+  // With HOLD a buffer is refilled one step earlier (see below).
   const size_t tail = size_t(std::max(0, R * kFusedT - ldmax)) * sizeof(double);
-  // with HOLD a buffer is refilled one step earlier, so two 2-column buffers
-  // keep the copy engine busy (profiles/r01b/sweep_hold.json: c5 6.86 ms with
-  // 2 x 2 columns vs 6.93 ms with 4 x 1)
   const bool hold = c.fused_hold && nn;  // NN only (the triangular AS variant spills with it at R = 12)
-  const size_t need_bufs = hold ? 2 : 3;
-  int cpb = (kFusedSmemCap - tail) / (size_t(2) * ldmax * sizeof(double)) >= need_bufs ? 2 : 1;
+  const size_t fit1 = (kFusedSmemCap - tail) / (size_t(ldmax) * sizeof(double));  // one-column buffers that fit
+  int cpb;
+  int nbuf_pref = 0;
+  if (hold) {
+    // measured (profiles/r01b/sweep_hold2.json): c2 (6 one-column buffers fit)
+    // 0.381 ms with 3 x 1 column vs 0.384 with 3 x 2; c5 (5 fit) 6.81 ms with
+    // 2 x 2 columns vs 6.90 with 3 x 1
+    cpb = fit1 >= 6 ? 1 : 2;
+    nbuf_pref = cpb == 1 ? 3 : 0;
+  } else {
+    cpb = fit1 / 2 >= 3 ? 2 : 1;
+  }
   if (c.fused_cpb == 1 || c.fused_cpb == 2) cpb = c.fused_cpb;
   const size_t buf_bytes = size_t(cpb) * ldmax * sizeof(double);
   int nbuf = int(std::min<size_t>(kFusedMaxBuf, (kFusedSmemCap - tail) / buf_bytes));
+  if (nbuf_pref > 0) nbuf = std::min(nbuf, nbuf_pref);
   if (c.fused_nbuf > 0) nbuf = std::min(nbuf, c.fused_nbuf);
   if (nbuf < 2) c.fail(AWG_E_STATE, "single-pass local solve: subdomain too large for the copy pipeline");
   const size_t smem = size_t(nbuf) * buf_bytes + tail;
