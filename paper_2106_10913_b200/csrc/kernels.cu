@@ -30,6 +30,17 @@ __device__ __forceinline__ bool gated(const int* gate) {
   return gate != nullptr && *gate != 0;
 }
 
+// The short coarse-chain kernels (Z^T x / A- dots, K+ GEMV, Z c prolongation)
+// release their dependents at entry: the successor grid is scheduled while
+// this one runs and still waits in pdl_wait() for its completion and memory
+// flush, so only the launch latency overlaps (AWG_PDL_EARLY=0 disables).
+// Not used by the single-pass kernel or its neighbours: waiting successor CTAs
+// next to the persistent local solve cost more than they hide.
+__device__ __forceinline__ bool gated_early(const int* gate, int early) {
+  if (early) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  return gated(gate);
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -147,8 +158,8 @@ struct Combine {
 
 template <int G>
 __global__ void k_prolong_sum(const int* __restrict__ gate, int n, BlockSum bs, double* __restrict__ y,
-                              Combine cb) {
-  if (gated(gate)) return;
+                              Combine cb, int early) {
+  if (gated_early(gate, early)) return;
   const int t = threadIdx.x & (G - 1);
   const int stride = int((gridDim.x * (long long)blockDim.x) / G);
   double rz = 0.0;
@@ -626,8 +637,8 @@ __global__ void __launch_bounds__(256) k_bs_gemvT(const int* __restrict__ gate, 
                                                   const int* __restrict__ ld, const long long* __restrict__ poff,
                                                   const int* __restrict__ pidx, const double* __restrict__ x,
                                                   const double* __restrict__ w, double* __restrict__ part,
-                                                  int* __restrict__ cnt, double* __restrict__ out) {
-  if (gated(gate)) return;
+                                                  int* __restrict__ cnt, double* __restrict__ out, int early) {
+  if (gated_early(gate, early)) return;
   __shared__ double red[8][kBsCols];
   __shared__ bool s_last;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -696,8 +707,8 @@ __global__ void __launch_bounds__(256) k_bs_gemvT(const int* __restrict__ gate, 
 // of K^+ (coalesced) against the gathered b_r (L1/L2 resident).
 __global__ void k_coarse_solve(const int* __restrict__ gate, int dim, int r, const double* __restrict__ kinv,
                                const int* __restrict__ pos, const int* __restrict__ ret,
-                               const double* __restrict__ b, double* __restrict__ x) {
-  if (gated(gate)) return;
+                               const double* __restrict__ b, double* __restrict__ x, int early) {
+  if (gated_early(gate, early)) return;
   // b_r = b[retained] staged once per CTA (kCoarseStage doubles of static
   // shared memory) instead of two dependent loads per element in every warp
   __shared__ double sb[kCoarseStage];
@@ -1212,7 +1223,7 @@ static void bs_gemvT(Ctx& c, BsPlan& b, const int* coff, const int* ccol, const 
                      const double* x, const double* w, double* out, const int* gate) {
   if (b.ntask == 0) return;
   launch(c, k_bs_gemvT, dim3(b.ntask, b.ncg), 256, 0, gate, b.ts.p, b.tc.p, b.nch.p, b.maxch, coff, ccol, M, moff, c.ns.p,
-                                            c.ld.p, c.poff.p, c.pidx.p, x, w, b.part.p, b.cnt.p, out);
+                                            c.ld.p, c.poff.p, c.pidx.p, x, w, b.part.p, b.cnt.p, out, c.pdl_early);
   ++c.launches;
   check_launch("bs_gemvT");
 }
@@ -1221,7 +1232,11 @@ static void neg_dot(Ctx& c, const double* x, const int* gate) {
   bs_gemvT(c, c.bs_neg, c.negoff.p, c.neg_k.p, c.V.p, c.voff.p, x, c.neg_w.p, c.neg_c.p, gate);
 }
 
-static int rows_group(const Ctx& c) { return c.n <= 300000 ? 4 : 1; }
+// lanes per dof of the block-sparse prolongations (AWG_ROWS_GROUP overrides: 1, 4 or 8)
+static int rows_group(const Ctx& c) {
+  if (c.rows_group == 1 || c.rows_group == 4 || c.rows_group == 8) return c.rows_group;
+  return c.n <= 300000 ? 4 : 1;
+}
 
 void aminus(Ctx& c, const double* x, double* y, const int* gate) {
   if (c.nneg == 0) {
@@ -1247,7 +1262,10 @@ static BlockSum neg_sum(const Ctx& c) {
 void aplus(Ctx& c, const double* x, double* y, int mode, const double* sub, const int* gate) {
   if (c.nneg > 0) neg_dot(c, x, gate);
   BlockSum bs = neg_sum(c);
-  if (rows_group(c) == 4)
+  if (rows_group(c) == 8)
+    launch(c, k_spmv_aplus<8>, grid_for(c, 8LL * c.n), kThreads, 0, gate, c.n, c.rp.p, c.ci.p, c.va.p, x, y, mode,
+           sub, bs);
+  else if (rows_group(c) == 4)
     launch(c, k_spmv_aplus<4>, grid_for(c, 4LL * c.n), kThreads, 0, gate, c.n, c.rp.p, c.ci.p, c.va.p, x, y, mode,
                                                                        sub, bs);
   else
@@ -1265,7 +1283,7 @@ void rr_solve(Ctx& c, const CoarseFactor& f, const double* b, double* x, const i
     return;
   }
   launch(c, k_coarse_solve, (f.dim + wpb - 1) / wpb, kThreads, 0, gate, f.dim, f.rank, f.kinv.p, f.pos.p,
-                                                                     f.retained.p, b, x);
+                                                                     f.retained.p, b, x, c.pdl_early);
   ++c.launches;
   check_launch("coarse_solve");
 }
@@ -1293,10 +1311,12 @@ void coarse_q_combine(Ctx& c, const double* x, double* y, const double* a, const
     cb.rz = c.rz_fuse;
     c.rz_fused = true;
   }
-  if (rows_group(c) == 4)
-    launch(c, k_prolong_sum<4>, grid_for(c, 4LL * c.n), kThreads, 0, gate, c.n, bs, y, cb);
+  if (rows_group(c) == 8)
+    launch(c, k_prolong_sum<8>, grid_for(c, 8LL * c.n), kThreads, 0, gate, c.n, bs, y, cb, c.pdl_early);
+  else if (rows_group(c) == 4)
+    launch(c, k_prolong_sum<4>, grid_for(c, 4LL * c.n), kThreads, 0, gate, c.n, bs, y, cb, c.pdl_early);
   else
-    launch(c, k_prolong_sum<1>, grid_for(c, c.n), kThreads, 0, gate, c.n, bs, y, cb);
+    launch(c, k_prolong_sum<1>, grid_for(c, c.n), kThreads, 0, gate, c.n, bs, y, cb, c.pdl_early);
   ++c.launches;
   check_launch("z_prolong");
 }

@@ -1,0 +1,35 @@
+"""Per-iteration device time of the c2 solve (op_times-style) under knob
+settings given as NAME=VALUE[,NAME=VALUE] arguments, one fresh context each.
+    python profiles/knob_sweep.py c2 "AWG_PDL_EARLY=0" "AWG_PDL_EARLY=1,AWG_ROWS_GROUP=8" ..."""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2106_10913_b200 import awg, problems  # noqa: E402
+
+cfg = sys.argv[1]
+p = problems.make(cfg)
+out = []
+for spec in sys.argv[2:]:
+    env = dict(kv.split("=") for kv in spec.split(",") if kv)
+    saved = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        ctx = awg.context_from_problem(p)
+        ctx.setup(awg.config_for(p))
+        best = 1e9
+        for _ in range(3):
+            x, rep = ctx.pcg(p.b, p.rtol, 10000)
+            best = min(best, rep.solve_ms / max(rep.iterations, 1))
+        out.append({"knobs": spec, "iterations": rep.iterations, "ms_per_iteration": best,
+                    "H3_ms": ctx.time_apply(awg.Op.H3, reps=20), "Q_ms": ctx.time_apply(awg.Op.Q, reps=20),
+                    "APLUS_ms": ctx.time_apply(awg.Op.APLUS, reps=20)})
+        ctx.close()
+    finally:
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+print(json.dumps({"config": cfg, "results": out}))

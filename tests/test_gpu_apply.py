@@ -185,3 +185,19 @@ def test_grouped_dgemm_matches_cublas(shape, ta):
     r = ctx.bench_dgemm(m, n, k, cnt, reps=1, transpose_a=ta)
     assert r["rel_err"] <= 1e-13, r
     assert r["ms_grouped"] > 0.0
+
+
+def test_single_pass_register_hold_is_bit_identical():
+    """The single-pass kernel's register-held variant (default) and the
+    re-read-from-shared-memory variant (AWG_FUSED_HOLD=0) perform the same
+    operations in the same order: H1 must agree bit for bit."""
+    g, s = golden_with_base("t2d")
+    ctx1 = make_ctx(g)
+    os.environ["AWG_FUSED_HOLD"] = "0"
+    try:
+        ctx2 = make_ctx(g)
+    finally:
+        del os.environ["AWG_FUSED_HOLD"]
+    for x in g["x_apply"]:
+        y1, y2 = ctx1.apply(awg.Op.H1, x), ctx2.apply(awg.Op.H1, x)
+        assert np.array_equal(y1, y2)
