@@ -428,7 +428,7 @@ int awg_create(awg_ctx** out, int device) {
     cc.fused_cpb = env_int("AWG_FUSED_CPB", 0);
     cc.fused_hold = env_int("AWG_FUSED_HOLD", 1) != 0;
     cc.rows_group = env_int("AWG_ROWS_GROUP", 0);
-    cc.pdl_early = env_int("AWG_PDL_EARLY", 1) != 0 ? 1 : 0;
+    cc.pdl_early = env_int("AWG_PDL_EARLY", 0) != 0 ? 1 : 0;
     cc.fused_nbuf = env_int("AWG_FUSED_NBUF", 0);
     cc.fused_chunks_per_sm = std::max(1, env_int("AWG_FUSED_CHUNKS", 8));
     cc.fused_reserve = std::max(0, env_int("AWG_FUSED_RESERVE", 0));

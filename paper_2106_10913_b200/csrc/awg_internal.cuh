@@ -286,7 +286,7 @@ struct Ctx {
   int fused_reserve = 0;
   int fused_min_cols = 128, fused_tail_pct = 0;  // single-pass task sizes (columns), guided tail share  // SMs the single-pass kernel leaves free (for the concurrent W branch)
   int fused_cpb = 0, fused_nbuf = 0, fused_chunks_per_sm = 8;  // 0: automatic
-  int pdl_early = 1;        // coarse-chain kernels release their dependents at entry (AWG_PDL_EARLY)
+  int pdl_early = 0;        // coarse-chain kernels release their dependents at entry (AWG_PDL_EARLY=1; measured neutral)
   int rows_group = 0;       // lanes per dof of the block-sparse prolongations (0: automatic)
   bool fused_hold = true;  // column values kept in registers across the step's reduction (AWG_FUSED_HOLD=0 off)
   BsPlan bs_neg, bs_z;   // A- dots (V^s columns k < n_nonpos), Z^T x (Y_s blocks)

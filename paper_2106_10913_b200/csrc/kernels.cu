@@ -33,7 +33,9 @@ __device__ __forceinline__ bool gated(const int* gate) {
 // The short coarse-chain kernels (Z^T x / A- dots, K+ GEMV, Z c prolongation)
 // release their dependents at entry: the successor grid is scheduled while
 // this one runs and still waits in pdl_wait() for its completion and memory
-// flush, so only the launch latency overlaps (AWG_PDL_EARLY=0 disables).
+// flush, so only the launch latency overlaps.  Off by default (AWG_PDL_EARLY=1):
+// measured neutral on c2 (profiles/r01c/knobs_c2.json, 0.511 vs 0.509-0.513 ms
+// per iteration), and the isolated Q / H3 applies slower by 1-2 us.
 // Not used by the single-pass kernel or its neighbours: waiting successor CTAs
 // next to the persistent local solve cost more than they hide.
 __device__ __forceinline__ bool gated_early(const int* gate, int early) {
