@@ -370,6 +370,27 @@ struct Ctx {
 // launch gap alone (+2.4% over no PDL).
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// CSR row product  sum_k va[k] x[ci[k]]  in ascending k with separately
+// rounded multiply and add — bit-identical to the reference build of
+// sparse.cpp:49-56 (GCC emits vmulsd + vaddsd there).  The row's loads are
+// issued in groups of 8 ahead of the dependent add chain (the plain loop
+// stalls on every add before it can issue the next load).  P(j) supplies the
+// vector entry (x[j], or p formed on the fly).
+template <class P>
+__device__ __forceinline__ double csr_row(const int* __restrict__ ci, const double* __restrict__ va, int k0, int k1,
+                                          P xv) {
+  double acc = 0.0;
+  for (int k = k0; k < k1; k += 8) {
+    double t[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) t[u] = (k + u < k1) ? __dmul_rn(va[k + u], xv(ci[k + u])) : 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (k + u < k1) acc = __dadd_rn(acc, t[u]);
+  }
+  return acc;
+}
+
 template <typename... P, typename... A>
 inline void launch(Ctx& c, void (*kern)(P...), dim3 grid, dim3 block, size_t smem, A&&... args) {
   cudaLaunchConfig_t cfg = {};

@@ -72,7 +72,7 @@ __global__ void k_spmv(const int* __restrict__ gate, int n, const int* __restric
     double acc = 0.0;
     // mul then add, not contracted: GCC emits vmulsd + vaddsd for this loop in
     // the reference build (sparse.cpp:53), so the result is bit-identical.
-    for (int k = k0; k < k1; ++k) acc = __dadd_rn(acc, __dmul_rn(va[k], __ldg(x + ci[k])));
+    acc = csr_row(ci, va, k0, k1, [&](int j) { return __ldg(x + j); });
     double out;
     if (mode == 0) out = acc;
     else if (mode == 1) out = add[i] + acc;
@@ -138,7 +138,7 @@ __global__ void k_spmv_aplus(const int* __restrict__ gate, int n, const int* __r
     const double m = am.at<G>(i, t, active);
     if (active && t == 0) {
       double acc = 0.0;
-      for (int k = rp[i]; k < rp[i + 1]; ++k) acc = __dadd_rn(acc, __dmul_rn(va[k], __ldg(x + ci[k])));
+      acc = csr_row(ci, va, rp[i], rp[i + 1], [&](int j) { return __ldg(x + j); });
       const double a = m + acc;
       y[i] = (mode == 1) ? a : sub[i] - a;
     }

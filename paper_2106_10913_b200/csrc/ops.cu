@@ -71,7 +71,7 @@ __global__ void k_pcg_spmv_dot(PcgState* st, int n, const int* __restrict__ rp, 
   double acc = 0.0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     double s = 0.0;
-    for (int k = rp[i]; k < rp[i + 1]; ++k) s = __dadd_rn(s, __dmul_rn(va[k], __ldg(p + ci[k])));
+    s = csr_row(ci, va, rp[i], rp[i + 1], [&](int j) { return __ldg(p + j); });
     if (add) s = add[i] + s;
     q[i] = s;
     acc = fma(p[i], s, acc);
@@ -102,10 +102,7 @@ __global__ void k_pcg_spmv_dot_p(PcgState* st, int n, const int* __restrict__ rp
   double acc = 0.0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     double s = 0.0;
-    for (int k = rp[i]; k < rp[i + 1]; ++k) {
-      const int j = ci[k];
-      s = __dadd_rn(s, __dmul_rn(va[k], fma(beta, __ldg(pold + j), __ldg(z + j))));
-    }
+    s = csr_row(ci, va, rp[i], rp[i + 1], [&](int j) { return fma(beta, __ldg(pold + j), __ldg(z + j)); });
     const double pi = fma(beta, pold[i], z[i]);
     pnew[i] = pi;
     q[i] = s;
@@ -161,7 +158,7 @@ __global__ void k_pcg_true(PcgState* st, int n, const int* __restrict__ rp, cons
   double acc = 0.0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     double s = 0.0;
-    for (int k = rp[i]; k < rp[i + 1]; ++k) s = __dadd_rn(s, __dmul_rn(va[k], __ldg(x + ci[k])));
+    s = csr_row(ci, va, rp[i], rp[i + 1], [&](int j) { return __ldg(x + j); });
     if (add) s = add[i] + s;
     const double d = b[i] - s;
     acc = fma(d, d, acc);

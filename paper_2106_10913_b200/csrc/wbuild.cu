@@ -57,7 +57,7 @@ __global__ void kb_spmv(int n, int ld, const int* __restrict__ rp, const int* __
   const size_t o = (size_t)b * ld;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     double acc = 0.0;
-    for (int k = rp[i]; k < rp[i + 1]; ++k) acc = __dadd_rn(acc, __dmul_rn(va[k], __ldg(X + o + ci[k])));
+    acc = csr_row(ci, va, rp[i], rp[i + 1], [&](int j) { return __ldg(X + o + j); });
     double out;
     if (mode == 0) out = acc;
     else if (mode == 1) out = add[o + i] + acc;

@@ -149,3 +149,24 @@ def test_wide_coarse_blocks():
         x = rng.uniform(-1, 1, n)
         assert rel(ctx.apply(awg.Op.Q, x), orc.coarse_correct(x)) <= 1e-11
         assert rel(ctx.apply(awg.Op.AMINUS, x), orc.apply_Aminus(x)) <= 1e-11
+
+
+@pytest.mark.parametrize("case", ["t3d", "telas8"])
+def test_wbuild_grouped_dgemm_matches_cublas_path(case):
+    """The W build's block one-level on the hand-written grouped FP64
+    tensor-core GEMM (default) against the per-subdomain cuBLAS DGEMM path
+    (AWG_WBUILD_GEMM=cublas): same inner iteration counts (+-1) and the same W
+    up to the inner solves' tolerance."""
+    import os
+
+    g, s = golden_with_base(case)
+    ctx1 = setup_ctx(g, s)
+    os.environ["AWG_WBUILD_GEMM"] = "cublas"
+    try:
+        ctx2 = setup_ctx(g, s)
+    finally:
+        del os.environ["AWG_WBUILD_GEMM"]
+    i1, i2 = ctx1.get("w_inner_iterations"), ctx2.get("w_inner_iterations")
+    assert np.max(np.abs(i1.astype(int) - i2.astype(int))) <= 1
+    w1, w2 = ctx1.get("W"), ctx2.get("W")
+    assert rel(w1, w2) <= 1e-8
