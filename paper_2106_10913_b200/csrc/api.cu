@@ -418,6 +418,7 @@ int awg_create(awg_ctx** out, int device) {
                                           cc.use_priority ? (side_first ? hi : lo) : 0));
     AWG_CUDA(cudaEventCreateWithFlags(&cc.ev_fork, cudaEventDisableTiming));
     AWG_CUDA(cudaEventCreateWithFlags(&cc.ev_join, cudaEventDisableTiming));
+    AWG_CUDA(cudaEventCreateWithFlags(&cc.ev_mid, cudaEventDisableTiming));
     AWG_CUDA(cudaDeviceGetAttribute(&cc.sm_count, cudaDevAttrMultiProcessorCount, device));
     const char* two_pass = std::getenv("AWG_NN_TWO_PASS");
     cc.use_fused = !(two_pass && two_pass[0] == '1');
@@ -429,6 +430,7 @@ int awg_create(awg_ctx** out, int device) {
     cc.fused_hold = env_int("AWG_FUSED_HOLD", 1) != 0;
     cc.rows_group = env_int("AWG_ROWS_GROUP", 0);
     cc.pdl_early = env_int("AWG_PDL_EARLY", 0) != 0 ? 1 : 0;
+    cc.w_split = env_int("AWG_W_SPLIT", -1);
     cc.fused_nbuf = env_int("AWG_FUSED_NBUF", 0);
     cc.fused_chunks_per_sm = std::max(1, env_int("AWG_FUSED_CHUNKS", 8));
     cc.fused_reserve = std::max(0, env_int("AWG_FUSED_RESERVE", 0));
@@ -446,12 +448,13 @@ void awg_destroy(awg_ctx* ctx) {
     if (ctx->c.stream) cudaStreamSynchronize(ctx->c.stream);
   }
   cudaStream_t s = ctx->c.stream, side = ctx->c.side;
-  cudaEvent_t e0 = ctx->c.ev_fork, e1 = ctx->c.ev_join;
+  cudaEvent_t e0 = ctx->c.ev_fork, e1 = ctx->c.ev_join, e2 = ctx->c.ev_mid;
   delete ctx;
   if (s) cudaStreamDestroy(s);
   if (side) cudaStreamDestroy(side);
   if (e0) cudaEventDestroy(e0);
   if (e1) cudaEventDestroy(e1);
+  if (e2) cudaEventDestroy(e2);
 }
 
 const char* awg_last_error(const awg_ctx* ctx) { return ctx ? ctx->c.err.c_str() : "null context"; }

@@ -224,6 +224,8 @@ void coarse_q(Ctx& c, const double* x, double* y, const int* gate);   // y = Z K
 void coarse_q_combine(Ctx& c, const double* x, double* y, const double* a, const double* d, const double* e,
                       cudaEvent_t wait_before_combine, const int* gate);
 void second_q(Ctx& c, const double* x, double* y, const int* gate);   // y = W KW+ W^T x
+void second_q_coef(Ctx& c, const double* x, const int* gate);         // c.cw second half = KW+ W^T x
+void second_q_apply(Ctx& c, double* y, const int* gate);              // y = W (c.cw second half)
 void inex_q(Ctx& c, const double* x, double* y, const int* gate);     // y = W core^-1 W^T x
 void axpby(Ctx& c, int n, const double* a, const double* b, const double* d, double* y, int mode, const int* gate);
 void rr_solve(Ctx& c, const CoarseFactor& f, const double* b, double* x, const int* gate);
@@ -242,6 +244,8 @@ struct Ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;  // concurrent branch (second coarse correction of H3,ad)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_mid = nullptr;  // main stream past the local solve (split W branch)
+  int w_split = -1;              // AD W branch split around the local solve: -1 automatic, 0 off, 1 on
   std::string err;
   int err_index = -1;
   long long launches = 0;

@@ -1374,12 +1374,16 @@ void second_q(Ctx& c, const double* x, double* y, const int* gate) {
     ++c.launches;
     return;
   }
-  double* wx = c.cw.p;
-  double* coef = c.cw.p + c.nm;
-  w_transpose_apply(c, x, wx, gate);
-  rr_solve(c, c.kw, wx, coef, gate);
-  w_apply(c, coef, y, gate);
+  second_q_coef(c, x, gate);
+  second_q_apply(c, y, gate);
 }
+
+void second_q_coef(Ctx& c, const double* x, const int* gate) {
+  w_transpose_apply(c, x, c.cw.p, gate);
+  rr_solve(c, c.kw, c.cw.p, c.cw.p + c.nm, gate);
+}
+
+void second_q_apply(Ctx& c, double* y, const int* gate) { w_apply(c, c.cw.p + c.nm, y, gate); }
 
 void inex_q(Ctx& c, const double* x, double* y, const int* gate) {
   double* wx = c.cw.p;

@@ -9,6 +9,7 @@
 //                          stopping rule (:93-102), breakdown handling (:79-82, :107-110)
 //                          and the Lanczos coefficients (:90-91)
 #include <cmath>
+#include <functional>
 #include <cstring>
 
 #include "awg_internal.cuh"
@@ -267,7 +268,7 @@ static void aplus(Ctx& c, const double* x, double* y, const int* gate) { k::aplu
 // `extra_ready` has fired) the hybrid composition's last kernel also adds it:
 // y = ((hp - Q A+ hp) + corr) + extra, the reference's two sums in order.
 static void h2(Ctx& c, const double* x, double* y, const int* gate, const double* extra = nullptr,
-               cudaEvent_t extra_ready = nullptr) {
+               cudaEvent_t extra_ready = nullptr, const std::function<void()>& after_h1 = {}) {
   auto add_extra = [&](const double* h2y) {
     if (extra_ready) AWG_CUDA(cudaStreamWaitEvent(c.stream, extra_ready, 0));
     k::axpby(c, c.n, h2y, extra, nullptr, y, 1, gate);
@@ -286,6 +287,7 @@ static void h2(Ctx& c, const double* x, double* y, const int* gate, const double
   }
   k::aplus(c, c.t0.p, c.t2.p, 2, x, gate);         // pt = x - A+ corr
   h1(c, c.t2.p, c.t3.p, gate);                     // hp
+  if (after_h1) after_h1();  // enqueues work that must follow the local solve
   aplus(c, c.t3.p, c.t4.p, gate);                  // A+ hp
   // (hp - Q A+ hp) + corr [+ extra], fused into the Z c prolongation
   k::coarse_q_combine(c, c.t4.p, y, c.t3.p, c.t0.p, extra, extra_ready, gate);
@@ -340,14 +342,35 @@ void op_apply(Ctx& c, int op, const double* x, double* y, const int* gate) {
         return;
       }
       if (mode == 1) {  // AD: W KW^+ W^T x and H2 x are independent — run them concurrently
+        // Split (small W): W^T x and the KW solve overlap the latency-bound
+        // coarse chain before the local solve, W c the one after it, so the
+        // W streams do not take HBM bandwidth from the single-pass local solve.
+        // Large W (c3, c5): the whole branch overlaps everything (pure
+        // bandwidth sharing is better there).
+        const bool split = c.w_split >= 0 ? c.w_split == 1
+                                          : (8.0 * c.n * c.nm <= 512.0 * (1 << 20) && c.n0 > 0 &&
+                                             c.cfg.composition != 0);
         AWG_CUDA(cudaEventRecord(c.ev_fork, c.stream));
         AWG_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
         cudaStream_t main = c.stream;
         c.stream = c.side;
-        k::second_q(c, x, c.t6.p, gate);
+        if (split) k::second_q_coef(c, x, gate);
+        else k::second_q(c, x, c.t6.p, gate);
         c.stream = main;
-        AWG_CUDA(cudaEventRecord(c.ev_join, c.side));
-        h2(c, x, y, gate, c.t6.p, c.ev_join);  // joins the branch before its last kernel
+        std::function<void()> tail;
+        if (split) {
+          tail = [&]() {  // on main right after the local solve: release W c on the side stream
+            AWG_CUDA(cudaEventRecord(c.ev_mid, c.stream));
+            AWG_CUDA(cudaStreamWaitEvent(c.side, c.ev_mid, 0));
+            c.stream = c.side;
+            k::second_q_apply(c, c.t6.p, gate);
+            c.stream = main;
+            AWG_CUDA(cudaEventRecord(c.ev_join, c.side));
+          };
+        } else {
+          AWG_CUDA(cudaEventRecord(c.ev_join, c.side));
+        }
+        h2(c, x, y, gate, c.t6.p, c.ev_join, tail);  // joins the branch before its last kernel
       } else if (mode == 2) {  // HYB
         k::second_q(c, x, c.t6.p, gate);                 // corr
         k::spmv(c, c.t6.p, c.t7.p, 3, nullptr, x, gate);  // pt = x - A corr
