@@ -608,6 +608,7 @@ int awg_load_factors(awg_ctx* ctx, const awg_config* cfg, const awg_factors* f) 
     // AS / AS+: the local Cholesky factors are computed here from A (and the
     // loaded V^s for the A+ blocks); Cholesky factors are unique
     if (c.one_level != 2) build_local_cholesky(c);
+    k::build_coarse_neg(c);
     AWG_CUDA(cudaStreamSynchronize(c.stream));
     c.have_factors = true;
   });

@@ -217,7 +217,10 @@ void nn_prolong(Ctx& c, double* y, const int* gate);                   // y = su
 void nn_fused(Ctx& c, const double* x, const int* gate);               // single pass over V^s into part
 void aminus(Ctx& c, const double* x, double* y, const int* gate);     // y = A- x
 // mode 1: y = A+ x;  mode 2: y = sub - A+ x  (A- prolongation fused into the SpMV)
-void aplus(Ctx& c, const double* x, double* y, int mode, const double* sub, const int* gate);
+// neg_ready: neg_c already holds the A- dots of x (from coarse_q_neg)
+void aplus(Ctx& c, const double* x, double* y, int mode, const double* sub, const int* gate, bool neg_ready = false);
+bool coarse_q_neg(Ctx& c, const double* x, double* y, const int* gate);  // Q x and the A- dots of Q x
+void build_coarse_neg(Ctx& c);  // M2 = M1 K+ (A- dots of the retained coarse columns), after K0 is set
 void coarse_q(Ctx& c, const double* x, double* y, const int* gate);   // y = Z K0+ Z^T x
 // y = ((a - Z K0+ Z^T x) + d) [+ e] in one epilogue (a == nullptr: y = Z K0+ Z^T x);
 // the stream waits on `wait_before_combine` (if set) before the combining kernel
@@ -295,6 +298,7 @@ struct Ctx {
   bool fused_hold = true;  // column values kept in registers across the step's reduction (AWG_FUSED_HOLD=0 off)
   BsPlan bs_neg, bs_z;   // A- dots (V^s columns k < n_nonpos), Z^T x (Y_s blocks)
   DArr<OwnEnt> ent_neg, ent_z;  // owner entries into V^s (A- modes) and Y_s (Z columns)
+  DArr<double> m2t;  // (K+ M1^T): r0 x n_neg column-major; M1(q, jj) = A- dot q of coarse column retained[jj]
   LocalPlan plan_nn;     // V^s with the eigenvalue mask (NN)
   LocalPlan plan_as;     // U^s = L^-T, triangular (AS / AS+)
   DArr<double> U;        // AS / AS+ local factors, same layout as V

@@ -12,7 +12,10 @@
 // OneLevel::apply (preconditioner.cpp:37-55).  Dense dot products use
 // fixed-shape warp trees (deterministic, not sequential): the parity bar for
 // the applies is 1e-11 relative.
+#include <cublas_v2.h>
+
 #include <algorithm>
+#include <cstdlib>
 
 #include "awg_internal.cuh"
 #include "pcg_device.cuh"
@@ -707,9 +710,14 @@ __global__ void __launch_bounds__(256) k_bs_gemvT(const int* __restrict__ gate, 
 // x = 0, x[retained] = y.  L^-T L^-1 = K^+ is formed once at setup (k_gram), so
 // the solve is ONE symmetric GEMV: warp per output entry, reading row pos[i]
 // of K^+ (coalesced) against the gathered b_r (L1/L2 resident).
+// Rows i >= dim (when m2t is set): out2[i - dim] = M2(i - dim, :) b_r with M2
+// stored transposed (r x nq, column-major): the A- dots of Z K+ b, precomputed
+// as M2 = M1 K+ (build_coarse_neg), so the hybrid H2's A+ (Z c) needs no
+// separate dot kernel over Z c.
 __global__ void k_coarse_solve(const int* __restrict__ gate, int dim, int r, const double* __restrict__ kinv,
                                const int* __restrict__ pos, const int* __restrict__ ret,
-                               const double* __restrict__ b, double* __restrict__ x, int early) {
+                               const double* __restrict__ b, double* __restrict__ x, int early, int nq,
+                               const double* __restrict__ m2t, double* __restrict__ out2) {
   if (gated_early(gate, early)) return;
   // b_r = b[retained] staged once per CTA (kCoarseStage doubles of static
   // shared memory) instead of two dependent loads per element in every warp
@@ -721,11 +729,11 @@ __global__ void k_coarse_solve(const int* __restrict__ gate, int dim, int r, con
   }
   const int lane = threadIdx.x & 31;
   const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (i >= dim) return;
-  const int k = pos[i];
+  if (i >= dim + (m2t ? nq : 0)) return;
+  const int k = i < dim ? pos[i] : 0;
   double acc = 0.0;
   if (k >= 0) {
-    const double* row = kinv + (size_t)k * r;
+    const double* row = i < dim ? kinv + (size_t)k * r : m2t + (size_t)(i - dim) * r;
     double a1 = 0.0;
     int j = lane;
     if (staged) {
@@ -743,7 +751,10 @@ __global__ void k_coarse_solve(const int* __restrict__ gate, int dim, int r, con
     }
     acc = warp_sum(acc + a1);
   }
-  if (lane == 0) x[i] = acc;
+  if (lane == 0) {
+    if (i < dim) x[i] = acc;
+    else out2[i - dim] = acc;
+  }
 }
 
 // g(i, j) = sum_k a(k, i) a(k, j) for a column-major lower r x r (so k >= max(i, j))
@@ -1261,8 +1272,8 @@ static BlockSum neg_sum(const Ctx& c) {
 
 // y = A+ x (mode 1) or y = sub - A+ x (mode 2): the A- dots, then one fused
 // SpMV + A- prolongation kernel
-void aplus(Ctx& c, const double* x, double* y, int mode, const double* sub, const int* gate) {
-  if (c.nneg > 0) neg_dot(c, x, gate);
+void aplus(Ctx& c, const double* x, double* y, int mode, const double* sub, const int* gate, bool neg_ready) {
+  if (c.nneg > 0 && !neg_ready) neg_dot(c, x, gate);
   BlockSum bs = neg_sum(c);
   if (rows_group(c) == 8)
     launch(c, k_spmv_aplus<8>, grid_for(c, 8LL * c.n), kThreads, 0, gate, c.n, c.rp.p, c.ci.p, c.va.p, x, y, mode,
@@ -1285,9 +1296,34 @@ void rr_solve(Ctx& c, const CoarseFactor& f, const double* b, double* x, const i
     return;
   }
   launch(c, k_coarse_solve, (f.dim + wpb - 1) / wpb, kThreads, 0, gate, f.dim, f.rank, f.kinv.p, f.pos.p,
-                                                                     f.retained.p, b, x, c.pdl_early);
+                                                                     f.retained.p, b, x, c.pdl_early, 0,
+         (const double*)nullptr, (double*)nullptr);
   ++c.launches;
   check_launch("coarse_solve");
+}
+
+// Q x into y and, in the same coarse-solve launch, the A- dots of y into
+// neg_c (the coefficients k::aplus's SpMV consumes with neg_ready = true).
+// Returns false (nothing enqueued) when M2 is not available.
+bool coarse_q_neg(Ctx& c, const double* x, double* y, const int* gate) {
+  if (!c.m2t.p || c.n0 == 0 || c.k0.rank == 0) return false;
+  zT(c, x, c.cz.p, gate);
+  double* coef = c.cz.p + c.n0;
+  const int wpb = kThreads / 32;
+  const CoarseFactor& f = c.k0;
+  launch(c, k_coarse_solve, (f.dim + c.nneg + wpb - 1) / wpb, kThreads, 0, gate, f.dim, f.rank, f.kinv.p, f.pos.p,
+         f.retained.p, (const double*)c.cz.p, coef, c.pdl_early, c.nneg, (const double*)c.m2t.p, c.neg_c.p);
+  ++c.launches;
+  check_launch("coarse_solve_neg");
+  const BlockSum bs{c.own_off.p, c.ent_z.p, nullptr, c.Y.p, coef};
+  const Combine cb{nullptr, nullptr, nullptr, RzFuse{}};
+  if (rows_group(c) == 4)
+    launch(c, k_prolong_sum<4>, grid_for(c, 4LL * c.n), kThreads, 0, gate, c.n, bs, y, cb, c.pdl_early);
+  else
+    launch(c, k_prolong_sum<1>, grid_for(c, c.n), kThreads, 0, gate, c.n, bs, y, cb, c.pdl_early);
+  ++c.launches;
+  check_launch("z_prolong");
+  return true;
 }
 
 void coarse_q(Ctx& c, const double* x, double* y, const int* gate) {
@@ -1430,6 +1466,46 @@ void coarse_inverse(Ctx& c, const double* l, CoarseFactor& f) {
   ++c.launches;
   check_launch("retained_pos");
   AWG_CUDA(cudaStreamSynchronize(c.stream));
+}
+
+// M2 for coarse_q_neg: M1(q, jj) = A- dot q of coarse column retained[jj]
+// (the dots k_bs_gemvT forms for A+ (Z c), one column at a time), M2 = M1 K+.
+// AWG_COARSE_NEG=0 disables (the hybrid H2 then runs the dot kernel on Z c).
+void build_coarse_neg(Ctx& c) {
+  c.m2t.release();
+  const char* e = std::getenv("AWG_COARSE_NEG");
+  if (e && e[0] == '0') return;
+  const int r = c.k0.rank, nq = c.nneg;
+  if (nq == 0 || c.n0 == 0 || r == 0) return;
+  if (double(nq) * r * 8.0 > 1024.0 * 1024.0 * 1024.0) return;  // memory guard: keep the dot kernel
+  std::vector<int> cs, ck;
+  for (int s = 0; s < c.N; ++s)
+    for (int k = 0; k < c.h_ks[s]; ++k) {
+      cs.push_back(s);
+      ck.push_back(k);
+    }
+  DArr<double> M1, t;
+  M1.alloc(size_t(nq) * r);
+  t.alloc(c.n);
+  for (int jj = 0; jj < r; ++jj) {
+    const int j = c.k0.h_retained[jj], s = cs[j], k = ck[j];
+    AWG_CUDA(cudaMemsetAsync(t.p, 0, sizeof(double) * c.n, c.stream));
+    scatter_col(c, s, c.Y.p + c.h_yoff[s] + size_t(k) * c.h_ld[s], t.p);
+    neg_dot(c, t.p, nullptr);
+    AWG_CUDA(cudaMemcpyAsync(M1.p + size_t(jj) * nq, c.neg_c.p, sizeof(double) * nq, cudaMemcpyDeviceToDevice,
+                             c.stream));
+  }
+  c.m2t.alloc(size_t(r) * nq);
+  cublasHandle_t h = nullptr;
+  if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) c.fail(AWG_E_CUDA, "build_coarse_neg: cublasCreate");
+  cublasSetStream(h, c.stream);
+  const double one = 1.0, zero = 0.0;
+  // M2^T (r x nq) = K+ (r x r, symmetric) M1^T
+  const cublasStatus_t st =
+      cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, r, nq, r, &one, c.k0.kinv.p, r, M1.p, nq, &zero, c.m2t.p, r);
+  AWG_CUDA(cudaStreamSynchronize(c.stream));
+  cublasDestroy(h);
+  if (st != CUBLAS_STATUS_SUCCESS) c.fail(AWG_E_CUDA, "build_coarse_neg: DGEMM");
 }
 
 }  // namespace k

@@ -278,14 +278,16 @@ static void h2(Ctx& c, const double* x, double* y, const int* gate, const double
     if (extra) add_extra(c.t1.p);
     return;
   }
-  k::coarse_q(c, x, c.t0.p, gate);  // corr
+  // corr (and, for the hybrid form, the A- dots of corr in the same coarse-solve launch)
+  const bool neg_ready = c.cfg.composition != 0 && k::coarse_q_neg(c, x, c.t0.p, gate);
+  if (!neg_ready) k::coarse_q(c, x, c.t0.p, gate);
   if (c.cfg.composition == 0) {
     h1(c, x, c.t1.p, gate);
     k::axpby(c, c.n, c.t1.p, c.t0.p, nullptr, extra ? c.t2.p : y, 1, gate);
     if (extra) add_extra(c.t2.p);
     return;
   }
-  k::aplus(c, c.t0.p, c.t2.p, 2, x, gate);         // pt = x - A+ corr
+  k::aplus(c, c.t0.p, c.t2.p, 2, x, gate, neg_ready);  // pt = x - A+ corr
   h1(c, c.t2.p, c.t3.p, gate);                     // hp
   if (after_h1) after_h1();  // enqueues work that must follow the local solve
   aplus(c, c.t3.p, c.t4.p, gate);                  // A+ hp

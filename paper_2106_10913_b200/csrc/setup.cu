@@ -799,6 +799,7 @@ void run_setup(Ctx& c, const awg_config& cfg) {
     k_symmetrize<<<int(((long long)c.n0 * c.n0 + kThreads - 1) / kThreads), kThreads, 0, c.stream>>>(c.n0, G.p);
     ++c.launches;
     pivoted_factor(c, G, c.n0, cfg.rrf_semantics, c.k0, c.n0);
+    k::build_coarse_neg(c);  // A- dots of the coarse columns for the hybrid H2 (apply path only)
   }
   c.t_setup_ms[2] = now_ms() - t0;
   trace(c, "coarse operator + pivoted factor (r0 = " + std::to_string(c.k0.rank) + ")", c.t_setup_ms[2]);

@@ -201,3 +201,21 @@ def test_single_pass_register_hold_is_bit_identical():
     for x in g["x_apply"]:
         y1, y2 = ctx1.apply(awg.Op.H1, x), ctx2.apply(awg.Op.H1, x)
         assert np.array_equal(y1, y2)
+
+
+@pytest.mark.parametrize("case", ["t2d", "t3d", "telas8"])
+def test_precomputed_coarse_neg_dots(case):
+    """The hybrid H2's A+ (Q x): the A- dots of Z c taken from the coarse solve
+    (M2 = M1 K+, default) against the dot kernel over Z c (AWG_COARSE_NEG=0) —
+    a re-association of the same sums."""
+    g, s = golden_with_base(case)
+    ctx1 = make_ctx(g)
+    os.environ["AWG_COARSE_NEG"] = "0"
+    try:
+        ctx2 = make_ctx(g)
+    finally:
+        del os.environ["AWG_COARSE_NEG"]
+    for x in g["x_apply"]:
+        for op in (awg.Op.H2, awg.Op.H3):
+            y1, y2 = ctx1.apply(op, x), ctx2.apply(op, x)
+            assert rel(y1, y2) <= 1e-12
