@@ -247,6 +247,37 @@ void finalize_factors(Ctx& c) {
         pl.kcmax_f = std::max(pl.kcmax_f, kc);
       }
       tf.insert(tf.end(), tail.begin(), tail.end());
+      pl.static_grid = 0;
+      pl.cta_off.release();
+      if (!tri && c.fused_static) {
+        // static split: CTA b takes columns [b T / G, (b + 1) T / G) of the
+        // subdomains' column lists laid end to end (cut at subdomain ends), so
+        // every CTA streams the same bytes and the last round has no idle SMs
+        const int G = int(std::max<long long>(1, std::min<long long>(cols_total, std::max(1, c.sm_count - c.fused_reserve))));
+        tf.clear();
+        std::fill(nkf.begin(), nkf.end(), 0);
+        std::vector<int> off(G + 1, 0);
+        int s = 0, j = c.h_m[0];
+        for (int b = 0; b < G; ++b) {
+          off[b] = int(tf.size());
+          long long want = (long long)cols_total * (b + 1) / G - (long long)cols_total * b / G;
+          while (want > 0 && s < N) {
+            const int end = c.h_ns[s];
+            const int take = int(std::min<long long>(want, end - j));
+            if (take > 0) {
+              tf.push_back({s, 0, j, j + take, nkf[s]++, 0});
+              j += take;
+              want -= take;
+            }
+            if (j >= end && ++s < N) j = c.h_m[s];
+          }
+        }
+        off[G] = int(tf.size());
+        pl.kcmax_f = 1;
+        for (int v : nkf) pl.kcmax_f = std::max(pl.kcmax_f, v);
+        pl.cta_off.upload(off, c.stream);
+        pl.static_grid = G;
+      }
       pl.tf.upload(tf, c.stream);
       pl.nkc_f.upload(nkf, c.stream);
     }
@@ -428,6 +459,8 @@ int awg_create(awg_ctx** out, int device) {
     };
     cc.fused_cpb = env_int("AWG_FUSED_CPB", 0);
     cc.fused_hold = env_int("AWG_FUSED_HOLD", 1) != 0;
+    cc.fused_prefetch = env_int("AWG_FUSED_PREFETCH", 1) != 0;
+    cc.fused_static = env_int("AWG_FUSED_STATIC", 1) != 0;
     cc.rows_group = env_int("AWG_ROWS_GROUP", 0);
     cc.pdl_early = env_int("AWG_PDL_EARLY", 0) != 0 ? 1 : 0;
     cc.w_split = env_int("AWG_W_SPLIT", -1);
@@ -807,6 +840,7 @@ int awg_query(awg_ctx* ctx, awg_stats* st) {
     for (int v : c.h_w_inner) st->w_inner_total += v;
     st->w_batches = c.w_batches;
     st->nn_single_pass = ((c.one_level == 2 && c.plan_nn.fused) || (c.one_level != 2 && c.plan_as.fused)) ? 1 : 0;
+    st->nn_static_split = (c.one_level == 2 && c.plan_nn.fused && c.plan_nn.static_grid > 0) ? 1 : 0;
   });
 }
 

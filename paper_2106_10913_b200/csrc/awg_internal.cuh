@@ -110,6 +110,8 @@ struct LocalPlan {
   // single-pass variant (k_nn_fused): column ranges per CTA, their chunk counts
   bool fused = false;
   DArr<GemvTask> tf;
+  DArr<int> cta_off;    // static split (AWG_FUSED_STATIC): tasks of CTA b are [cta_off[b], cta_off[b + 1])
+  int static_grid = 0;
   DArr<int> nkc_f;
   int kcmax_f = 1;
   DArr<int2> own_nkc, own_nkc_f;  // per owner entry: (p, nkc / nkc_f of its subdomain)
@@ -295,6 +297,8 @@ struct Ctx {
   int fused_cpb = 0, fused_nbuf = 0, fused_chunks_per_sm = 8;  // 0: automatic
   int pdl_early = 0;        // coarse-chain kernels release their dependents at entry (AWG_PDL_EARLY=1; measured neutral)
   int rows_group = 0;       // lanes per dof of the block-sparse prolongations (0: automatic)
+  bool fused_static = true;  // NN: equal column shares per CTA instead of the atomic queue (AWG_FUSED_STATIC=0 off)
+  bool fused_prefetch = true;  // next task's first steps issued during the current one (AWG_FUSED_PREFETCH=0 off)
   bool fused_hold = true;  // column values kept in registers across the step's reduction (AWG_FUSED_HOLD=0 off)
   BsPlan bs_neg, bs_z;   // A- dots (V^s columns k < n_nonpos), Z^T x (Y_s blocks)
   DArr<OwnEnt> ent_neg, ent_z;  // owner entries into V^s (A- modes) and Y_s (Z columns)

@@ -403,7 +403,8 @@ __global__ void __launch_bounds__(kFusedT, 1) k_nn_fused(const int* __restrict__
                                                          const int* __restrict__ pidx, const double* __restrict__ ds,
                                                          const double* __restrict__ x, const double* __restrict__ rlam,
                                                          long long P, double* __restrict__ part, int ntasks,
-                                                         int* __restrict__ queue, int nbuf, int ldmax, int smem_doubles,
+                                                         int* __restrict__ queue, const int* __restrict__ cta_off, int nbuf, int ldmax,
+                                                         int smem_doubles, int prefetch,
                                                          unsigned long long* __restrict__ tmr) {
   if (gated(gate)) return;
   if (tmr && threadIdx.x == 0) atomicMin(&tmr[0], globaltimer_ns());
@@ -431,42 +432,74 @@ __global__ void __launch_bounds__(kFusedT, 1) k_nn_fused(const int* __restrict__
   // the steps this CTA has consumed: buffer g % nbuf, mbarrier parity
   // (g / nbuf) & 1.  One barrier per step: red is double-buffered, and the
   // buffer of the previous step is refilled right after the barrier.
+  // Cross-task prefetch: thread 0 claims the CTA's NEXT task while the current
+  // one runs and issues its first steps into the ring as soon as buffers free
+  // up, so the copy pipeline does not drain at task boundaries (the global step
+  // count g, buffer g % nbuf and parity (g / nbuf) & 1 simply run on).
+  auto issue = [&](const double* Vs, int L, int j0, int j1, int p, unsigned gbase) {
+    const int j = j0 + CPB * p;
+    const int cols = min(CPB, j1 - j);
+    const unsigned b = (gbase + p) % nbuf;
+    if (!TRI) {
+      const unsigned bytes = unsigned(cols) * unsigned(L) * 8u;
+      mbar_arm(&bar[b], bytes);
+      bulk_load(fsm + b * bstride, Vs + (size_t)j * L, bytes, &bar[b], pol);
+    } else {
+      // upper-triangular U^s: column c holds rows 0..c; copy an even row count
+      unsigned rows[CPB], total = 0;
+#pragma unroll
+      for (int c = 0; c < CPB; ++c) {
+        rows[c] = c < cols ? unsigned(min(L, (j + c + 2) & ~1)) : 0u;
+        total += rows[c];
+      }
+      mbar_arm(&bar[b], total * 8u);
+#pragma unroll
+      for (int c = 0; c < CPB; ++c)
+        if (rows[c])
+          bulk_load(fsm + b * bstride + (size_t)c * L, Vs + (size_t)(j + c) * L, rows[c] * 8u, &bar[b], pol);
+    }
+  };
   unsigned g = 0;
-  for (;;) {
-    __syncthreads();
-    if (tid == 0) s_task = atomicAdd(queue, 1);
-    __syncthreads();
-    if (s_task >= ntasks) break;
-    const GemvTask t = tasks[s_task];
+  // static split: this CTA's own task range, no queue
+  const int lim = cta_off ? cta_off[blockIdx.x + 1] : ntasks;
+  if (tid == 0) s_task = cta_off ? cta_off[blockIdx.x] : atomicAdd(queue, 1);
+  __syncthreads();
+  int cur = s_task;
+  // thread 0 only: steps of the current task already issued; the next task
+  int pre = 0, nxt = lim, pre_n = 0, nstep_n = 0, j0_n = 0, j1_n = 0, s_n = 0, L_n = 0, fstage = 0;
+  const double* V_n = V;
+  // the next task's descriptor is a chain of dependent loads (queue -> task ->
+  // ld / voff): one link per step, so thread 0 never stalls the CTA for the
+  // whole chain at once
+  auto advance = [&]() {
+    if (fstage == 0) {
+      nxt = cta_off ? cur + 1 : atomicAdd(queue, 1);
+      fstage = nxt < lim ? 1 : 3;
+    } else if (fstage == 1) {
+      const GemvTask tn = tasks[nxt];
+      j0_n = tn.j0;
+      j1_n = tn.j1;
+      s_n = tn.s;
+      nstep_n = (tn.j1 - tn.j0 + CPB - 1) / CPB;
+      fstage = 2;
+    } else if (fstage == 2) {
+      L_n = ld[s_n];
+      V_n = V + voff[s_n];
+      fstage = 3;
+    }
+  };
+  while (cur < lim) {
+    const GemvTask t = tasks[cur];
     const int s = t.s, n = ns[s], L = ld[s];
     const long long p0 = poff[s];
     const double* Vs = V + voff[s];
     const int nstep = (t.j1 - t.j0 + CPB - 1) / CPB;
-    auto issue = [&](int p) {
-      const int j = t.j0 + CPB * p;
-      const int cols = min(CPB, t.j1 - j);
-      const unsigned b = (g + p) % nbuf;
-      if (!TRI) {
-        const unsigned bytes = unsigned(cols) * unsigned(L) * 8u;
-        mbar_arm(&bar[b], bytes);
-        bulk_load(fsm + b * bstride, Vs + (size_t)j * L, bytes, &bar[b], pol);
-      } else {
-        // upper-triangular U^s: column c holds rows 0..c; copy an even row count
-        unsigned rows[CPB], total = 0;
-#pragma unroll
-        for (int c = 0; c < CPB; ++c) {
-          rows[c] = c < cols ? unsigned(min(L, (j + c + 2) & ~1)) : 0u;
-          total += rows[c];
-        }
-        mbar_arm(&bar[b], total * 8u);
-#pragma unroll
-        for (int c = 0; c < CPB; ++c)
-          if (rows[c])
-            bulk_load(fsm + b * bstride + (size_t)c * L, Vs + (size_t)(j + c) * L, rows[c] * 8u, &bar[b], pol);
-      }
-    };
-    if (tid == 0)
-      for (int p = 0; p < nbuf && p < nstep; ++p) issue(p);
+    if (tid == 0) {
+      for (int p = pre; p < nbuf && p < nstep; ++p) issue(Vs, L, t.j0, t.j1, p, g);
+      nxt = lim;
+      pre_n = 0;
+      fstage = 0;
+    }
     double xr[R], yr[R];
 #pragma unroll
     for (int k = 0; k < R; ++k) {
@@ -508,12 +541,18 @@ __global__ void __launch_bounds__(kFusedT, 1) k_nn_fused(const int* __restrict__
       }
       __syncthreads();
       // the previous step's buffer is no longer read by anyone (with HOLD this
-      // step's buffer is already consumed too: refill it now)
-      if (HOLD) {
-        if (tid == 0 && p + nbuf < nstep) issue(p + nbuf);
-      } else {
-        if (tid == 0 && p >= 1 && p - 1 + nbuf < nstep) issue(p - 1 + nbuf);
+      // step's buffer is already consumed too: refill it now) — with this
+      // task's next step, or past its end with the next task's
+      if (tid == 0 && (HOLD || p >= 1)) {
+        const int q = HOLD ? p + nbuf : p - 1 + nbuf;
+        if (q < nstep) {
+          issue(Vs, L, t.j0, t.j1, q, g);
+        } else if (prefetch && fstage == 3 && nxt < lim && q - nstep == pre_n && pre_n < nstep_n) {
+          issue(V_n, L_n, j0_n, j1_n, pre_n, g + nstep);
+          ++pre_n;
+        }
       }
+      if (tid == 0) advance();
       // the 16 warp partials: lane l reads partial l & 15 (one shared load per
       // warp instead of 16 broadcast loads per thread), then an xor butterfly
       // over 16 lanes — the fixed tree ((r0+r8)+(r4+r12)) + ((r2+r10)+(r6+r14))
@@ -550,6 +589,16 @@ __global__ void __launch_bounds__(kFusedT, 1) k_nn_fused(const int* __restrict__
       if (i < n) out[i] = yr[k];
     }
     g += nstep;
+    // every thread is past this task's last buffer read before the next task's
+    // remaining first steps are issued into it
+    __syncthreads();
+    if (tid == 0) {
+      while (fstage < 3) advance();
+      s_task = nxt;
+      pre = pre_n;
+    }
+    __syncthreads();
+    cur = s_task;
   }
   // the queue resets itself: the last CTA out (queue[1] counts finished CTAs,
   // each after its last queue[0] access) rewinds both counters for the next launch
@@ -1137,8 +1186,9 @@ void launch_fused(Ctx& c, const LocalPlan& pl, const double* F, const double* D,
     configured = true;
   }
   launch(c, k_nn_fused<TRI, R, CPB, HOLD>, grid, kFusedT, smem, gate, pl.tf.p, F, c.voff.p, c.ns.p, c.ld.p, c.poff.p,
-         c.pidx.p, D, x, TRI ? nullptr : c.rlam.p, c.P, c.wpart_nn.p, int(pl.tf.n), c.fused_queue.p, nbuf, ldmax,
-         int(smem / sizeof(double)), c.fused_timer.p);
+         c.pidx.p, D, x, TRI ? nullptr : c.rlam.p, c.P, c.wpart_nn.p, int(pl.tf.n), c.fused_queue.p,
+         pl.static_grid ? pl.cta_off.p : nullptr, nbuf, ldmax,
+         int(smem / sizeof(double)), int(c.fused_prefetch), c.fused_timer.p);
 }
 
 template <bool TRI, int CPB, bool HOLD>
@@ -1199,7 +1249,8 @@ void nn_fused(Ctx& c, const double* x, const int* gate) {
     AWG_CUDA(cudaMemcpyAsync(c.fused_timer.p, init, sizeof(init), cudaMemcpyHostToDevice, c.stream));
   }
   // persistent CTAs: one per SM, less the SMs left to the concurrent W branch
-  const int grid = std::min(int(pl.tf.n), std::max(1, c.sm_count - c.fused_reserve));
+  const int grid =
+      pl.static_grid ? pl.static_grid : std::min(int(pl.tf.n), std::max(1, c.sm_count - c.fused_reserve));
   const double* F = nn ? c.V.p : c.U.p;
   const double* D = nn ? c.ds.p : nullptr;
   if (nn && cpb == 2)

@@ -19,10 +19,14 @@ for spec in sys.argv[2:]:
         ctx = awg.context_from_problem(p)
         ctx.setup(awg.config_for(p))
         best = 1e9
+        x, rep = ctx.pcg(p.b, p.rtol, 10000)
+        ctx.kernel_timer(reset=True)
         for _ in range(3):
             x, rep = ctx.pcg(p.b, p.rtol, 10000)
             best = min(best, rep.solve_ms / max(rep.iterations, 1))
+        kms, kl = ctx.kernel_timer()
         out.append({"knobs": spec, "iterations": rep.iterations, "ms_per_iteration": best,
+                    "local_solve_ms_in_solve": kms / max(kl, 1), "H1_ms": ctx.time_apply(awg.Op.H1, reps=20),
                     "H3_ms": ctx.time_apply(awg.Op.H3, reps=20), "Q_ms": ctx.time_apply(awg.Op.Q, reps=20),
                     "APLUS_ms": ctx.time_apply(awg.Op.APLUS, reps=20)})
         ctx.close()

@@ -19,6 +19,13 @@ for cfg in sys.argv[1:] or ["c2"]:
             settings.append((f"min{mincols}_chunks{chunks}_tail{tail}",
                              {"AWG_FUSED_MINCOLS": str(mincols), "AWG_FUSED_CHUNKS": str(chunks),
                               "AWG_FUSED_TAIL": str(tail)}))
+    elif mode == "static":  # static per-CTA column shares vs the atomic queue, cross-task prefetch
+        for st, pf, cpb in itertools.product([0, 1], [0, 1], [0, 1]):
+            settings.append((f"static{st}_prefetch{pf}_cpb{cpb or 'auto'}",
+                             {"AWG_FUSED_STATIC": str(st), "AWG_FUSED_PREFETCH": str(pf),
+                              "AWG_FUSED_CPB": str(cpb)}))
+        settings.append(("static0_prefetch1_cpbauto_again", {"AWG_FUSED_STATIC": "0"}))
+        settings.append(("static1_prefetch1_cpbauto_again", {"AWG_FUSED_STATIC": "1"}))
     elif mode == "hold":  # column values held in registers across the reduction (AWG_FUSED_HOLD)
         for hold, cpb, nbuf in itertools.product([0, 1], [1, 2], [3, 4, 6]):
             settings.append((f"hold{hold}_cpb{cpb}_nbuf{nbuf}",
@@ -30,7 +37,7 @@ for cfg in sys.argv[1:] or ["c2"]:
                               "AWG_FUSED_CHUNKS": str(chunks)}))
     for name, env in settings:
         for k in ("AWG_NN_TWO_PASS", "AWG_FUSED_CPB", "AWG_FUSED_NBUF", "AWG_FUSED_CHUNKS", "AWG_FUSED_MINCOLS",
-                  "AWG_FUSED_TAIL", "AWG_FUSED_HOLD"):
+                  "AWG_FUSED_TAIL", "AWG_FUSED_HOLD", "AWG_FUSED_STATIC", "AWG_FUSED_PREFETCH"):
             os.environ.pop(k, None)
         os.environ.update(env)
         try:
