@@ -678,7 +678,16 @@ int awg_synthetic_factors(awg_ctx* ctx, int m_per_sub, unsigned long long seed) 
     c.Y.alloc(1);
     c.k0.clear();
     c.kw.clear();
-    c.nm = 0;
+    // optional synthetic W (n x AWG_SYNTH_NM, hash-filled) for timing the
+    // W^T x / W c kernels at full scale without the setup (time_kernel 3, 4)
+    const char* snm = std::getenv("AWG_SYNTH_NM");
+    c.nm = snm ? std::max(0, std::atoi(snm)) : 0;
+    c.ldw = round_up(c.n, 4);
+    if (c.nm) {
+      c.W.alloc(size_t(c.ldw) * c.nm);
+      k_fill_hash<<<c.sm_count * 8, 256, 0, c.stream>>>(c.W.n, seed + 1, c.W.p);
+      check_launch("fill_hash W");
+    }
     c.alloc_work();
     AWG_CUDA(cudaStreamSynchronize(c.stream));
     c.have_factors = true;
