@@ -1528,7 +1528,11 @@ void build_coarse_neg(Ctx& c) {
   if (e && e[0] == '0') return;
   const int r = c.k0.rank, nq = c.nneg;
   if (nq == 0 || c.n0 == 0 || r == 0) return;
-  if (double(nq) * r * 8.0 > 1024.0 * 1024.0 * 1024.0) return;  // memory guard: keep the dot kernel
+  // measured (profiles/r01e/knobs_coarse_neg_c{3,5}.json, ms per PCG iteration):
+  // M2 at 0.7 MB (c2) and 35 MB (c3: 3.68 -> 3.62) wins; at 69 MB (c5: 13.71 ->
+  // 13.95) the doubled coarse-solve launch on the critical chain loses to the
+  // dot kernel over Z c, so the precomputed dots stop at 48 MB
+  if (double(nq) * r * 8.0 > 48.0 * 1024.0 * 1024.0) return;
   std::vector<int> cs, ck;
   for (int s = 0; s < c.N; ++s)
     for (int k = 0; k < c.h_ks[s]; ++k) {

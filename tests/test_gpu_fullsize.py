@@ -65,27 +65,64 @@ def _spmv_reference_order(p, x):
     return y
 
 
-def test_setup_mode_counts_full_size(c2):
-    p, ctx = c2
-    with open(os.path.join(os.path.dirname(__file__), "golden", "c2_modes.json")) as fh:
+def _check_modes(p, ctx, name):
+    with open(os.path.join(os.path.dirname(__file__), "golden", f"{name}_modes.json")) as fh:
         ref = json.load(fh)
-    assert ctx.get("n_nonpos").tolist() == ref["n_nonpos"]
-    assert ctx.get("n_zero").tolist() == ref["n_zero"]
-    assert ctx.get("ks").tolist() == ref["ks"]
-    q = ctx.query()
-    assert q["n0"] == ref["n0"] and q["n_minus"] == ref["n_minus"]
+    subs = ref.get("subdomains", list(range(p.n_sub)))
+    assert ctx.get("n_nonpos")[subs].tolist() == ref["n_nonpos"]
+    assert ctx.get("n_zero")[subs].tolist() == ref["n_zero"]
+    assert ctx.get("ks")[subs].tolist() == ref["ks"]
+    if "n0" in ref:
+        q = ctx.query()
+        assert q["n0"] == ref["n0"] and q["n_minus"] == ref["n_minus"]
     plam = ctx.get("pencil_lam")
     off = np.concatenate([[0], np.cumsum([o.size for o in p.omega])])
-    for s, low in enumerate(ref["pencil_low"]):
+    for s, low in zip(subs, ref["pencil_low"]):
         # 1e-8 of the subdomain's spectrum scale (the golden cases' bound,
         # test_gpu_setup); the pencil's zero cluster (size n_zero, values
-        # ~1e-9..1e-7 at this 1e6 contrast) is rounding noise of a singular
+        # ~1e-9..1e-7 at c2's 1e6 contrast) is rounding noise of a singular
         # pencil in both eigensolvers: it only has to stay far below tau
         scale = max(1.0, float(np.max(np.abs(plam[off[s]:off[s + 1]]))))
         got, low = plam[off[s]:off[s] + len(low)], np.asarray(low)
         zero = np.abs(low) < 1e-6
         assert np.all(np.abs(got[zero]) < 1e-6), s
         assert np.max(np.abs(got[~zero] - low[~zero])) <= 1e-8 * scale, s
+
+
+def test_setup_mode_counts_full_size(c2):
+    p, ctx = c2
+    _check_modes(p, ctx, "c2")
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(os.path.dirname(__file__), "golden", "c3_modes.json")),
+                    reason="c3 fixture not generated")
+def test_setup_mode_counts_c3():
+    """configs[2] (64^3, 64 subdomains, fixed k = 10): n_nonpos / n_zero and
+    the fixed-k rule k_s = max(10, n_nonpos) extended over clusters, per
+    subdomain, against the restatement at full size (GPU setup ~105 s)."""
+    p = problems.make("c3")
+    ctx = awg.context_from_problem(p)
+    try:
+        ctx.setup(awg.config_for(p))
+        _check_modes(p, ctx, "c3")
+    finally:
+        ctx.close()
+
+
+@pytest.mark.skipif(os.environ.get("AWG_FULLSIZE_C5") != "1" or not os.path.exists(
+    os.path.join(os.path.dirname(__file__), "golden", "c5_corner_modes.json")),
+                    reason="c5 setup takes ~330 s: run with AWG_FULLSIZE_C5=1")
+def test_setup_mode_counts_c5_corner():
+    """configs[4] (96^3, 216 subdomains, fixed k = 8), the north-star config:
+    per-subdomain counts on the 2x2x2 corner boxes against the restatement
+    (whose pencils there need only the 27 surrounding eigensplits)."""
+    p = problems.make("c5")
+    ctx = awg.context_from_problem(p)
+    try:
+        ctx.setup(awg.config_for(p))
+        _check_modes(p, ctx, "c5_corner")
+    finally:
+        ctx.close()
 
 
 def test_spmv_bit_identical_full_size(c2):
