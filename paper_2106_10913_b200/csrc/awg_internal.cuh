@@ -297,6 +297,7 @@ struct Ctx {
   int fused_cpb = 0, fused_nbuf = 0, fused_chunks_per_sm = 8;  // 0: automatic
   int pdl_early = 0;        // coarse-chain kernels release their dependents at entry (AWG_PDL_EARLY=1; measured neutral)
   int rows_group = 0;       // lanes per dof of the block-sparse prolongations (0: automatic)
+  bool pcg_adaptive = true;  // host batch sizes from the convergence rate (AWG_PCG_ADAPTIVE=0: doubling only)
   bool fused_static = true;  // NN: equal column shares per CTA instead of the atomic queue (AWG_FUSED_STATIC=0 off)
   bool fused_prefetch = true;  // next task's first steps issued during the current one (AWG_FUSED_PREFETCH=0 off)
   bool fused_hold = true;  // column values kept in registers across the step's reduction (AWG_FUSED_HOLD=0 off)

@@ -504,8 +504,15 @@ void run_pcg(Ctx& c, const double* b_dev, double rtol, int maxit, awg_solve_repo
     c.launches = before;
   }
   const long long per_graph = c.graph_launches[key];
-  int batch = 2;  // iterations enqueued before the next host check
+  // Iterations enqueued before the next host check: doubling up to 16, but
+  // capped by the iterations the recent convergence rate still needs to reach
+  // rtol — every iteration enqueued past the stop runs ~20 gated no-op
+  // kernels, and a 16-iteration batch could overshoot by up to 15 (c2: ~1% of
+  // the solve).  Host-side scheduling only: the device state decides.
+  int batch = 2;
   int issued = 0;
+  int prev_it = 0;
+  double prev_rel = 0.0;
   while (true) {
     for (int b = 0; b < batch && issued < maxit; b += kItersPerGraph, issued += kItersPerGraph) {
       AWG_CUDA(cudaGraphLaunch(exec, c.stream));
@@ -514,7 +521,15 @@ void run_pcg(Ctx& c, const double* b_dev, double rtol, int maxit, awg_solve_repo
     AWG_CUDA(cudaMemcpyAsync(&h, st, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
     AWG_CUDA(cudaStreamSynchronize(c.stream));
     if (h.done || issued >= maxit) break;
-    batch = std::min(batch * 2, 16);
+    int next = std::min(batch * 2, 16);
+    if (c.pcg_adaptive && prev_rel > 0.0 && h.it > prev_it && h.relres > rtol && h.relres < prev_rel) {
+      const double per_it = std::log(h.relres / prev_rel) / double(h.it - prev_it);  // < 0
+      const double need = std::log(rtol / h.relres) / per_it;                      // iterations left
+      if (need >= 0.0 && need < next) next = std::max(kItersPerGraph, int(std::ceil(need)));
+    }
+    prev_rel = h.relres;
+    prev_it = h.it;
+    batch = next;
   }
 
   if (!h.converged && h.it > 0 && !h.error) {

@@ -174,5 +174,13 @@ def test_pcg_full_size(c2):
     assert rep1.converged and rep1.iterations == rep2.iterations
     assert np.array_equal(x1, x2), "fixed-order reductions: repeated solves are bit-identical"
     true = np.linalg.norm(p.b - _spmv_reference_order(p, x1)) / np.linalg.norm(p.b)
+    # the host's batch sizing (convergence-rate estimate vs plain doubling) only
+    # schedules graph launches: the device state decides, results identical
+    fixed = _ctx_with(p, {"AWG_PCG_ADAPTIVE": "0"})
+    try:
+        x3, rep3 = fixed.pcg(p.b, p.rtol, 10000)
+    finally:
+        fixed.close()
+    assert rep3.iterations == rep1.iterations and np.array_equal(x3, x1)
     assert abs(true - rep1.final_relative_residual) <= 1e-6 * true  # krylov.cpp:98: the true residual
     assert true <= p.rtol or abs(true - rep1.recurrence_residual_at_exit) <= 1e-8  # krylov.cpp:93-101
