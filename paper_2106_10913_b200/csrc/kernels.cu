@@ -426,9 +426,12 @@ __global__ void __launch_bounds__(kFusedT, 1) k_nn_fused(const int* __restrict__
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   const size_t bstride = (size_t)CPB * ldmax;  // buffer b starts at fsm + b * bstride
   const unsigned long long pol = l2_evict_first();
-  // Persistent CTAs (one per SM) pull column chunks from an atomic queue; the
-  // chunk -> partial-slot map is fixed by the task list, so the result does not
-  // depend on which CTA ran which chunk.  A step covers CPB columns; g counts
+  // Persistent CTAs (one per SM).  NN: CTA b runs its own static task range
+  // [cta_off[b], cta_off[b + 1]) — equal column shares, so no SM idles at the
+  // end (profiles/r01e/knobs_static_c2.json); AS / AS+ (cta_off == nullptr):
+  // column chunks pulled from an atomic queue.  The chunk -> partial-slot map
+  // is fixed by the task list, so the result does not depend on which CTA ran
+  // which chunk.  A step covers CPB columns; g counts
   // the steps this CTA has consumed: buffer g % nbuf, mbarrier parity
   // (g / nbuf) & 1.  One barrier per step: red is double-buffered, and the
   // buffer of the previous step is refilled right after the barrier.
