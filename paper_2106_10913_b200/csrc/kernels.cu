@@ -883,19 +883,21 @@ __global__ void k_transpose(int r, const double* __restrict__ a, double* __restr
 
 // ---------------------------------------------------------------------------
 // Tall-skinny W (n x nm, column-major, ld): split-K W^T x, then W c.
-// CTA per (row chunk of kWChunk rows, group of 32 columns): the x chunk is staged
+// CTA per (row chunk of CH rows, group of 32 columns): the x chunk is staged
 // in shared memory (zero past n), one warp per column, 16-byte loads, 4 in flight
-// per lane; part[chunk * nm + j] holds the chunk's partial dot.
-constexpr int kWChunk = 4096;
+// per lane; part[chunk * nm + j] holds the chunk's partial dot.  CH = 4096, or
+// 1024 when that leaves fewer than 4 CTAs per SM (small W: c2's 262 columns
+// over 65,536 rows were 144 CTAs at 3.6 TB/s).
+template <int CH>
 __global__ void __launch_bounds__(kThreads) k_dense_gemvT_part(const int* __restrict__ gate, int n, int nm, int ldw,
                                                             const double* __restrict__ W, const double* __restrict__ x,
                                                             double* __restrict__ part) {
   if (gated(gate)) return;
-  __shared__ double2 sx2[kWChunk / 2];
+  __shared__ double2 sx2[CH / 2];
   double* sx = reinterpret_cast<double*>(sx2);
-  const int r0 = blockIdx.y * kWChunk;
-  const int rows = min(kWChunk, ldw - r0);  // ldw is a multiple of 4: pad rows of W are zero
-  for (int i = threadIdx.x; i < kWChunk; i += blockDim.x) sx[i] = (r0 + i < n) ? x[r0 + i] : 0.0;
+  const int r0 = blockIdx.y * CH;
+  const int rows = min(CH, ldw - r0);  // ldw is a multiple of 4: pad rows of W are zero
+  for (int i = threadIdx.x; i < CH; i += blockDim.x) sx[i] = (r0 + i < n) ? x[r0 + i] : 0.0;
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int npair = rows >> 1;
@@ -1418,9 +1420,14 @@ void zT(Ctx& c, const double* x, double* out, const int* gate) {
 }
 
 static void w_transpose_apply(Ctx& c, const double* x, double* out, const int* gate) {
-  const int nch = (c.ldw + kWChunk - 1) / kWChunk;
-  dim3 grid((c.nm + 31) / 32, nch);
-  launch(c, k_dense_gemvT_part, grid, kThreads, 0, gate, c.n, c.nm, c.ldw, c.W.p, x, c.wpart.p);
+  const int groups = (c.nm + 31) / 32;
+  const int ch = (long long)groups * ((c.ldw + 4095) / 4096) >= 4LL * c.sm_count ? 4096 : 1024;
+  const int nch = (c.ldw + ch - 1) / ch;
+  dim3 grid(groups, nch);
+  if (ch == 4096)
+    launch(c, k_dense_gemvT_part<4096>, grid, kThreads, 0, gate, c.n, c.nm, c.ldw, c.W.p, x, c.wpart.p);
+  else
+    launch(c, k_dense_gemvT_part<1024>, grid, kThreads, 0, gate, c.n, c.nm, c.ldw, c.W.p, x, c.wpart.p);
   ++c.launches;
   check_launch("dense_gemvT_part");
   launch(c, k_colsum, (c.nm + kThreads - 1) / kThreads, kThreads, 0, gate, c.nm, nch, c.wpart.p, out);

@@ -250,7 +250,7 @@ void Ctx::alloc_work() {
   const size_t cdim = size_t(std::max(n0, nm)) * 2 + 2;
   cz.alloc(cdim);
   cw.alloc(cdim);
-  const int nch = (round_up(n, 4) + 4095) / 4096;
+  const int nch = (round_up(n, 4) + 1023) / 1024;  // W^T x row chunks (1024 or 4096 rows, k::wT)
   wpart.alloc(size_t(std::max(nm, 1)) * nch);
   wpart2.alloc(size_t(w_chunks(*this)) * round_up(n, 4));
   red.alloc(size_t(sm_count) * 16);
