@@ -462,6 +462,7 @@ int awg_create(awg_ctx** out, int device) {
     cc.fused_prefetch = env_int("AWG_FUSED_PREFETCH", 1) != 0;
     cc.fused_static = env_int("AWG_FUSED_STATIC", 1) != 0;
     cc.pcg_adaptive = env_int("AWG_PCG_ADAPTIVE", 1) != 0;
+    cc.pdl_local = env_int("AWG_PDL_LOCAL", 1) != 0;
     cc.rows_group = env_int("AWG_ROWS_GROUP", 0);
     cc.pdl_early = env_int("AWG_PDL_EARLY", 0) != 0 ? 1 : 0;
     cc.w_split = env_int("AWG_W_SPLIT", -1);

@@ -297,6 +297,8 @@ struct Ctx {
   int fused_cpb = 0, fused_nbuf = 0, fused_chunks_per_sm = 8;  // 0: automatic
   int pdl_early = 0;        // coarse-chain kernels release their dependents at entry (AWG_PDL_EARLY=1; measured neutral)
   int rows_group = 0;       // lanes per dof of the block-sparse prolongations (0: automatic)
+  bool pdl_local = true;     // early trigger into the single-pass local solve + its pre-wait prologue (AWG_PDL_LOCAL=0 off)
+  int trigger_next = 0;     // set around the launch that precedes the local solve
   bool pcg_adaptive = true;  // host batch sizes from the convergence rate (AWG_PCG_ADAPTIVE=0: doubling only)
   bool fused_static = true;  // NN: equal column shares per CTA instead of the atomic queue (AWG_FUSED_STATIC=0 off)
   bool fused_prefetch = true;  // next task's first steps issued during the current one (AWG_FUSED_PREFETCH=0 off)
@@ -380,7 +382,10 @@ struct Ctx {
 // No kernel triggers its dependents early (griddepcontrol.launch_dependents):
 // measured on c2, waiting successor CTAs then crowd the running grid
 // (1,797 vs 1,875 applies/s); the implicit trigger at grid exit hides the
-// launch gap alone (+2.4% over no PDL).
+// launch gap alone (+2.4% over no PDL).  One exception: the A+ SpMV right
+// before the single-pass local solve triggers early, and the local solve
+// issues its first (constant) V^s copies before its griddepcontrol.wait
+// (AWG_PDL_LOCAL; H3 apply 0.475 -> 0.467 ms at c2, profiles/r01f/knobs_pdl_local_c2.json).
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // CSR row product  sum_k va[k] x[ci[k]]  in ascending k with separately

@@ -39,8 +39,10 @@ __device__ __forceinline__ bool gated(const int* gate) {
 // flush, so only the launch latency overlaps.  Off by default (AWG_PDL_EARLY=1):
 // measured neutral on c2 (profiles/r01c/knobs_c2.json, 0.511 vs 0.509-0.513 ms
 // per iteration), and the isolated Q / H3 applies slower by 1-2 us.
-// Not used by the single-pass kernel or its neighbours: waiting successor CTAs
-// next to the persistent local solve cost more than they hide.
+// Not used after the single-pass kernel: waiting successor CTAs next to the
+// persistent local solve cost more than they hide.  Before it (the pt SpMV,
+// AWG_PDL_LOCAL) the trigger lets the local solve's CTAs start their constant
+// V^s copies while the SpMV drains.
 __device__ __forceinline__ bool gated_early(const int* gate, int early) {
   if (early) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   return gated(gate);
@@ -130,8 +132,8 @@ template <int G>
 __global__ void k_spmv_aplus(const int* __restrict__ gate, int n, const int* __restrict__ rp,
                              const int* __restrict__ ci, const double* __restrict__ va,
                              const double* __restrict__ x, double* __restrict__ y, int mode,
-                             const double* __restrict__ sub, BlockSum am) {
-  if (gated(gate)) return;
+                             const double* __restrict__ sub, BlockSum am, int early) {
+  if (gated_early(gate, early)) return;
   // G lanes per row; the loop runs warp-uniformly (the lanes meet in shuffles)
   const int t = threadIdx.x & (G - 1);
   const int stride = int((gridDim.x * (long long)blockDim.x) / G);
@@ -404,10 +406,8 @@ __global__ void __launch_bounds__(kFusedT, 1) k_nn_fused(const int* __restrict__
                                                          const double* __restrict__ x, const double* __restrict__ rlam,
                                                          long long P, double* __restrict__ part, int ntasks,
                                                          int* __restrict__ queue, const int* __restrict__ cta_off, int nbuf, int ldmax,
-                                                         int smem_doubles, int prefetch,
+                                                         int smem_doubles, int prefetch, int prewait,
                                                          unsigned long long* __restrict__ tmr) {
-  if (gated(gate)) return;
-  if (tmr && threadIdx.x == 0) atomicMin(&tmr[0], globaltimer_ns());
   extern __shared__ __align__(128) double fsm[];
   __shared__ __align__(8) unsigned long long bar[kFusedMaxBuf];
   __shared__ double red[2][CPB][kFusedT / 32];
@@ -465,11 +465,30 @@ __global__ void __launch_bounds__(kFusedT, 1) k_nn_fused(const int* __restrict__
   unsigned g = 0;
   // static split: this CTA's own task range, no queue
   const int lim = cta_off ? cta_off[blockIdx.x + 1] : ntasks;
+  // prewait (static split): V^s is constant, so the first task's first copies
+  // are issued before griddepcontrol.wait — under the predecessor's early
+  // trigger they land while it finishes.  A gated launch drains them first.
+  __syncthreads();  // zero fill and barrier init before any copy
+  int issued0 = 0;
+  if (prewait && cta_off) {
+    const int c0 = cta_off[blockIdx.x];
+    if (c0 < lim) {
+      const GemvTask t0 = tasks[c0];
+      issued0 = min(nbuf, (t0.j1 - t0.j0 + CPB - 1) / CPB);
+      if (tid == 0)
+        for (int p = 0; p < issued0; ++p) issue(V + voff[t0.s], ld[t0.s], t0.j0, t0.j1, p, 0u);
+    }
+  }
+  if (gated(gate)) {
+    for (int b = 0; b < issued0; ++b) mbar_wait(&bar[b], 0);
+    return;
+  }
+  if (tmr && tid == 0) atomicMin(&tmr[0], globaltimer_ns());
   if (tid == 0) s_task = cta_off ? cta_off[blockIdx.x] : atomicAdd(queue, 1);
   __syncthreads();
   int cur = s_task;
   // thread 0 only: steps of the current task already issued; the next task
-  int pre = 0, nxt = lim, pre_n = 0, nstep_n = 0, j0_n = 0, j1_n = 0, s_n = 0, L_n = 0, fstage = 0;
+  int pre = issued0, nxt = lim, pre_n = 0, nstep_n = 0, j0_n = 0, j1_n = 0, s_n = 0, L_n = 0, fstage = 0;
   const double* V_n = V;
   // the next task's descriptor is a chain of dependent loads (queue -> task ->
   // ld / voff): one link per step, so thread 0 never stalls the CTA for the
@@ -1193,7 +1212,8 @@ void launch_fused(Ctx& c, const LocalPlan& pl, const double* F, const double* D,
   launch(c, k_nn_fused<TRI, R, CPB, HOLD>, grid, kFusedT, smem, gate, pl.tf.p, F, c.voff.p, c.ns.p, c.ld.p, c.poff.p,
          c.pidx.p, D, x, TRI ? nullptr : c.rlam.p, c.P, c.wpart_nn.p, int(pl.tf.n), c.fused_queue.p,
          pl.static_grid ? pl.cta_off.p : nullptr, nbuf, ldmax,
-         int(smem / sizeof(double)), int(c.fused_prefetch), c.fused_timer.p);
+         int(smem / sizeof(double)), int(c.fused_prefetch), int(c.pdl_local && pl.static_grid > 0),
+         c.fused_timer.p);
 }
 
 template <bool TRI, int CPB, bool HOLD>
@@ -1333,13 +1353,13 @@ void aplus(Ctx& c, const double* x, double* y, int mode, const double* sub, cons
   BlockSum bs = neg_sum(c);
   if (rows_group(c) == 8)
     launch(c, k_spmv_aplus<8>, grid_for(c, 8LL * c.n), kThreads, 0, gate, c.n, c.rp.p, c.ci.p, c.va.p, x, y, mode,
-           sub, bs);
+           sub, bs, c.trigger_next);
   else if (rows_group(c) == 4)
     launch(c, k_spmv_aplus<4>, grid_for(c, 4LL * c.n), kThreads, 0, gate, c.n, c.rp.p, c.ci.p, c.va.p, x, y, mode,
-                                                                       sub, bs);
+                                                                       sub, bs, c.trigger_next);
   else
     launch(c, k_spmv_aplus<1>, grid_for(c, c.n), kThreads, 0, gate, c.n, c.rp.p, c.ci.p, c.va.p, x, y, mode, sub,
-                                                                bs);
+                                                                bs, c.trigger_next);
   ++c.launches;
   check_launch("spmv_aplus");
 }

@@ -287,7 +287,9 @@ static void h2(Ctx& c, const double* x, double* y, const int* gate, const double
     if (extra) add_extra(c.t2.p);
     return;
   }
+  c.trigger_next = (c.pdl_local && c.use_pdl) ? 1 : 0;  // the local solve may start its copies early
   k::aplus(c, c.t0.p, c.t2.p, 2, x, gate, neg_ready);  // pt = x - A+ corr
+  c.trigger_next = 0;
   h1(c, c.t2.p, c.t3.p, gate);                     // hp
   if (after_h1) after_h1();  // enqueues work that must follow the local solve
   aplus(c, c.t3.p, c.t4.p, gate);                  // A+ hp

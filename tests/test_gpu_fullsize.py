@@ -155,7 +155,16 @@ def test_local_solve_variants_full_size(c2):
     two = _ctx_with(p, {"AWG_NN_TWO_PASS": "1"})
     nopf = _ctx_with(p, {"AWG_FUSED_PREFETCH": "0"})
     flip = _ctx_with(p, {"AWG_FUSED_STATIC": "0" if q["nn_static_split"] else "1"})
+    pdl = _ctx_with(p, {"AWG_PDL_LOCAL": "0" if os.environ.get("AWG_PDL_LOCAL") == "1" else "1"})
     try:
+        # the early trigger into the local solve and its pre-wait copies change
+        # scheduling only
+        for x in xs:
+            assert np.array_equal(pdl.apply(awg.Op.H1, x), ctx.apply(awg.Op.H1, x))
+            assert np.array_equal(pdl.apply(awg.Op.H3, x), ctx.apply(awg.Op.H3, x))
+        xa, ra = pdl.pcg(p.b, p.rtol, 10000)
+        xb, rb = ctx.pcg(p.b, p.rtol, 10000)
+        assert ra.iterations == rb.iterations and np.array_equal(xa, xb)
         for x, y in zip(xs, ref):
             assert rel(two.apply(awg.Op.H1, x), y) <= 1e-13
             assert np.array_equal(nopf.apply(awg.Op.H1, x), y)
@@ -165,6 +174,7 @@ def test_local_solve_variants_full_size(c2):
         two.close()
         nopf.close()
         flip.close()
+        pdl.close()
 
 
 def test_pcg_full_size(c2):
