@@ -133,7 +133,7 @@ typedef struct awg_stats {
   int w_inner_total;    /* sum of inner PCG iterations of build_w */
   int w_batches;        /* block passes of the batched W build (continuous batching) */
   int nn_single_pass;   /* 1: the NN local solve streams V^s once per apply (k_nn_fused) */
-  int nn_static_split;  /* 1: k_nn_fused runs equal static column shares per CTA (no work queue) */
+  int nn_static_split;  /* 1: k_nn_fused runs equal static byte shares per CTA (no work queue) */
 } awg_stats;
 
 int awg_create(struct awg_ctx** ctx, int device);

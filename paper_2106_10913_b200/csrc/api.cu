@@ -250,29 +250,41 @@ void finalize_factors(Ctx& c) {
       pl.static_grid = 0;
       pl.cta_off.release();
       if (!tri && c.fused_static) {
-        // static split: CTA b takes columns [b T / G, (b + 1) T / G) of the
-        // subdomains' column lists laid end to end (cut at subdomain ends), so
-        // every CTA streams the same bytes and the last round has no idle SMs
+        // static split (NN): the subdomains' column lists laid end to end and
+        // cut into G shares of equal column counts, each CTA's share split at
+        // subdomain ends into tasks, so no SM idles at the end as in the work
+        // queue's last round.  Equal columns, not equal bytes: every column
+        // costs a CTA the same R rows per thread of shared-memory traffic and
+        // FMAs whatever its ld_s, and equal-byte shares measured 2% slower
+        // (AWG_FUSED_STATIC_COLS=0, profiles/r01f/knobs_static_cols_c2.json).
+        // Not for the triangular U^s (AS / AS+): there a column moves j + 1
+        // rows but still costs a full column of compute, and equal-byte shares
+        // measured 18% slower than the queue (profiles/r01f/knobs_static_as_c2.json)
         const int G = int(std::max<long long>(1, std::min<long long>(cols_total, std::max(1, c.sm_count - c.fused_reserve))));
+        const char* by_cols = std::getenv("AWG_FUSED_STATIC_COLS");  // "0": equal bytes instead (A/B)
+        const bool cols_only = !(by_cols && by_cols[0] == '0');
+        auto cost = [&](int s, int) -> long long { return cols_only ? 1LL : c.h_ld[s]; };
+        long long T = 0;
+        for (int s = 0; s < N; ++s)
+          for (int j = c.h_m[s]; j < c.h_ns[s]; ++j) T += cost(s, j);
         tf.clear();
         std::fill(nkf.begin(), nkf.end(), 0);
         std::vector<int> off(G + 1, 0);
-        int s = 0, j = c.h_m[0];
-        for (int b = 0; b < G; ++b) {
-          off[b] = int(tf.size());
-          long long want = (long long)cols_total * (b + 1) / G - (long long)cols_total * b / G;
-          while (want > 0 && s < N) {
-            const int end = c.h_ns[s];
-            const int take = int(std::min<long long>(want, end - j));
-            if (take > 0) {
-              tf.push_back({s, 0, j, j + take, nkf[s]++, 0});
-              j += take;
-              want -= take;
+        int b = 0;
+        long long acc = 0;
+        for (int s = 0; s < N; ++s) {
+          int j0 = c.h_m[s];
+          for (int j = j0; j < c.h_ns[s]; ++j) {
+            acc += cost(s, j);
+            while (b < G - 1 && acc * G >= T * (b + 1)) {  // CTA b's share ends after column j
+              if (j + 1 > j0) tf.push_back({s, 0, j0, j + 1, nkf[s]++, 0});
+              j0 = j + 1;
+              off[++b] = int(tf.size());
             }
-            if (j >= end && ++s < N) j = c.h_m[s];
           }
+          if (c.h_ns[s] > j0) tf.push_back({s, 0, j0, c.h_ns[s], nkf[s]++, 0});
         }
-        off[G] = int(tf.size());
+        for (int bb = b + 1; bb <= G; ++bb) off[bb] = int(tf.size());
         pl.kcmax_f = 1;
         for (int v : nkf) pl.kcmax_f = std::max(pl.kcmax_f, v);
         pl.cta_off.upload(off, c.stream);
@@ -851,7 +863,10 @@ int awg_query(awg_ctx* ctx, awg_stats* st) {
     for (int v : c.h_w_inner) st->w_inner_total += v;
     st->w_batches = c.w_batches;
     st->nn_single_pass = ((c.one_level == 2 && c.plan_nn.fused) || (c.one_level != 2 && c.plan_as.fused)) ? 1 : 0;
-    st->nn_static_split = (c.one_level == 2 && c.plan_nn.fused && c.plan_nn.static_grid > 0) ? 1 : 0;
+    {
+      const LocalPlan& lp = c.one_level == 2 ? c.plan_nn : c.plan_as;
+      st->nn_static_split = (lp.fused && lp.static_grid > 0) ? 1 : 0;
+    }
   });
 }
 

@@ -300,7 +300,7 @@ struct Ctx {
   bool pdl_local = true;     // early trigger into the single-pass local solve + its pre-wait prologue (AWG_PDL_LOCAL=0 off)
   int trigger_next = 0;     // set around the launch that precedes the local solve
   bool pcg_adaptive = true;  // host batch sizes from the convergence rate (AWG_PCG_ADAPTIVE=0: doubling only)
-  bool fused_static = true;  // NN: equal column shares per CTA instead of the atomic queue (AWG_FUSED_STATIC=0 off)
+  bool fused_static = true;  // equal byte shares per CTA instead of the atomic queue (AWG_FUSED_STATIC=0 off)
   bool fused_prefetch = true;  // next task's first steps issued during the current one (AWG_FUSED_PREFETCH=0 off)
   bool fused_hold = true;  // column values kept in registers across the step's reduction (AWG_FUSED_HOLD=0 off)
   BsPlan bs_neg, bs_z;   // A- dots (V^s columns k < n_nonpos), Z^T x (Y_s blocks)

@@ -427,9 +427,9 @@ __global__ void __launch_bounds__(kFusedT, 1) k_nn_fused(const int* __restrict__
   const size_t bstride = (size_t)CPB * ldmax;  // buffer b starts at fsm + b * bstride
   const unsigned long long pol = l2_evict_first();
   // Persistent CTAs (one per SM).  NN: CTA b runs its own static task range
-  // [cta_off[b], cta_off[b + 1]) — equal column shares, so no SM idles at the
-  // end (profiles/r01e/knobs_static_c2.json); AS / AS+ (cta_off == nullptr):
-  // column chunks pulled from an atomic queue.  The chunk -> partial-slot map
+  // [cta_off[b], cta_off[b + 1]) — equal byte shares, so no SM idles at the
+  // end (profiles/r01e/knobs_static_c2.json); AS / AS+ and AWG_FUSED_STATIC=0
+  // (cta_off == nullptr): column chunks pulled from an atomic queue.  The chunk -> partial-slot map
   // is fixed by the task list, so the result does not depend on which CTA ran
   // which chunk.  A step covers CPB columns; g counts
   // the steps this CTA has consumed: buffer g % nbuf, mbarrier parity

@@ -17,7 +17,8 @@ for spec in sys.argv[2:]:
     os.environ.update(env)
     try:
         ctx = awg.context_from_problem(p)
-        ctx.setup(awg.config_for(p))
+        kind = os.environ.get("ONE_LEVEL", "NN")  # NN | AS | AS_PLUS
+        ctx.setup(awg.config_for(p, one_level=getattr(awg.OneLevelKind, kind)))
         best = 1e9
         x, rep = ctx.pcg(p.b, p.rtol, 10000)
         ctx.kernel_timer(reset=True)
