@@ -167,10 +167,34 @@ int awg_assemble_elasticity(struct awg_ctx* ctx, int nodes_x, int nodes_y, int l
 int awg_partition_owner(struct awg_ctx* ctx, const int* owner, int n_sub, int overlap);
 int awg_partition_boxes(struct awg_ctx* ctx, const int* boxes, int overlap);
 
+/* Experiment switches for tests and profiles (no reference counterpart; the
+ * product defaults are frozen in the library and no environment variable is
+ * read).  Names: pdl, nn_two_pass, fused_cpb, fused_hold, fused_prefetch,
+ * fused_static, fused_static_cols, pcg_adaptive, pdl_local, pdl_early,
+ * rows_group, w_split, fused_nbuf, fused_chunks, fused_reserve,
+ * fused_min_cols, fused_tail, synth_nm, dgemm_variant, coarse_neg, verbose,
+ * wbuild_cublas.  Unknown names return AWG_E_ARG. */
+int awg_set_option(struct awg_ctx* ctx, const char* name, long long value);
+
 int awg_setup(struct awg_ctx* ctx, const awg_config* cfg);
+
+/* rank_revealing_sym_factor (src/dense.cpp:299-346; RankRevealingFactor,
+ * include/awg/dense.hpp:78-89) on a caller-supplied symmetric n x n G
+ * (column-major, host): the device pivoted factor that awg_setup runs on
+ * Z^T A+ Z (coarse.cpp:145-152) and W^T A W (preconditioner.cpp:119-126),
+ * exposed so its retained set can be checked directly.  exact = 0: the
+ * reference's semantics (stale-upper swap), 1: exact pivoted Cholesky.
+ * Writes rank r, retained[r] (pivot order) and l11[r*r] (lower, column-major;
+ * caller sizes both for r = n). */
+int awg_pivoted_factor(struct awg_ctx* ctx, int n, const double* G, int exact, int* rank, int* retained,
+                       double* l11);
 int awg_load_factors(struct awg_ctx* ctx, const awg_config* cfg, const awg_factors* f);
 
 int awg_apply(struct awg_ctx* ctx, int op, const double* x, double* y, int ptr_kind);
+/* rank_revealing_solve (src/dense.cpp:348-366) with the factor awg_setup built:
+ * which = 0 K0 (dimension n0, coarse.cpp:156-166), 1 KW (n_minus,
+ * preconditioner.cpp:149-159); b and x host vectors of that dimension. */
+int awg_coarse_solve(struct awg_ctx* ctx, int which, const double* b, double* x);
 int awg_pcg(struct awg_ctx* ctx, const double* b, double* x, double rtol, int maxit, int ptr_kind,
             awg_solve_report* report);
 

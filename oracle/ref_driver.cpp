@@ -124,6 +124,8 @@ struct Args {
   int export_dense = 0;
   int w_probe = 0;          // > 0: run build_w's inner solve for this many W columns, bounded, then exit
   int w_probe_maxit = 3000;
+  std::string phase;        // "", "bs", "pencil", "w": fill the memo cache (oracle/memo.cpp) for one worker's share
+  int worker = 0, nworkers = 1;
 };
 
 Args parse(int argc, char** argv) {
@@ -162,6 +164,9 @@ Args parse(int argc, char** argv) {
     else if (k == "--export-dense") a.export_dense = std::stoi(next());
     else if (k == "--w-probe") a.w_probe = std::stoi(next());
     else if (k == "--w-probe-maxit") a.w_probe_maxit = std::stoi(next());
+    else if (k == "--phase") a.phase = next();
+    else if (k == "--worker") a.worker = std::stoi(next());
+    else if (k == "--nworkers") a.nworkers = std::stoi(next());
     else {
       std::fprintf(stderr, "unknown flag %s\n", k.c_str());
       std::exit(2);
@@ -300,11 +305,37 @@ int sample_mode(const std::string& prefix, double budget_s, int n0, int n_minus,
     return timeit([&] { rank_revealing_solve(f, b.data(), xx.data()); }, std::min(slot, 0.5));
   };
   const double t_k0 = rrs_time(n0), t_kw = rrs_time(n_minus);
-  // A- x: per subdomain q_s ~ m_avg dot+axpy pairs over n_s (splitting.cpp:119-140)
-  double sum_ns = 0;
-  for (int s = 0; s < N; ++s) sum_ns += part.size_of(s);
-  const double t_vec_elem = t_spmv / std::max(1, a.nnz());  // per fused element, as a lower bound
-  const double t_aminus = 4.0 * m_avg * sum_ns * t_vec_elem;
+  // A- x (splitting.cpp:119-140, the same loop on random modes): per subdomain
+  // restrict, m_avg dot + axpy pairs over n_s, prolong_add — timed on a sample
+  // of subdomains and scaled to all of them
+  double t_am_sum = 0.0;
+  int am_sampled = 0;
+  t_start = now_s();
+  for (int s = 0; s < N && (am_sampled < 4 || (now_s() - t_start) < slot * 0.5); ++s) {
+    const int ns = part.size_of(s);
+    const int q = std::max(1, std::min(m_avg, ns));
+    DenseMatrix v(ns, q);
+    std::vector<double> r = uniform_vec(300 + s, ns, -1.0, 1.0);
+    for (size_t i = 0; i < v.a.size(); ++i) v.a[i] = r[i % ns];
+    std::vector<double> xs(ns), u(ns), lam(q, -1e-3);
+    const auto& om = part.omega[s];
+    t_am_sum += timeit(
+        [&] {
+          for (int k = 0; k < ns; ++k) xs[k] = x[om[k]];
+          std::fill(u.begin(), u.end(), 0.0);
+          for (int k = 0; k < q; ++k) {
+            const double* vk = v.col(k);
+            double dot = 0.0;
+            for (int i = 0; i < ns; ++i) dot += vk[i] * xs[i];
+            const double f = -lam[k] * dot;
+            for (int i = 0; i < ns; ++i) u[i] += f * vk[i];
+          }
+          for (int k = 0; k < ns; ++k) y[om[k]] += u[k];
+        },
+        0.0);
+    ++am_sampled;
+  }
+  const double t_aminus = t_am_sum / std::max(am_sampled, 1) * N;
   const double t_q = t_z + t_k0;
   const double t_h2 = 3.0 * t_q + 2.0 * (t_aminus + t_spmv) + t_h1;
   const double t_h3 = t_h2 + t_w + t_kw;
@@ -313,17 +344,40 @@ int sample_mode(const std::string& prefix, double budget_s, int n0, int n_minus,
   std::fprintf(js,
                "{\"t_h3_apply_s\": %.9g, \"t_iter_s\": %.9g, \"t_spmv_s\": %.9g, \"t_h1_s\": %.9g, "
                "\"t_z_pair_s\": %.9g, \"t_w_pair_s\": %.9g, \"t_k0_solve_s\": %.9g, \"t_kw_solve_s\": %.9g, "
+               "\"t_aminus_s\": %.9g, \"aminus_sampled\": %d, "
                "\"sampled_subdomains\": %d, \"n_sub\": %d, \"n\": %d, \"n0\": %d, \"n_minus\": %d, "
                "\"elapsed_s\": %.3f}\n",
-               t_h3, t_iter, t_spmv, t_h1, t_z, t_w, t_k0, t_kw, sampled, N, n, n0, n_minus,
+               t_h3, t_iter, t_spmv, t_h1, t_z, t_w, t_k0, t_kw, t_aminus, am_sampled, sampled, N, n, n0, n_minus,
                now_s() - t_start);
   std::fclose(js);
+  return 0;
+}
+
+// ref_driver --rrf <G.bin> <outdir>: rank_revealing_sym_factor (dense.cpp:299-346)
+// of one symmetric matrix (G.bin = int32 n, then n*n float64 column-major);
+// exports retained and l11 for the device pivoted-factor parity test.
+int rrf_mode(const std::string& in, const std::string& out) {
+  FILE* f = std::fopen(in.c_str(), "rb");
+  if (!f) return 2;
+  int n = 0;
+  if (std::fread(&n, sizeof n, 1, f) != 1 || n < 0) return 2;
+  DenseMatrix g(n, n);
+  if (std::fread(g.a.data(), sizeof(double), g.a.size(), f) != g.a.size()) return 2;
+  std::fclose(f);
+  const RankRevealingFactor rf = rank_revealing_sym_factor(g);
+  npy_i(out, "retained", rf.retained);
+  npy_mat(out, "l11", rf.l11);
   return 0;
 }
 
 }  // namespace
 
 int main(int argc, char** argv) {
+  if (argc >= 4 && std::string(argv[1]) == "--rrf") {
+    std::string cmd = "mkdir -p '" + std::string(argv[3]) + "'";
+    if (std::system(cmd.c_str()) != 0) return 2;
+    return rrf_mode(argv[2], argv[3]);
+  }
   if (argc >= 3 && std::string(argv[1]) == "--sample") {
     // ref_driver --sample <prefix> <outdir> <budget_s> <n0> <n_minus> <m_avg>
     if (argc < 8) {
@@ -353,6 +407,13 @@ int main(int argc, char** argv) {
   }
   double t_read = now_s() - t0;
 
+  if (args.phase == "bs") {
+    // Worker share of the Splitting constructor's eigsplits (splitting.cpp:86-90):
+    // the memoised dense_sym_eig stores each result for the replay run.
+    auto bs = build_Bs(a, part);
+    for (int s = args.worker; s < part.count(); s += args.nworkers) (void)eigsplit(bs[s], s);
+    return 0;
+  }
   t0 = now_s();
   PartitionOfUnity pou = build_pou(part);
   Splitting split(a, part, pou);
@@ -370,6 +431,20 @@ int main(int argc, char** argv) {
     eps[s] = split.splits()[s].eps_zero;
   }
 
+  const OneLevelKind kind0 =
+      args.one_level == "AS" ? OneLevelKind::AS : args.one_level == "AS_PLUS" ? OneLevelKind::AS_PLUS : OneLevelKind::NN;
+  if (args.phase == "pencil") {
+    // Worker share of the GenEO pencils (coarse.cpp:98-111), memoised.
+    for (int s = args.worker; s < N; s += args.nworkers) {
+      if (kind0 == OneLevelKind::AS) {
+        (void)geneo.pencil_as1(s);
+        (void)geneo.pencil_as2(s);
+      } else {
+        (void)geneo.pencil_nn(s);
+      }
+    }
+    return 0;
+  }
   t0 = now_s();
   std::vector<int> ks;
   CoarseSpace cs;
@@ -414,6 +489,25 @@ int main(int argc, char** argv) {
   const Composition comp = args.comp == "additive" ? Composition::ADDITIVE : Composition::HYBRID;
   auto h2 = std::make_shared<TwoLevel>(OneLevel(kind, split), cs, comp, split);
 
+  if (args.phase == "w") {
+    // Worker share of build_w's inner solves (preconditioner.cpp:97-113):
+    // the same right-hand sides, tolerance and iteration cap, memoised pcg.
+    const ApplyFn aplus = [&split](const double* u, double* v) { split.apply_Aplus(u, v); };
+    const ApplyFn happly = [&h2](const double* u, double* v) { h2->apply(u, v); };
+    std::vector<double> rhs(n);
+    int col = 0;
+    for (int s = 0; s < N; ++s) {
+      const LocalSplit& ls = split.splits()[s];
+      for (int k = 0; k < ls.n_nonpos; ++k) {
+        if (ls.eig.eigenvalues[k] == 0.0) continue;
+        if (col++ % args.nworkers != args.worker) continue;
+        std::fill(rhs.begin(), rhs.end(), 0.0);
+        split.prolong_add(s, ls.eig.eigenvectors.col(k), rhs.data());
+        (void)pcg(aplus, happly, rhs, args.w_rtol, 10 * n);
+      }
+    }
+    return 0;
+  }
   if (args.w_probe > 0) {
     // The inner solve of build_w (preconditioner.cpp:97-113) for the first
     // w_probe strictly negative modes, with maxit bounded: reports how the

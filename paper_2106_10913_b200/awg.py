@@ -165,7 +165,8 @@ EXPORTED_SYMBOLS = [
     "awg_set_partition", "awg_setup", "awg_load_factors", "awg_apply", "awg_pcg", "awg_query",
     "awg_get_history", "awg_get_array", "awg_launch_count", "awg_time_apply", "awg_time_kernel",
     "awg_synthetic_factors", "awg_kernel_timer", "awg_assemble_fd", "awg_assemble_elasticity", "awg_partition_owner",
-    "awg_partition_boxes", "awg_bench_dgemm",
+    "awg_partition_boxes", "awg_bench_dgemm", "awg_set_option", "awg_pivoted_factor",
+    "awg_coarse_solve",
 ]
 
 _lib = None
@@ -194,6 +195,9 @@ def load_library(path: str = LIB_PATH):
     lib.awg_assemble_elasticity.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _dp, _dp, _dp]
     lib.awg_partition_owner.argtypes = [vp, _ip, ctypes.c_int, ctypes.c_int]
     lib.awg_partition_boxes.argtypes = [vp, _ip, ctypes.c_int]
+    lib.awg_set_option.argtypes = [vp, ctypes.c_char_p, ctypes.c_longlong]
+    lib.awg_coarse_solve.argtypes = [vp, ctypes.c_int, _dp, _dp]
+    lib.awg_pivoted_factor.argtypes = [vp, ctypes.c_int, _dp, ctypes.c_int, _ip, _ip, _dp]
     lib.awg_setup.argtypes = [vp, ctypes.POINTER(_Config)]
     lib.awg_load_factors.argtypes = [vp, ctypes.POINTER(_Config), ctypes.POINTER(_Factors)]
     lib.awg_apply.argtypes = [vp, ctypes.c_int, vp, vp, ctypes.c_int]
@@ -498,7 +502,7 @@ class ProblemContext:
         which, kind = _ARRAYS[name]
         cnt = ctypes.c_longlong()
         self._check(self._lib.awg_get_array(self._h, which, None, 0, ctypes.byref(cnt)))
-        arr = np.zeros(max(cnt.value, 1), dtype=np.int32 if kind == "i" else np.float64)
+        arr = np.empty(max(cnt.value, 1), dtype=np.int32 if kind == "i" else np.float64)
         self._check(self._lib.awg_get_array(self._h, which, arr.ctypes.data_as(ctypes.c_void_p), cnt.value,
                                              ctypes.byref(cnt)))
         return arr[:cnt.value]
@@ -509,6 +513,26 @@ class ProblemContext:
 
     def launch_count(self) -> int:
         return int(self._lib.awg_launch_count(self._h))
+
+    def coarse_solve(self, which: str, b) -> np.ndarray:
+        """rank_revealing_solve (dense.cpp:348-366) with the device's K0
+        (which="k0") or KW ("kw") factor."""
+        b = _f64(b)
+        x = np.zeros_like(b)
+        self._check(self._lib.awg_coarse_solve(self._h, 0 if which == "k0" else 1, b.ctypes.data_as(_dp),
+                                               x.ctypes.data_as(_dp)))
+        return x
+
+    def set_option(self, name: str, value: int) -> "ProblemContext":
+        """Experiment switch (tests / profiles only; awg_set_option): the
+        product defaults are frozen in the library."""
+        self._check(self._lib.awg_set_option(self._h, name.encode(), int(value)))
+        return self
+
+    def set_options(self, opts: Optional[Dict[str, int]]) -> "ProblemContext":
+        for k, v in (opts or {}).items():
+            self.set_option(k, v)
+        return self
 
     # -- reference-shaped views -------------------------------------------------
     def splitting(self) -> "Splitting":
@@ -570,10 +594,29 @@ def pcg(ctx: ProblemContext, b, rtol: float, maxit: int):
     return ctx.pcg(b, rtol, maxit)
 
 
-def context_from_problem(p, device: int = 0) -> ProblemContext:
-    """ProblemContext from a problems.Problem."""
+def pivoted_factor(g, exact: bool = False, device: int = 0) -> Tuple[np.ndarray, np.ndarray]:
+    """rank_revealing_sym_factor (dense.cpp:299-346) of a symmetric matrix on
+    the device (awg_pivoted_factor): (retained pivot order, l11 r x r lower)."""
+    g = np.asfortranarray(np.asarray(g, dtype=np.float64))
+    n = g.shape[0]
+    ctx = ProblemContext._bare(device)
+    try:
+        rank = ctypes.c_int()
+        ret = np.zeros(max(n, 1), dtype=np.int32)
+        l11 = np.zeros(max(n * n, 1), dtype=np.float64)
+        ctx._check(ctx._lib.awg_pivoted_factor(ctx._h, n, g.ctypes.data_as(_dp), int(bool(exact)), ctypes.byref(rank),
+                                               ret.ctypes.data_as(_ip), l11.ctypes.data_as(_dp)))
+        r = rank.value
+        return ret[:r].copy(), l11[:r * r].reshape(r, r, order="F").copy()
+    finally:
+        ctx.close()
+
+
+def context_from_problem(p, device: int = 0, options: Optional[Dict[str, int]] = None) -> ProblemContext:
+    """ProblemContext from a problems.Problem (``options``: awg_set_option
+    switches, tests / profiles only)."""
     a = SparseSymMatrix(p.n, p.row_offsets, p.col_indices, p.values)
-    return ProblemContext(a, p.b, Partition(list(p.omega), p.n), device=device)
+    return ProblemContext(a, p.b, Partition(list(p.omega), p.n), device=device).set_options(options)
 
 
 def context_from_spec(sp: dict, device: int = 0) -> ProblemContext:

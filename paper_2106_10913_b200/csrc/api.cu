@@ -256,13 +256,12 @@ void finalize_factors(Ctx& c) {
         // queue's last round.  Equal columns, not equal bytes: every column
         // costs a CTA the same R rows per thread of shared-memory traffic and
         // FMAs whatever its ld_s, and equal-byte shares measured 2% slower
-        // (AWG_FUSED_STATIC_COLS=0, profiles/r01f/knobs_static_cols_c2.json).
+        // (option fused_static_cols=0, profiles/r01f/knobs_static_cols_c2.json).
         // Not for the triangular U^s (AS / AS+): there a column moves j + 1
         // rows but still costs a full column of compute, and equal-byte shares
         // measured 18% slower than the queue (profiles/r01f/knobs_static_as_c2.json)
         const int G = int(std::max<long long>(1, std::min<long long>(cols_total, std::max(1, c.sm_count - c.fused_reserve))));
-        const char* by_cols = std::getenv("AWG_FUSED_STATIC_COLS");  // "0": equal bytes instead (A/B)
-        const bool cols_only = !(by_cols && by_cols[0] == '0');
+        const bool cols_only = c.opt("fused_static_cols", 1) != 0;  // 0: equal bytes instead (A/B)
         auto cost = [&](int s, int) -> long long { return cols_only ? 1LL : c.h_ld[s]; };
         long long T = 0;
         for (int s = 0; s < N; ++s)
@@ -448,41 +447,14 @@ int awg_create(awg_ctx** out, int device) {
     AWG_CUDA(cudaSetDevice(device));
     // the solve's critical path (main stream) outranks the concurrent W branch
     // (side stream); graph kernel nodes keep these priorities (ops.cu)
-    const char* prio = std::getenv("AWG_STREAM_PRIORITY");
-    cc.use_priority = !(prio && prio[0] == '0');
-    const char* pdl = std::getenv("AWG_PDL");
-    cc.use_pdl = !(pdl && pdl[0] == '0');
     int lo = 0, hi = 0;
     AWG_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    const bool side_first = prio && prio[0] == '2';  // experiment: the W branch outranks the main stream
-    AWG_CUDA(cudaStreamCreateWithPriority(&cc.stream, cudaStreamNonBlocking,
-                                          cc.use_priority ? (side_first ? lo : hi) : 0));
-    AWG_CUDA(cudaStreamCreateWithPriority(&cc.side, cudaStreamNonBlocking,
-                                          cc.use_priority ? (side_first ? hi : lo) : 0));
+    AWG_CUDA(cudaStreamCreateWithPriority(&cc.stream, cudaStreamNonBlocking, hi));
+    AWG_CUDA(cudaStreamCreateWithPriority(&cc.side, cudaStreamNonBlocking, lo));
     AWG_CUDA(cudaEventCreateWithFlags(&cc.ev_fork, cudaEventDisableTiming));
     AWG_CUDA(cudaEventCreateWithFlags(&cc.ev_join, cudaEventDisableTiming));
     AWG_CUDA(cudaEventCreateWithFlags(&cc.ev_mid, cudaEventDisableTiming));
     AWG_CUDA(cudaDeviceGetAttribute(&cc.sm_count, cudaDevAttrMultiProcessorCount, device));
-    const char* two_pass = std::getenv("AWG_NN_TWO_PASS");
-    cc.use_fused = !(two_pass && two_pass[0] == '1');
-    auto env_int = [](const char* k, int dflt) {
-      const char* v = std::getenv(k);
-      return v ? std::atoi(v) : dflt;
-    };
-    cc.fused_cpb = env_int("AWG_FUSED_CPB", 0);
-    cc.fused_hold = env_int("AWG_FUSED_HOLD", 1) != 0;
-    cc.fused_prefetch = env_int("AWG_FUSED_PREFETCH", 1) != 0;
-    cc.fused_static = env_int("AWG_FUSED_STATIC", 1) != 0;
-    cc.pcg_adaptive = env_int("AWG_PCG_ADAPTIVE", 1) != 0;
-    cc.pdl_local = env_int("AWG_PDL_LOCAL", 1) != 0;
-    cc.rows_group = env_int("AWG_ROWS_GROUP", 0);
-    cc.pdl_early = env_int("AWG_PDL_EARLY", 0) != 0 ? 1 : 0;
-    cc.w_split = env_int("AWG_W_SPLIT", -1);
-    cc.fused_nbuf = env_int("AWG_FUSED_NBUF", 0);
-    cc.fused_chunks_per_sm = std::max(1, env_int("AWG_FUSED_CHUNKS", 8));
-    cc.fused_reserve = std::max(0, env_int("AWG_FUSED_RESERVE", 0));
-    cc.fused_min_cols = std::max(8, env_int("AWG_FUSED_MINCOLS", 128));
-    cc.fused_tail_pct = std::max(0, std::min(90, env_int("AWG_FUSED_TAIL", 0)));
   });
   *out = ctx;
   return rc;
@@ -507,6 +479,63 @@ void awg_destroy(awg_ctx* ctx) {
 const char* awg_last_error(const awg_ctx* ctx) { return ctx ? ctx->c.err.c_str() : "null context"; }
 int awg_last_error_index(const awg_ctx* ctx) { return ctx ? ctx->c.err_index : -1; }
 long long awg_launch_count(const awg_ctx* ctx) { return ctx ? ctx->c.launches : 0; }
+
+int awg_set_option(awg_ctx* ctx, const char* name, long long value) {
+  return guarded(ctx, [&](Ctx& c) {
+    if (!name) c.fail(AWG_E_ARG, "set_option: null name");
+    const std::string k = name;
+    const int v = int(value);
+    if (k == "pdl") c.use_pdl = v != 0;
+    else if (k == "nn_two_pass") c.use_fused = v == 0;
+    else if (k == "fused_cpb") c.fused_cpb = v;
+    else if (k == "fused_hold") c.fused_hold = v != 0;
+    else if (k == "fused_prefetch") c.fused_prefetch = v != 0;
+    else if (k == "fused_static") c.fused_static = v != 0;
+    else if (k == "pcg_adaptive") c.pcg_adaptive = v != 0;
+    else if (k == "pdl_local") c.pdl_local = v != 0;
+    else if (k == "rows_group") c.rows_group = v;
+    else if (k == "pdl_early") c.pdl_early = v != 0 ? 1 : 0;
+    else if (k == "w_split") c.w_split = v;
+    else if (k == "fused_nbuf") c.fused_nbuf = v;
+    else if (k == "fused_chunks") c.fused_chunks_per_sm = std::max(1, v);
+    else if (k == "fused_reserve") c.fused_reserve = std::max(0, v);
+    else if (k == "fused_min_cols") c.fused_min_cols = std::max(8, v);
+    else if (k == "fused_tail") c.fused_tail_pct = std::max(0, std::min(90, v));
+    else if (k == "fused_static_cols" || k == "synth_nm" || k == "dgemm_variant" || k == "coarse_neg" ||
+             k == "verbose" || k == "wbuild_cublas" || k == "rrf_exact_probe")
+      c.opts[k] = value;
+    else
+      c.fail(AWG_E_ARG, "set_option: unknown option " + k);
+  });
+}
+
+int awg_pivoted_factor(awg_ctx* ctx, int n, const double* G, int exact, int* rank, int* retained, double* l11) {
+  return guarded(ctx, [&](Ctx& c) {
+    if (n < 0 || (n > 0 && !G) || !rank) c.fail(AWG_E_ARG, "pivoted_factor: bad arguments");
+    CoarseFactor f;
+    pivoted_factor_of(c, n, G, exact ? 1 : 0, f);
+    *rank = f.rank;
+    if (retained) std::copy(f.h_retained.begin(), f.h_retained.end(), retained);
+    if (l11) std::copy(f.h_l11.begin(), f.h_l11.end(), l11);
+  });
+}
+
+int awg_coarse_solve(awg_ctx* ctx, int which, const double* b, double* x) {
+  return guarded(ctx, [&](Ctx& c) {
+    if (!c.have_factors) c.fail(AWG_E_STATE, "coarse_solve: preconditioner not set up");
+    if (which != 0 && which != 1) c.fail(AWG_E_ARG, "coarse_solve: which must be 0 (K0) or 1 (KW)");
+    const CoarseFactor& f = which == 0 ? c.k0 : c.kw;
+    if (!b || !x) c.fail(AWG_E_ARG, "coarse_solve: null vector");
+    if (f.dim == 0) return;
+    DArr<double> db, dx;
+    db.alloc(f.dim);
+    dx.alloc(f.dim);
+    AWG_CUDA(cudaMemcpyAsync(db.p, b, sizeof(double) * f.dim, cudaMemcpyHostToDevice, c.stream));
+    k::rr_solve(c, f, db.p, dx.p, nullptr);
+    AWG_CUDA(cudaMemcpyAsync(x, dx.p, sizeof(double) * f.dim, cudaMemcpyDeviceToHost, c.stream));
+    AWG_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
 
 int awg_set_matrix(awg_ctx* ctx, int n, const int* rp, const int* ci, const double* va) {
   return guarded(ctx, [&](Ctx& c) {
@@ -636,6 +665,8 @@ int awg_load_factors(awg_ctx* ctx, const awg_config* cfg, const awg_factors* f) 
       c.k0.clear();
     }
     c.nm = (cfg->awg_mode != 0) ? f->n_minus : 0;
+    if (c.nm > 0 && c.nm != c.nneg)
+      c.fail(AWG_E_ARG, "load_factors: n_minus does not match the strictly negative modes of lam / n_nonpos");
     c.ldw = round_up(c.n, 4);
     if (c.nm > 0) {
       if (!f->W || !f->kw_retained || !f->kw_l11) c.fail(AWG_E_ARG, "load_factors: W factors missing");
@@ -692,10 +723,9 @@ int awg_synthetic_factors(awg_ctx* ctx, int m_per_sub, unsigned long long seed) 
     c.Y.alloc(1);
     c.k0.clear();
     c.kw.clear();
-    // optional synthetic W (n x AWG_SYNTH_NM, hash-filled) for timing the
+    // optional synthetic W (n x option synth_nm, hash-filled) for timing the
     // W^T x / W c kernels at full scale without the setup (time_kernel 3, 4)
-    const char* snm = std::getenv("AWG_SYNTH_NM");
-    c.nm = snm ? std::max(0, std::atoi(snm)) : 0;
+    c.nm = int(std::max(0LL, c.opt("synth_nm", 0)));
     c.ldw = round_up(c.n, 4);
     if (c.nm) {
       c.W.alloc(size_t(c.ldw) * c.nm);
@@ -723,7 +753,7 @@ int awg_apply(awg_ctx* ctx, int op, const double* x, double* y, int ptr_kind) {
     if (op != AWG_OP_A && !c.have_factors) c.fail(AWG_E_STATE, "apply: preconditioner not set up");
     if (c.n == 0) c.fail(AWG_E_STATE, "apply: no matrix");
     if (!x || !y) c.fail(AWG_E_ARG, "apply: null vector");
-    if (!c.pb.p) c.alloc_work();
+    if (!c.pb.p || c.pb.n != size_t(c.n)) c.alloc_work();
     if (ptr_kind == AWG_PTR_HOST) {
       AWG_CUDA(cudaMemcpyAsync(c.pb.p, x, sizeof(double) * c.n, cudaMemcpyHostToDevice, c.stream));
       op_apply(c, op, c.pb.p, c.pz.p, nullptr);
@@ -1000,35 +1030,39 @@ int awg_get_array(awg_ctx* ctx, int which, void* out, long long cap, long long* 
       case 7: dv = c.k0.h_l11; break;
       case 8: iv = c.kw.h_retained; is_int = true; break;
       case 9: dv = c.kw.h_l11; break;
-      case 10: {
-        dv.assign(size_t(c.n) * c.nm, 0.0);
-        for (int j = 0; j < c.nm; ++j)
-          AWG_CUDA(cudaMemcpy(dv.data() + size_t(j) * c.n, c.W.p + size_t(j) * c.ldw, sizeof(double) * c.n,
-                              cudaMemcpyDeviceToHost));
-        break;
+      // the large device arrays go straight into `out` (no host staging copy:
+      // V^s is 50 GB at c5): count first, then copy whatever fits in cap
+      case 10:
+      case 13:
+      case 14: {
+        long long cnt = 0;
+        if (which == 10) cnt = (long long)c.n * c.nm;
+        for (int s = 0; which != 10 && s < c.N; ++s)
+          cnt += (long long)c.h_ns[s] * (which == 13 ? c.h_ks[s] : c.h_ns[s]);
+        if (n_elems) *n_elems = cnt;
+        if (!out) return;
+        double* o = static_cast<double*>(out);
+        long long pos = 0;
+        auto put = [&](const double* src, long long spitch, int rows, int cols) {
+          // rows x cols column-major block with device pitch spitch -> packed at o + pos
+          const int fit = int(std::max(0LL, std::min<long long>(cols, (cap - pos) / std::max(rows, 1))));
+          if (rows > 0 && fit > 0)
+            AWG_CUDA(cudaMemcpy2D(o + pos, sizeof(double) * rows, src, sizeof(double) * spitch,
+                                  sizeof(double) * rows, fit, cudaMemcpyDeviceToHost));
+          pos += (long long)rows * cols;
+        };
+        if (which == 10) {
+          put(c.W.p, c.ldw, c.n, c.nm);
+        } else {
+          for (int s = 0; s < c.N; ++s) {
+            if (which == 13) put(c.Y.p + c.h_yoff[s], c.h_ld[s], c.h_ns[s], c.h_ks[s]);
+            else put(c.V.p + c.h_voff[s], c.h_ld[s], c.h_ns[s], c.h_ns[s]);
+          }
+        }
+        return;
       }
       case 11: dv = c.h_neg_weights; break;
       case 12: iv = c.h_w_inner; is_int = true; break;
-      case 13: {
-        for (int s = 0; s < c.N; ++s)
-          for (int k = 0; k < c.h_ks[s]; ++k) {
-            std::vector<double> col(c.h_ns[s]);
-            AWG_CUDA(cudaMemcpy(col.data(), c.Y.p + c.h_yoff[s] + size_t(k) * c.h_ld[s],
-                                sizeof(double) * c.h_ns[s], cudaMemcpyDeviceToHost));
-            dv.insert(dv.end(), col.begin(), col.end());
-          }
-        break;
-      }
-      case 14: {
-        for (int s = 0; s < c.N; ++s) {
-          std::vector<double> blk(size_t(c.h_ns[s]) * c.h_ns[s]);
-          AWG_CUDA(cudaMemcpy2D(blk.data(), sizeof(double) * c.h_ns[s], c.V.p + c.h_voff[s],
-                                sizeof(double) * c.h_ld[s], sizeof(double) * c.h_ns[s], c.h_ns[s],
-                                cudaMemcpyDeviceToHost));
-          dv.insert(dv.end(), blk.begin(), blk.end());
-        }
-        break;
-      }
       case 15: dv = c.h_eps; break;
       case 16: dv = c.h_rhs_asm; break;
       case 17: iv = c.h_rp; is_int = true; break;

@@ -25,6 +25,7 @@
 
 #include <cstdint>
 #include <map>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -50,6 +51,22 @@ struct AwgError : std::runtime_error {
 inline void check_launch(const char* what) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) throw AwgError(AWG_E_CUDA, std::string("launch ") + what + ": " + cudaGetErrorString(e));
+}
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device attribute of a
+// kernel: remember what was set per (kernel, device) so a context on another
+// GPU of the same process raises it there too.
+inline void ensure_dyn_smem(const void* func, size_t bytes) {
+  static std::map<std::pair<const void*, int>, size_t> done;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  int dev = 0;
+  AWG_CUDA(cudaGetDevice(&dev));
+  size_t& have = done[{func, dev}];
+  if (bytes > have) {
+    AWG_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+    have = bytes;
+  }
 }
 
 template <class T>
@@ -284,7 +301,7 @@ struct Ctx {
   int rows_per_gemv = 512;
   int gemv_cols = 1024;  // column chunk of the split GEMV
   int one_level = 2;     // OneLevelKind of the configuration: 0 AS, 1 AS_PLUS, 2 NN
-  bool use_fused = true; // single-pass NN local solve (env AWG_NN_TWO_PASS=1 disables)
+  bool use_fused = true; // single-pass NN local solve (option nn_two_pass=1 disables)
   // single-pass tuning (env AWG_FUSED_CPB / AWG_FUSED_NBUF / AWG_FUSED_CHUNKS; 0 = automatic)
   bool use_priority = true;  // main stream high priority, W branch low
   bool use_pdl = true;       // programmatic dependent launch on the solve path
@@ -295,14 +312,14 @@ struct Ctx {
   int fused_reserve = 0;
   int fused_min_cols = 128, fused_tail_pct = 0;  // single-pass task sizes (columns), guided tail share  // SMs the single-pass kernel leaves free (for the concurrent W branch)
   int fused_cpb = 0, fused_nbuf = 0, fused_chunks_per_sm = 8;  // 0: automatic
-  int pdl_early = 0;        // coarse-chain kernels release their dependents at entry (AWG_PDL_EARLY=1; measured neutral)
+  int pdl_early = 0;        // coarse-chain kernels release their dependents at entry (option pdl_early=1; measured neutral)
   int rows_group = 0;       // lanes per dof of the block-sparse prolongations (0: automatic)
-  bool pdl_local = true;     // early trigger into the single-pass local solve + its pre-wait prologue (AWG_PDL_LOCAL=0 off)
+  bool pdl_local = true;     // early trigger into the single-pass local solve + its pre-wait prologue (option pdl_local=0 off)
   int trigger_next = 0;     // set around the launch that precedes the local solve
-  bool pcg_adaptive = true;  // host batch sizes from the convergence rate (AWG_PCG_ADAPTIVE=0: doubling only)
-  bool fused_static = true;  // equal byte shares per CTA instead of the atomic queue (AWG_FUSED_STATIC=0 off)
-  bool fused_prefetch = true;  // next task's first steps issued during the current one (AWG_FUSED_PREFETCH=0 off)
-  bool fused_hold = true;  // column values kept in registers across the step's reduction (AWG_FUSED_HOLD=0 off)
+  bool pcg_adaptive = true;  // host batch sizes from the convergence rate (option pcg_adaptive=0: doubling only)
+  bool fused_static = true;  // equal byte shares per CTA instead of the atomic queue (option fused_static=0 off)
+  bool fused_prefetch = true;  // next task's first steps issued during the current one (option fused_prefetch=0 off)
+  bool fused_hold = true;  // column values kept in registers across the step's reduction (option fused_hold=0 off)
   BsPlan bs_neg, bs_z;   // A- dots (V^s columns k < n_nonpos), Z^T x (Y_s blocks)
   DArr<OwnEnt> ent_neg, ent_z;  // owner entries into V^s (A- modes) and Y_s (Z columns)
   DArr<double> m2t;  // (K+ M1^T): r0 x n_neg column-major; M1(q, jj) = A- dot q of coarse column retained[jj]
@@ -370,6 +387,13 @@ struct Ctx {
   int hist_cap = 0;
   std::vector<double> h_hist_res, h_hist_diag, h_hist_off;
 
+  // experiment switches set through awg_set_option (tests / profiles only;
+  // the product defaults are the literals at each use)
+  std::map<std::string, long long> opts;
+  long long opt(const char* name, long long dflt) const {
+    auto it = opts.find(name);
+    return it == opts.end() ? dflt : it->second;
+  }
   void alloc_work();  // also invalidates cached graphs
   void fail(int code, const std::string& m, int idx = -1) { throw AwgError(code, m, idx); }
 };
@@ -385,7 +409,7 @@ struct Ctx {
 // launch gap alone (+2.4% over no PDL).  One exception: the A+ SpMV right
 // before the single-pass local solve triggers early, and the local solve
 // issues its first (constant) V^s copies before its griddepcontrol.wait
-// (AWG_PDL_LOCAL; H3 apply 0.475 -> 0.467 ms at c2, profiles/r01f/knobs_pdl_local_c2.json).
+// (option pdl_local; H3 apply 0.475 -> 0.467 ms at c2, profiles/r01f/knobs_pdl_local_c2.json).
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // CSR row product  sum_k va[k] x[ci[k]]  in ascending k with separately
@@ -441,6 +465,7 @@ void partition_closure(Ctx& c, const std::vector<int>& owner, int nsub, int ring
 void bench_grouped_dgemm(Ctx& c, int m, int n, int k, int count, bool transpose_a, int reps, double* out);
 void build_core(Ctx& c);        // INEX core LU
 void run_setup(Ctx& c, const awg_config& cfg);  // setup.cu
+void pivoted_factor_of(Ctx& c, int n, const double* G_host, int exact, CoarseFactor& f);  // setup.cu
 void build_local_cholesky(Ctx& c);              // setup.cu: AS / AS+ factors U^s = L^-T
 // wbuild.cu: batched inner PCGs for W (modes = (s, k) list, ascending)
 void build_w_batched(Ctx& c, struct cublasContext* h, const std::vector<std::pair<int, int>>& modes, int maxit,

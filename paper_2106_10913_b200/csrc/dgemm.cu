@@ -180,33 +180,22 @@ __global__ void __launch_bounds__(GCfg<BN, BK, ST, WM, TA>::kT, MINB)
     }
 }
 
-// tile variants (AWG_DGEMM_VARIANT; measured in profiles/r01/dgemm_variants.json):
+// tile variants (option dgemm_variant; measured in profiles/r01/dgemm_variants.json):
 // 0 = 128x64, K 16, 4 stages, 2 CTAs/SM;
 // 1 = 128x128, K 16, 4 stages; 2 = 128x128, K 32, 3 stages; 3 = 128x64, K 32, 3 stages;
 // warp tile 32 x 32 instead of 64 x 32: 4 = 128x64 (8 warps, 2 CTAs/SM; default —
 // 4 warps per scheduler keep the DMMA pipe fed), 5 = 128x128
 // (16 warps).  (3 CTAs/SM of 32 x 32 warps spills.)
-int gemm_variant() {
-  static int v = [] {
-    const char* e = std::getenv("AWG_DGEMM_VARIANT");
-    return e ? std::atoi(e) : 4;
-  }();
-  return v;
-}
-int gemm_bn() {
-  const int v = gemm_variant();
+int gemm_variant(const Ctx& c) { return int(c.opt("dgemm_variant", 4)); }
+int gemm_bn(const Ctx& c) {
+  const int v = gemm_variant(c);
   return (v == 1 || v == 2 || v == 5) ? 128 : 64;
 }
 
 template <int BN, int BK, int ST, int MINB, int WM = 64, bool TA = false>
 void launch_gemm(Ctx& c, int ntiles, const GemmDesc* d, const GemmTile* t) {
   using C = GCfg<BN, BK, ST, WM, TA>;
-  static bool configured = false;
-  if (!configured) {
-    AWG_CUDA(cudaFuncSetAttribute(k_dgemm_grouped<BN, BK, ST, MINB, WM, TA>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::kSmem)));
-    configured = true;
-  }
+  ensure_dyn_smem((const void*)k_dgemm_grouped<BN, BK, ST, MINB, WM, TA>, C::kSmem);
   k_dgemm_grouped<BN, BK, ST, MINB, WM, TA><<<ntiles, C::kT, C::kSmem, c.stream>>>(d, t);
 }
 
@@ -225,7 +214,7 @@ void GroupedGemm::set(Ctx& c, const std::vector<GemmDesc>& probs, bool transpose
     flops += 2.0 * d.M * d.N * std::max(d.K, 0);
     // n tiles of one A panel are adjacent in launch order: they run together and
     // share the panel through L2 (A is read from HBM once; B^s stays L2-resident)
-    const int bn = ta ? 64 : gemm_bn();
+    const int bn = ta ? 64 : gemm_bn(c);
     for (int m0 = 0; m0 < d.M; m0 += kBM)
       for (int n0 = 0; n0 < d.N; n0 += bn) tl.push_back({p, m0, n0, 0});
   }
@@ -242,7 +231,7 @@ void GroupedGemm::run(Ctx& c) const {
     check_launch("dgemm_grouped_tn");
     return;
   }
-  switch (gemm_variant()) {
+  switch (gemm_variant(c)) {
     case 1: launch_gemm<128, 16, 4, 1>(c, ntiles, desc.p, tiles.p); break;
     case 2: launch_gemm<128, 32, 3, 1>(c, ntiles, desc.p, tiles.p); break;
     case 3: launch_gemm<64, 32, 3, 1>(c, ntiles, desc.p, tiles.p); break;

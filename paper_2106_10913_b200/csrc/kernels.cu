@@ -36,7 +36,7 @@ __device__ __forceinline__ bool gated(const int* gate) {
 // The short coarse-chain kernels (Z^T x / A- dots, K+ GEMV, Z c prolongation)
 // release their dependents at entry: the successor grid is scheduled while
 // this one runs and still waits in pdl_wait() for its completion and memory
-// flush, so only the launch latency overlaps.  Off by default (AWG_PDL_EARLY=1):
+// flush, so only the launch latency overlaps.  Off by default (option pdl_early=1):
 // measured neutral on c2 (profiles/r01c/knobs_c2.json, 0.511 vs 0.509-0.513 ms
 // per iteration), and the isolated Q / H3 applies slower by 1-2 us.
 // Not used after the single-pass kernel: waiting successor CTAs next to the
@@ -428,7 +428,7 @@ __global__ void __launch_bounds__(kFusedT, 1) k_nn_fused(const int* __restrict__
   const unsigned long long pol = l2_evict_first();
   // Persistent CTAs (one per SM).  NN: CTA b runs its own static task range
   // [cta_off[b], cta_off[b + 1]) — equal byte shares, so no SM idles at the
-  // end (profiles/r01e/knobs_static_c2.json); AS / AS+ and AWG_FUSED_STATIC=0
+  // end (profiles/r01e/knobs_static_c2.json); AS / AS+ and option fused_static=0
   // (cta_off == nullptr): column chunks pulled from an atomic queue.  The chunk -> partial-slot map
   // is fixed by the task list, so the result does not depend on which CTA ran
   // which chunk.  A step covers CPB columns; g counts
@@ -1140,12 +1140,8 @@ static size_t nn_smem(Ctx& c) {
   int ldmax = 0;
   for (int v : c.h_ld) ldmax = std::max(ldmax, v);
   const size_t smem = size_t(ldmax) * sizeof(double);
-  static size_t configured = 0;
-  if (smem > configured) {
-    AWG_CUDA(cudaFuncSetAttribute(k_nn_gemvT<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    AWG_CUDA(cudaFuncSetAttribute(k_nn_gemvT<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    configured = smem;
-  }
+  ensure_dyn_smem((const void*)k_nn_gemvT<8, false>, smem);
+  ensure_dyn_smem((const void*)k_nn_gemvT<8, true>, smem);
   return smem;
 }
 
@@ -1203,12 +1199,7 @@ void nn_prolong(Ctx& c, double* y, const int* gate) {
 template <bool TRI, int R, int CPB, bool HOLD>
 void launch_fused(Ctx& c, const LocalPlan& pl, const double* F, const double* D, const double* x, const int* gate,
                   int grid, size_t smem, int nbuf, int ldmax) {
-  static bool configured = false;
-  if (!configured) {
-    AWG_CUDA(cudaFuncSetAttribute(k_nn_fused<TRI, R, CPB, HOLD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  int(kFusedSmemCap)));
-    configured = true;
-  }
+  ensure_dyn_smem((const void*)k_nn_fused<TRI, R, CPB, HOLD>, kFusedSmemCap);
   launch(c, k_nn_fused<TRI, R, CPB, HOLD>, grid, kFusedT, smem, gate, pl.tf.p, F, c.voff.p, c.ns.p, c.ld.p, c.poff.p,
          c.pidx.p, D, x, TRI ? nullptr : c.rlam.p, c.P, c.wpart_nn.p, int(pl.tf.n), c.fused_queue.p,
          pl.static_grid ? pl.cta_off.p : nullptr, nbuf, ldmax,
@@ -1459,11 +1450,7 @@ static void w_apply(Ctx& c, const double* coef, double* y, const int* gate) {
   const int nkc = w_chunks(c);
   const int chunk = (c.nm + nkc - 1) / nkc + 1;
   const size_t smem = size_t(chunk) * sizeof(double);
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    AWG_CUDA(cudaFuncSetAttribute(k_dense_gemv, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    configured = smem;
-  }
+  if (smem > 48 * 1024) ensure_dyn_smem((const void*)k_dense_gemv, smem);
   dim3 grid((c.n + 2 * kThreads - 1) / (2 * kThreads), nkc);
   launch(c, k_dense_gemv, grid, kThreads, smem, gate, c.n, c.nm, c.ldw, nkc, c.W.p, coef, y, c.wpart2.p);
   ++c.launches;
@@ -1551,11 +1538,10 @@ void coarse_inverse(Ctx& c, const double* l, CoarseFactor& f) {
 
 // M2 for coarse_q_neg: M1(q, jj) = A- dot q of coarse column retained[jj]
 // (the dots k_bs_gemvT forms for A+ (Z c), one column at a time), M2 = M1 K+.
-// AWG_COARSE_NEG=0 disables (the hybrid H2 then runs the dot kernel on Z c).
+// option coarse_neg=0 disables (the hybrid H2 then runs the dot kernel on Z c).
 void build_coarse_neg(Ctx& c) {
   c.m2t.release();
-  const char* e = std::getenv("AWG_COARSE_NEG");
-  if (e && e[0] == '0') return;
+  if (c.opt("coarse_neg", 1) == 0) return;
   const int r = c.k0.rank, nq = c.nneg;
   if (nq == 0 || c.n0 == 0 || r == 0) return;
   // measured (profiles/r01e/knobs_coarse_neg_c{3,5}.json, ms per PCG iteration):

@@ -351,9 +351,10 @@ void op_apply(Ctx& c, int op, const double* x, double* y, const int* gate) {
         // W streams do not take HBM bandwidth from the single-pass local solve.
         // Large W (c3, c5): the whole branch overlaps everything (pure
         // bandwidth sharing is better there).
-        const bool split = c.w_split >= 0 ? c.w_split == 1
-                                          : (8.0 * c.n * c.nm <= 512.0 * (1 << 20) && c.n0 > 0 &&
-                                             c.cfg.composition != 0);
+        // (the split needs h2's hybrid branch, whose after_h1 hook runs the
+        // second half: never split without it, whatever the knob says)
+        const bool can_split = c.n0 > 0 && c.cfg.composition != 0;
+        const bool split = can_split && (c.w_split >= 0 ? c.w_split == 1 : 8.0 * c.n * c.nm <= 512.0 * (1 << 20));
         AWG_CUDA(cudaEventRecord(c.ev_fork, c.stream));
         AWG_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
         cudaStream_t main = c.stream;

@@ -51,11 +51,9 @@ double now_ms() {
   return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
-// progress trace on stderr when AWG_VERBOSE=1
+// progress trace on stderr with option verbose=1
 void trace(const Ctx& c, const std::string& what, double ms) {
-  (void)c;
-  const char* v = std::getenv("AWG_VERBOSE");
-  if (v && v[0] == '1') std::fprintf(stderr, "[awg setup] %s: %.1f s\n", what.c_str(), ms / 1e3);
+  if (c.opt("verbose", 0) == 1) std::fprintf(stderr, "[awg setup] %s: %.1f s\n", what.c_str(), ms / 1e3);
 }
 
 // --------------------------------------------------------------------------
@@ -858,6 +856,18 @@ void run_setup(Ctx& c, const awg_config& cfg) {
   c.alloc_work();
   AWG_CUDA(cudaStreamSynchronize(c.stream));
   c.t_setup_ms[5] = now_ms() - t_start;
+}
+
+// The device pivoted factor on a caller-supplied symmetric G (n x n,
+// column-major, host memory): the k_rrf run of build_coarse / build_w,
+// exposed for direct retained-set parity checks (awg_pivoted_factor).
+void pivoted_factor_of(Ctx& c, int n, const double* G_host, int exact, CoarseFactor& f) {
+  DArr<double> G;
+  G.alloc(size_t(std::max(n, 1)) * std::max(n, 1));
+  if (n > 0) {
+    AWG_CUDA(cudaMemcpyAsync(G.p, G_host, sizeof(double) * size_t(n) * n, cudaMemcpyHostToDevice, c.stream));
+  }
+  pivoted_factor(c, G, n, exact, f, n);
 }
 
 }  // namespace awgb

@@ -409,7 +409,7 @@ struct Block {
   DArr<double> X, R, Z, Pm, Q, Bm, T, C0, C1, C2, C3, C4, C5;
   DArr<double> XS, WS;  // block-P layout
   DArr<double> Pinv;    // optional P^s = V+ L+^-1 V+^T (NN), V layout
-  GroupedGemm pgemm;    // P^s X^s over all subdomains (empty: per-subdomain cuBLAS, AWG_WBUILD_GEMM=cublas)
+  GroupedGemm pgemm;    // P^s X^s over all subdomains (empty: per-subdomain cuBLAS, option wbuild_cublas=1)
   DArr<double> zx, zr, zt, zc, negc, part;
   DArr<ColState> st;
   DArr<int> done, any_true;
@@ -465,7 +465,7 @@ struct BlockOps {
   cublasHandle_t h;
   const CoarseFactor& k0;
   std::vector<int> qs, negoff, koff;  // per subdomain: negative modes, their offset, coarse column offset
-  // phase profile of one block pass (AWG_VERBOSE=2): events between phases
+  // phase profile of one block pass (option verbose=2): events between phases
   std::vector<std::pair<std::string, cudaEvent_t>> marks;
   bool prof = false;
   void mark(const char* name) {
@@ -742,8 +742,7 @@ void build_w_batched(Ctx& c, cublasHandle_t h, const std::vector<std::pair<int, 
   k.any_true.alloc(1);
   AWG_BLAS(cublasSetStream(h, c.stream));
   if (k.Pinv.p) {
-    const char* g = std::getenv("AWG_WBUILD_GEMM");
-    if (!(g && std::string(g) == "cublas")) {
+    if (c.opt("wbuild_cublas", 0) == 0) {
       std::vector<GemmDesc> pd;
       for (int s = 0; s < c.N; ++s) {
         const int n = c.h_ns[s], L = c.h_ld[s];
@@ -790,8 +789,7 @@ void build_w_batched(Ctx& c, cublasHandle_t h, const std::vector<std::pair<int, 
   };
   refill();
   const dim3 gn = ops.grid_n();
-  const char* vb = std::getenv("AWG_VERBOSE");
-  const bool prof_pass = vb && vb[0] == '2';
+  const bool prof_pass = c.opt("verbose", 0) == 2;
   while (finished < total) {
     ops.prof = prof_pass && passes == 5;
     ops.mark("start");
@@ -835,8 +833,7 @@ void build_w_batched(Ctx& c, cublasHandle_t h, const std::vector<std::pair<int, 
     }
     refill();
     if (passes % 250 == 0) {
-      const char* v = std::getenv("AWG_VERBOSE");
-      if (v && v[0] == '1')
+      if (c.opt("verbose", 0) == 1)
         std::fprintf(stderr, "[awg setup]   W block pass %d: %d of %d columns done (B = %d)\n", passes, finished,
                      total, B);
     }

@@ -1,6 +1,7 @@
 """Per-iteration device time of the c2 solve (op_times-style) under knob
-settings given as NAME=VALUE[,NAME=VALUE] arguments, one fresh context each.
-    python profiles/knob_sweep.py c2 "AWG_PDL_EARLY=0" "AWG_PDL_EARLY=1,AWG_ROWS_GROUP=8" ..."""
+settings given as NAME=VALUE[,NAME=VALUE] arguments (awg_set_option names),
+one fresh context each.
+    python profiles/knob_sweep.py c2 "pdl_early=0" "pdl_early=1,rows_group=8" ..."""
 import json
 import os
 import sys
@@ -12,11 +13,9 @@ cfg = sys.argv[1]
 p = problems.make(cfg)
 out = []
 for spec in sys.argv[2:]:
-    env = dict(kv.split("=") for kv in spec.split(",") if kv)
-    saved = {k: os.environ.get(k) for k in env}
-    os.environ.update(env)
+    opts = {k: int(v) for k, v in (kv.split("=") for kv in spec.split(",") if kv)}
     try:
-        ctx = awg.context_from_problem(p)
+        ctx = awg.context_from_problem(p, options=opts)
         kind = os.environ.get("ONE_LEVEL", "NN")  # NN | AS | AS_PLUS
         ctx.setup(awg.config_for(p, one_level=getattr(awg.OneLevelKind, kind)))
         best = 1e9
@@ -32,9 +31,5 @@ for spec in sys.argv[2:]:
                     "APLUS_ms": ctx.time_apply(awg.Op.APLUS, reps=20)})
         ctx.close()
     finally:
-        for k, v in saved.items():
-            if v is None:
-                os.environ.pop(k, None)
-            else:
-                os.environ[k] = v
+        pass
 print(json.dumps({"config": cfg, "results": out}))

@@ -2,7 +2,7 @@
 factors (V^s hash-filled with the config's subdomain sizes, W with n_minus
 columns), no setup.  The profiler range covers one launch of each:
 single-pass local solve, W^T x, W c, SpMV.
-    AWG_SYNTH_NM=2913 ncu --profile-from-start off --set full ... python profiles/prof_synthetic.py c5"""
+    ncu --profile-from-start off --set full ... python profiles/prof_synthetic.py c5 2913"""
 import os
 import sys
 
@@ -13,9 +13,10 @@ from paper_2106_10913_b200 import awg, problems  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c5"
 p = problems.make(cfg)
-ctx = awg.context_from_problem(p)
+nm = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+ctx = awg.context_from_problem(p, options={"synth_nm": nm})
 ctx.synthetic_factors(m_per_sub=8)
-names = ["nn_fused", "spmv"] + (["w_gemvT", "w_gemv"] if int(os.environ.get("AWG_SYNTH_NM", "0")) else [])
+names = ["nn_fused", "spmv"] + (["w_gemvT", "w_gemv"] if nm else [])
 for name in names:  # warm-up (module load, first-launch attributes)
     ctx.time_kernel(name, reps=1)
 torch.cuda.synchronize()

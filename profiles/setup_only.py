@@ -1,4 +1,4 @@
-"""GPU setup only (phase timings on stderr with AWG_VERBOSE=1/2).
+"""GPU setup only (phase timings on stderr: option verbose=1/2 from VERBOSE).
     python profiles/setup_only.py <config> [rrf]"""
 import json
 import os
@@ -10,7 +10,7 @@ from paper_2106_10913_b200 import awg, problems  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "c3"
 p = problems.make(name)
-ctx = awg.context_from_problem(p)
+ctx = awg.context_from_problem(p, options={"verbose": int(os.environ.get("VERBOSE", "1"))})
 t = time.time()
 ctx.setup(awg.config_for(p, rrf_semantics=sys.argv[2] if len(sys.argv) > 2 else "reference"))
 q = ctx.query()

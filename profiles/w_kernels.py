@@ -1,5 +1,5 @@
 """Time the second-coarse-space kernels (W^T x split-K + column sum, W c) at
-full scale on a synthetic W (AWG_SYNTH_NM columns, hash-filled), next to the
+full scale on a synthetic W (option synth_nm columns, hash-filled), next to the
 single-pass local solve on synthetic factors — no setup needed.
     python profiles/w_kernels.py c3:2105 c5:2913"""
 import json
@@ -12,9 +12,8 @@ from paper_2106_10913_b200 import awg, problems  # noqa: E402
 out = []
 for spec in sys.argv[1:] or ["c5:2913"]:
     cfg, nm = spec.split(":")
-    os.environ["AWG_SYNTH_NM"] = nm
     p = problems.make(cfg)
-    ctx = awg.context_from_problem(p)
+    ctx = awg.context_from_problem(p, options={"synth_nm": int(nm)})
     ctx.synthetic_factors(m_per_sub=8)
     row = {"config": cfg, "n": p.n, "n_minus": int(nm)}
     for name in ("w_gemvT", "w_gemv", "nn_fused", "spmv"):

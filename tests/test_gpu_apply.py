@@ -22,12 +22,12 @@ OPS = {"A": awg.Op.A, "Aminus": awg.Op.AMINUS, "Aplus": awg.Op.APLUS, "H1": awg.
 TOL = {"H3inex": 1e-8, "PI3": 1e-10, "PI3T": 1e-10}
 
 
-def make_ctx(g, mode=awg.AwgMode.AD, composition=awg.Composition.HYBRID, lu="reference", one_level="NN"):
+def make_ctx(g, mode=awg.AwgMode.AD, composition=awg.Composition.HYBRID, lu="reference", one_level="NN", options=None):
     n = len(g["b"])
     off, idx = g["part_offsets"], g["part_indices"]
     omega = [idx[a:b] for a, b in zip(off[:-1], off[1:])]
     a = awg.SparseSymMatrix(n, g["A_row_offsets"], g["A_col_indices"], g["A_values"])
-    ctx = awg.ProblemContext(a, g["b"], awg.Partition(omega, n))
+    ctx = awg.ProblemContext(a, g["b"], awg.Partition(omega, n)).set_options(options)
     cfg = awg.PreconditionerConfig(awg=mode, composition=composition, lu_semantics=lu, one_level=KINDS[one_level])
     ctx.load_factors(cfg, g)
     return ctx
@@ -147,11 +147,7 @@ def test_single_pass_matches_two_pass():
     g, s = golden_with_base("t2d")
     ctx1 = make_ctx(g)
     assert ctx1.query()["nn_single_pass"] == 1
-    os.environ["AWG_NN_TWO_PASS"] = "1"
-    try:
-        ctx2 = make_ctx(g)
-    finally:
-        del os.environ["AWG_NN_TWO_PASS"]
+    ctx2 = make_ctx(g, options={"nn_two_pass": 1})
     assert ctx2.query()["nn_single_pass"] == 0
     for x, ref in zip(g["x_apply"], g["y_H1"]):
         y1, y2 = ctx1.apply(awg.Op.H1, x), ctx2.apply(awg.Op.H1, x)
@@ -189,15 +185,11 @@ def test_grouped_dgemm_matches_cublas(shape, ta):
 
 def test_single_pass_register_hold_is_bit_identical():
     """The single-pass kernel's register-held variant (default) and the
-    re-read-from-shared-memory variant (AWG_FUSED_HOLD=0) perform the same
+    re-read-from-shared-memory variant (option fused_hold=0) perform the same
     operations in the same order: H1 must agree bit for bit."""
     g, s = golden_with_base("t2d")
     ctx1 = make_ctx(g)
-    os.environ["AWG_FUSED_HOLD"] = "0"
-    try:
-        ctx2 = make_ctx(g)
-    finally:
-        del os.environ["AWG_FUSED_HOLD"]
+    ctx2 = make_ctx(g, options={"fused_hold": 0})
     for x in g["x_apply"]:
         y1, y2 = ctx1.apply(awg.Op.H1, x), ctx2.apply(awg.Op.H1, x)
         assert np.array_equal(y1, y2)
@@ -206,15 +198,11 @@ def test_single_pass_register_hold_is_bit_identical():
 @pytest.mark.parametrize("case", ["t2d", "t3d", "telas8"])
 def test_precomputed_coarse_neg_dots(case):
     """The hybrid H2's A+ (Q x): the A- dots of Z c taken from the coarse solve
-    (M2 = M1 K+, default) against the dot kernel over Z c (AWG_COARSE_NEG=0) —
+    (M2 = M1 K+, default) against the dot kernel over Z c (option coarse_neg=0) —
     a re-association of the same sums."""
     g, s = golden_with_base(case)
     ctx1 = make_ctx(g)
-    os.environ["AWG_COARSE_NEG"] = "0"
-    try:
-        ctx2 = make_ctx(g)
-    finally:
-        del os.environ["AWG_COARSE_NEG"]
+    ctx2 = make_ctx(g, options={"coarse_neg": 0})
     for x in g["x_apply"]:
         for op in (awg.Op.H2, awg.Op.H3):
             y1, y2 = ctx1.apply(op, x), ctx2.apply(op, x)

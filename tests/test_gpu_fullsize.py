@@ -24,32 +24,27 @@ import numpy as np
 import pytest
 
 from conftest import rel
+from fullsize_parity import FullSize, check_applies, check_coarse_solves, check_pcg, record
 from paper_2106_10913_b200 import awg, problems
 
 pytestmark = pytest.mark.gpu
 
 
 @pytest.fixture(scope="module")
-def c2():
-    p = problems.make("c2")
-    ctx = awg.context_from_problem(p)
+def c2fs():
+    fs = FullSize("c2")
+    yield fs
+    fs.close()
+
+
+@pytest.fixture(scope="module")
+def c2(c2fs):
+    return c2fs.p, c2fs.ctx
+
+
+def _ctx_with(p, options):
+    ctx = awg.context_from_problem(p, options=options)
     ctx.setup(awg.config_for(p))
-    yield p, ctx
-    ctx.close()
-
-
-def _ctx_with(p, env):
-    saved = {k: os.environ.get(k) for k in env}
-    os.environ.update(env)
-    try:
-        ctx = awg.context_from_problem(p)
-        ctx.setup(awg.config_for(p))
-    finally:
-        for k, v in saved.items():
-            if v is None:
-                os.environ.pop(k, None)
-            else:
-                os.environ[k] = v
     return ctx
 
 
@@ -94,35 +89,22 @@ def test_setup_mode_counts_full_size(c2):
     _check_modes(p, ctx, "c2")
 
 
-@pytest.mark.skipif(not os.path.exists(os.path.join(os.path.dirname(__file__), "golden", "c3_modes.json")),
-                    reason="c3 fixture not generated")
-def test_setup_mode_counts_c3():
-    """configs[2] (64^3, 64 subdomains, fixed k = 10): n_nonpos / n_zero and
-    the fixed-k rule k_s = max(10, n_nonpos) extended over clusters, per
-    subdomain, against the restatement at full size (GPU setup ~105 s)."""
-    p = problems.make("c3")
-    ctx = awg.context_from_problem(p)
-    try:
-        ctx.setup(awg.config_for(p))
-        _check_modes(p, ctx, "c3")
-    finally:
-        ctx.close()
+def test_apply_parity_full_size(c2fs):
+    """Every operator of the path on the device's own c2 factors within 1e-11
+    of the restatement (preconditioner.cpp:32-82, 149-221; splitting.cpp:119-147;
+    coarse.cpp:156-166)."""
+    record("c2_applies", check_applies(c2fs))
 
 
-@pytest.mark.skipif(os.environ.get("AWG_FULLSIZE_C5") != "1" or not os.path.exists(
-    os.path.join(os.path.dirname(__file__), "golden", "c5_corner_modes.json")),
-                    reason="c5 setup takes ~330 s: run with AWG_FULLSIZE_C5=1")
-def test_setup_mode_counts_c5_corner():
-    """configs[4] (96^3, 216 subdomains, fixed k = 8), the north-star config:
-    per-subdomain counts on the 2x2x2 corner boxes against the restatement
-    (whose pencils there need only the 27 surrounding eigensplits)."""
-    p = problems.make("c5")
-    ctx = awg.context_from_problem(p)
-    try:
-        ctx.setup(awg.config_for(p))
-        _check_modes(p, ctx, "c5_corner")
-    finally:
-        ctx.close()
+def test_coarse_solves_full_size(c2fs):
+    """K0 / KW solves (the reference's stale-upper factors: rw < n_minus at c2)."""
+    record("c2_coarse_solves", check_coarse_solves(c2fs))
+
+
+def test_pcg_parity_full_size(c2fs):
+    """The device PCG against the restatement's pcg on the same factors:
+    iterations +-1, x within 1e-7 (krylov.cpp:36-124)."""
+    record("c2_pcg", check_pcg(c2fs))
 
 
 def test_spmv_bit_identical_full_size(c2):
@@ -152,10 +134,10 @@ def test_local_solve_variants_full_size(c2):
     ref = [ctx.apply(awg.Op.H1, x) for x in xs]
     q = ctx.query()
     assert q["nn_single_pass"] == 1
-    two = _ctx_with(p, {"AWG_NN_TWO_PASS": "1"})
-    nopf = _ctx_with(p, {"AWG_FUSED_PREFETCH": "0"})
-    flip = _ctx_with(p, {"AWG_FUSED_STATIC": "0" if q["nn_static_split"] else "1"})
-    pdl = _ctx_with(p, {"AWG_PDL_LOCAL": "0" if os.environ.get("AWG_PDL_LOCAL") == "1" else "1"})
+    two = _ctx_with(p, {"nn_two_pass": 1})
+    nopf = _ctx_with(p, {"fused_prefetch": 0})
+    flip = _ctx_with(p, {"fused_static": 0 if q["nn_static_split"] else 1})
+    pdl = _ctx_with(p, {"pdl_local": 0})
     try:
         # the early trigger into the local solve and its pre-wait copies change
         # scheduling only
@@ -186,7 +168,7 @@ def test_pcg_full_size(c2):
     true = np.linalg.norm(p.b - _spmv_reference_order(p, x1)) / np.linalg.norm(p.b)
     # the host's batch sizing (convergence-rate estimate vs plain doubling) only
     # schedules graph launches: the device state decides, results identical
-    fixed = _ctx_with(p, {"AWG_PCG_ADAPTIVE": "0"})
+    fixed = _ctx_with(p, {"pcg_adaptive": 0})
     try:
         x3, rep3 = fixed.pcg(p.b, p.rtol, 10000)
     finally:

@@ -1,0 +1,43 @@
+"""Device pivoted factor (k_rrf, setup.cu) against the reference's
+rank_revealing_sym_factor (dense.cpp:299-346), directly through the C ABI
+(awg_pivoted_factor): index work, so the retained set (pivot order) must be
+identical and l11 agree to rounding.  Inputs: the G = Z^T A+ Z and W^T A W
+matrices the reference itself factored in every golden case (k0_G / kw_G,
+shipped or probe-fixed semantics as the case was generated), and the seeded
+probe matrices of tests/golden/make_rrf_golden.py under both semantics."""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import ALL_CASES, GOLDEN, golden_with_base, rel
+from paper_2106_10913_b200 import awg
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("case", ALL_CASES + ["t2d_as", "t2d_asplus", "telas_as"])
+def test_device_rrf_on_reference_G(case):
+    g, s = golden_with_base(case)
+    exact = case.endswith("_exact")
+    seen = 0
+    for tag in ("k0", "kw"):
+        if tag + "_G" not in g or g[tag + "_G"].size == 0:
+            continue
+        ret, l11 = awg.pivoted_factor(g[tag + "_G"], exact=exact)
+        assert np.array_equal(ret, g[tag + "_retained"]), (case, tag, ret, g[tag + "_retained"])
+        assert rel(l11, g[tag + "_l11"]) <= 1e-12, (case, tag)
+        seen += 1
+    assert seen >= 1
+
+
+@pytest.mark.parametrize("semantics", ["ref", "exact"])
+def test_device_rrf_probe_matrices(semantics):
+    z = np.load(os.path.join(GOLDEN, "rrf_cases.npz"))
+    for name in [str(n) for n in z["names"]]:
+        ret, l11 = awg.pivoted_factor(z[f"{name}_G"], exact=semantics == "exact")
+        assert np.array_equal(ret, z[f"{name}_{semantics}_retained"]), (name, ret)
+        assert rel(l11, z[f"{name}_{semantics}_l11"]) <= 1e-13, name
+    # SURVEY.md §0.4's 12 x 12 SPD probe: rank lost under the shipped semantics only
+    r = [len(awg.pivoted_factor(z[f"spd12_s{k}_G"], exact=semantics == "exact")[0]) for k in range(4)]
+    assert (max(r) < 12) if semantics == "ref" else (min(r) == 12)

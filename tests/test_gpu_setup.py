@@ -20,12 +20,12 @@ COMPS = {"hybrid": awg.Composition.HYBRID, "additive": awg.Composition.ADDITIVE}
 MODES = {"none": awg.AwgMode.NONE, "ad": awg.AwgMode.AD}
 
 
-def setup_ctx(g, s, rrf="reference"):
+def setup_ctx(g, s, rrf="reference", options=None):
     n = len(g["b"])
     off, idx = g["part_offsets"], g["part_indices"]
     omega = [idx[a:b] for a, b in zip(off[:-1], off[1:])]
     a = awg.SparseSymMatrix(n, g["A_row_offsets"], g["A_col_indices"], g["A_values"])
-    ctx = awg.ProblemContext(a, g["b"], awg.Partition(omega, n))
+    ctx = awg.ProblemContext(a, g["b"], awg.Partition(omega, n)).set_options(options)
     comp, mode = case_options(s)
     cfg = awg.PreconditionerConfig(rrf_semantics=rrf, one_level=KINDS[one_level_of(s)], composition=COMPS[comp],
                                    awg=MODES[mode], tau_flat=float(s.get("tau_flat", 10.0)))
@@ -155,17 +155,11 @@ def test_wide_coarse_blocks():
 def test_wbuild_grouped_dgemm_matches_cublas_path(case):
     """The W build's block one-level on the hand-written grouped FP64
     tensor-core GEMM (default) against the per-subdomain cuBLAS DGEMM path
-    (AWG_WBUILD_GEMM=cublas): same inner iteration counts (+-1) and the same W
+    (option wbuild_cublas=1): same inner iteration counts (+-1) and the same W
     up to the inner solves' tolerance."""
-    import os
-
     g, s = golden_with_base(case)
     ctx1 = setup_ctx(g, s)
-    os.environ["AWG_WBUILD_GEMM"] = "cublas"
-    try:
-        ctx2 = setup_ctx(g, s)
-    finally:
-        del os.environ["AWG_WBUILD_GEMM"]
+    ctx2 = setup_ctx(g, s, options={"wbuild_cublas": 1})
     i1, i2 = ctx1.get("w_inner_iterations"), ctx2.get("w_inner_iterations")
     assert np.max(np.abs(i1.astype(int) - i2.astype(int))) <= 1
     w1, w2 = ctx1.get("W"), ctx2.get("W")

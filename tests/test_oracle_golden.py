@@ -1,9 +1,11 @@
 """The CPU restatement (oracle/awg_oracle.py) pinned against the unmodified
 reference's outputs (tests/golden, made by oracle/_ref/ref_driver)."""
+import os
+
 import numpy as np
 import pytest
 
-from conftest import ALL_CASES, case_options, golden_with_base, omega_of, one_level_of, rel
+from conftest import ALL_CASES, GOLDEN, case_options, golden_with_base, omega_of, one_level_of, rel
 from oracle import awg_oracle as O
 
 CASES = ALL_CASES + ["t2d_as", "t2d_asplus", "telas_as"]
@@ -114,3 +116,25 @@ def test_shipped_factor_bug_is_reproduced():
         recon = l @ l.T
         err = np.linalg.norm(recon - m[np.ix_(r, r)]) / np.linalg.norm(m)
         assert (err < 1e-12) == ok
+
+
+def _rrf_cases():
+    z = np.load(os.path.join(GOLDEN, "rrf_cases.npz"))
+    return z, [str(n) for n in z["names"]]
+
+
+@pytest.mark.parametrize("semantics", ["ref", "exact"])
+def test_rank_revealing_factor_port_probe_matrices(semantics):
+    """The restatement against the reference's own rank_revealing_sym_factor
+    (ref_driver --rrf; ref_driver_fixed for the exact semantics) on seeded
+    matrices covering every branch: random SPD (SURVEY.md §0.4's 12 x 12 probe:
+    the shipped factor loses rank), rank-deficient PSD (drop rule), a unit
+    diagonal (first-maximum ties), graded pivots (tests/golden/make_rrf_golden.py)."""
+    z, names = _rrf_cases()
+    for name in names:
+        l, r = O.rank_revealing_sym_factor(z[f"{name}_G"], exact=semantics == "exact")
+        assert np.array_equal(r, z[f"{name}_{semantics}_retained"]), name
+        assert rel(l, z[f"{name}_{semantics}_l11"]) <= 1e-13, name
+    # SURVEY.md §0.4: the shipped factor loses rank on a random 12 x 12 SPD matrix
+    ranks = [len(z[f"{n}_{semantics}_retained"]) for n in names if n.startswith("spd12")]
+    assert (max(ranks) < 12) if semantics == "ref" else (min(ranks) == 12)
