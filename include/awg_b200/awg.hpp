@@ -26,9 +26,7 @@
 
 #include <algorithm>
 #include <cstdio>
-#include <fstream>
 #include <memory>
-#include <sstream>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -90,92 +88,10 @@ struct SolveReport {
   double solve_ms = 0.0;
 };
 
-// ---- reference external formats (sparse.cpp:89-138, partition.cpp:212-233) ----
-inline SparseSymMatrix read_matrix_market(const std::string& path) {
-  std::ifstream in(path);
-  if (!in) throw std::runtime_error("cannot open: " + path);
-  std::string line;
-  if (!std::getline(in, line)) throw std::runtime_error("empty matrix file: " + path);
-  {
-    std::istringstream h(line);
-    std::string banner, object, format, field, symmetry;
-    h >> banner >> object >> format >> field >> symmetry;
-    if (banner != "%%MatrixMarket" || object != "matrix" || format != "coordinate" || field != "real" ||
-        symmetry != "symmetric")
-      throw std::runtime_error("unsupported matrix market header: " + line);
-  }
-  while (std::getline(in, line))
-    if (!line.empty() && line[0] != '%') break;
-  int rows = 0, cols = 0, nnz = 0;
-  {
-    std::istringstream s(line);
-    if (!(s >> rows >> cols >> nnz)) throw std::runtime_error("bad size line: " + line);
-  }
-  if (rows != cols) throw std::runtime_error("matrix not square: " + path);
-  // symmetric entries expanded to both triangles, duplicates summed in file
-  // order, columns ascending per row
-  std::vector<std::vector<std::pair<int, double>>> r(rows);
-  for (int k = 0; k < nnz; ++k) {
-    int i = 0, j = 0;
-    double v = 0.0;
-    if (!(in >> i >> j >> v)) throw std::runtime_error("truncated matrix file: " + path);
-    --i;
-    --j;
-    if (i < 0 || i >= rows || j < 0 || j >= rows) throw std::out_of_range("matrix index out of range");
-    r[i].push_back({j, v});
-    if (i != j) r[j].push_back({i, v});
-  }
-  SparseSymMatrix a;
-  a.n = rows;
-  a.row_offsets.assign(rows + 1, 0);
-  for (int i = 0; i < rows; ++i) {
-    auto& row = r[i];
-    std::stable_sort(row.begin(), row.end(), [](auto& x, auto& y) { return x.first < y.first; });
-    for (size_t k = 0; k < row.size();) {
-      const int j = row[k].first;
-      double acc = 0.0;
-      while (k < row.size() && row[k].first == j) acc += row[k++].second;
-      a.col_indices.push_back(j);
-      a.values.push_back(acc);
-    }
-    a.row_offsets[i + 1] = static_cast<int>(a.col_indices.size());
-  }
-  return a;
-}
-
-inline std::vector<double> read_vector(const std::string& path) {
-  std::ifstream in(path);
-  if (!in) throw std::runtime_error("cannot open: " + path);
-  size_t n = 0;
-  if (!(in >> n)) throw std::runtime_error("bad vector file: " + path);
-  std::vector<double> v(n);
-  for (size_t i = 0; i < n; ++i)
-    if (!(in >> v[i])) throw std::runtime_error("truncated vector file: " + path);
-  return v;
-}
-
-inline Partition read_partition(const std::string& path, int n) {
-  std::ifstream in(path);
-  if (!in) throw std::runtime_error("cannot open: " + path);
-  Partition p;
-  p.n = n;
-  std::string line;
-  while (std::getline(in, line)) {
-    if (line.empty()) continue;
-    std::istringstream s(line);
-    std::vector<int> dofs;
-    int v = 0;
-    while (s >> v) {
-      if (v < 0 || v >= n) throw std::runtime_error("partition index out of range: " + path);
-      dofs.push_back(v);
-    }
-    std::sort(dofs.begin(), dofs.end());
-    dofs.erase(std::unique(dofs.begin(), dofs.end()), dofs.end());
-    if (!dofs.empty()) p.omega.push_back(std::move(dofs));
-  }
-  if (p.omega.empty()) throw std::runtime_error("empty partition file: " + path);
-  return p;
-}
+// The reference's file readers (read_matrix_market / read_vector /
+// read_partition, sparse.cpp:89-138, partition.cpp:212-233) stay with the
+// reference caller: it parses its files as before and hands the resulting
+// SparseSymMatrix / vector / Partition to ProblemContext below.
 
 // ---- the device-backed problem context -----------------------------------------
 class ProblemContext {

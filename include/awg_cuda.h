@@ -173,7 +173,8 @@ int awg_partition_boxes(struct awg_ctx* ctx, const int* boxes, int overlap);
  * fused_static, fused_static_cols, pcg_adaptive, pdl_local, pdl_early,
  * rows_group, w_split, fused_nbuf, fused_chunks, fused_reserve,
  * fused_min_cols, fused_tail, synth_nm, dgemm_variant, coarse_neg, verbose,
- * wbuild_cublas.  Unknown names return AWG_E_ARG. */
+ * wbuild_cublas, setup_cusolver (1: cuSOLVER eigensolvers / Cholesky in the
+ * setup instead of the hand-written ones, for A/B checks).  Unknown names return AWG_E_ARG. */
 int awg_set_option(struct awg_ctx* ctx, const char* name, long long value);
 
 int awg_setup(struct awg_ctx* ctx, const awg_config* cfg);
@@ -238,6 +239,14 @@ int awg_synthetic_factors(struct awg_ctx* ctx, int m_per_sub, unsigned long long
  * cuBLAS DGEMM on the same operands.  out[0] max |C - C_cublas| / max |C_cublas|,
  * out[1] ms per grouped launch, out[2] ms for the same products as `count`
  * cuBLAS calls, out[3] grouped TFLOP/s, out[4] cuBLAS TFLOP/s. */
+/* Check / benchmark hook of the setup's batched symmetric eigensolver (eig.cu,
+ * the dense_sym_eig of dense.cpp:117-209 for B^s and the GenEO pencils):
+ * `count` seeded symmetric matrices of order n (kind 0 random, 1 the 5-point
+ * Laplacian of a sqrt(n) x sqrt(n) grid with repeated eigenvalues, 2 graded
+ * spectrum), checked against cuSOLVER Dsyevd on the same matrices.
+ * out[0] max eigenvalue error / ||A||, out[1] max residual ||A z - w z|| / ||A||,
+ * out[2] max |Z^T Z - I|, out[3] ms for the batch, out[4] cuSOLVER ms. */
+int awg_bench_eig(struct awg_ctx* ctx, int n, int count, int kind, unsigned long long seed, double* out);
 int awg_bench_dgemm(struct awg_ctx* ctx, int m, int n, int k, int count, int transpose_a, int reps, double* out);
 
 #ifdef __cplusplus

@@ -166,7 +166,7 @@ EXPORTED_SYMBOLS = [
     "awg_get_history", "awg_get_array", "awg_launch_count", "awg_time_apply", "awg_time_kernel",
     "awg_synthetic_factors", "awg_kernel_timer", "awg_assemble_fd", "awg_assemble_elasticity", "awg_partition_owner",
     "awg_partition_boxes", "awg_bench_dgemm", "awg_set_option", "awg_pivoted_factor",
-    "awg_coarse_solve",
+    "awg_coarse_solve", "awg_bench_eig",
 ]
 
 _lib = None
@@ -196,6 +196,7 @@ def load_library(path: str = LIB_PATH):
     lib.awg_partition_owner.argtypes = [vp, _ip, ctypes.c_int, ctypes.c_int]
     lib.awg_partition_boxes.argtypes = [vp, _ip, ctypes.c_int]
     lib.awg_set_option.argtypes = [vp, ctypes.c_char_p, ctypes.c_longlong]
+    lib.awg_bench_eig.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_ulonglong, _dp]
     lib.awg_coarse_solve.argtypes = [vp, ctypes.c_int, _dp, _dp]
     lib.awg_pivoted_factor.argtypes = [vp, ctypes.c_int, _dp, ctypes.c_int, _ip, _ip, _dp]
     lib.awg_setup.argtypes = [vp, ctypes.POINTER(_Config)]
@@ -592,6 +593,18 @@ def spmv(ctx: ProblemContext, x):
 
 def pcg(ctx: ProblemContext, b, rtol: float, maxit: int):
     return ctx.pcg(b, rtol, maxit)
+
+
+def bench_eig(n: int, count: int = 1, kind: int = 0, seed: int = 1, device: int = 0) -> dict:
+    """The setup eigensolver (eig.cu) on seeded matrices against cuSOLVER
+    (awg_bench_eig): eigenvalue error, residual, orthogonality, timings."""
+    ctx = ProblemContext._bare(device)
+    try:
+        out = (ctypes.c_double * 5)()
+        ctx._check(ctx._lib.awg_bench_eig(ctx._h, int(n), int(count), int(kind), int(seed), out))
+        return {"eig_err": out[0], "resid": out[1], "orth": out[2], "ms": out[3], "ms_cusolver": out[4]}
+    finally:
+        ctx.close()
 
 
 def pivoted_factor(g, exact: bool = False, device: int = 0) -> Tuple[np.ndarray, np.ndarray]:

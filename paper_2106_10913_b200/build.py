@@ -21,7 +21,7 @@ NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "--expt-relaxed-constexpr", "--extended-lambda",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-O3", "-Xptxas", "-O3"]
-SOURCES = ["api.cu", "kernels.cu", "ops.cu", "setup.cu", "wbuild.cu", "assemble.cu", "dgemm.cu"]
+SOURCES = ["api.cu", "kernels.cu", "ops.cu", "setup.cu", "wbuild.cu", "assemble.cu", "dgemm.cu", "eig.cu", "chol.cu"]
 
 
 def _needs(obj: str, deps) -> bool:

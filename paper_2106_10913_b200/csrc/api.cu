@@ -502,7 +502,7 @@ int awg_set_option(awg_ctx* ctx, const char* name, long long value) {
     else if (k == "fused_min_cols") c.fused_min_cols = std::max(8, v);
     else if (k == "fused_tail") c.fused_tail_pct = std::max(0, std::min(90, v));
     else if (k == "fused_static_cols" || k == "synth_nm" || k == "dgemm_variant" || k == "coarse_neg" ||
-             k == "verbose" || k == "wbuild_cublas" || k == "rrf_exact_probe")
+             k == "verbose" || k == "wbuild_cublas" || k == "setup_cusolver")
       c.opts[k] = value;
     else
       c.fail(AWG_E_ARG, "set_option: unknown option " + k);
@@ -534,6 +534,13 @@ int awg_coarse_solve(awg_ctx* ctx, int which, const double* b, double* x) {
     k::rr_solve(c, f, db.p, dx.p, nullptr);
     AWG_CUDA(cudaMemcpyAsync(x, dx.p, sizeof(double) * f.dim, cudaMemcpyDeviceToHost, c.stream));
     AWG_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int awg_bench_eig(awg_ctx* ctx, int n, int count, int kind, unsigned long long seed, double* out) {
+  return guarded(ctx, [&](Ctx& c) {
+    if (n < 2 || count < 1 || !out) c.fail(AWG_E_ARG, "bench_eig: bad arguments");
+    eig_check(c, n, count, kind, seed, out);
   });
 }
 

@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <stdexcept>
@@ -152,6 +153,8 @@ struct GemmDesc {
   const double* B;
   double* C;
   int M, N, K, lda, ldb, ldc;
+  int sub;    // 0: C = A B;  1: C = C - A B
+  int lower;  // 1: only tiles that touch the lower triangle (m >= n) are computed
 };
 struct GemmTile {
   int prob, m0, n0, pad;
@@ -465,6 +468,36 @@ void partition_closure(Ctx& c, const std::vector<int>& owner, int nsub, int ring
 void bench_grouped_dgemm(Ctx& c, int m, int n, int k, int count, bool transpose_a, int reps, double* out);
 void build_core(Ctx& c);        // INEX core LU
 void run_setup(Ctx& c, const awg_config& cfg);  // setup.cu
+// batched dense symmetric eigensolver (eig.cu): A (n x n, ld, lower; destroyed),
+// w (n eigenvalues, ascending), Z (n x nvec eigenvectors of the nvec smallest, ldz)
+struct SyevJob {
+  double* A;
+  int n, ld;
+  double* w;
+  double* Z;
+  int ldz, nvec;
+};
+// pick(q, w): after the eigenvalues of problem q are known (host copy, ascending),
+// the number of eigenvectors it needs (<= its nvec); null: nvec as given
+void eig_batched(Ctx& c, const std::vector<SyevJob>& jobs,
+                 const std::function<int(int, const double*)>& pick);  // on c.stream
+void eig_check(Ctx& c, int n, int count, int kind, unsigned long long seed, double* out);  // awg_bench_eig
+// batched Cholesky + block triangular solves (chol.cu), all on c.stream
+struct CholJob {
+  double* A;  // n x n, ld (lower; the factor L on return)
+  int n, ld;
+};
+struct CholBatch {
+  std::vector<CholJob> jobs;
+  int nmax = 0, npan = 0;
+  DArr<double> di, dit;  // inverted 64 x 64 diagonal blocks and their transposes
+  DArr<int> info;
+  void factor(Ctx& c, const std::vector<CholJob>& jobs);  // AWG_E_NOT_SPD with the pivot index
+  void solve_lower(Ctx& c, const std::vector<double*>& B, const std::vector<int>& ldb, const std::vector<int>& nrhs);
+  void solve_upper_t(Ctx& c, const std::vector<double*>& B, const std::vector<int>& ldb, const std::vector<int>& nrhs);
+  void reduce_pencil(Ctx& c, const std::vector<double*>& MA, const std::vector<double*>& T);  // MA <- sym(L^-1 MA L^-T)
+  void inverse_transpose(Ctx& c, const std::vector<double*>& U, const std::vector<double*>& T);  // U <- L^-T
+};
 void pivoted_factor_of(Ctx& c, int n, const double* G_host, int exact, CoarseFactor& f);  // setup.cu
 void build_local_cholesky(Ctx& c);              // setup.cu: AS / AS+ factors U^s = L^-T
 // wbuild.cu: batched inner PCGs for W (modes = (s, k) list, ascending)

@@ -17,7 +17,8 @@
 // fragment loads are bank-conflict free:
 //   A tile as [k][m] with 132 doubles per k (1056 B = 32 B mod 128 B)
 //   B tile as [n][k] with 20 doubles per n  (160 B = 32 B mod 128 B)
-// Every product is column-major C = A B (A: M x K, B: K x N), alpha 1, beta 0.
+// Every product is column-major C = A B (A: M x K, B: K x N), or C -= A B
+// (GemmDesc::sub), optionally only on the tiles touching the lower triangle.
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -175,7 +176,7 @@ __global__ void __launch_bounds__(GCfg<BN, BK, ST, WM, TA>::kT, MINB)
 #pragma unroll
       for (int i = 0; i < MI; ++i) {
         const int m = m0 + wm + 8 * i + fr;
-        if (m < pr.M) cn[m] = acc[i][j][e];
+        if (m < pr.M) cn[m] = pr.sub ? cn[m] - acc[i][j][e] : acc[i][j][e];
       }
     }
 }
@@ -216,7 +217,8 @@ void GroupedGemm::set(Ctx& c, const std::vector<GemmDesc>& probs, bool transpose
     // share the panel through L2 (A is read from HBM once; B^s stays L2-resident)
     const int bn = ta ? 64 : gemm_bn(c);
     for (int m0 = 0; m0 < d.M; m0 += kBM)
-      for (int n0 = 0; n0 < d.N; n0 += bn) tl.push_back({p, m0, n0, 0});
+      for (int n0 = 0; n0 < d.N; n0 += bn)
+        if (!d.lower || m0 + kBM > n0) tl.push_back({p, m0, n0, 0});
   }
   desc.upload(probs, c.stream);
   tiles.upload(tl, c.stream);

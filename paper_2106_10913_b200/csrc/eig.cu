@@ -1,0 +1,925 @@
+// Batched dense symmetric eigensolver for the setup (hand-written, sm_100a):
+// the B^s eigendecompositions of the splitting (dense_sym_eig, dense.cpp:117-209,
+// called from eigsplit, splitting.cpp:64-84) and the standard problems the
+// GenEO pencils reduce to (generalized_sym_eig, dense.cpp:211-224).  The
+// reference runs cyclic Jacobi; any accurate symmetric eigensolver produces
+// the same spectra (parity on eigenvalues, mode counts and
+// basis-invariant operators).  Three stages, one problem per CTA where the
+// stage is sequential, grouped FP64 tensor-core GEMMs (dgemm.cu) where it is
+// not:
+//
+// 1. Householder tridiagonalisation Q^T A Q = T (LAPACK's dsytrd / dlatrd
+//    algorithm, lower storage, panels of kNB = 64 columns).  k_latrd (one
+//    persistent CTA per problem) reduces the panel's columns one by one; the
+//    symmetric matrix-vector product of each column streams the trailing
+//    lower triangle column by column from HBM into shared memory with TMA
+//    bulk copies (cp.async.bulk + mbarrier ring, the single-pass local solve's
+//    pipeline) and uses each column for both halves of the product (the dot
+//    into w_c and the rank-1 update w += A(:,c) v_c), so the triangle is read
+//    once per column.  The rank-2k update of the trailing matrix after each
+//    panel (A22 -= V W^T + W V^T) is one grouped DMMA GEMM over all problems,
+//    lower tiles only.
+// 2. Eigenvalues of T by bisection on Sturm counts (thread per eigenvalue),
+//    eigenvectors of T by the twisted factorisation (thread per vector, in place
+//    in the output column: no scratch), and inverse iteration with
+//    reorthogonalisation (LAPACK dstein's scheme) for clusters of close
+//    eigenvalues, where single twisted vectors would not be orthogonal.
+// 3. Back-transformation Z <- Q Z with the compact WY form of each panel
+//    (Q_p = I - V_p T_p V_p^T; T_p accumulated by k_latrd, LAPACK dlarft):
+//    three grouped DMMA GEMMs per panel over all problems.
+#include <cublas_v2.h>
+#include <cusolverDn.h>
+
+#include <algorithm>
+#include <cfloat>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <vector>
+
+#include "awg_internal.cuh"
+
+namespace awgb {
+namespace {
+
+constexpr int kNB = 64;        // panel width
+constexpr int kLT = 512;       // k_latrd threads
+constexpr int kLW = kLT / 32;  // warps
+constexpr size_t kLatrdSmemCap = size_t(225) * 1024;
+
+struct EigDev {
+  double* A;     // n x n, ld (lower referenced; reflectors on return)
+  double* VW;    // ld x 2 kNB: panel V (columns 0..kNB-1) and W (kNB..2kNB-1)
+  double* Bt;    // (2 kNB) x n, column-major: row-major [W V] (the rank-2k update's B operand)
+  double* d;     // n: diagonal of T
+  double* e;     // n: off-diagonal of T (e[j] = T(j+1, j))
+  double* tau;   // n
+  double* T;     // panels x kNB x kNB: upper triangular block-reflector factors
+  int n, ld;
+};
+
+__device__ __forceinline__ unsigned smem_addr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mb_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mb_arm(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mb_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ double wsum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// CTA-wide sum (all threads get the result).  red: kLW doubles of shared memory.
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = wsum(v);
+  __syncthreads();  // red reusable
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double a = red[lane & (kLW - 1)];
+#pragma unroll
+  for (int o = kLW / 2; o >= 1; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+  return a;
+}
+
+// ---------------------------------------------------------------------------
+// 1. Panel reduction (dlatrd, lower).  Columns j = k0 .. k0 + jmax - 1.
+// Rows are owned cyclically: row i = tid + kLT * k, k < R, held in registers.
+// Shared memory: nslot column slots of L doubles (the TMA ring) + v (L).
+template <int R>
+__global__ void __launch_bounds__(kLT, 1) k_latrd(const EigDev* __restrict__ jobs, int k0, int L, int nslot) {
+  extern __shared__ __align__(128) double esm[];
+  __shared__ __align__(8) unsigned long long bar[16];
+  __shared__ double red[kLW], red2[2][kLW];
+  __shared__ double s_rowv[kNB], s_roww[kNB], s_s1[kNB], s_s2[kNB];
+  __shared__ double s_scal[4];
+  const EigDev J = jobs[blockIdx.x];
+  const int n = J.n, ld = J.ld, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (k0 >= n - 1) return;
+  const int jmax = min(kNB, n - 1 - k0);
+  double* vsm = esm + (size_t)nslot * L;
+  double* Vp = J.VW;
+  double* Wp = J.VW + (size_t)kNB * ld;
+  double* Tp = J.T + (size_t)(k0 / kNB) * kNB * kNB;
+  if (tid == 0) {
+    for (int b = 0; b < nslot; ++b) mb_init(&bar[b], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // zero the panel (unused columns must be zero for the rank-2k update) and T
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    const int i = tid + kLT * k;
+    if (i < n) {
+      for (int p = 0; p < 2 * kNB; ++p) {
+        J.VW[i + (size_t)p * ld] = 0.0;
+        J.Bt[(size_t)i * 2 * kNB + p] = 0.0;
+      }
+    }
+  }
+  for (int t = tid; t < kNB * kNB; t += kLT) Tp[t] = 0.0;
+  __syncthreads();
+  unsigned g = 0;  // ring steps consumed by this CTA: slot g % nslot, parity (g / nslot) & 1
+
+  for (int jj = 0; jj < jmax; ++jj) {
+    const int j = k0 + jj;
+    // (1) column j of the trailing matrix with the panel's earlier updates:
+    //     a = A(j:n, j) - V(j:n, 0:jj) W(j, 0:jj)^T - W(j:n, 0:jj) V(j, 0:jj)^T
+    if (tid < jj) {
+      s_rowv[tid] = Vp[j + (size_t)tid * ld];
+      s_roww[tid] = Wp[j + (size_t)tid * ld];
+    }
+    __syncthreads();
+    double ar[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const int i = tid + kLT * k;
+      double a = 0.0;
+      if (i >= j && i < n) {
+        a = J.A[i + (size_t)j * ld];
+        for (int p = 0; p < jj; ++p)
+          a -= Vp[i + (size_t)p * ld] * s_roww[p] + Wp[i + (size_t)p * ld] * s_rowv[p];
+      }
+      ar[k] = a;
+      if (i == j) s_scal[0] = a;        // diagonal d_j
+      if (i == j + 1) s_scal[1] = a;    // alpha
+    }
+    // (2) Householder reflector of a(j+1:n) (dlarfg): H = I - tau v v^T, v(j+1) = 1
+    double ss = 0.0;
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const int i = tid + kLT * k;
+      if (i > j + 1 && i < n) ss = fma(ar[k], ar[k], ss);
+    }
+    const double xnorm2 = block_sum(ss, red);  // (the barrier inside also publishes s_scal)
+    const double dj = s_scal[0], alpha = s_scal[1];
+    double beta, tau, scale;
+    if (xnorm2 == 0.0) {
+      beta = alpha;
+      tau = 0.0;
+      scale = 0.0;
+    } else {
+      beta = -copysign(sqrt(fma(alpha, alpha, xnorm2)), alpha);
+      tau = (beta - alpha) / beta;
+      scale = 1.0 / (alpha - beta);
+    }
+    double vr[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const int i = tid + kLT * k;
+      const double v = (i == j + 1) ? 1.0 : (i > j + 1 && i < n ? ar[k] * scale : 0.0);
+      vr[k] = v;
+      if (i < n) {
+        vsm[i] = v;
+        Vp[i + (size_t)jj * ld] = v;
+        if (i > j) J.A[i + (size_t)j * ld] = v;  // reflector storage (explicit 1 at j + 1)
+      }
+    }
+    __syncthreads();  // vsm complete before the product reads v_c
+    // (3) y = A(j+1:n, j+1:n) v over the stored lower triangle (not yet
+    //     updated by this panel): column c contributes the dot
+    //     sum_{i > c} A(i, c) v_i to y_c and A(i, c) v_c to y_i (i >= c).
+    double yr[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) yr[k] = 0.0;
+    const int c_begin = j + 1, ncol = n - c_begin;
+    auto issue = [&](int q) {  // copy column c_begin + q into slot (g + q) % nslot
+      const int c = c_begin + q;
+      const int c0 = c & ~1;
+      const unsigned bytes = unsigned(((n - c0) + 1) & ~1) * 8u;
+      const unsigned b = (g + q) % nslot;
+      mb_arm(&bar[b], bytes);
+      bulk_copy(esm + (size_t)b * L, J.A + c0 + (size_t)c * ld, bytes, &bar[b]);
+    };
+    if (tid == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      for (int q = 0; q < nslot && q < ncol; ++q) issue(q);
+    }
+    for (int q = 0; q < ncol; ++q) {
+      const int c = c_begin + q, c0 = c & ~1;
+      const unsigned gq = g + q;
+      mb_wait(&bar[gq % nslot], (gq / nslot) & 1);
+      const double* col = esm + (size_t)(gq % nslot) * L - c0;  // col[i] = A(i, c), i >= c0
+      const double vc = vsm[c];
+      double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        const int i = tid + kLT * k;
+        const bool in = (i >= c) && (i < n);
+        const double a = in ? col[in ? i : c] : 0.0;
+        yr[k] = fma(a, vc, yr[k]);
+        const double t = (i > c) ? a * vr[k] : 0.0;
+        if (k & 1) a1 += t;
+        else a0 += t;
+      }
+      const double dot = wsum(a0 + a1);
+      if (lane == 0) red2[q & 1][warp] = dot;
+      __syncthreads();
+      if (tid == 0 && q + nslot < ncol) issue(q + nslot);  // this slot is free again
+      if (warp == 0) {
+        double s = red2[q & 1][lane & (kLW - 1)];
+#pragma unroll
+        for (int o = kLW / 2; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) Wp[c + (size_t)jj * ld] = s;  // the dot, parked in W(:, jj) until (4)
+      }
+    }
+    g += ncol;
+    __syncthreads();
+    // (4) w = tau (y - V (W^T v) - W (V^T v)); w += (-tau/2 w^T v) v
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const int i = tid + kLT * k;
+      if (i > j && i < n) yr[k] += Wp[i + (size_t)jj * ld];
+    }
+    for (int p = warp; p < 2 * jj; p += kLW) {  // s1 = W^T v, s2 = V^T v over rows > j
+      const double* colp = (p < jj) ? Wp + (size_t)p * ld : Vp + (size_t)(p - jj) * ld;
+      double acc = 0.0;
+      for (int i = j + 1 + lane; i < n; i += 32) acc = fma(colp[i], vsm[i], acc);
+      acc = wsum(acc);
+      if (lane == 0) {
+        if (p < jj) s_s1[p] = acc;
+        else s_s2[p - jj] = acc;
+      }
+    }
+    __syncthreads();
+    double wv = 0.0;
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const int i = tid + kLT * k;
+      double y = 0.0;
+      if (i > j && i < n) {
+        y = yr[k];
+        for (int p = 0; p < jj; ++p) y -= Vp[i + (size_t)p * ld] * s_s1[p] + Wp[i + (size_t)p * ld] * s_s2[p];
+        y *= tau;
+      }
+      yr[k] = y;
+      wv = fma(y, vr[k], wv);
+    }
+    const double alpha2 = -0.5 * tau * block_sum(wv, red);
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const int i = tid + kLT * k;
+      if (i < n) {
+        const double w = (i > j) ? fma(alpha2, vr[k], yr[k]) : 0.0;
+        Wp[i + (size_t)jj * ld] = w;
+        J.Bt[(size_t)i * 2 * kNB + jj] = w;
+        J.Bt[(size_t)i * 2 * kNB + kNB + jj] = vr[k];
+      }
+    }
+    if (tid == 0) {
+      // T(0:jj, jj) = -tau T(0:jj, 0:jj) (V^T v); T(jj, jj) = tau  (dlarft, forward, columnwise)
+      for (int p = 0; p < jj; ++p) {
+        double t = 0.0;
+        for (int q = p; q < jj; ++q) t += Tp[p + q * kNB] * s_s2[q];
+        Tp[p + jj * kNB] = -tau * t;
+      }
+      Tp[jj + jj * kNB] = tau;
+      J.d[j] = dj;
+      J.e[j] = beta;
+      J.tau[j] = tau;
+    }
+    __syncthreads();
+  }
+}
+
+// the last diagonal entry: A(n-1, n-1) after its final panel's rank-2 update
+// (that panel ends at column n-2, so its trailing matrix is this one entry:
+// A(n-1,n-1) - 2 V(n-1,:) W(n-1,:)^T; done here instead of a 1 x 1 GEMM)
+__global__ void k_last_diag(const EigDev* __restrict__ jobs) {
+  const EigDev J = jobs[blockIdx.x];
+  if (threadIdx.x != 0 || J.n <= 0) return;
+  const int n = J.n;
+  double a = J.A[(n - 1) + (size_t)(n - 1) * J.ld];
+  if (n >= 2) {
+    const double* Vp = J.VW;
+    const double* Wp = J.VW + (size_t)kNB * J.ld;
+    for (int p = 0; p < kNB; ++p) a -= 2.0 * Vp[(n - 1) + (size_t)p * J.ld] * Wp[(n - 1) + (size_t)p * J.ld];
+  }
+  J.d[n - 1] = a;
+}
+
+// ---------------------------------------------------------------------------
+// 2. Tridiagonal eigenproblem.
+struct TriDev {
+  const double* d;
+  const double* e;
+  double* w;      // n eigenvalues, ascending (output)
+  double* wu;     // n: unsorted scratch
+  double* Z;      // n x nvec eigenvectors of T (ldz)
+  double* scr;    // 5 n scratch (cluster inverse iteration)
+  int n, ldz, nvec;
+};
+
+__device__ double tnorm_of(const double* d, const double* e, int n) {
+  double m = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const double r = fabs(d[i]) + (i > 0 ? fabs(e[i - 1]) : 0.0) + (i < n - 1 ? fabs(e[i]) : 0.0);
+    m = fmax(m, r);
+  }
+  return m;
+}
+
+constexpr double kPivmin = 1e-290;
+
+// number of eigenvalues of T strictly below x (Sturm sequence of the LDL^T of T - x)
+__device__ __forceinline__ int sturm(const double* d, const double* e2, int n, double x) {
+  int cnt = 0;
+  double q = d[0] - x;
+  if (fabs(q) < kPivmin) q = -kPivmin;
+  cnt += q < 0.0;
+  for (int i = 1; i < n; ++i) {
+    q = (d[i] - x) - e2[i - 1] / q;
+    if (fabs(q) < kPivmin) q = -kPivmin;
+    cnt += q < 0.0;
+  }
+  return cnt;
+}
+
+// thread per eigenvalue index; d and e^2 staged in shared memory (one problem per CTA row)
+__global__ void k_bisect(const TriDev* __restrict__ jobs, int per_cta) {
+  extern __shared__ double tsm[];
+  const TriDev J = jobs[blockIdx.y];
+  const int n = J.n;
+  const int k = blockIdx.x * per_cta + threadIdx.x;
+  if (blockIdx.x * per_cta >= n) return;
+  double* d = tsm;
+  double* e2 = tsm + n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    d[i] = J.d[i];
+    e2[i] = (i < n - 1) ? J.e[i] * J.e[i] : 0.0;
+  }
+  __syncthreads();
+  if (k >= n || threadIdx.x >= per_cta) return;
+  double lo = INFINITY, hi = -INFINITY;
+  for (int i = 0; i < n; ++i) {
+    const double r = (i > 0 ? fabs(J.e[i - 1]) : 0.0) + (i < n - 1 ? fabs(J.e[i]) : 0.0);
+    lo = fmin(lo, d[i] - r);
+    hi = fmax(hi, d[i] + r);
+  }
+  const double tn = fmax(fabs(lo), fabs(hi));
+  lo -= 2.0 * DBL_EPSILON * tn + kPivmin;
+  hi += 2.0 * DBL_EPSILON * tn + kPivmin;
+  for (int it = 0; it < 200; ++it) {
+    const double mid = 0.5 * (lo + hi);
+    if (mid <= lo || mid >= hi) break;
+    if (hi - lo <= 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + kPivmin) break;
+    if (sturm(d, e2, n, mid) > k) hi = mid;
+    else lo = mid;
+  }
+  J.wu[k] = 0.5 * (lo + hi);
+}
+
+// per problem: ascending sort of the bisection results (bitonic, in shared memory)
+__global__ void k_sort_eigs(const TriDev* __restrict__ jobs, int pow2) {
+  extern __shared__ double ssm[];
+  const TriDev J = jobs[blockIdx.x];
+  const int n = J.n;
+  for (int i = threadIdx.x; i < pow2; i += blockDim.x) ssm[i] = i < n ? J.wu[i] : INFINITY;
+  __syncthreads();
+  for (int k = 2; k <= pow2; k <<= 1)
+    for (int jx = k >> 1; jx > 0; jx >>= 1) {
+      for (int i = threadIdx.x; i < pow2; i += blockDim.x) {
+        const int l = i ^ jx;
+        if (l > i) {
+          const bool up = (i & k) == 0;
+          const double a = ssm[i], b = ssm[l];
+          if ((a > b) == up) {
+            ssm[i] = b;
+            ssm[l] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) J.w[i] = ssm[i];
+}
+
+// eigenvector of T for eigenvalue w[p] by the twisted factorisation
+// T - lam = L+ D+ L+^T = U- D- U-^T, twist r = argmin |gamma_r|,
+// gamma_r = D+_r + D-_r - (d_r - lam); z_r = 1, z_i = -(e_i / D+_i) z_{i+1}
+// upwards, z_{i+1} = -(e_i / D-_{i+1}) z_i downwards.  In place in column p.
+__global__ void k_twisted(const TriDev* __restrict__ jobs, int per_cta) {
+  const TriDev J = jobs[blockIdx.y];
+  const int p = blockIdx.x * per_cta + threadIdx.x;
+  if (threadIdx.x >= per_cta || p >= J.nvec) return;
+  const int n = J.n;
+  const double* d = J.d;
+  const double* e = J.e;
+  const double lam = J.w[p];
+  double* z = J.Z + (size_t)p * J.ldz;
+  auto guard = [](double v) { return fabs(v) < kPivmin ? -kPivmin : v; };
+  if (n == 1) {
+    z[0] = 1.0;
+    return;
+  }
+  // backward: D-_i into z[i]
+  double dm = guard(d[n - 1] - lam);
+  z[n - 1] = dm;
+  for (int i = n - 2; i >= 0; --i) {
+    dm = guard((d[i] - lam) - e[i] * e[i] / dm);
+    z[i] = dm;
+  }
+  // forward: D+_i, gamma_i, argmin; z[i] <- D+_i
+  double dp = guard(d[0] - lam);
+  double best = fabs(dp + z[0] - (d[0] - lam));
+  int r = 0;
+  z[0] = dp;
+  for (int i = 1; i < n; ++i) {
+    dp = guard((d[i] - lam) - e[i - 1] * e[i - 1] / dp);
+    const double gam = fabs(dp + z[i] - (d[i] - lam));
+    if (gam < best) {
+      best = gam;
+      r = i;
+    }
+    z[i] = dp;
+  }
+  // D-_i again below the twist
+  dm = guard(d[n - 1] - lam);
+  if (n - 1 > r) z[n - 1] = dm;
+  for (int i = n - 2; i > r; --i) {
+    dm = guard((d[i] - lam) - e[i] * e[i] / dm);
+    z[i] = dm;
+  }
+  // the vector
+  double nrm = 1.0, zi = 1.0;
+  for (int i = r - 1; i >= 0; --i) {
+    zi = -(e[i] / z[i]) * zi;
+    z[i] = zi;
+    nrm = fma(zi, zi, nrm);
+  }
+  zi = 1.0;
+  for (int i = r; i < n - 1; ++i) {
+    zi = -(e[i] / z[i + 1]) * zi;
+    z[i + 1] = zi;
+    nrm = fma(zi, zi, nrm);
+  }
+  z[r] = 1.0;
+  const double s = 1.0 / sqrt(nrm);
+  for (int i = 0; i < n; ++i) z[i] *= s;
+  J.wu[p] = isfinite(nrm) && nrm < 1e280 ? 0.0 : 1.0;  // 1: recompute by inverse iteration (k_clusters)
+}
+
+// Clusters (consecutive eigenvalues closer than kClusterTol * ||T||): the
+// twisted vectors of close eigenvalues are not orthogonal (error ~ eps ||T|| /
+// gap), so their columns are recomputed by inverse iteration with
+// reorthogonalisation against the cluster's earlier members in every step
+// (LAPACK dstein), on the LU factorisation with partial pivoting of T - lam
+// (dlagtf / dlagts).  One CTA per problem walks its clusters in order.
+constexpr double kClusterTol = 1e-6;
+
+__global__ void k_clusters(const TriDev* __restrict__ jobs) {
+  __shared__ double red[8];
+  __shared__ int s_cl[2];
+  const TriDev J = jobs[blockIdx.x];
+  const int n = J.n, nv = J.nvec, tid = threadIdx.x;
+  if (n < 2 || nv < 2) return;
+  double* u1 = J.scr;
+  double* u2 = J.scr + n;
+  double* u3 = J.scr + 2 * n;
+  double* lm = J.scr + 3 * n;
+  int* piv = reinterpret_cast<int*>(J.scr + 4 * n);
+  const double tn = tnorm_of(J.d, J.e, n);
+  const double tol = kClusterTol * tn;
+  const double small = DBL_EPSILON * tn + kPivmin;
+  auto bsum = [&](double v) {
+    const int lane = tid & 31, warp = tid >> 5;
+    v = wsum(v);
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    double a = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) a += red[w];
+    return a;
+  };
+  int p = 0;
+  while (p < nv) {
+    // cluster [p, q): consecutive gaps below tol
+    int q = p + 1;
+    while (q < n && J.w[q] - J.w[q - 1] < tol) ++q;
+    const int qend = min(q, nv);
+    if (qend - p >= 2 || J.wu[p] != 0.0) {  // a cluster, or a twisted vector that broke down
+      for (int m = p; m < qend; ++m) {
+        // separate equal eigenvalues slightly so the factorisations differ (dstein's pertol)
+        double lam = J.w[m];
+        if (m > p && lam - J.w[m - 1] < 10.0 * DBL_EPSILON * tn) lam = J.w[m - 1] + 10.0 * DBL_EPSILON * tn * (m - p);
+        if (tid == 0) {  // LU of T - lam with partial pivoting (banded, 3 diagonals of U)
+          double r0 = J.d[0] - lam, r1 = (n > 1) ? J.e[0] : 0.0, r2 = 0.0;
+          for (int i = 0; i < n - 1; ++i) {
+            const double n0 = J.e[i], n1 = J.d[i + 1] - lam, n2 = (i + 1 < n - 1) ? J.e[i + 1] : 0.0;
+            if (fabs(r0) >= fabs(n0)) {
+              const double l = (r0 != 0.0) ? n0 / r0 : 0.0;
+              u1[i] = (r0 != 0.0) ? r0 : small;
+              u2[i] = r1;
+              u3[i] = r2;
+              lm[i] = l;
+              piv[i] = 0;
+              r0 = n1 - l * r1;
+              r1 = n2 - l * r2;
+              r2 = 0.0;
+            } else {
+              const double l = r0 / n0;
+              u1[i] = n0;
+              u2[i] = n1;
+              u3[i] = n2;
+              lm[i] = l;
+              piv[i] = 1;
+              r0 = r1 - l * n1;
+              r1 = r2 - l * n2;
+              r2 = 0.0;
+            }
+          }
+          u1[n - 1] = (r0 != 0.0) ? r0 : small;
+        }
+        double* z = J.Z + (size_t)m * J.ldz;
+        // deterministic start vector
+        for (int i = tid; i < n; i += blockDim.x) {
+          unsigned long long h = (unsigned long long)(i + 1) * 0x9E3779B97F4A7C15ull + (unsigned long long)(m + 1);
+          h ^= h >> 31;
+          h *= 0xBF58476D1CE4E5B9ull;
+          h ^= h >> 29;
+          z[i] = double(h >> 11) * 0x1.0p-53 - 0.5;
+        }
+        __syncthreads();
+        for (int it = 0; it < 4; ++it) {
+          if (tid == 0) {  // solve (T - lam) x = z in place: P L U
+            for (int i = 0; i < n - 1; ++i) {
+              if (piv[i]) {
+                const double t = z[i];
+                z[i] = z[i + 1];
+                z[i + 1] = t;
+              }
+              z[i + 1] -= lm[i] * z[i];
+            }
+            double mx = 0.0;
+            for (int i = n - 1; i >= 0; --i) {
+              double v = z[i];
+              if (i + 1 < n) v -= u2[i] * z[i + 1];
+              if (i + 2 < n) v -= u3[i] * z[i + 2];
+              double piv0 = u1[i];
+              if (fabs(piv0) < small) piv0 = copysign(small, piv0);
+              v /= piv0;
+              z[i] = v;
+              mx = fmax(mx, fabs(v));
+              if (mx > 1e150) {  // rescale (dlagts overflow guard)
+                for (int t = i; t < n; ++t) z[t] *= 1e-150;
+                mx *= 1e-150;
+              }
+            }
+          }
+          __syncthreads();
+          // reorthogonalise against the cluster's earlier (final) members, then normalise
+          for (int o = p; o < m; ++o) {
+            const double* zo = J.Z + (size_t)o * J.ldz;
+            double a = 0.0;
+            for (int i = tid; i < n; i += blockDim.x) a = fma(zo[i], z[i], a);
+            const double dotp = bsum(a);
+            for (int i = tid; i < n; i += blockDim.x) z[i] = fma(-dotp, zo[i], z[i]);
+            __syncthreads();
+          }
+          double a = 0.0;
+          for (int i = tid; i < n; i += blockDim.x) a = fma(z[i], z[i], a);
+          const double nrm = sqrt(bsum(a));
+          const double s = nrm > 0.0 ? 1.0 / nrm : 0.0;
+          for (int i = tid; i < n; i += blockDim.x) z[i] *= s;
+          __syncthreads();
+        }
+      }
+    }
+    if (tid == 0) s_cl[0] = q;
+    __syncthreads();
+    p = s_cl[0];
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// 3. Back-transformation helpers: the clean panel V_p (rows k0 .. n-1,
+// column jj holds the reflector of column k0 + jj: zero above row k0 + jj + 1).
+__global__ void k_panel_v(const EigDev* __restrict__ jobs, int k0, double* __restrict__ vbuf, long long vstride) {
+  const EigDev J = jobs[blockIdx.y];
+  if (k0 >= J.n - 1) return;
+  const int jmax = min(kNB, J.n - 1 - k0);
+  const int m = J.n - k0;
+  double* out = vbuf + blockIdx.y * vstride;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < (long long)m * kNB;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int r = int(t % m), jj = int(t / m);
+    double v = 0.0;
+    if (jj < jmax && r >= jj + 1) v = J.A[(k0 + r) + (size_t)(k0 + jj) * J.ld];
+    out[r + (size_t)jj * J.ld] = v;
+  }
+}
+
+int rows_per_thread(int nmax) {
+  const int R = (nmax + kLT - 1) / kLT;
+  return R <= 1 ? 1 : R <= 2 ? 2 : R <= 4 ? 4 : R <= 8 ? 8 : R <= 11 ? 11 : R <= 12 ? 12 : -1;
+}
+
+template <int R>
+void launch_latrd(Ctx& c, const EigDev* jobs, int count, int k0, int L, int nslot, size_t smem) {
+  ensure_dyn_smem((const void*)k_latrd<R>, smem);
+  k_latrd<R><<<count, kLT, smem, c.stream>>>(jobs, k0, L, nslot);
+  ++c.launches;
+  check_launch("latrd");
+}
+
+}  // namespace
+
+// jobs: A (n x n, ld, lower), w (n eigenvalues ascending), Z (n x nvec, ldz):
+// the eigenvectors of the nvec smallest eigenvalues.  A is destroyed.
+void eig_batched(Ctx& c, const std::vector<SyevJob>& jobs_in, const std::function<int(int, const double*)>& pick) {
+  std::vector<SyevJob> jobs = jobs_in;
+  const int J = int(jobs.size());
+  if (J == 0) return;
+  int nmax = 0, ldmax = 0;
+  for (const auto& j : jobs) {
+    nmax = std::max(nmax, j.n);
+    ldmax = std::max(ldmax, j.ld);
+    if (j.ld % 4 || j.ldz % 2) c.fail(AWG_E_ARG, "eig: leading dimensions must be multiples of 4 (A) and 2 (Z)");
+  }
+  const int R = rows_per_thread(nmax);
+  if (R < 0) c.fail(AWG_E_ARG, "eig: matrix larger than 6,144 rows");
+  // ---- workspace
+  const int npan = (nmax - 1 + kNB - 1) / kNB;
+  std::vector<long long> off(J + 1, 0);
+  DArr<double> vw, bt, dd, ee, tt, tp, wu, scr, vbuf, xb, xb2;
+  vw.alloc(size_t(J) * ldmax * 2 * kNB);
+  bt.alloc(size_t(J) * 2 * kNB * ldmax);
+  dd.alloc(size_t(J) * ldmax);
+  ee.alloc(size_t(J) * ldmax);
+  tt.alloc(size_t(J) * ldmax);
+  tp.alloc(size_t(J) * std::max(npan, 1) * kNB * kNB);
+  wu.alloc(size_t(J) * ldmax);
+  scr.alloc(size_t(J) * 5 * ldmax);
+  ee.zero(c.stream);
+  std::vector<EigDev> ed(J);
+  std::vector<TriDev> td(J);
+  int nvmax = 0;
+  for (int q = 0; q < J; ++q) {
+    const SyevJob& s = jobs[q];
+    ed[q] = EigDev{s.A, vw.p + size_t(q) * ldmax * 2 * kNB, bt.p + size_t(q) * 2 * kNB * ldmax, dd.p + size_t(q) * ldmax,
+                   ee.p + size_t(q) * ldmax, tt.p + size_t(q) * ldmax, tp.p + size_t(q) * std::max(npan, 1) * kNB * kNB,
+                   s.n, s.ld};
+    // the panel buffers use the problem's own ld (their row stride); ld <= ldmax
+    td[q] = TriDev{ed[q].d, ed[q].e, s.w, wu.p + size_t(q) * ldmax, s.Z, scr.p + size_t(q) * 5 * ldmax, s.n, s.ldz,
+                   s.nvec};
+    nvmax = std::max(nvmax, s.nvec);
+  }
+  DArr<EigDev> d_ed;
+  DArr<TriDev> d_td;
+  d_ed.upload(ed, c.stream);
+  d_td.upload(td, c.stream);
+
+  // ---- 1. tridiagonalisation
+  const int L = round_up(ldmax, 2);
+  int nslot = int(std::min<size_t>(8, kLatrdSmemCap / (size_t(L) * 8) - 1));
+  if (nslot < 2) c.fail(AWG_E_ARG, "eig: matrix too large for the shared-memory ring");
+  const size_t smem = size_t(nslot + 1) * L * 8;
+  for (int k0 = 0; k0 < nmax - 1; k0 += kNB) {
+    switch (R) {
+      case 1: launch_latrd<1>(c, d_ed.p, J, k0, L, nslot, smem); break;
+      case 2: launch_latrd<2>(c, d_ed.p, J, k0, L, nslot, smem); break;
+      case 4: launch_latrd<4>(c, d_ed.p, J, k0, L, nslot, smem); break;
+      case 8: launch_latrd<8>(c, d_ed.p, J, k0, L, nslot, smem); break;
+      case 11: launch_latrd<11>(c, d_ed.p, J, k0, L, nslot, smem); break;
+      default: launch_latrd<12>(c, d_ed.p, J, k0, L, nslot, smem); break;
+    }
+    // A22 -= V W^T + W V^T on rows / columns >= k1 (lower tiles)
+    std::vector<GemmDesc> pd;
+    for (int q = 0; q < J; ++q) {
+      const int n = jobs[q].n;
+      if (k0 >= n - 1) continue;
+      const int k1 = k0 + std::min(kNB, n - 1 - k0);
+      const int m = n - k1;
+      if (m <= 1) continue;  // the final panel (k1 = n - 1): k_last_diag
+      pd.push_back({ed[q].VW + k1, ed[q].Bt + size_t(k1) * 2 * kNB, jobs[q].A + k1 + size_t(k1) * jobs[q].ld, m, m,
+                    2 * kNB, jobs[q].ld, 2 * kNB, jobs[q].ld, 1, 1});
+    }
+    if (!pd.empty()) {
+      GroupedGemm g;
+      g.set(c, pd);
+      g.run(c);
+    }
+  }
+  k_last_diag<<<J, 32, 0, c.stream>>>(d_ed.p);
+  ++c.launches;
+
+  // ---- 2. tridiagonal eigenvalues and vectors
+  {
+    const int per = 128;
+    dim3 gb((nmax + per - 1) / per, J);
+    const size_t sm = size_t(2) * nmax * 8;
+    ensure_dyn_smem((const void*)k_bisect, sm);
+    k_bisect<<<gb, per, sm, c.stream>>>(d_td.p, per);
+    int pow2 = 1;
+    while (pow2 < nmax) pow2 <<= 1;
+    ensure_dyn_smem((const void*)k_sort_eigs, size_t(pow2) * 8);
+    k_sort_eigs<<<J, 1024, size_t(pow2) * 8, c.stream>>>(d_td.p, pow2);
+    if (pick) {  // the caller chooses how many eigenvectors each problem needs from its spectrum
+      std::vector<double> hw(nmax);
+      nvmax = 0;
+      for (int q = 0; q < J; ++q) {
+        AWG_CUDA(cudaMemcpyAsync(hw.data(), jobs[q].w, sizeof(double) * jobs[q].n, cudaMemcpyDeviceToHost, c.stream));
+        AWG_CUDA(cudaStreamSynchronize(c.stream));
+        const int nv = pick(q, hw.data());
+        if (nv > jobs[q].nvec) c.fail(AWG_E_STATE, "eig: more eigenvectors requested than the output holds");
+        jobs[q].nvec = nv;
+        td[q].nvec = nv;
+        nvmax = std::max(nvmax, nv);
+      }
+      d_td.upload(td, c.stream);
+    }
+    if (nvmax > 0) {
+      dim3 gt((nvmax + per - 1) / per, J);
+      k_twisted<<<gt, per, 0, c.stream>>>(d_td.p, per);
+      k_clusters<<<J, 256, 0, c.stream>>>(d_td.p);
+    }
+    c.launches += 4;
+    check_launch("tridiagonal eigensolver");
+  }
+
+  // ---- 3. Z <- Q Z, panels in reverse order: Z(k0:n, :) -= V_p (T_p (V_p^T Z(k0:n, :)))
+  if (nvmax > 0) {
+    vbuf.alloc(size_t(J) * ldmax * kNB);
+    xb.alloc(size_t(J) * kNB * nvmax);
+    xb2.alloc(size_t(J) * kNB * nvmax);
+    for (int pnl = npan - 1; pnl >= 0; --pnl) {
+      const int k0 = pnl * kNB;
+      dim3 gv(64, J);
+      k_panel_v<<<gv, 256, 0, c.stream>>>(d_ed.p, k0, vbuf.p, (long long)ldmax * kNB);
+      ++c.launches;
+      std::vector<GemmDesc> p1, p2, p3;
+      for (int q = 0; q < J; ++q) {
+        const SyevJob& s = jobs[q];
+        if (k0 >= s.n - 1 || s.nvec == 0) continue;
+        const int m = s.n - k0;
+        double* V = vbuf.p + size_t(q) * ldmax * kNB;
+        double* X = xb.p + size_t(q) * kNB * nvmax;
+        double* X2 = xb2.p + size_t(q) * kNB * nvmax;
+        double* Zk = s.Z + k0;
+        // X = V^T Z   (kNB x nvec)
+        p1.push_back({V, Zk, X, kNB, s.nvec, m, s.ld, s.ldz, kNB, 0, 0});
+        // X2 = T X
+        p2.push_back({ed[q].T + size_t(pnl) * kNB * kNB, X, X2, kNB, s.nvec, kNB, kNB, kNB, kNB, 0, 0});
+        // Z -= V X2
+        p3.push_back({V, X2, Zk, m, s.nvec, kNB, s.ld, kNB, s.ldz, 1, 0});
+      }
+      if (p1.empty()) continue;
+      GroupedGemm g1, g2, g3;
+      g1.set(c, p1, /*transpose_a=*/true);
+      g1.run(c);
+      g2.set(c, p2);
+      g2.run(c);
+      g3.set(c, p3);
+      g3.run(c);
+    }
+  }
+  AWG_CUDA(cudaStreamSynchronize(c.stream));
+}
+
+namespace {
+__global__ void k_fill_sym(int n, int ld, int kind, unsigned long long seed, double* __restrict__ A) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= (long long)n * n) return;
+  const int i = int(t % n), j = int(t / n);
+  const int a = min(i, j), b = max(i, j);
+  double v;
+  if (kind == 1) {  // 5-point Laplacian on an m x m grid
+    const int m = int(llrint(sqrt(double(n))));
+    const int ax = a % m, ay = a / m, bx = b % m, by = b / m;
+    v = (a == b) ? 4.0 : ((ay == by && bx - ax == 1) || (ax == bx && by - ay == 1)) ? -1.0 : 0.0;
+  } else {
+    unsigned long long h = seed + (unsigned long long)a * 0x9E3779B97F4A7C15ull + (unsigned long long)b * 0xD1B54A32D192ED03ull;
+    h ^= h >> 31;
+    h *= 0xBF58476D1CE4E5B9ull;
+    h ^= h >> 29;
+    v = double(h >> 11) * 0x1.0p-53 - 0.5;
+    if (kind == 2 && a == b) v += 1e-6 * pow(1e6, double(a) / n) * n;
+  }
+  A[i + (size_t)j * ld] = v;
+}
+__global__ void k_maxabs_diff(long long cnt, const double* __restrict__ a, const double* __restrict__ b,
+                              unsigned long long* __restrict__ out) {
+  double m = 0.0;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < cnt; t += (long long)gridDim.x * blockDim.x)
+    m = fmax(m, fabs(a[t] - (b ? b[t] : 0.0)));
+  atomicMax(out, __double_as_longlong(m));
+}
+// R = A Z - Z diag(w), column-scaled residual; and G = Z^T Z - I
+__global__ void k_resid_prep(int n, int ld, const double* __restrict__ w, double* __restrict__ AZ,
+                             const double* __restrict__ Z, double* __restrict__ G) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= (long long)n * n) return;
+  const int i = int(t % n), j = int(t / n);
+  AZ[i + (size_t)j * ld] -= w[j] * Z[i + (size_t)j * ld];
+  if (i == j) G[i + (size_t)j * ld] -= 1.0;
+}
+}  // namespace
+
+// Check / benchmark hook (awg_bench_eig): `count` seeded symmetric matrices
+// of order n — kind 0: random entries; kind 1: the 5-point Laplacian of an
+// m x m grid (n = m^2; exactly repeated eigenvalues); kind 2: random with a
+// graded spectrum — through eig_batched, against cuSOLVER Dsyevd on the same
+// matrices.  out: [0] max |w - w_ref| / ||A||, [1] max ||A z - w z|| / ||A||,
+// [2] max |Z^T Z - I|, [3] ms eig_batched, [4] ms cuSOLVER (all count).
+void eig_check(Ctx& c, int n, int count, int kind, unsigned long long seed, double* out) {
+  const int ld = round_up(n, 4);
+  const size_t blk = size_t(ld) * n;
+  DArr<double> A0, A, Z, w, wref, AZ, G;
+  A0.alloc(blk * count);
+  A.alloc(blk * count);
+  Z.alloc(blk * count);
+  w.alloc(size_t(n) * count);
+  wref.alloc(size_t(n) * count);
+  AZ.alloc(blk);
+  G.alloc(blk);
+  A0.zero(c.stream);
+  for (int q = 0; q < count; ++q)
+    k_fill_sym<<<int(((long long)n * n + 255) / 256), 256, 0, c.stream>>>(n, ld, kind, seed + q, A0.p + blk * q);
+  AWG_CUDA(cudaMemcpyAsync(A.p, A0.p, sizeof(double) * blk * count, cudaMemcpyDeviceToDevice, c.stream));
+  std::vector<SyevJob> jobs;
+  for (int q = 0; q < count; ++q) jobs.push_back({A.p + blk * q, n, ld, w.p + size_t(n) * q, Z.p + blk * q, ld, n});
+  cudaEvent_t e0, e1;
+  AWG_CUDA(cudaEventCreate(&e0));
+  AWG_CUDA(cudaEventCreate(&e1));
+  AWG_CUDA(cudaEventRecord(e0, c.stream));
+  eig_batched(c, jobs, nullptr);
+  AWG_CUDA(cudaEventRecord(e1, c.stream));
+  AWG_CUDA(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  AWG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  out[3] = ms;
+  // reference: cuSOLVER on copies
+  cusolverDnHandle_t h;
+  cublasHandle_t bh;
+  if (cusolverDnCreate(&h) != CUSOLVER_STATUS_SUCCESS || cublasCreate(&bh) != CUBLAS_STATUS_SUCCESS)
+    c.fail(AWG_E_CUDA, "eig_check: library handles");
+  cusolverDnSetStream(h, c.stream);
+  cublasSetStream(bh, c.stream);
+  int lw = 0;
+  cusolverDnDsyevd_bufferSize(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, A0.p, ld, wref.p, &lw);
+  DArr<double> work;
+  DArr<int> info;
+  work.alloc(size_t(lw) + 1);
+  info.alloc(1);
+  DArr<double> Aref;
+  Aref.alloc(blk);
+  AWG_CUDA(cudaEventRecord(e0, c.stream));
+  for (int q = 0; q < count; ++q) {
+    AWG_CUDA(cudaMemcpyAsync(Aref.p, A0.p + blk * q, sizeof(double) * blk, cudaMemcpyDeviceToDevice, c.stream));
+    cusolverDnDsyevd(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, Aref.p, ld, wref.p + size_t(n) * q, work.p,
+                     lw, info.p);
+  }
+  AWG_CUDA(cudaEventRecord(e1, c.stream));
+  AWG_CUDA(cudaEventSynchronize(e1));
+  AWG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  out[4] = ms;
+  // errors
+  DArr<unsigned long long> mx;
+  mx.alloc(4);
+  mx.zero(c.stream);
+  double anorm = 0.0;
+  {
+    std::vector<double> hw = wref.download(c.stream);
+    for (double v : hw) anorm = std::max(anorm, std::fabs(v));
+  }
+  k_maxabs_diff<<<256, 256, 0, c.stream>>>((long long)n * count, w.p, wref.p, mx.p);
+  const double one = 1.0, zero = 0.0;
+  for (int q = 0; q < count; ++q) {
+    const double* Aq = A0.p + blk * q;
+    const double* Zq = Z.p + blk * q;
+    cublasDsymm(bh, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, n, n, &one, Aq, ld, Zq, ld, &zero, AZ.p, ld);
+    cublasDgemm(bh, CUBLAS_OP_T, CUBLAS_OP_N, n, n, n, &one, Zq, ld, Zq, ld, &zero, G.p, ld);
+    k_resid_prep<<<int(((long long)n * n + 255) / 256), 256, 0, c.stream>>>(n, ld, w.p + size_t(n) * q, AZ.p, Zq, G.p);
+    k_maxabs_diff<<<256, 256, 0, c.stream>>>((long long)blk, AZ.p, nullptr, mx.p + 1);
+    k_maxabs_diff<<<256, 256, 0, c.stream>>>((long long)blk, G.p, nullptr, mx.p + 2);
+  }
+  std::vector<unsigned long long> hm = mx.download(c.stream);
+  double v[3];
+  for (int i = 0; i < 3; ++i) std::memcpy(&v[i], &hm[i], 8);
+  out[0] = v[0] / std::max(anorm, 1e-300);
+  out[1] = v[1] / std::max(anorm, 1e-300);
+  out[2] = v[2];
+  cusolverDnDestroy(h);
+  cublasDestroy(bh);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+}
+
+}  // namespace awgb

@@ -23,6 +23,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <functional>
 #include <numeric>
 
 #include "awg_internal.cuh"
@@ -477,6 +478,63 @@ struct LocalBlocks {
   }
 };
 
+// Subdomains grouped into waves whose per-problem workspace (bytes_of(s))
+// fits in a share of the free device memory.
+std::vector<std::vector<int>> waves_of(Ctx& c, const std::function<size_t(int)>& bytes_of, double share = 0.6) {
+  size_t fr = 0, tot = 0;
+  AWG_CUDA(cudaMemGetInfo(&fr, &tot));
+  const size_t budget = size_t(double(fr) * share);
+  std::vector<std::vector<int>> w(1);
+  size_t used = 0;
+  for (int s = 0; s < c.N; ++s) {
+    const size_t b = bytes_of(s);
+    if (!w.back().empty() && used + b > budget) {
+      w.emplace_back();
+      used = 0;
+    }
+    w.back().push_back(s);
+    used += b;
+  }
+  return w;
+}
+
+// GenEO pencil (generalized_sym_eig, dense.cpp:211-224) of every subdomain in
+// `wave`: MB = L L^T (hand-written batched Cholesky), C = sym(L^-1 MA L^-T),
+// eigenvalues of C into plam (all n_s), eigenvectors of the `pick` smallest
+// (MB-normalised: Y = L^-T Z) into Ycol[s].  MA and MB are destroyed.
+void pencil_wave(Ctx& c, const std::vector<int>& wave, const std::vector<double*>& MA, const std::vector<double*>& MB,
+                 const std::vector<double*>& T, double* plam, std::vector<DArr<double>>& Ycol, int cap,
+                 const std::function<int(int, const double*)>& pick) {
+  const int J = int(wave.size());
+  std::vector<CholJob> cj(J);
+  for (int q = 0; q < J; ++q) cj[q] = {MB[q], c.h_ns[wave[q]], c.h_ld[wave[q]]};
+  CholBatch ch;
+  ch.factor(c, cj);
+  ch.reduce_pencil(c, MA, T);
+  // eigenvectors of C land in T (free again), then Y = L^-T Z in place
+  std::vector<SyevJob> ej(J);
+  for (int q = 0; q < J; ++q) {
+    const int s = wave[q];
+    ej[q] = {MA[q], c.h_ns[s], c.h_ld[s], plam + c.h_poff[s], T[q], c.h_ld[s], std::min(cap, c.h_ns[s])};
+  }
+  std::vector<int> nv(J, 0);
+  eig_batched(c, ej, [&](int q, const double* w) {
+    nv[q] = std::min(pick(wave[q], w), ej[q].nvec);
+    return nv[q];
+  });
+  std::vector<int> ldv(J);
+  for (int q = 0; q < J; ++q) ldv[q] = c.h_ld[wave[q]];
+  ch.solve_upper_t(c, T, ldv, nv);
+  for (int q = 0; q < J; ++q) {
+    const int s = wave[q];
+    Ycol[s].alloc(size_t(c.h_ld[s]) * std::max(nv[q], 1));
+    if (nv[q])
+      AWG_CUDA(cudaMemcpyAsync(Ycol[s].p, T[q], sizeof(double) * c.h_ld[s] * nv[q], cudaMemcpyDeviceToDevice,
+                               c.stream));
+  }
+  AWG_CUDA(cudaStreamSynchronize(c.stream));
+}
+
 // AS / AS+ one-level factors (OneLevel ctor, preconditioner.cpp:20-30):
 // M^s = R A R^T (AS) or R A+ R^T (AS+), M^s = L L^T (cusolver potrf),
 // U^s = L^-T (triangular solve against the identity), stored in c.U.
@@ -485,6 +543,32 @@ void local_cholesky(Ctx& c, Solvers& sv, LocalBlocks& lb) {
   c.U.alloc(size_t(c.h_voff[N]));
   c.U.zero(c.stream);
   AWG_CUDA(cudaStreamSynchronize(c.stream));
+  if (c.opt("setup_cusolver", 0) == 0) {
+    // M^s = L L^T (batched, chol.cu), U^s = L^-T
+    auto waves = waves_of(c, [&](int s) { return size_t(2) * c.h_ld[s] * c.h_ns[s] * 8; });
+    for (const auto& wave : waves) {
+      std::vector<DArr<double>> M(wave.size()), T(wave.size());
+      std::vector<CholJob> cj;
+      std::vector<double*> U, Tp;
+      for (size_t q = 0; q < wave.size(); ++q) {
+        const int s = wave[q];
+        M[q].alloc(size_t(c.h_ld[s]) * c.h_ns[s]);
+        T[q].alloc(size_t(c.h_ld[s]) * c.h_ns[s]);
+        const int st = int(q % Solvers::S);
+        if (c.one_level == 0) lb.a_block(s, st, M[q].p);
+        else lb.aplus_block(s, st, M[q].p);
+        cj.push_back({M[q].p, c.h_ns[s], c.h_ld[s]});
+        U.push_back(c.U.p + c.h_voff[s]);
+        Tp.push_back(T[q].p);
+      }
+      sv.sync();
+      CholBatch ch;
+      ch.factor(c, cj);
+      ch.inverse_transpose(c, U, Tp);
+      AWG_CUDA(cudaStreamSynchronize(c.stream));
+    }
+    return;
+  }
   size_t blk_max = 1;
   int lw_max = 1;
   for (int s = 0; s < N; ++s) {
@@ -601,7 +685,33 @@ void run_setup(Ctx& c, const awg_config& cfg) {
 
   // ---- 1+2. B^s and its eigendecomposition ------------------------------------
   double t0 = now_ms();
-  {
+  if (c.opt("setup_cusolver", 0) == 0) {
+    // hand-written batched eigensolver (eig.cu): B^s assembled in place in V^s,
+    // eigenvectors through a workspace, copied back over the reflectors
+    for (int s = 0; s < N; ++s) {
+      const int n = c.h_ns[s];
+      k_assemble<<<(n + kThreads - 1) / kThreads, kThreads, 0, c.stream>>>(
+          s, n, c.h_ld[s], c.poff.p, c.pidx.p, c.rp.p, c.ci.p, c.va.p, c.emult.p, 0, c.V.p + c.h_voff[s]);
+      ++c.launches;
+    }
+    auto waves = waves_of(c, [&](int s) { return size_t(c.h_ld[s]) * c.h_ns[s] * 8 + (size_t(4) << 20); });
+    for (const auto& wave : waves) {
+      long long zt = 0;
+      for (int s : wave) zt += (long long)c.h_ld[s] * c.h_ns[s];
+      DArr<double> Z;
+      Z.alloc(size_t(zt));
+      std::vector<SyevJob> jobs;
+      long long zo = 0;
+      for (int s : wave) {
+        jobs.push_back({c.V.p + c.h_voff[s], c.h_ns[s], c.h_ld[s], c.lam.p + c.h_poff[s], Z.p + zo, c.h_ld[s], c.h_ns[s]});
+        zo += (long long)c.h_ld[s] * c.h_ns[s];
+      }
+      eig_batched(c, jobs, nullptr);
+      AWG_CUDA(cudaMemcpyAsync(c.V.p + c.h_voff[wave.front()], Z.p, sizeof(double) * zt, cudaMemcpyDeviceToDevice,
+                               c.stream));  // the wave's blocks are contiguous in V, in the same layout
+      AWG_CUDA(cudaStreamSynchronize(c.stream));
+    }
+  } else {
     int lwork_max = 0;
     int nmax = 0;
     for (int s = 0; s < N; ++s) nmax = std::max(nmax, c.h_ns[s]);
@@ -666,16 +776,68 @@ void run_setup(Ctx& c, const awg_config& cfg) {
       lw_max = std::max(lw_max, lw);
       blk_max = std::max(blk_max, size_t(c.h_ld[s]) * c.h_ns[s]);
     }
+    DArr<double> plam, plam2;
+    plam.alloc(c.P);
+    if (as) plam2.alloc(c.P);
+    std::vector<DArr<double>> Ycol(N), Ycol2(N);
+    if (c.opt("setup_cusolver", 0) == 0) {
+      // how many GenEO vectors each pencil needs (the selection rule of k_select)
+      auto count_rule = [&](double tau, int fixed_k) {
+        return [&, tau, fixed_k](int s, const double* w) {
+          const int n = c.h_ns[s];
+          int k = 0;
+          if (fixed_k > 0) {
+            k = std::min(std::max(fixed_k, c.h_m[s]), n);
+            while (k > 0 && k < n && std::fabs(w[k] - w[k - 1]) <= 1e-8) ++k;
+          } else {
+            while (k < n && w[k] < tau) ++k;
+          }
+          return k;
+        };
+      };
+      const int cap = 512;
+      const int nb = as ? 5 : 3;
+      auto waves = waves_of(c, [&](int s) {
+        return size_t(nb) * c.h_ld[s] * c.h_ns[s] * 8 + size_t(c.h_ld[s]) * cap * 8 + (size_t(8) << 20);
+      });
+      for (const auto& wave : waves) {
+        const int J = int(wave.size());
+        std::vector<DArr<double>> B(size_t(J) * nb);
+        std::vector<double*> MA(J), MB(J), T(J), AB(J), AB2(J);
+        for (int q = 0; q < J; ++q) {
+          const int s = wave[q];
+          const size_t blk = size_t(c.h_ld[s]) * c.h_ns[s];
+          for (int b = 0; b < nb; ++b) B[size_t(q) * nb + b].alloc(blk);
+          MA[q] = B[size_t(q) * nb].p;
+          MB[q] = B[size_t(q) * nb + 1].p;
+          T[q] = B[size_t(q) * nb + 2].p;
+          const int st = q % Solvers::S;
+          lb.weighted(s, st, MA[q]);
+          lb.aplus_block(s, st, MB[q]);
+          if (as) {
+            AB[q] = B[size_t(q) * nb + 3].p;
+            AB2[q] = B[size_t(q) * nb + 4].p;
+            lb.a_block(s, st, AB[q]);
+            AWG_CUDA(cudaMemcpyAsync(AB2[q], AB[q], sizeof(double) * blk, cudaMemcpyDeviceToDevice, sv.st[st]));
+          }
+        }
+        sv.sync();
+        if (!as) {
+          const double tau = cfg.one_level == 1 ? 1.0 / cfg.tau_flat : cfg.tau_sharp;
+          pencil_wave(c, wave, MA, MB, T, plam.p, Ycol, cap, count_rule(tau, cfg.fixed_k));
+        } else {
+          // pencil_as1 = (weighted A+^s, R A R^T) below 1/tau_flat; pencil_as2 = (R A R^T, R A+ R^T) below tau_sharp
+          pencil_wave(c, wave, MA, AB, T, plam.p, Ycol, cap, count_rule(1.0 / cfg.tau_flat, 0));
+          pencil_wave(c, wave, AB2, MB, T, plam2.p, Ycol2, cap, count_rule(cfg.tau_sharp, 0));
+        }
+      }
+    } else {
     const int nbuf = as ? 4 : 2;
     std::vector<DArr<double>> buf(Solvers::S * nbuf);
     for (int i = 0; i < Solvers::S; ++i) {
       sv.work[i].alloc(size_t(lw_max) + 1);
       for (int b = 0; b < nbuf; ++b) buf[i * nbuf + b].alloc(blk_max);
     }
-    DArr<double> plam, plam2;
-    plam.alloc(c.P);
-    if (as) plam2.alloc(c.P);
-    std::vector<DArr<double>> Ycol(N), Ycol2(N);
     DArr<int> info2;
     info2.alloc(N);
     info2.zero(nullptr);
@@ -724,6 +886,7 @@ void run_setup(Ctx& c, const awg_config& cfg) {
                  v - c.h_ns[s] - 1);
         if (v != 0) c.fail(AWG_E_NO_CONVERGENCE, "generalized_sym_eig: eigensolver failed");
       }
+    }  // cuSOLVER path (option setup_cusolver=1)
     DArr<int> dks, dks2;
     dks.alloc(N);
     if (!as) {
@@ -751,7 +914,7 @@ void run_setup(Ctx& c, const awg_config& cfg) {
       if (ks[s] == 0) continue;
       const size_t ld = c.h_ld[s];
       if (!as) {
-        if (Ycol[s].n < ld * ks[s]) c.fail(AWG_E_STATE, "setup: fixed-k cluster extension beyond the kept eigenvectors");
+        if (Ycol[s].n < ld * ks[s]) c.fail(AWG_E_STATE, "setup: selected GenEO modes beyond the kept eigenvectors");
         AWG_CUDA(cudaMemcpyAsync(c.Y.p + c.h_yoff[s], Ycol[s].p, sizeof(double) * ld * ks[s], cudaMemcpyDeviceToDevice,
                                  c.stream));
       } else {  // [as1 low modes, as2 low modes] (coarse.cpp:127-130 push order)

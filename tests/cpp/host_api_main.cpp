@@ -1,12 +1,41 @@
 // C++ caller of the host API (include/awg_b200/awg.hpp), written the way the
 // reference's run_with_context (proj/src/harness.cpp:131-139) drives its
-// library: external files in, preconditioner build, PCG with H3 — on the GPU.
+// library: a problem in, preconditioner build, PCG with H3 — on the GPU.
+// The problem comes as one binary dump written by tests/test_host_api.py
+// (the reference caller would use its own file readers instead).
 //   host_api_main <prefix> <tau|-k K> [exact]
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <stdexcept>
 
 #include "awg_b200/awg.hpp"
+
+namespace {
+// <prefix>.bin: int32 n, nnz, N; int32 row_offsets[n+1], col_indices[nnz];
+// f64 values[nnz], b[n]; int32 part_offsets[N+1], part_indices[...]
+template <class T>
+std::vector<T> take(std::FILE* f, size_t count) {
+  std::vector<T> v(count);
+  if (count && std::fread(v.data(), sizeof(T), count, f) != count) throw std::runtime_error("truncated problem dump");
+  return v;
+}
+void load_dump(const std::string& path, awg_b200::SparseSymMatrix& a, std::vector<double>& b, awg_b200::Partition& p) {
+  std::FILE* f = std::fopen(path.c_str(), "rb");
+  if (!f) throw std::runtime_error("cannot open " + path);
+  const auto hdr = take<int>(f, 3);
+  a.n = hdr[0];
+  a.row_offsets = take<int>(f, size_t(hdr[0]) + 1);
+  a.col_indices = take<int>(f, size_t(hdr[1]));
+  a.values = take<double>(f, size_t(hdr[1]));
+  b = take<double>(f, size_t(hdr[0]));
+  const auto off = take<int>(f, size_t(hdr[2]) + 1);
+  const auto idx = take<int>(f, size_t(off.back()));
+  std::fclose(f);
+  p.n = a.n;
+  for (int s = 0; s < hdr[2]; ++s) p.omega.emplace_back(idx.begin() + off[s], idx.begin() + off[s + 1]);
+}
+}  // namespace
 
 int main(int argc, char** argv) {
   if (argc < 3) {
@@ -26,9 +55,10 @@ int main(int argc, char** argv) {
   }
   if (argc > argi && std::strcmp(argv[argi], "exact") == 0) cfg.exact_rank_revealing = true;
   try {
-    SparseSymMatrix a = read_matrix_market(prefix + ".mtx");
-    std::vector<double> b = read_vector(prefix + ".rhs");
-    Partition p = read_partition(prefix + ".part", a.n);
+    SparseSymMatrix a;
+    std::vector<double> b;
+    Partition p;
+    load_dump(prefix + ".bin", a, b, p);
     ProblemContext ctx(a, b, p);
     ctx.setup(cfg);
     auto [x, rep] = pcg(ctx, ctx.rhs(), 1e-8, 10000);

@@ -49,12 +49,16 @@ def oracle_of(p, f) -> O.AwgOracle:
     return O.AwgOracle(p.n, p.row_offsets, p.col_indices, p.values, list(p.omega), f)
 
 
+def name_of(fs) -> str:
+    return fs.p.name
+
+
 class FullSize:
     """One GPU setup of a BASELINE config plus the restatement on its factors."""
 
-    def __init__(self, name: str, rrf: str = "reference"):
+    def __init__(self, name: str, rrf: str = "reference", options=None):
         self.p = problems.make(name)
-        self.ctx = awg.context_from_problem(self.p)
+        self.ctx = awg.context_from_problem(self.p, options=options)
         t = time.time()
         self.ctx.setup(awg.config_for(self.p, rrf_semantics=rrf))
         self.setup_s = time.time() - t
@@ -112,14 +116,23 @@ def check_pcg(fs: FullSize, rtol: float = None) -> dict:
     xo, ro = O.pcg(lambda v: O.spmv(fs.orc.a, v), lambda v: fs.orc.h3(v, "ad"), p.b, rtol, 10 * p.n)
     t_oracle = time.time() - t
     e = rel(x, xo)
+    h_dev = np.asarray(fs.ctx._history(0))
+    h_orc = np.asarray(ro.residual_history)
+    k = min(len(h_dev), len(h_orc))
+    dev = np.abs(h_dev[:k] - h_orc[:k]) / h_orc[:k]
+    diverge = int(np.argmax(dev > 1e-3)) if np.any(dev > 1e-3) else -1
+    info = {"iterations": rep.iterations, "oracle_iterations": ro.iterations, "x_rel": e,
+            "kappa": rep.kappa_estimate, "oracle_kappa": ro.kappa_estimate, "oracle_s": t_oracle,
+            "resid_hist_max_reldiff": float(dev.max()) if k else 0.0, "first_iter_reldiff_gt_1e-3": diverge,
+            "tail_dev": h_dev[-4:].tolist(), "tail_oracle": h_orc[-4:].tolist()}
+    record(f"{name_of(fs)}_pcg_detail", info)
     assert rep.converged and ro.converged
-    assert abs(rep.iterations - ro.iterations) <= 1, (rep.iterations, ro.iterations)
+    assert abs(rep.iterations - ro.iterations) <= 1, info
     assert e <= 1e-7, e
     # krylov.cpp:93-101 on the device's own exit
     true = np.linalg.norm(p.b - O.spmv(fs.orc.a, x)) / np.linalg.norm(p.b)
     assert true <= rtol or abs(true - rep.recurrence_residual_at_exit) <= 1e-8
-    return {"iterations": rep.iterations, "oracle_iterations": ro.iterations, "x_rel": e,
-            "kappa": rep.kappa_estimate, "oracle_kappa": ro.kappa_estimate, "oracle_s": t_oracle}
+    return info
 
 
 

@@ -1,6 +1,6 @@
 """The C++ host API (include/awg_b200/awg.hpp) over the C ABI: a C++ caller
 compiles and links against libawg_b200.so here; on the GPU it runs the
-reference's external-file pathway end to end."""
+reference's run_with_context pathway end to end."""
 import json
 import os
 import subprocess
@@ -33,7 +33,14 @@ def test_cpp_host_api_runs(tmp_path):
     p = problems.make("t2d")
     assert np.array_equal(p.values, g["A_values"])
     prefix = str(tmp_path / "t2d")
-    p.write(prefix)
+    with open(prefix + ".bin", "wb") as f:
+        np.asarray([p.n, p.nnz, p.n_sub], dtype=np.int32).tofile(f)
+        np.asarray(p.row_offsets, dtype=np.int32).tofile(f)
+        np.asarray(p.col_indices, dtype=np.int32).tofile(f)
+        np.asarray(p.values, dtype=np.float64).tofile(f)
+        np.asarray(p.b, dtype=np.float64).tofile(f)
+        np.asarray(p.part_offsets(), dtype=np.int32).tofile(f)
+        np.asarray(p.part_indices(), dtype=np.int32).tofile(f)
     out = subprocess.run([exe, prefix, repr(p.tau_sharp)], check=True, capture_output=True, text=True).stdout
     r = json.loads(out)
     assert r["converged"] == 1 and abs(r["iterations"] - s["iterations"]) <= 1
