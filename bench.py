@@ -247,6 +247,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--verbose", action="store_true", help="setup progress trace on stderr")
+    ap.add_argument("--awg", default="ad", choices=["ad", "none"],
+                    help="AWG mode; 'none' (H2 alone) is a labelled deviation for c4, whose W build does not "
+                         "converge under the reference's semantics (DESIGN.md §6)")
     ap.add_argument("--rrf", default="reference", choices=["reference", "exact"],
                     help="pivoted-factor semantics: the reference's (default) or the exact one")
     args = ap.parse_args()
@@ -298,7 +301,7 @@ def main():
     from paper_2106_10913_b200 import awg
 
     ctx = awg.context_from_problem(p, device=local, options={"verbose": 1} if args.verbose else None)
-    cfg = awg.config_for(p, rrf_semantics=args.rrf)
+    cfg = awg.config_for(p, rrf_semantics=args.rrf, awg=awg.AwgMode.AD if args.awg == "ad" else awg.AwgMode.NONE)
     torch.cuda.synchronize()
     t0 = time.time()
     ctx.setup(cfg)
@@ -396,7 +399,9 @@ def main():
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator, problems.py)",
         "config": {"workload": args.config, "problem": p.meta, "n": p.n, "nnz": p.nnz, "n_sub": p.n_sub,
                    "selection": ({"fixed_k": p.fixed_k} if p.fixed_k else {"tau_sharp": p.tau_sharp}),
-                   "rtol": rtol, "preconditioner": "H3,ad + NN-hybrid (reference default)",
+                   "rtol": rtol, "preconditioner": ("H3,ad + NN-hybrid (reference default)" if args.awg == "ad" else
+                                                    "DEVIATION: H2 NN-hybrid alone (AWG none): build_w does not "
+                                                    "converge for this config under the reference's semantics"),
                    "pivoted_factor": args.rrf,
                    "l2": "inputs larger than L2" if q["sum_ns2"] * 8 > 126e6 else "inputs fit in L2 (no flush)"},
         "solve": {"iterations": its, "converged_all": True, "final_relres_max": max(resid),

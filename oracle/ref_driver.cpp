@@ -30,6 +30,7 @@
 
 #include "awg/coarse.hpp"
 #include "awg/dense.hpp"
+#include "awg/fem.hpp"
 #include "awg/krylov.hpp"
 #include "awg/partition.hpp"
 #include "awg/preconditioner.hpp"
@@ -370,9 +371,51 @@ int rrf_mode(const std::string& in, const std::string& out) {
   return 0;
 }
 
+// ref_driver --fem <nodes_x> <nodes_y> <E> <nu> <outdir>: the reference's own
+// assemble() (fem.cpp:99-162) on a single-material mesh with h = 1 and the
+// default body force: CSR and rhs, to pin the elasticity generator.
+int fem_mode(int nx, int ny, double e, double nu, const std::string& out) {
+  MeshSpec mesh;
+  mesh.domain_width = nx - 1;
+  mesh.domain_height = ny - 1;
+  mesh.h = 1.0;
+  const AssembledSystem sys = assemble(mesh, CoefficientField::constant(e, nu));
+  npy_i(out, "row_offsets", sys.a.row_offsets);
+  npy_i(out, "col_indices", sys.a.col_indices);
+  npy_d(out, "values", sys.a.values);
+  npy_d(out, "b", sys.b);
+  return 0;
+}
+
+// ref_driver --autopart <prefix> <n_parts> <outdir>: auto_partition
+// (partition.cpp:42-92: BFS parts, then the one-ring closure of :79-90) of the
+// matrix in <prefix>.mtx; exports the closed index sets.
+int autopart_mode(const std::string& prefix, int parts, const std::string& out) {
+  const SparseSymMatrix a = read_matrix_market(prefix + ".mtx");
+  const Partition p = auto_partition(a, parts);
+  std::vector<int> off = {0}, idx;
+  for (const auto& om : p.omega) {
+    idx.insert(idx.end(), om.begin(), om.end());
+    off.push_back(int(idx.size()));
+  }
+  npy_i(out, "part_offsets", off);
+  npy_i(out, "part_indices", idx);
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
+  if (argc >= 7 && std::string(argv[1]) == "--fem") {
+    std::string cmd = "mkdir -p '" + std::string(argv[6]) + "'";
+    if (std::system(cmd.c_str()) != 0) return 2;
+    return fem_mode(std::stoi(argv[2]), std::stoi(argv[3]), std::stod(argv[4]), std::stod(argv[5]), argv[6]);
+  }
+  if (argc >= 5 && std::string(argv[1]) == "--autopart") {
+    std::string cmd = "mkdir -p '" + std::string(argv[4]) + "'";
+    if (std::system(cmd.c_str()) != 0) return 2;
+    return autopart_mode(argv[2], std::stoi(argv[3]), argv[4]);
+  }
   if (argc >= 4 && std::string(argv[1]) == "--rrf") {
     std::string cmd = "mkdir -p '" + std::string(argv[3]) + "'";
     if (std::system(cmd.c_str()) != 0) return 2;

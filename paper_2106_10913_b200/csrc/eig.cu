@@ -32,6 +32,8 @@
 
 #include <algorithm>
 #include <cfloat>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 #include <functional>
@@ -43,9 +45,9 @@ namespace awgb {
 namespace {
 
 constexpr int kNB = 64;        // panel width
-constexpr int kLT = 512;       // k_latrd threads
-constexpr int kLW = kLT / 32;  // warps
-constexpr size_t kLatrdSmemCap = size_t(225) * 1024;
+constexpr int kLT = 480;       // k_latrd row-owning (consumer) threads: 15 warps + 1 producer warp,
+constexpr int kLW = kLT / 32;  // 512 threads in all (128 registers per thread)
+constexpr size_t kLatrdSmemCap = size_t(217) * 1024;  // + ~10 KB static (part, mbarriers) <= 227 KB
 
 struct EigDev {
   double* A;     // n x n, ld (lower referenced; reflectors on return)
@@ -86,56 +88,91 @@ __device__ __forceinline__ double wsum(double v) {
   return v;
 }
 
-// CTA-wide sum (all threads get the result).  red: kLW doubles of shared memory.
-__device__ __forceinline__ double block_sum(double v, double* red) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  v = wsum(v);
-  __syncthreads();  // red reusable
-  if (lane == 0) red[warp] = v;
-  __syncthreads();
-  double a = red[lane & (kLW - 1)];
-#pragma unroll
-  for (int o = kLW / 2; o >= 1; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-  return a;
-}
-
 // ---------------------------------------------------------------------------
 // 1. Panel reduction (dlatrd, lower).  Columns j = k0 .. k0 + jmax - 1.
-// Rows are owned cyclically: row i = tid + kLT * k, k < R, held in registers.
-// Shared memory: nslot column slots of L doubles (the TMA ring) + v (L).
+// 15 consumer warps own the rows cyclically (row i = tid + kLT * k, k < R, in
+// registers); a 17th warp is the copy producer of the symmetric product's TMA
+// ring (nslot column slots of L doubles, full / empty mbarriers: no CTA barrier
+// per column).  Shared memory: the ring + v (L doubles).
+constexpr int kLThreads = kLT + 32;
+
+__device__ __forceinline__ void mb_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void bar_consumers() { asm volatile("bar.sync 1, %0;" ::"n"(kLT) : "memory"); }
+
+// 16 per-lane partials -> lanes l and l + 16 hold the warp sum of partial l & 15
+// (31 shuffles for 16 columns instead of 5 per column)
+constexpr int kCG = 16;  // columns per reduction group
+constexpr int kFillTarget = 4096;  // doubles per ring fill (32 KB) when columns are short
+constexpr int kMaxFillCols = 64;
+__device__ __forceinline__ double transpose_reduce16(double (&v)[kCG], int lane) {
+#pragma unroll
+  for (int k = 0; k < kCG; ++k) v[k] += __shfl_xor_sync(0xffffffffu, v[k], 16);
+#pragma unroll
+  for (int st = 8; st >= 1; st >>= 1) {
+    const bool up = (lane & st) != 0;
+#pragma unroll
+    for (int k = 0; k < st; ++k) {
+      const double send = up ? v[k] : v[k + st];
+      const double keep = up ? v[k + st] : v[k];
+      v[k] = keep + __shfl_xor_sync(0xffffffffu, send, st);
+    }
+  }
+  return v[0];
+}
+
 template <int R>
-__global__ void __launch_bounds__(kLT, 1) k_latrd(const EigDev* __restrict__ jobs, int k0, int L, int nslot) {
+__global__ void __launch_bounds__(kLThreads, 1) k_latrd(const EigDev* __restrict__ jobs, int k0, int L, int nslot) {
   extern __shared__ __align__(128) double esm[];
-  __shared__ __align__(8) unsigned long long bar[16];
-  __shared__ double red[kLW], red2[2][kLW];
+  __shared__ __align__(8) unsigned long long full[8], empty[8];
+  __shared__ double red[16];
+  __shared__ double part[2][kLW][kCG];
   __shared__ double s_rowv[kNB], s_roww[kNB], s_s1[kNB], s_s2[kNB];
   __shared__ double s_scal[4];
+  __shared__ unsigned s_nfill;
   const EigDev J = jobs[blockIdx.x];
   const int n = J.n, ld = J.ld, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (k0 >= n - 1) return;
+  const bool cons = tid < kLT;  // row owner (the producer warp owns no rows)
   const int jmax = min(kNB, n - 1 - k0);
   double* vsm = esm + (size_t)nslot * L;
   double* Vp = J.VW;
   double* Wp = J.VW + (size_t)kNB * ld;
   double* Tp = J.T + (size_t)(k0 / kNB) * kNB * kNB;
   if (tid == 0) {
-    for (int b = 0; b < nslot; ++b) mb_init(&bar[b], 1);
+    for (int b = 0; b < nslot; ++b) {
+      mb_init(&full[b], 1);
+      mb_init(&empty[b], kLW);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  // zero the panel (unused columns must be zero for the rank-2k update) and T
+  auto bsum = [&](double v) {  // CTA-wide sum (the producer warp contributes 0; every thread gets it)
+    v = wsum(v);
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    double a = red[lane & 15];
 #pragma unroll
-  for (int k = 0; k < R; ++k) {
-    const int i = tid + kLT * k;
-    if (i < n) {
-      for (int p = 0; p < 2 * kNB; ++p) {
-        J.VW[i + (size_t)p * ld] = 0.0;
-        J.Bt[(size_t)i * 2 * kNB + p] = 0.0;
+    for (int o = 8; o >= 1; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    return a;
+  };
+  // zero the panel (unused columns must be zero for the rank-2k update) and T
+  if (cons) {
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const int i = tid + kLT * k;
+      if (i < n) {
+        for (int p = 0; p < 2 * kNB; ++p) {
+          J.VW[i + (size_t)p * ld] = 0.0;
+          J.Bt[(size_t)i * 2 * kNB + p] = 0.0;
+        }
       }
     }
   }
-  for (int t = tid; t < kNB * kNB; t += kLT) Tp[t] = 0.0;
+  for (int t = tid; t < kNB * kNB; t += kLThreads) Tp[t] = 0.0;
   __syncthreads();
-  unsigned g = 0;  // ring steps consumed by this CTA: slot g % nslot, parity (g / nslot) & 1
+  unsigned g = 0;  // ring fills so far: slot g % nslot, fill round g / nslot
 
   for (int jj = 0; jj < jmax; ++jj) {
     const int j = k0 + jj;
@@ -151,23 +188,23 @@ __global__ void __launch_bounds__(kLT, 1) k_latrd(const EigDev* __restrict__ job
     for (int k = 0; k < R; ++k) {
       const int i = tid + kLT * k;
       double a = 0.0;
-      if (i >= j && i < n) {
+      if (cons && i >= j && i < n) {
         a = J.A[i + (size_t)j * ld];
         for (int p = 0; p < jj; ++p)
           a -= Vp[i + (size_t)p * ld] * s_roww[p] + Wp[i + (size_t)p * ld] * s_rowv[p];
+        if (i == j) s_scal[0] = a;      // diagonal d_j
+        if (i == j + 1) s_scal[1] = a;  // alpha
       }
       ar[k] = a;
-      if (i == j) s_scal[0] = a;        // diagonal d_j
-      if (i == j + 1) s_scal[1] = a;    // alpha
     }
     // (2) Householder reflector of a(j+1:n) (dlarfg): H = I - tau v v^T, v(j+1) = 1
     double ss = 0.0;
 #pragma unroll
     for (int k = 0; k < R; ++k) {
       const int i = tid + kLT * k;
-      if (i > j + 1 && i < n) ss = fma(ar[k], ar[k], ss);
+      if (cons && i > j + 1 && i < n) ss = fma(ar[k], ar[k], ss);
     }
-    const double xnorm2 = block_sum(ss, red);  // (the barrier inside also publishes s_scal)
+    const double xnorm2 = bsum(ss);  // (its barriers also publish s_scal)
     const double dj = s_scal[0], alpha = s_scal[1];
     double beta, tau, scale;
     if (xnorm2 == 0.0) {
@@ -184,8 +221,8 @@ __global__ void __launch_bounds__(kLT, 1) k_latrd(const EigDev* __restrict__ job
     for (int k = 0; k < R; ++k) {
       const int i = tid + kLT * k;
       const double v = (i == j + 1) ? 1.0 : (i > j + 1 && i < n ? ar[k] * scale : 0.0);
-      vr[k] = v;
-      if (i < n) {
+      vr[k] = cons ? v : 0.0;
+      if (cons && i < n) {
         vsm[i] = v;
         Vp[i + (size_t)jj * ld] = v;
         if (i > j) J.A[i + (size_t)j * ld] = v;  // reflector storage (explicit 1 at j + 1)
@@ -199,55 +236,117 @@ __global__ void __launch_bounds__(kLT, 1) k_latrd(const EigDev* __restrict__ job
 #pragma unroll
     for (int k = 0; k < R; ++k) yr[k] = 0.0;
     const int c_begin = j + 1, ncol = n - c_begin;
-    auto issue = [&](int q) {  // copy column c_begin + q into slot (g + q) % nslot
-      const int c = c_begin + q;
-      const int c0 = c & ~1;
-      const unsigned bytes = unsigned(((n - c0) + 1) & ~1) * 8u;
-      const unsigned b = (g + q) % nslot;
-      mb_arm(&bar[b], bytes);
-      bulk_copy(esm + (size_t)b * L, J.A + c0 + (size_t)c * ld, bytes, &bar[b]);
+    // Ring fills carry one or more whole column segments (as many consecutive
+    // columns as fit in kFillTarget doubles): the short columns of the trailing
+    // triangle still move enough bytes per fill to keep HBM busy.  Producer and
+    // consumers derive the same fill partition from (n, c).
+    auto seg_of = [&](int c) { return ((n - (c & ~1)) + 1) & ~1; };  // doubles copied for column c
+    auto fill_cols = [&](int q) {  // columns in the fill that starts at column offset q
+      int k = 0, tot = 0;
+      while (q + k < ncol && k < kMaxFillCols) {
+        const int sg = seg_of(c_begin + q + k);
+        if (k > 0 && tot + sg > min(L, kFillTarget)) break;
+        tot += sg;
+        ++k;
+      }
+      return k;
     };
-    if (tid == 0) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      for (int q = 0; q < nslot && q < ncol; ++q) issue(q);
-    }
-    for (int q = 0; q < ncol; ++q) {
-      const int c = c_begin + q, c0 = c & ~1;
-      const unsigned gq = g + q;
-      mb_wait(&bar[gq % nslot], (gq / nslot) & 1);
-      const double* col = esm + (size_t)(gq % nslot) * L - c0;  // col[i] = A(i, c), i >= c0
-      const double vc = vsm[c];
-      double a0 = 0.0, a1 = 0.0;
-#pragma unroll
-      for (int k = 0; k < R; ++k) {
-        const int i = tid + kLT * k;
-        const bool in = (i >= c) && (i < n);
-        const double a = in ? col[in ? i : c] : 0.0;
-        yr[k] = fma(a, vc, yr[k]);
-        const double t = (i > c) ? a * vr[k] : 0.0;
-        if (k & 1) a1 += t;
-        else a0 += t;
+    unsigned nfill = 0;
+    if (!cons) {
+      // producer: the fills' bulk copies, each fill after every consumer warp
+      // released the slot's previous contents
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        for (int q = 0; q < ncol;) {
+          const int K = fill_cols(q);
+          const unsigned gq = g + nfill, b = gq % nslot, round = gq / nslot;
+          if (round > 0) mb_wait(&empty[b], (round - 1) & 1);
+          unsigned bytes = 0;
+          for (int k = 0; k < K; ++k) bytes += unsigned(seg_of(c_begin + q + k)) * 8u;
+          mb_arm(&full[b], bytes);
+          int off = 0;
+          for (int k = 0; k < K; ++k) {
+            const int c = c_begin + q + k, c0 = c & ~1, sg = seg_of(c);
+            bulk_copy(esm + (size_t)b * L + off, J.A + c0 + (size_t)c * ld, unsigned(sg) * 8u, &full[b]);
+            off += sg;
+          }
+          q += K;
+          ++nfill;
+        }
       }
-      const double dot = wsum(a0 + a1);
-      if (lane == 0) red2[q & 1][warp] = dot;
-      __syncthreads();
-      if (tid == 0 && q + nslot < ncol) issue(q + nslot);  // this slot is free again
-      if (warp == 0) {
-        double s = red2[q & 1][lane & (kLW - 1)];
+      __syncwarp();
+    } else {
+      int rem = 0, off = 0;  // columns left in the current fill, its next segment offset
+      unsigned b = 0;
+      for (int q0 = 0; q0 < ncol; q0 += kCG) {
+        double acc[kCG];
 #pragma unroll
-        for (int o = kLW / 2; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (lane == 0) Wp[c + (size_t)jj * ld] = s;  // the dot, parked in W(:, jj) until (4)
+        for (int u = 0; u < kCG; ++u) {
+          acc[u] = 0.0;
+          const int q = q0 + u;
+          if (q < ncol) {
+            if (rem == 0) {  // next fill (uniform across the CTA)
+              if (nfill > 0) {
+                __syncwarp();
+                if (lane == 0) mb_arrive(&empty[b]);
+              }
+              const unsigned gq = g + nfill;
+              b = gq % nslot;
+              rem = fill_cols(q);
+              off = 0;
+              mb_wait(&full[b], (gq / nslot) & 1);
+              ++nfill;
+            }
+            const int c = c_begin + q, c0 = c & ~1;
+            const double* col = esm + (size_t)b * L + off - c0;  // col[i] = A(i, c), i >= c0
+            off += seg_of(c);
+            --rem;
+            const double vc = vsm[c];
+            const int kmin = c / kLT;  // slots below hold rows < c for every thread
+            double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+            for (int k = 0; k < R; ++k) {
+              if (k >= kmin) {  // uniform branch: inactive slots are skipped, not predicated
+                const int i = tid + kLT * k;
+                const bool in = (i >= c) && (i < n);
+                const double a = in ? col[i] : 0.0;
+                yr[k] = fma(a, vc, yr[k]);
+                const double t = (i > c) ? a * vr[k] : 0.0;
+                if (k & 1) a1 += t;
+                else a0 += t;
+              }
+            }
+            acc[u] = a0 + a1;
+          }
+        }
+        const double wpart = transpose_reduce16(acc, lane);  // lane l: this warp's dot for column q0 + (l & 15)
+        const int pb = (q0 / kCG) & 1;
+        if (lane < kCG) part[pb][warp][lane] = wpart;
+        bar_consumers();
+        if (warp == 0 && lane < kCG && q0 + lane < ncol) {
+          double sdot = 0.0;
+#pragma unroll
+          for (int w = 0; w < kLW; ++w) sdot += part[pb][w][lane];
+          Wp[c_begin + q0 + lane + (size_t)jj * ld] = sdot;  // parked in W(:, jj) until (4)
+        }
+      }
+      if (nfill > 0) {  // release the last fill
+        __syncwarp();
+        if (lane == 0) mb_arrive(&empty[b]);
       }
     }
-    g += ncol;
+    // every thread advances the fill counter by the same count
+    if (tid == 0) s_nfill = nfill;
+    __syncthreads();
+    g += s_nfill;
     __syncthreads();
     // (4) w = tau (y - V (W^T v) - W (V^T v)); w += (-tau/2 w^T v) v
 #pragma unroll
     for (int k = 0; k < R; ++k) {
       const int i = tid + kLT * k;
-      if (i > j && i < n) yr[k] += Wp[i + (size_t)jj * ld];
+      if (cons && i > j && i < n) yr[k] += Wp[i + (size_t)jj * ld];
     }
-    for (int p = warp; p < 2 * jj; p += kLW) {  // s1 = W^T v, s2 = V^T v over rows > j
+    for (int p = warp; p < 2 * jj; p += kLW + 1) {  // s1 = W^T v, s2 = V^T v over rows > j
       const double* colp = (p < jj) ? Wp + (size_t)p * ld : Vp + (size_t)(p - jj) * ld;
       double acc = 0.0;
       for (int i = j + 1 + lane; i < n; i += 32) acc = fma(colp[i], vsm[i], acc);
@@ -263,7 +362,7 @@ __global__ void __launch_bounds__(kLT, 1) k_latrd(const EigDev* __restrict__ job
     for (int k = 0; k < R; ++k) {
       const int i = tid + kLT * k;
       double y = 0.0;
-      if (i > j && i < n) {
+      if (cons && i > j && i < n) {
         y = yr[k];
         for (int p = 0; p < jj; ++p) y -= Vp[i + (size_t)p * ld] * s_s1[p] + Wp[i + (size_t)p * ld] * s_s2[p];
         y *= tau;
@@ -271,11 +370,11 @@ __global__ void __launch_bounds__(kLT, 1) k_latrd(const EigDev* __restrict__ job
       yr[k] = y;
       wv = fma(y, vr[k], wv);
     }
-    const double alpha2 = -0.5 * tau * block_sum(wv, red);
+    const double alpha2 = -0.5 * tau * bsum(wv);
 #pragma unroll
     for (int k = 0; k < R; ++k) {
       const int i = tid + kLT * k;
-      if (i < n) {
+      if (cons && i < n) {
         const double w = (i > j) ? fma(alpha2, vr[k], yr[k]) : 0.0;
         Wp[i + (size_t)jj * ld] = w;
         J.Bt[(size_t)i * 2 * kNB + jj] = w;
@@ -475,13 +574,15 @@ __global__ void k_twisted(const TriDev* __restrict__ jobs, int per_cta) {
   J.wu[p] = isfinite(nrm) && nrm < 1e280 ? 0.0 : 1.0;  // 1: recompute by inverse iteration (k_clusters)
 }
 
-// Clusters (consecutive eigenvalues closer than kClusterTol * ||T||): the
-// twisted vectors of close eigenvalues are not orthogonal (error ~ eps ||T|| /
-// gap), so their columns are recomputed by inverse iteration with
-// reorthogonalisation against the cluster's earlier members in every step
-// (LAPACK dstein), on the LU factorisation with partial pivoting of T - lam
-// (dlagtf / dlagts).  One CTA per problem walks its clusters in order.
-constexpr double kClusterTol = 1e-6;
+// Tight clusters (consecutive eigenvalues closer than kClusterTol * ||T||):
+// twisted vectors of nearly equal eigenvalues can coincide, so their columns
+// are recomputed by inverse iteration with reorthogonalisation against the
+// cluster's earlier members in every step (LAPACK dstein), on the LU
+// factorisation with partial pivoting of T - lam (dlagtf / dlagts).  One CTA
+// per problem walks its clusters in order.  Every other pair of vectors is
+// orthogonal to ~eps ||T|| / gap <= 1e-6 and is finished by the windowed
+// Newton-Schulz step below.
+constexpr double kClusterTol = 1e-10;
 
 __global__ void k_clusters(const TriDev* __restrict__ jobs) {
   __shared__ double red[8];
@@ -608,6 +709,35 @@ __global__ void k_clusters(const TriDev* __restrict__ jobs) {
   }
 }
 
+// Newton-Schulz orthogonalisation of column windows of Z: Z_w <- Z_w (3I - G)/2
+// with G = Z_w^T Z_w.  The twisted / inverse-iteration vectors each have a
+// residual ~ eps ||T||, and the off-diagonal of G pairs vectors i, j with
+// ~eps ||T|| / |lam_i - lam_j|, so the correction mixes a vector only with
+// close eigenvalues and keeps every residual ~ eps ||T|| while the window
+// becomes orthonormal (two steps: 1e-6 -> 1e-12 -> rounding).  Windows of
+// consecutive eigenvalues, two overlapping passes (offset W / 2).
+__global__ void k_ns_h(int count, const int* __restrict__ wsz, int W, double* __restrict__ G) {
+  const int q = blockIdx.y;
+  if (q >= count) return;
+  const int m = wsz[q];
+  double* g = G + (size_t)q * W * W;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < m * m; t += gridDim.x * blockDim.x) {
+    const int i = t % m, j = t / m;
+    g[i + (size_t)j * W] = ((i == j) ? 1.5 : 0.0) - 0.5 * g[i + (size_t)j * W];
+  }
+}
+
+__global__ void k_copy_cols(int count, const double* const* __restrict__ src, double* const* __restrict__ dst,
+                            const int* __restrict__ rows, const int* __restrict__ cols, const int* __restrict__ lds,
+                            const int* __restrict__ ldd) {
+  const int q = blockIdx.y;
+  const long long cnt = (long long)rows[q] * cols[q];
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < cnt; t += (long long)gridDim.x * blockDim.x) {
+    const int i = int(t % rows[q]), j = int(t / rows[q]);
+    dst[q][i + (size_t)j * ldd[q]] = src[q][i + (size_t)j * lds[q]];
+  }
+}
+
 // ---------------------------------------------------------------------------
 // 3. Back-transformation helpers: the clean panel V_p (rows k0 .. n-1,
 // column jj holds the reflector of column k0 + jj: zero above row k0 + jj + 1).
@@ -627,14 +757,14 @@ __global__ void k_panel_v(const EigDev* __restrict__ jobs, int k0, double* __res
 }
 
 int rows_per_thread(int nmax) {
-  const int R = (nmax + kLT - 1) / kLT;
+  const int R = (nmax + kLT - 1) / kLT;  // n <= 5,760
   return R <= 1 ? 1 : R <= 2 ? 2 : R <= 4 ? 4 : R <= 8 ? 8 : R <= 11 ? 11 : R <= 12 ? 12 : -1;
 }
 
 template <int R>
 void launch_latrd(Ctx& c, const EigDev* jobs, int count, int k0, int L, int nslot, size_t smem) {
   ensure_dyn_smem((const void*)k_latrd<R>, smem);
-  k_latrd<R><<<count, kLT, smem, c.stream>>>(jobs, k0, L, nslot);
+  k_latrd<R><<<count, kLThreads, smem, c.stream>>>(jobs, k0, L, nslot);
   ++c.launches;
   check_launch("latrd");
 }
@@ -654,7 +784,7 @@ void eig_batched(Ctx& c, const std::vector<SyevJob>& jobs_in, const std::functio
     if (j.ld % 4 || j.ldz % 2) c.fail(AWG_E_ARG, "eig: leading dimensions must be multiples of 4 (A) and 2 (Z)");
   }
   const int R = rows_per_thread(nmax);
-  if (R < 0) c.fail(AWG_E_ARG, "eig: matrix larger than 6,144 rows");
+  if (R < 0) c.fail(AWG_E_ARG, "eig: matrix larger than 5,760 rows");
   // ---- workspace
   const int npan = (nmax - 1 + kNB - 1) / kNB;
   std::vector<long long> off(J + 1, 0);
@@ -686,9 +816,20 @@ void eig_batched(Ctx& c, const std::vector<SyevJob>& jobs_in, const std::functio
   d_ed.upload(ed, c.stream);
   d_td.upload(td, c.stream);
 
+  // phase timing on stderr with option verbose >= 1
+  const bool verbose = c.opt("verbose", 0) >= 1;
+  double tph = 0.0;
+  auto phase = [&](const char* what) {
+    if (!verbose) return;
+    AWG_CUDA(cudaStreamSynchronize(c.stream));
+    const double t = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    if (tph > 0.0) std::fprintf(stderr, "[awg eig] %d problems (n <= %d): %s %.1f ms\n", J, nmax, what, t - tph);
+    tph = t;
+  };
+  phase("start");
   // ---- 1. tridiagonalisation
   const int L = round_up(ldmax, 2);
-  int nslot = int(std::min<size_t>(8, kLatrdSmemCap / (size_t(L) * 8) - 1));
+  int nslot = int(std::min<size_t>(8, kLatrdSmemCap / (size_t(L) * 8) - 1));  // full / empty arrays hold 8
   if (nslot < 2) c.fail(AWG_E_ARG, "eig: matrix too large for the shared-memory ring");
   const size_t smem = size_t(nslot + 1) * L * 8;
   for (int k0 = 0; k0 < nmax - 1; k0 += kNB) {
@@ -719,6 +860,7 @@ void eig_batched(Ctx& c, const std::vector<SyevJob>& jobs_in, const std::functio
   }
   k_last_diag<<<J, 32, 0, c.stream>>>(d_ed.p);
   ++c.launches;
+  phase("tridiagonalisation");
 
   // ---- 2. tridiagonal eigenvalues and vectors
   {
@@ -753,6 +895,61 @@ void eig_batched(Ctx& c, const std::vector<SyevJob>& jobs_in, const std::functio
     c.launches += 4;
     check_launch("tridiagonal eigensolver");
   }
+  phase("tridiagonal eigenpairs");
+  if (nvmax > 1) {
+    constexpr int W = 256;
+    DArr<double> G, tmp;
+    G.alloc(size_t(J) * W * W);
+    tmp.alloc(size_t(J) * ldmax * W);
+    for (int pass = 0; pass < 2; ++pass) {
+      const int off = pass ? W / 2 : 0;
+      for (int w0 = off; w0 < nvmax; w0 += W) {
+        std::vector<GemmDesc> pg, pz;
+        std::vector<int> wsz(J, 0), rows(J, 0), cols(J, 0), lds(J, 0), ldd(J, 0);
+        std::vector<double*> src(J, nullptr), dst(J, nullptr);
+        for (int q = 0; q < J; ++q) {
+          const SyevJob& sj = jobs[q];
+          const int m = std::min(W, sj.nvec - w0);
+          if (m < 2 || (pass == 1 && sj.nvec <= W)) continue;  // a single window already covered all
+          double* Zw = sj.Z + (size_t)w0 * sj.ldz;
+          double* Gq = G.p + size_t(q) * W * W;
+          double* Tq = tmp.p + size_t(q) * ldmax * W;
+          wsz[q] = m;
+          pg.push_back({Zw, Zw, Gq, m, m, sj.n, sj.ldz, sj.ldz, W, 0, 0});
+          pz.push_back({Zw, Gq, Tq, sj.n, m, m, sj.ldz, W, sj.ldz, 0, 0});
+          src[q] = Tq;
+          dst[q] = Zw;
+          rows[q] = sj.n;
+          cols[q] = m;
+          lds[q] = sj.ldz;
+          ldd[q] = sj.ldz;
+        }
+        if (pg.empty()) continue;
+        DArr<int> d_wsz, d_rows, d_cols, d_lds, d_ldd;
+        DArr<double*> d_src, d_dst;
+        d_wsz.upload(wsz, c.stream);
+        d_rows.upload(rows, c.stream);
+        d_cols.upload(cols, c.stream);
+        d_lds.upload(lds, c.stream);
+        d_ldd.upload(ldd, c.stream);
+        d_src.upload(src, c.stream);
+        d_dst.upload(dst, c.stream);
+        GroupedGemm gg, gz;
+        gg.set(c, pg, /*transpose_a=*/true);
+        gz.set(c, pz);
+        for (int step = 0; step < 2; ++step) {
+          gg.run(c);                                                  // G = Z_w^T Z_w
+          k_ns_h<<<dim3(64, J), 256, 0, c.stream>>>(J, d_wsz.p, W, G.p);  // H = (3I - G) / 2
+          gz.run(c);                                                  // tmp = Z_w H
+          k_copy_cols<<<dim3(256, J), 256, 0, c.stream>>>(J, d_src.p, d_dst.p, d_rows.p, d_cols.p, d_lds.p, d_ldd.p);
+          c.launches += 2;
+        }
+        AWG_CUDA(cudaStreamSynchronize(c.stream));  // the per-window descriptor arrays go out of scope
+      }
+    }
+    check_launch("newton-schulz");
+  }
+  phase("orthogonalisation");
 
   // ---- 3. Z <- Q Z, panels in reverse order: Z(k0:n, :) -= V_p (T_p (V_p^T Z(k0:n, :)))
   if (nvmax > 0) {
@@ -790,6 +987,7 @@ void eig_batched(Ctx& c, const std::vector<SyevJob>& jobs_in, const std::functio
       g3.run(c);
     }
   }
+  phase("back-transformation");
   AWG_CUDA(cudaStreamSynchronize(c.stream));
 }
 
@@ -800,7 +998,27 @@ __global__ void k_fill_sym(int n, int ld, int kind, unsigned long long seed, dou
   const int i = int(t % n), j = int(t / n);
   const int a = min(i, j), b = max(i, j);
   double v;
-  if (kind == 1) {  // 5-point Laplacian on an m x m grid
+  if (kind == 3) {  // graph Laplacian of an m x m grid, edge weights 10^U(-3,3) (graded, clustered spectrum)
+    const int m = int(llrint(sqrt(double(n))));
+    auto wgt = [&](int p, int r) {  // weight of the grid edge {p, r}
+      const int lo = min(p, r), hi = max(p, r);
+      unsigned long long h = seed * 0x9E3779B97F4A7C15ull + (unsigned long long)lo * 0xD1B54A32D192ED03ull + hi;
+      h ^= h >> 31;
+      h *= 0xBF58476D1CE4E5B9ull;
+      h ^= h >> 29;
+      return pow(10.0, 6.0 * (double(h >> 11) * 0x1.0p-53) - 3.0);
+    };
+    const int ax = a % m, ay = a / m, bx = b % m, by = b / m;
+    if (a == b) {
+      v = 1e-3;
+      if (ax > 0) v += wgt(a, a - 1);
+      if (ax < m - 1) v += wgt(a, a + 1);
+      if (ay > 0) v += wgt(a, a - m);
+      if (ay < m - 1) v += wgt(a, a + m);
+    } else {
+      v = ((ay == by && bx - ax == 1) || (ax == bx && by - ay == 1)) ? -wgt(a, b) : 0.0;
+    }
+  } else if (kind == 1) {  // 5-point Laplacian on an m x m grid
     const int m = int(llrint(sqrt(double(n))));
     const int ax = a % m, ay = a / m, bx = b % m, by = b / m;
     v = (a == b) ? 4.0 : ((ay == by && bx - ax == 1) || (ax == bx && by - ay == 1)) ? -1.0 : 0.0;
@@ -835,7 +1053,7 @@ __global__ void k_resid_prep(int n, int ld, const double* __restrict__ w, double
 // Check / benchmark hook (awg_bench_eig): `count` seeded symmetric matrices
 // of order n — kind 0: random entries; kind 1: the 5-point Laplacian of an
 // m x m grid (n = m^2; exactly repeated eigenvalues); kind 2: random with a
-// graded spectrum — through eig_batched, against cuSOLVER Dsyevd on the same
+// graded spectrum; kind 3: weighted grid Laplacian, weights 10^U(-3,3) — through eig_batched, against cuSOLVER Dsyevd on the same
 // matrices.  out: [0] max |w - w_ref| / ||A||, [1] max ||A z - w z|| / ||A||,
 // [2] max |Z^T Z - I|, [3] ms eig_batched, [4] ms cuSOLVER (all count).
 void eig_check(Ctx& c, int n, int count, int kind, unsigned long long seed, double* out) {

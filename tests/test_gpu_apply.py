@@ -18,8 +18,27 @@ MODES = {"none": awg.AwgMode.NONE, "ad": awg.AwgMode.AD, "hyb": awg.AwgMode.HYB,
 COMPS = {"hybrid": awg.Composition.HYBRID, "additive": awg.Composition.ADDITIVE}
 OPS = {"A": awg.Op.A, "Aminus": awg.Op.AMINUS, "Aplus": awg.Op.APLUS, "H1": awg.Op.H1, "Q": awg.Op.Q,
        "QW": awg.Op.QW, "H2": awg.Op.H2, "PI3": awg.Op.PI3, "PI3T": awg.Op.PI3T}
-# Same bound the oracle restatement meets on these inputs (see test_oracle_golden).
-TOL = {"H3inex": 1e-8, "PI3": 1e-10, "PI3T": 1e-10}
+# 1e-11 everywhere (north_star), except on the elasticity cases with the 1e7
+# Young's-modulus contrast, where the INEX core solve (the reference's own
+# lu_solve, bug 2: relative error O(1) on indefinite systems)
+# and Pi3 = I - W KW+ W^T A (A ~ 1e7) amplify rounding: there the bound is the
+# one the restatement itself meets against the reference (test_oracle_golden).
+TOL = {"H3inex": 1e-11, "PI3": 1e-11, "PI3T": 1e-11}
+TOL_ELAS = {"H3inex": 1e-9, "PI3": 1e-11, "PI3T": 1e-11}
+
+
+def tol_for(case, name):
+    t = TOL_ELAS if case.startswith("telas") else TOL
+    return t.get(name, 1e-11)
+
+
+def _record(check, **kw):
+    path = os.environ.get("AWG_PARITY_LOG")
+    if path:
+        import json
+
+        with open(path, "a") as fh:
+            fh.write(json.dumps({"check": check, **kw}) + "\n")
 
 
 def make_ctx(g, mode=awg.AwgMode.AD, composition=awg.Composition.HYBRID, lu="reference", one_level="NN", options=None):
@@ -47,13 +66,16 @@ def test_operator_parity(case):
             if name == "A":
                 assert np.array_equal(got, y), "spmv must be bit-identical (sparse.cpp:49-56)"
             else:
-                assert rel(got, y) <= TOL.get(name, 1e-11), (case, name, rel(got, y))
+                _record("golden_apply", case=case, op=name, rel=rel(got, y))
+                assert rel(got, y) <= tol_for(case, name), (case, name, rel(got, y))
     for mode, key in ((awg.AwgMode.AD, "H3ad"), (awg.AwgMode.HYB, "H3hyb"), (awg.AwgMode.INEX, "H3inex")):
         if "y_" + key not in g:
             continue
         c2 = make_ctx(g, mode=mode, composition=COMPS[comp], one_level=kind)
         for x, y in zip(g["x_apply"], g["y_" + key]):
-            assert rel(c2.apply(awg.Op.H3, x), y) <= TOL.get(key, 1e-11), (case, key)
+            e = rel(c2.apply(awg.Op.H3, x), y)
+            _record("golden_apply", case=case, op=key, rel=e)
+            assert e <= tol_for(case, key), (case, key, e)
 
 
 @pytest.mark.parametrize("case", CASES)
@@ -66,11 +88,15 @@ def test_pcg_parity(case):
     assert abs(rep.iterations - s["iterations"]) <= 1
     assert rel(x, g["pcg_x"]) <= 1e-7
     k = min(len(rep.residual_history), len(g["pcg_residuals"]))
+    rh = np.asarray(rep.residual_history[:k])
+    rg = np.asarray(g["pcg_residuals"][:k])
+    _record("golden_pcg", case=case, iterations=rep.iterations, ref_iterations=s["iterations"],
+            x_rel=rel(x, g["pcg_x"]), resid_max_reldiff=float(np.max(np.abs(rh - rg) / rg)) if k else 0.0)
     # recursive residuals agree to rounding growth (the gates are iterations and x);
     # on telas8 (1e7 contrast, 8-element layers) rounding alone moves single
     # recursive residuals by up to 55% (the numpy restatement against the
     # reference shows the same), so there only the factor-2 shape is checked
-    rtol = 1.0 if case == "telas8" else 1e-3
+    rtol = 0.5 if case == "telas8" else 1e-3
     assert np.allclose(rep.residual_history[:k], g["pcg_residuals"][:k], rtol=rtol, atol=1e-14)
     assert abs(rep.kappa_estimate - s["kappa"]) <= 1e-4 * s["kappa"]
     assert rep.final_relative_residual <= s["rtol_solve"] or abs(rep.final_relative_residual -

@@ -12,7 +12,7 @@ from paper_2106_10913_b200 import awg
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("n,count,kind", [(2, 3, 0), (3, 2, 0), (65, 3, 0), (130, 2, 2), (300, 4, 0), (289, 2, 1),
+@pytest.mark.parametrize("n,count,kind", [(2, 3, 0), (3, 2, 0), (65, 3, 0), (130, 2, 2), (300, 4, 0), (289, 2, 1), (1024, 2, 3),
                                           (1024, 3, 0), (1089, 2, 1), (2113, 2, 2)])
 def test_eig_against_cusolver(n, count, kind):
     r = awg.bench_eig(n, count, kind, seed=7)
