@@ -595,13 +595,15 @@ def pcg(ctx: ProblemContext, b, rtol: float, maxit: int):
     return ctx.pcg(b, rtol, maxit)
 
 
-def bench_eig(n: int, count: int = 1, kind: int = 0, seed: int = 1, device: int = 0, verbose: int = 0) -> dict:
+def bench_eig(n: int, count: int = 1, kind: int = 0, seed: int = 1, device: int = 0, verbose: int = 0,
+              options: Optional[Dict[str, int]] = None) -> dict:
     """The setup eigensolver (eig.cu) on seeded matrices against cuSOLVER
     (awg_bench_eig): eigenvalue error, residual, orthogonality, timings."""
     ctx = ProblemContext._bare(device)
     try:
         if verbose:
             ctx.set_option("verbose", verbose)
+        ctx.set_options(options)
         out = (ctypes.c_double * 5)()
         ctx._check(ctx._lib.awg_bench_eig(ctx._h, int(n), int(count), int(kind), int(seed), out))
         return {"eig_err": out[0], "resid": out[1], "orth": out[2], "ms": out[3], "ms_cusolver": out[4]}
