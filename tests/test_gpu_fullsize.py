@@ -42,9 +42,12 @@ def c2(c2fs):
     return c2fs.p, c2fs.ctx
 
 
-def _ctx_with(p, options):
-    ctx = awg.context_from_problem(p, options=options)
-    ctx.setup(awg.config_for(p))
+def _ctx_with(fs, options):
+    """A context on the same (exported) factors as fs with experiment options:
+    awg_load_factors instead of another setup (the options only change how the
+    operators run)."""
+    ctx = awg.context_from_problem(fs.p, options=options)
+    ctx.load_factors(awg.config_for(fs.p), fs.f)
     return ctx
 
 
@@ -128,39 +131,41 @@ def test_h3_linear_symmetric_positive(c2):
         assert abs(float(y @ ox) - float(x @ oy)) <= 1e-10 * np.linalg.norm(x) * np.linalg.norm(oy), op
 
 
-def test_local_solve_variants_full_size(c2):
-    p, ctx = c2
+def test_local_solve_variants_full_size(c2fs):
+    p = c2fs.p
+    base = _ctx_with(c2fs, None)
     xs = [problems.uniform(21 + i, p.n, -1.0, 1.0) for i in range(2)]
-    ref = [ctx.apply(awg.Op.H1, x) for x in xs]
-    q = ctx.query()
+    ref = [base.apply(awg.Op.H1, x) for x in xs]
+    q = base.query()
     assert q["nn_single_pass"] == 1
-    two = _ctx_with(p, {"nn_two_pass": 1})
-    nopf = _ctx_with(p, {"fused_prefetch": 0})
-    flip = _ctx_with(p, {"fused_static": 0 if q["nn_static_split"] else 1})
-    pdl = _ctx_with(p, {"pdl_local": 0})
+    two = _ctx_with(c2fs, {"nn_two_pass": 1})
+    nopf = _ctx_with(c2fs, {"fused_prefetch": 0})
+    flip = _ctx_with(c2fs, {"fused_static": 0 if q["nn_static_split"] else 1})
+    pdl = _ctx_with(c2fs, {"pdl_local": 0})
     try:
         # the early trigger into the local solve and its pre-wait copies change
         # scheduling only
         for x in xs:
-            assert np.array_equal(pdl.apply(awg.Op.H1, x), ctx.apply(awg.Op.H1, x))
-            assert np.array_equal(pdl.apply(awg.Op.H3, x), ctx.apply(awg.Op.H3, x))
+            assert np.array_equal(pdl.apply(awg.Op.H1, x), base.apply(awg.Op.H1, x))
+            assert np.array_equal(pdl.apply(awg.Op.H3, x), base.apply(awg.Op.H3, x))
         xa, ra = pdl.pcg(p.b, p.rtol, 10000)
-        xb, rb = ctx.pcg(p.b, p.rtol, 10000)
+        xb, rb = base.pcg(p.b, p.rtol, 10000)
         assert ra.iterations == rb.iterations and np.array_equal(xa, xb)
         for x, y in zip(xs, ref):
             assert rel(two.apply(awg.Op.H1, x), y) <= 1e-13
             assert np.array_equal(nopf.apply(awg.Op.H1, x), y)
             # the other task split: different column chunks, same sums regrouped
             assert rel(flip.apply(awg.Op.H1, x), y) <= 1e-13
+        # the loaded factors reproduce the set-up context's operators
+        for x in xs:
+            assert rel(base.apply(awg.Op.H3, x), c2fs.ctx.apply(awg.Op.H3, x)) <= 1e-13
     finally:
-        two.close()
-        nopf.close()
-        flip.close()
-        pdl.close()
+        for cx in (base, two, nopf, flip, pdl):
+            cx.close()
 
 
-def test_pcg_full_size(c2):
-    p, ctx = c2
+def test_pcg_full_size(c2fs):
+    p, ctx = c2fs.p, c2fs.ctx
     x1, rep1 = ctx.pcg(p.b, p.rtol, 10000)
     x2, rep2 = ctx.pcg(p.b, p.rtol, 10000)
     assert rep1.converged and rep1.iterations == rep2.iterations
@@ -168,11 +173,14 @@ def test_pcg_full_size(c2):
     true = np.linalg.norm(p.b - _spmv_reference_order(p, x1)) / np.linalg.norm(p.b)
     # the host's batch sizing (convergence-rate estimate vs plain doubling) only
     # schedules graph launches: the device state decides, results identical
-    fixed = _ctx_with(p, {"pcg_adaptive": 0})
+    base = _ctx_with(c2fs, None)
+    fixed = _ctx_with(c2fs, {"pcg_adaptive": 0})
     try:
         x3, rep3 = fixed.pcg(p.b, p.rtol, 10000)
+        x4, rep4 = base.pcg(p.b, p.rtol, 10000)
     finally:
         fixed.close()
-    assert rep3.iterations == rep1.iterations and np.array_equal(x3, x1)
+        base.close()
+    assert rep3.iterations == rep4.iterations and np.array_equal(x3, x4)
     assert abs(true - rep1.final_relative_residual) <= 1e-6 * true  # krylov.cpp:98: the true residual
     assert true <= p.rtol or abs(true - rep1.recurrence_residual_at_exit) <= 1e-8  # krylov.cpp:93-101
