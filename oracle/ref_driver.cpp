@@ -556,10 +556,26 @@ int main(int argc, char** argv) {
     // w_probe strictly negative modes, with maxit bounded: reports how the
     // reference's own pcg(A+, H2) behaves when build_w would take 10 n iterations.
     const ApplyFn aplus = [&split](const double* u, double* v) { split.apply_Aplus(u, v); };
-    const ApplyFn happly = [&h2](const double* u, double* v) { h2->apply(u, v); };
+    // pcg hands its residual r to the preconditioner once per iteration, so the
+    // wrapper can log the recursive relative residual of a long run as it goes
+    // (<out>/w_probe_progress.jsonl: a bounded session still leaves evidence).
+    std::vector<double> rhs(n);
+    long calls = 0;
+    double t_col = 0;
+    FILE* prog = std::fopen((out + "/w_probe_progress.jsonl").c_str(), "w");
+    const ApplyFn happly = [&](const double* u, double* v) {
+      if (prog && calls % 500 == 0) {
+        double rr = 0, bb = 0;
+        for (int i = 0; i < n; ++i) rr += u[i] * u[i], bb += rhs[i] * rhs[i];
+        std::fprintf(prog, "{\"iteration\": %ld, \"relres\": %.6e, \"seconds\": %.1f}\n", calls,
+                     std::sqrt(rr / bb), now_s() - t_col);
+        std::fflush(prog);
+      }
+      ++calls;
+      h2->apply(u, v);
+    };
     std::fprintf(js, "  \"n0\": %d, \"r0\": %d, \"n_minus\": %d,\n  \"w_probe\": [", cs.dim(), cs.retained_rank(),
                  split.n_minus());
-    std::vector<double> rhs(n);
     int col = 0;
     for (int s = 0; s < N && col < args.w_probe; ++s) {
       const LocalSplit& ls = split.splits()[s];
@@ -568,6 +584,7 @@ int main(int argc, char** argv) {
         std::fill(rhs.begin(), rhs.end(), 0.0);
         split.prolong_add(s, ls.eig.eigenvectors.col(k), rhs.data());
         const double tp = now_s();
+        calls = 0, t_col = tp;
         auto res = pcg(aplus, happly, rhs, args.w_rtol, args.w_probe_maxit);
         const SolveReport& rep = res.second;
         std::fprintf(js, "%s{\"s\": %d, \"k\": %d, \"iterations\": %d, \"converged\": %d, \"kappa\": %.6e, "

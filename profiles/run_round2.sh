@@ -24,3 +24,5 @@ timeout 900 python bench.py --config c3 --steps 5 --warmup 3 > $OUT/bench_c3_$TA
 echo "bench c3 rc=$?"
 timeout 600 python bench.py --impl reference --steps 5 --warmup 1 > $OUT/bench_ref_c5_$TAG.json 2> $OUT/bench_ref_c5_$TAG.err
 echo "reference arm rc=$?"
+VERBOSE=2 timeout 900 python profiles/setup_only.py c5 > $OUT/setup_c5_$TAG.json 2> $OUT/setup_c5_trace_$TAG.txt
+echo "setup trace rc=$?"
