@@ -502,7 +502,7 @@ int awg_set_option(awg_ctx* ctx, const char* name, long long value) {
     else if (k == "fused_min_cols") c.fused_min_cols = std::max(8, v);
     else if (k == "fused_tail") c.fused_tail_pct = std::max(0, std::min(90, v));
     else if (k == "fused_static_cols" || k == "synth_nm" || k == "dgemm_variant" || k == "coarse_neg" ||
-             k == "verbose" || k == "wbuild_cublas" || k == "setup_cusolver" || k == "eig_probe")
+             k == "verbose" || k == "wbuild_cublas" || k == "setup_cusolver" || k == "eig_probe" || k == "eig_split")
       c.opts[k] = value;
     else
       c.fail(AWG_E_ARG, "set_option: unknown option " + k);

@@ -425,6 +425,317 @@ __global__ void __launch_bounds__(kLThreads, 1) k_latrd(const EigDev* __restrict
   }
 }
 
+// ---------------------------------------------------------------------------
+// 1b. Split form of the panel reduction for batches with fewer problems than
+// SMs (c2: 16 subdomains, c3: 64).  k_latrd keeps one CTA per problem, so 16
+// problems use 16 of 148 SMs while the symmetric product, 85% of the work,
+// streams each trailing triangle through one SM.  Here one column step is two
+// launches: k_symv_part splits the column groups of the product over C CTAs
+// per problem (cyclically: column lengths fall linearly) — each CTA owns the
+// whole dot of its columns (parked in W(:, jj) as in k_latrd) and writes a
+// partial of the rank-1 half for all rows —, then k_col_step (one CTA per
+// problem) sums the partials in CTA order, finishes w of that column (step 4)
+// and forms the next column and its reflector (steps 1-2).  Same arithmetic per
+// phase as k_latrd; only y's summation is regrouped by CTA.  Fixed C per
+// batch: results are deterministic.
+template <int R>
+__global__ void __launch_bounds__(kLThreads, 1) k_symv_part(const EigDev* __restrict__ jobs, int k0, int jj, int C,
+                                                            int L, int nslot, double* __restrict__ ypart) {
+  extern __shared__ __align__(128) double esm[];
+  __shared__ double part[2][kLW][kTC];
+  __shared__ __align__(8) unsigned long long full[8], empty[8];
+  const int q = blockIdx.x / C, cta = blockIdx.x % C;
+  const EigDev J = jobs[q];
+  const int n = J.n, ld = J.ld, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (k0 >= n - 1) return;
+  const int jmax = min(kNB, n - 1 - k0);
+  if (jj >= jmax) return;
+  const int j = k0 + jj;
+  const bool cons = tid < kLT;
+  double* vsm = esm + (size_t)nslot * kTile;
+  const double* Vj = J.VW + (size_t)jj * ld;      // this column's reflector v (zero above row j + 1)
+  double* Wj = J.VW + (size_t)(kNB + jj) * ld;    // dots parked here
+  if (tid == 0) {
+    for (int b = 0; b < nslot; ++b) {
+      mb_init(&full[b], 1);
+      mb_init(&empty[b], kLW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int t = tid; t < nslot * kTile; t += kLThreads) esm[t] = 0.0;  // stale slot entries must be finite
+  for (int i = tid; i < L; i += kLThreads) vsm[i] = (i < n) ? Vj[i] : 0.0;
+  double vr[R], yr[R];
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    const int i = tid + kLT * k;
+    vr[k] = (cons && i < n) ? Vj[i] : 0.0;
+    yr[k] = 0.0;
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  const int c_begin = j + 1;
+  const int gstep = kTC * C;
+  unsigned nfill = 0;
+  if (!cons) {
+    for (int G0 = c_begin + kTC * cta; G0 < n; G0 += gstep) {
+      const int K = min(kTC, n - G0);
+      for (int k = G0 / kLT; k * kLT < n; ++k) {
+        const unsigned b = nfill % nslot, round = nfill / nslot;
+        const int r0 = k * kLT, rows = min(kLT, n - r0);
+        const unsigned bytes = unsigned((rows + 1) & ~1) * 8u;
+        if (lane == 0) {
+          if (round > 0) mb_wait(&empty[b], (round - 1) & 1);
+          mb_arm(&full[b], bytes * unsigned(K));
+        }
+        __syncwarp();
+        if (lane < K)
+          bulk_copy(esm + (size_t)b * kTile + (size_t)lane * kLT, J.A + r0 + (size_t)(G0 + lane) * ld, bytes, &full[b]);
+        ++nfill;
+      }
+    }
+    __syncwarp();
+  } else {
+    int gi = 0;
+    for (int G0 = c_begin + kTC * cta; G0 < n; G0 += gstep, ++gi) {
+      const int kstart = G0 / kLT;
+      double acc[kTC], vcol[kTC];
+#pragma unroll
+      for (int u = 0; u < kTC; ++u) {
+        acc[u] = 0.0;
+        vcol[u] = (G0 + u < n) ? vsm[G0 + u] : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        if (k >= kstart && k * kLT < n) {  // uniform
+          const unsigned b = nfill % nslot;
+          mb_wait(&full[b], (nfill / nslot) & 1);
+          const double* tile = esm + (size_t)b * kTile + tid;
+          const int i = tid + kLT * k;
+          const double vi = vr[k];
+          double y = yr[k];
+          if (k * kLT >= G0 + kTC) {  // the chunk lies strictly below the group's columns (see k_latrd)
+#pragma unroll
+            for (int u = 0; u < kTC; ++u) {
+              const double a = tile[u * kLT];
+              y = fma(a, vcol[u], y);
+              acc[u] = fma(a, vi, acc[u]);
+            }
+          } else {
+#pragma unroll
+            for (int u = 0; u < kTC; ++u) {
+              const int c = G0 + u;
+              const double a = (i >= c) ? tile[u * kLT] : 0.0;
+              y = fma(a, vcol[u], y);
+              acc[u] = (i > c) ? fma(a, vi, acc[u]) : acc[u];
+            }
+          }
+          yr[k] = y;
+          __syncwarp();
+          if (lane == 0) mb_arrive(&empty[b]);
+          ++nfill;
+        }
+      }
+      const double wpart = transpose_reduce8(acc, lane);
+      const int pb = gi & 1;
+      if (lane < kTC) part[pb][warp][lane] = wpart;
+      bar_consumers();
+      if (warp == 0 && lane < kTC && G0 + lane < n) {
+        double sdot = 0.0;
+#pragma unroll
+        for (int w = 0; w < kLW; ++w) sdot += part[pb][w][lane];
+        Wj[G0 + lane] = sdot;
+      }
+    }
+    double* yp = ypart + ((size_t)q * C + cta) * L;
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const int i = tid + kLT * k;
+      if (i < n) yp[i] = yr[k];
+    }
+  }
+}
+
+template <int R>
+__global__ void __launch_bounds__(kLThreads, 1) k_col_step(const EigDev* __restrict__ jobs, int k0, int jj, int C, int L,
+                                                           const double* __restrict__ ypart) {
+  extern __shared__ __align__(128) double vsm[];  // L doubles
+  __shared__ double red[16];
+  __shared__ double s_rowv[kNB], s_roww[kNB], s_s1[kNB], s_s2[kNB];
+  __shared__ double s_scal[4];
+  const EigDev J = jobs[blockIdx.x];
+  const int n = J.n, ld = J.ld, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (k0 >= n - 1) return;
+  const bool cons = tid < kLT;
+  const int jmax = min(kNB, n - 1 - k0);
+  double* Vp = J.VW;
+  double* Wp = J.VW + (size_t)kNB * ld;
+  auto bsum = [&](double v) {
+    v = wsum(v);
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    double a = red[lane & 15];
+#pragma unroll
+    for (int o = 8; o >= 1; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    return a;
+  };
+  if (jj == 0) {  // new panel: unused columns must be zero for the rank-2k update
+    if (cons) {
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        const int i = tid + kLT * k;
+        if (i < n) {
+          for (int p = 0; p < 2 * kNB; ++p) {
+            J.VW[i + (size_t)p * ld] = 0.0;
+            J.Bt[(size_t)i * 2 * kNB + p] = 0.0;
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // ---- finish column jj - 1: step (4) of k_latrd on the summed product
+  if (jj > 0 && jj - 1 < jmax) {
+    const int jp = jj - 1, j = k0 + jp;
+    const double tau = J.tau[j];
+    double vr[R], yr[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const int i = tid + kLT * k;
+      double v = 0.0, y = 0.0;
+      if (cons && i < n) {
+        v = Vp[i + (size_t)jp * ld];
+        vsm[i] = v;
+        if (i > j) {
+          const double* yp = ypart + (size_t)blockIdx.x * C * L + i;
+          for (int cta = 0; cta < C; ++cta) y += yp[(size_t)cta * L];
+          y += Wp[i + (size_t)jp * ld];
+        }
+      }
+      vr[k] = v;
+      yr[k] = y;
+    }
+    __syncthreads();
+    for (int p = warp; p < 2 * jp; p += kLW + 1) {  // s1 = W^T v, s2 = V^T v over rows > j
+      const double* colp = (p < jp) ? Wp + (size_t)p * ld : Vp + (size_t)(p - jp) * ld;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      int i = j + 1 + lane;
+      for (; i + 96 < n; i += 128) {
+        a0 = fma(colp[i], vsm[i], a0);
+        a1 = fma(colp[i + 32], vsm[i + 32], a1);
+        a2 = fma(colp[i + 64], vsm[i + 64], a2);
+        a3 = fma(colp[i + 96], vsm[i + 96], a3);
+      }
+      for (; i < n; i += 32) a0 = fma(colp[i], vsm[i], a0);
+      const double acc = wsum((a0 + a1) + (a2 + a3));
+      if (lane == 0) {
+        if (p < jp) s_s1[p] = acc;
+        else s_s2[p - jp] = acc;
+      }
+    }
+    __syncthreads();
+    double wv = 0.0;
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const int i = tid + kLT * k;
+      double y = 0.0;
+      if (cons && i > j && i < n) {
+        double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
+        int p = 0;
+        for (; p + 2 <= jp; p += 2) {
+          c0 = fma(Vp[i + (size_t)p * ld], s_s1[p], c0);
+          c1 = fma(Wp[i + (size_t)p * ld], s_s2[p], c1);
+          c2 = fma(Vp[i + (size_t)(p + 1) * ld], s_s1[p + 1], c2);
+          c3 = fma(Wp[i + (size_t)(p + 1) * ld], s_s2[p + 1], c3);
+        }
+        if (p < jp) {
+          c0 = fma(Vp[i + (size_t)p * ld], s_s1[p], c0);
+          c1 = fma(Wp[i + (size_t)p * ld], s_s2[p], c1);
+        }
+        y = (yr[k] - ((c0 + c2) + (c1 + c3))) * tau;
+      }
+      yr[k] = y;
+      wv = fma(y, vr[k], wv);
+    }
+    const double alpha2 = -0.5 * tau * bsum(wv);
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const int i = tid + kLT * k;
+      if (cons && i < n) {
+        const double w = (i > j) ? fma(alpha2, vr[k], yr[k]) : 0.0;
+        Wp[i + (size_t)jp * ld] = w;
+        J.Bt[(size_t)i * 2 * kNB + jp] = w;
+        J.Bt[(size_t)i * 2 * kNB + kNB + jp] = vr[k];
+      }
+    }
+    __syncthreads();  // W(:, jp) complete before the next column's row reads
+  }
+  if (jj >= jmax) return;
+  // ---- start column jj: steps (1)-(2) of k_latrd
+  const int j = k0 + jj;
+  if (tid < jj) {
+    s_rowv[tid] = Vp[j + (size_t)tid * ld];
+    s_roww[tid] = Wp[j + (size_t)tid * ld];
+  }
+  __syncthreads();
+  double ar[R];
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    const int i = tid + kLT * k;
+    double a = 0.0;
+    if (cons && i >= j && i < n) {
+      double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
+      int p = 0;
+      for (; p + 2 <= jj; p += 2) {
+        c0 = fma(Vp[i + (size_t)p * ld], s_roww[p], c0);
+        c1 = fma(Wp[i + (size_t)p * ld], s_rowv[p], c1);
+        c2 = fma(Vp[i + (size_t)(p + 1) * ld], s_roww[p + 1], c2);
+        c3 = fma(Wp[i + (size_t)(p + 1) * ld], s_rowv[p + 1], c3);
+      }
+      if (p < jj) {
+        c0 = fma(Vp[i + (size_t)p * ld], s_roww[p], c0);
+        c1 = fma(Wp[i + (size_t)p * ld], s_rowv[p], c1);
+      }
+      a = J.A[i + (size_t)j * ld] - ((c0 + c2) + (c1 + c3));
+      if (i == j) s_scal[0] = a;
+      if (i == j + 1) s_scal[1] = a;
+    }
+    ar[k] = a;
+  }
+  double ss = 0.0;
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    const int i = tid + kLT * k;
+    if (cons && i > j + 1 && i < n) ss = fma(ar[k], ar[k], ss);
+  }
+  const double xnorm2 = bsum(ss);
+  const double dj = s_scal[0], alpha = s_scal[1];
+  double beta, tau, scale;
+  if (xnorm2 == 0.0) {
+    beta = alpha;
+    tau = 0.0;
+    scale = 0.0;
+  } else {
+    beta = -copysign(sqrt(fma(alpha, alpha, xnorm2)), alpha);
+    tau = (beta - alpha) / beta;
+    scale = 1.0 / (alpha - beta);
+  }
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    const int i = tid + kLT * k;
+    const double v = (i == j + 1) ? 1.0 : (i > j + 1 && i < n ? ar[k] * scale : 0.0);
+    if (cons && i < n) {
+      Vp[i + (size_t)jj * ld] = v;
+      if (i > j) J.A[i + (size_t)j * ld] = v;
+    }
+  }
+  if (tid == 0) {
+    J.d[j] = dj;
+    J.e[j] = beta;
+    J.tau[j] = tau;
+  }
+}
+
 // the last diagonal entry: A(n-1, n-1) after its final panel's rank-2 update
 // (that panel ends at column n-2, so its trailing matrix is this one entry:
 // A(n-1,n-1) - 2 V(n-1,:) W(n-1,:)^T; done here instead of a 1 x 1 GEMM)
@@ -611,6 +922,177 @@ __global__ void k_twisted(const TriDev* __restrict__ jobs, int per_cta) {
 // orthogonal to ~eps ||T|| / gap <= 1e-6 and is finished by the windowed
 // Newton-Schulz step below.
 constexpr double kClusterTol = 1e-10;
+// Clusters of at most kSmallCluster vectors go to k_clusters_small (thread per
+// cluster); larger ones stay with the CTA-per-problem walk below.
+constexpr int kSmallCluster = 32;
+
+// A problem's small clusters go to the thread-per-cluster kernel only when
+// there are enough of them to fill warps (a lone thread is ~6x slower per
+// vector than the CTA walk: a pencil's single zero cluster of ~20 vectors is
+// faster on the CTA); both kernels take the same decision from the same walk.
+constexpr int kMinThreadClusters = 64;
+__device__ int count_small_clusters(const TriDev& J, double tol) {
+  int cnt = 0, walk = 0;
+  while (walk < J.nvec) {
+    int q = walk + 1;
+    while (q < J.n && J.w[q] - J.w[q - 1] < tol) ++q;
+    const int sz = min(q, J.nvec) - walk;
+    if ((sz >= 2 || J.wu[walk] != 0.0) && sz <= kSmallCluster) ++cnt;
+    walk = q;
+  }
+  return cnt;
+}
+
+// Thread per cluster.  c2's B^s (1e6 contrast: ||T|| ~ 4e6, so the cluster
+// gap is 4e-4 while ~3,700 eigenvalues lie in (0.1, 10)) have ~3,300 of their
+// ~4,600 eigenvalues in ~1,000 clusters of 2-14 vectors: inverse iteration is
+// serial along n, but the clusters are independent, so each thread takes
+// whole clusters (cluster index = t mod T within its problem) and runs the
+// same dstein scheme as k_clusters alone: dlagtf, four dlagts solves per
+// vector, modified Gram-Schmidt against the cluster's earlier vectors.  The
+// LU scratch is interleaved by thread (element i of thread t at (a L + i) T + t),
+// so lock-stepped lanes store and load contiguous doubles; z is the output
+// column itself.
+__global__ void k_clusters_small(const TriDev* __restrict__ jobs, int T, int L, double* __restrict__ scratch) {
+  const TriDev J = jobs[blockIdx.y];
+  const int n = J.n, nv = J.nvec;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n < 2 || nv < 2 || t >= T) return;
+  double* S = scratch + (size_t)blockIdx.y * 5 * L * T + t;
+  const size_t LT = (size_t)L * T;
+  double* u1 = S;
+  double* u2 = S + LT;
+  double* u3 = S + 2 * LT;
+  double* lm = S + 3 * LT;
+  double* pv = S + 4 * LT;  // pivot flags (0.0 / 1.0)
+  const double tn = tnorm_of(J.d, J.e, n);
+  const double tol = kClusterTol * tn;
+  const double small = DBL_EPSILON * tn + kPivmin;
+  if (count_small_clusters(J, tol) < kMinThreadClusters) return;  // k_clusters takes them
+  int walk = 0, ci = 0;  // eigenvalue index and small-cluster count of the walk so far
+  for (int target = t;; target += T) {
+    // advance the walk to this thread's next cluster; every lane then works on
+    // its own cluster at the same time
+    int p = -1, qend = 0;
+    while (walk < nv) {
+      int q = walk + 1;
+      while (q < n && J.w[q] - J.w[q - 1] < tol) ++q;
+      const int qe = min(q, nv);
+      const int sz = qe - walk;
+      const bool mine = (sz >= 2 || J.wu[walk] != 0.0) && sz <= kSmallCluster;
+      const int start = walk;
+      walk = q;
+      if (mine) {
+        if (ci++ == target) {
+          p = start;
+          qend = qe;
+          break;
+        }
+      }
+    }
+    if (p < 0) return;
+    for (int m = p; m < qend; ++m) {
+      double lam = J.w[m];
+      if (m > p && lam - J.w[m - 1] < 10.0 * DBL_EPSILON * tn) lam = J.w[m - 1] + 10.0 * DBL_EPSILON * tn * (m - p);
+      {  // LU of T - lam with partial pivoting (dlagtf)
+        double r0 = J.d[0] - lam, r1 = J.e[0], r2 = 0.0;
+        for (int i = 0; i < n - 1; ++i) {
+          const double n0 = J.e[i], n1 = J.d[i + 1] - lam, n2 = (i + 1 < n - 1) ? J.e[i + 1] : 0.0;
+          const size_t o = (size_t)i * T;
+          if (fabs(r0) >= fabs(n0)) {
+            const double l = (r0 != 0.0) ? n0 / r0 : 0.0;
+            u1[o] = (r0 != 0.0) ? r0 : small;
+            u2[o] = r1;
+            u3[o] = r2;
+            lm[o] = l;
+            pv[o] = 0.0;
+            r0 = n1 - l * r1;
+            r1 = n2 - l * r2;
+            r2 = 0.0;
+          } else {
+            const double l = r0 / n0;
+            u1[o] = n0;
+            u2[o] = n1;
+            u3[o] = n2;
+            lm[o] = l;
+            pv[o] = 1.0;
+            r0 = r1 - l * n1;
+            r1 = r2 - l * n2;
+            r2 = 0.0;
+          }
+        }
+        u1[(size_t)(n - 1) * T] = (r0 != 0.0) ? r0 : small;
+      }
+      double* z = J.Z + (size_t)m * J.ldz;
+      for (int i = 0; i < n; ++i) {  // the same deterministic start vector as k_clusters
+        unsigned long long h = (unsigned long long)(i + 1) * 0x9E3779B97F4A7C15ull + (unsigned long long)(m + 1);
+        h ^= h >> 31;
+        h *= 0xBF58476D1CE4E5B9ull;
+        h ^= h >> 29;
+        z[i] = double(h >> 11) * 0x1.0p-53 - 0.5;
+      }
+      for (int it = 0; it < 4; ++it) {
+        // solve (T - lam) x = z in place: P L U (dlagts)
+        double zi = z[0];
+        for (int i = 0; i < n - 1; ++i) {
+          double zn = z[i + 1];
+          const size_t o = (size_t)i * T;
+          if (pv[o] != 0.0) {
+            const double tmp = zi;
+            zi = zn;
+            zn = tmp;
+          }
+          z[i] = zi;
+          zi = zn - lm[o] * zi;
+        }
+        z[n - 1] = zi;
+        double mx = 0.0, z1 = 0.0, z2 = 0.0;  // z[i + 1], z[i + 2]
+        for (int i = n - 1; i >= 0; --i) {
+          const size_t o = (size_t)i * T;
+          double v = z[i];
+          if (i + 1 < n) v -= u2[o] * z1;
+          if (i + 2 < n) v -= u3[o] * z2;
+          double piv0 = u1[o];
+          if (fabs(piv0) < small) piv0 = copysign(small, piv0);
+          v /= piv0;
+          z[i] = v;
+          mx = fmax(mx, fabs(v));
+          if (mx > 1e150) {  // rescale (dlagts overflow guard)
+            for (int k = i; k < n; ++k) z[k] *= 1e-150;
+            mx *= 1e-150;
+            v *= 1e-150;
+            z1 *= 1e-150;
+          }
+          z2 = z1;
+          z1 = v;
+        }
+        // reorthogonalise against the cluster's earlier (final) members, then normalise
+        for (int o = p; o < m; ++o) {
+          const double* zo = J.Z + (size_t)o * J.ldz;
+          double a0 = 0.0, a1 = 0.0;
+          int i = 0;
+          for (; i + 1 < n; i += 2) {
+            a0 = fma(zo[i], z[i], a0);
+            a1 = fma(zo[i + 1], z[i + 1], a1);
+          }
+          if (i < n) a0 = fma(zo[i], z[i], a0);
+          const double dotp = a0 + a1;
+          for (i = 0; i < n; ++i) z[i] = fma(-dotp, zo[i], z[i]);
+        }
+        double a0 = 0.0, a1 = 0.0;
+        int i = 0;
+        for (; i + 1 < n; i += 2) {
+          a0 = fma(z[i], z[i], a0);
+          a1 = fma(z[i + 1], z[i + 1], a1);
+        }
+        if (i < n) a0 = fma(z[i], z[i], a0);
+        const double nrm = sqrt(a0 + a1);
+        const double sc = nrm > 0.0 ? 1.0 / nrm : 0.0;
+        for (i = 0; i < n; ++i) z[i] *= sc;
+      }
+    }
+  }
+}
 
 __global__ void k_clusters(const TriDev* __restrict__ jobs) {
   __shared__ double red[8];
@@ -636,13 +1118,16 @@ __global__ void k_clusters(const TriDev* __restrict__ jobs) {
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) a += red[w];
     return a;
   };
+  // (clusters of <= kSmallCluster vectors and broken-down single vectors were
+  // done by k_clusters_small when the problem has enough of them)
+  const bool threads_took_small = count_small_clusters(J, tol) >= kMinThreadClusters;
   int p = 0;
   while (p < nv) {
     // cluster [p, q): consecutive gaps below tol
     int q = p + 1;
     while (q < n && J.w[q] - J.w[q - 1] < tol) ++q;
     const int qend = min(q, nv);
-    if (qend - p >= 2 || J.wu[p] != 0.0) {  // a cluster, or a twisted vector that broke down
+    if (qend - p > kSmallCluster || (!threads_took_small && (qend - p >= 2 || J.wu[p] != 0.0))) {
       for (int m = p; m < qend; ++m) {
         // separate equal eigenvalues slightly so the factorisations differ (dstein's pertol)
         double lam = J.w[m];
@@ -831,6 +1316,20 @@ void launch_latrd(Ctx& c, const EigDev* jobs, int count, int k0, int L, int nslo
   check_launch("latrd");
 }
 
+// one panel in split form: (finish column jj - 1, start column jj), product of column jj, ...
+template <int R>
+void launch_panel_split(Ctx& c, const EigDev* jobs, int count, int k0, int C, int L, int nslot, size_t smem,
+                        double* ypart) {
+  ensure_dyn_smem((const void*)k_symv_part<R>, smem);
+  ensure_dyn_smem((const void*)k_col_step<R>, size_t(L) * 8);
+  for (int jj = 0; jj <= kNB; ++jj) {
+    k_col_step<R><<<count, kLThreads, size_t(L) * 8, c.stream>>>(jobs, k0, jj, C, L, ypart);
+    if (jj < kNB) k_symv_part<R><<<count * C, kLThreads, smem, c.stream>>>(jobs, k0, jj, C, L, nslot, ypart);
+  }
+  c.launches += 2 * kNB + 1;
+  check_launch("latrd (split)");
+}
+
 }  // namespace
 
 // jobs: A (n x n, ld, lower), w (n eigenvalues ascending), Z (n x nvec, ldz):
@@ -897,7 +1396,23 @@ void eig_batched(Ctx& c, const std::vector<SyevJob>& jobs_in, const std::functio
     prof.alloc(4);
     prof.zero(c.stream);
   }
+  // fewer problems than SMs: split every symmetric product over C CTAs (1b);
+  // option eig_split = 0 keeps one CTA per problem, k >= 2 forces C = k
+  int C = std::min(8, c.sm_count / J);
+  if (c.opt("eig_split", -1) >= 0) C = int(std::max(1LL, std::min(16LL, c.opt("eig_split", -1))));
+  DArr<double> ypart;
+  if (C >= 2) ypart.alloc(size_t(J) * C * L);
   for (int k0 = 0; k0 < nmax - 1; k0 += kNB) {
+    if (C >= 2) {
+      switch (R) {
+        case 1: launch_panel_split<1>(c, d_ed.p, J, k0, C, L, nslot, smem, ypart.p); break;
+        case 2: launch_panel_split<2>(c, d_ed.p, J, k0, C, L, nslot, smem, ypart.p); break;
+        case 4: launch_panel_split<4>(c, d_ed.p, J, k0, C, L, nslot, smem, ypart.p); break;
+        case 8: launch_panel_split<8>(c, d_ed.p, J, k0, C, L, nslot, smem, ypart.p); break;
+        case 11: launch_panel_split<11>(c, d_ed.p, J, k0, C, L, nslot, smem, ypart.p); break;
+        default: launch_panel_split<12>(c, d_ed.p, J, k0, C, L, nslot, smem, ypart.p); break;
+      }
+    } else
     switch (R) {
       case 1: launch_latrd<1>(c, d_ed.p, J, k0, L, nslot, smem, prof.p); break;
       case 2: launch_latrd<2>(c, d_ed.p, J, k0, L, nslot, smem, prof.p); break;
@@ -960,9 +1475,17 @@ void eig_batched(Ctx& c, const std::vector<SyevJob>& jobs_in, const std::functio
     if (nvmax > 0) {
       dim3 gt((nvmax + per - 1) / per, J);
       k_twisted<<<gt, per, 0, c.stream>>>(d_td.p, per);
+      // small clusters: thread per cluster, T threads per problem with an
+      // interleaved LU scratch of 5 L doubles per thread (at most 8 GB in all)
+      const size_t per_t = size_t(J) * 5 * ldmax * 8;
+      const int T = int(std::max<size_t>(32, std::min<size_t>(1024, (size_t(8) << 30) / per_t / 32 * 32)));
+      DArr<double> cscr;
+      cscr.alloc(size_t(J) * 5 * ldmax * T);
+      k_clusters_small<<<dim3((T + 63) / 64, J), 64, 0, c.stream>>>(d_td.p, T, ldmax, cscr.p);
       k_clusters<<<J, 256, 0, c.stream>>>(d_td.p);
+      AWG_CUDA(cudaStreamSynchronize(c.stream));  // cscr goes out of scope
     }
-    c.launches += 4;
+    c.launches += 5;
     check_launch("tridiagonal eigensolver");
   }
   phase("tridiagonal eigenpairs");

@@ -19,3 +19,16 @@ def test_eig_against_cusolver(n, count, kind):
     assert r["eig_err"] <= 1e-13, r
     assert r["resid"] <= 1e-12, r
     assert r["orth"] <= 1e-11, r
+
+
+@pytest.mark.parametrize("split", [0, 3, 8])
+@pytest.mark.parametrize("n,count,kind", [(65, 3, 0), (300, 4, 0), (1089, 2, 1), (2113, 2, 2)])
+def test_eig_both_panel_forms(n, count, kind, split):
+    """One CTA per problem (k_latrd, eig_split = 0: what batches of >= 74
+    problems take) and the split form with C CTAs per symmetric product
+    (k_col_step + k_symv_part, the default for small batches) are the same
+    algorithm; both meet the bounds."""
+    r = awg.bench_eig(n, count, kind, seed=11, options={"eig_split": split})
+    assert r["eig_err"] <= 1e-13, r
+    assert r["resid"] <= 1e-12, r
+    assert r["orth"] <= 1e-11, r
