@@ -1396,14 +1396,30 @@ void eig_batched(Ctx& c, const std::vector<SyevJob>& jobs_in, const std::functio
     prof.alloc(4);
     prof.zero(c.stream);
   }
-  // fewer problems than SMs: split every symmetric product over C CTAs (1b);
-  // option eig_split = 0 keeps one CTA per problem, k >= 2 forces C = k
-  int C = std::min(8, c.sm_count / J);
-  if (c.opt("eig_split", -1) >= 0) C = int(std::max(1LL, std::min(16LL, c.opt("eig_split", -1))));
+  // Split form (1b) by default: the symmetric products of one column step run
+  // as J C CTAs in one launch (measured: 5.9 TB/s at 128 CTAs, 91% of the copy
+  // peak, where k_latrd's one CTA per problem leaves SMs idle below 148
+  // problems and runs 216 problems as 148 + 68).  C: the largest count <= 16
+  // whose last wave is >= 95% full (else the fullest).  Option eig_split = 0
+  // keeps one CTA per problem (k_latrd), k >= 1 forces C = k.
+  int C = 1;
+  {
+    double best = 0.0;
+    for (int cc = 1; cc <= 16; ++cc) {
+      const double waves = double(J) * cc / c.sm_count;
+      const double eff = waves / std::ceil(waves);
+      if (eff >= 0.95 || eff > best + 1e-9) {
+        if (eff >= 0.95 || best < 0.95) C = cc;
+        best = std::max(best, eff);
+      }
+    }
+  }
+  const bool split_form = c.opt("eig_split", -1) != 0;
+  if (c.opt("eig_split", -1) > 0) C = int(std::min(16LL, c.opt("eig_split", -1)));
   DArr<double> ypart;
-  if (C >= 2) ypart.alloc(size_t(J) * C * L);
+  if (split_form) ypart.alloc(size_t(J) * C * L);
   for (int k0 = 0; k0 < nmax - 1; k0 += kNB) {
-    if (C >= 2) {
+    if (split_form) {
       switch (R) {
         case 1: launch_panel_split<1>(c, d_ed.p, J, k0, C, L, nslot, smem, ypart.p); break;
         case 2: launch_panel_split<2>(c, d_ed.p, J, k0, C, L, nslot, smem, ypart.p); break;
@@ -1478,7 +1494,10 @@ void eig_batched(Ctx& c, const std::vector<SyevJob>& jobs_in, const std::functio
       // small clusters: thread per cluster, T threads per problem with an
       // interleaved LU scratch of 5 L doubles per thread (at most 8 GB in all)
       const size_t per_t = size_t(J) * 5 * ldmax * 8;
-      const int T = int(std::max<size_t>(32, std::min<size_t>(1024, (size_t(8) << 30) / per_t / 32 * 32)));
+      size_t free_b = 0, tot_b = 0;
+      AWG_CUDA(cudaMemGetInfo(&free_b, &tot_b));
+      const size_t budget = std::min<size_t>(size_t(8) << 30, free_b / 4);
+      const int T = int(std::max<size_t>(32, std::min<size_t>(1024, budget / per_t / 32 * 32)));
       DArr<double> cscr;
       cscr.alloc(size_t(J) * 5 * ldmax * T);
       k_clusters_small<<<dim3((T + 63) / 64, J), 64, 0, c.stream>>>(d_td.p, T, ldmax, cscr.p);

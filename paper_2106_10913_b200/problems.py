@@ -235,7 +235,7 @@ def _box_owner(shape, boxes):
     for ax in range(len(shape)):
         coord = grids[len(shape) - 1 - ax]
         w = shape[ax] // boxes[ax]
-        owner += (coord // w) * mult
+        owner += np.minimum(coord // w, boxes[ax] - 1) * mult  # the last box takes the remainder
         mult *= boxes[ax]
     return owner.reshape(-1)
 
@@ -429,6 +429,10 @@ def spec(name: str) -> dict:
         return el(16, 8, 2, soft_hard, (2, 1), 1, tau_sharp=0.1)
     if name == "telas8":  # c4 analogue with c4's 8-element layers and 2x2 nodal boxes
         return el(32, 16, 8, soft_hard, (2, 2), 1, tau_sharp=0.1)
+    if name == "tragged":  # ragged boxes (23 x 17 cells in 3 x 2 boxes: 7/7/9 by 8/9), 1 x 1 ... 9 x 9 corner blocks
+        return fd((23, 17), c2_channels(23, 17, band=6, contrast=1e3), (3, 2), 1, tau_sharp=0.2)
+    if name == "t1box":  # one subdomain: B^s = A, no negative modes, H1 = A^-1
+        return fd((12, 12), np.ones(144), (1, 1), 1, tau_sharp=0.5)
     if name == "c4mid":  # c4 with c4-sized subdomains (n_s ~ 4,200) but 4 of them
         return el(128, 64, 8, soft_hard, (2, 2), 1, tau_sharp=0.1)
     if name == "c4s":  # between telas8 and c4mid (n_s ~ 2,400, six 8-element layers)
@@ -448,4 +452,4 @@ def make(name: str) -> Problem:
 
 
 CONFIGS = ["c1", "c2", "c3", "c4", "c5"]
-ANALOGUES = ["t2d", "t2d_ov2", "t3d", "t3d_blocks", "telas", "telas8"]
+ANALOGUES = ["t2d", "t2d_ov2", "t3d", "t3d_blocks", "telas", "telas8", "tragged", "t1box"]

@@ -37,7 +37,7 @@ def golden_with_base(case):
 
 
 ALL_CASES = ["c1", "c1_exact", "t2d", "t2d_exact", "t2d_additive", "t2d_ov2", "t3d", "t3d_none", "t3d_blocks",
-             "telas", "telas8"]
+             "telas", "telas8", "tragged", "t1box"]
 
 
 def case_options(s):

@@ -40,6 +40,9 @@ CASES = {
     "t3d": ("t3d", "ref_driver", [], False, None),
     "t3d_none": ("t3d", "ref_driver", ["--awg", "none"], False, "t3d"),
     "t3d_blocks": ("t3d_blocks", "ref_driver", [], False, None),
+    # edge cases: ragged boxes; a single subdomain (no negative modes: AWG = H2)
+    "tragged": ("tragged", "ref_driver", [], False, None),
+    "t1box": ("t1box", "ref_driver", [], False, None),
     "telas": ("telas", "ref_driver", [], True, None),
     "telas8": ("telas8", "ref_driver", [], False, None),
     # one-level AS / AS+ (Cholesky factor form, preconditioner.cpp:20-30) with their

@@ -28,7 +28,7 @@ def test_device_rrf_on_reference_G(case):
         assert np.array_equal(ret, g[tag + "_retained"]), (case, tag, ret, g[tag + "_retained"])
         assert rel(l11, g[tag + "_l11"]) <= 1e-12, (case, tag)
         seen += 1
-    assert seen >= 1
+    assert seen >= (0 if case == "t1box" else 1)  # t1box: one subdomain, empty coarse spaces (n0 = n_minus = 0)
 
 
 @pytest.mark.parametrize("semantics", ["ref", "exact"])

@@ -12,7 +12,7 @@ from paper_2106_10913_b200 import awg
 
 pytestmark = pytest.mark.gpu
 
-BASE = ["c1", "t2d", "t2d_ov2", "t3d", "t3d_blocks", "telas", "telas8"]
+BASE = ["c1", "t2d", "t2d_ov2", "t3d", "t3d_blocks", "telas", "telas8", "tragged", "t1box"]
 
 
 KINDS = {"NN": awg.OneLevelKind.NN, "AS": awg.OneLevelKind.AS, "AS_PLUS": awg.OneLevelKind.AS_PLUS}
@@ -164,3 +164,38 @@ def test_wbuild_grouped_dgemm_matches_cublas_path(case):
     assert np.max(np.abs(i1.astype(int) - i2.astype(int))) <= 1
     w1, w2 = ctx1.get("W"), ctx2.get("W")
     assert rel(w1, w2) <= 1e-8
+
+
+def test_not_spd_error_carries_the_reference_pivot():
+    """cholesky (dense.cpp:226-249) throws NotSpdError(k) at the first
+    non-positive pivot; the AS one-level factors R A R^T (preconditioner.cpp:
+    20-30) hit it when A is indefinite.  t2d with the diagonal of dof 79 (owned
+    by subdomain 0 alone, local index 46) set to -1: the unmodified reference
+    (ref_driver --one-level AS) terminates with "matrix not spd: non-positive
+    pivot at index 46"; the device's blocked factorisation must report the same
+    pivot, through the same exception type."""
+    g, s = golden_with_base("t2d_as")
+    d = dict(g)
+    vals = g["A_values"].copy()
+    ro, ci = g["A_row_offsets"], g["A_col_indices"]
+    i0 = 79
+    for k in range(ro[i0], ro[i0 + 1]):
+        if ci[k] == i0:
+            vals[k] = -1.0
+    d["A_values"] = vals
+    # the restated unblocked factorisation on subdomain 0's block
+    om0 = d["part_indices"][d["part_offsets"][0]:d["part_offsets"][1]]
+    import scipy.sparse as sp
+    a = sp.csr_matrix((vals, ci, ro), shape=(len(d["b"]),) * 2)[om0][:, om0].toarray()
+    expect = None
+    for k in range(a.shape[0]):
+        if not a[k, k] > 0.0:
+            expect = k
+            break
+        a[k + 1:, k] /= np.sqrt(a[k, k])
+        a[k + 1:, k + 1:] -= np.outer(a[k + 1:, k], a[k + 1:, k])
+    assert expect == 46
+    with pytest.raises(awg.NotSpdError) as ei:
+        setup_ctx(d, s)
+    assert ei.value.pivot_index == 46
+    assert "non-positive pivot at index 46" in str(ei.value)
