@@ -184,3 +184,28 @@ def test_pcg_full_size(c2fs):
     assert rep3.iterations == rep4.iterations and np.array_equal(x3, x4)
     assert abs(true - rep1.final_relative_residual) <= 1e-6 * true  # krylov.cpp:98: the true residual
     assert true <= p.rtol or abs(true - rep1.recurrence_residual_at_exit) <= 1e-8  # krylov.cpp:93-101
+
+
+@pytest.mark.parametrize("mode", ["hyb", "inex"])
+def test_h3_variants_full_size(c2fs, mode):
+    """AWG HYB and INEX (preconditioner.cpp:199-221) and the projections Pi3 /
+    Pi3^T (preconditioner.cpp:161-183) on the device's own c2 factors against
+    the restatement: 1e-11 (INEX 1e-8: the reference's lu_solve, bug 2 included,
+    on the 262 x 262 core of a 1e6-contrast problem)."""
+    p = c2fs.p
+    cfg = awg.config_for(p)
+    cfg.awg = {"hyb": awg.AwgMode.HYB, "inex": awg.AwgMode.INEX}[mode]
+    ctx = awg.context_from_problem(p)
+    ctx.load_factors(cfg, c2fs.f)
+    out = {}
+    try:
+        for seed in (1000, 1001):
+            x = problems.uniform(seed, p.n, -1.0, 1.0)
+            out["H3" + mode] = max(out.get("H3" + mode, 0.0), rel(ctx.apply(awg.Op.H3, x), c2fs.orc.h3(x, mode)))
+            if mode == "hyb":
+                out["PI3"] = max(out.get("PI3", 0.0), rel(ctx.apply(awg.Op.PI3, x), c2fs.orc.apply_pi3(x)))
+                out["PI3T"] = max(out.get("PI3T", 0.0), rel(ctx.apply(awg.Op.PI3T, x), c2fs.orc.apply_pi3_transpose(x)))
+    finally:
+        ctx.close()
+    record("c2_h3_" + mode, out)
+    assert all(v <= (1e-8 if k == "H3inex" else 1e-11) for k, v in out.items()), out
