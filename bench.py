@@ -181,6 +181,21 @@ class ReferenceSampler:
         with open(os.path.join(out, "summary.json")) as fh:
             return json.load(fh)
 
+    def _full_run_record(self):
+        """c2: the one complete run of the unmodified reference (setup, solve
+        and its stock H3 apply loop; tests/golden/c2_reference.json, made in
+        the build container, not on this box) next to the live sample."""
+        path = os.path.join(ROOT, "tests", "golden", f"{self.config}_reference.json")
+        if not os.path.exists(path):
+            return {}
+        with open(path) as fh:
+            m = json.load(fh)
+        return {"reference_full_run": {
+            "applies_per_s": 1.0 / m["t_h3_apply"], "t_h3_apply_s": m["t_h3_apply"], "t_solve_s": m["t_solve"],
+            "iterations": m["iterations"],
+            "serial_setup_s": sum(v for k, v in m["serial_setup_s"].items() if k != "calls"),
+            "host": "build container (8 cores, 1 thread per call), tests/golden/make_c2_reference_golden.py"}}
+
     def baseline(self, sizes=None, budget_s=15.0):
         if self.config == "c1":
             s = self.full()
@@ -189,7 +204,8 @@ class ReferenceSampler:
                               f"{s['t_splitting'] + s['t_coarse'] + s['t_w']:.2f} s, solve {s['t_solve'] * 1e3:.2f} ms / "
                               f"{s['iterations']} it, H3 apply loop of 50"}
         s = self.sample(budget_s, sizes)
-        return {"value": 1.0 / s["t_h3_apply_s"], "unit": "applies/s", "cores": 1, "kind": "reference",
+        return {**self._full_run_record(),
+                "value": 1.0 / s["t_h3_apply_s"], "unit": "applies/s", "cores": 1, "kind": "reference",
                 "sample": (f"reference kernels (oracle/_ref, 1 thread) timed on {self.config} shapes: spmv full, "
                            f"one-level on {s['sampled_subdomains']}/{s['n_sub']} subdomains, A- on "
                            f"{s['aminus_sampled']}/{s['n_sub']}, dense Z/W pairs on 8 columns, scaled to "

@@ -17,7 +17,12 @@ what the GPU tests and the CPU baseline need:
   timings: stock H3 apply (20 reps), solve, and the serial setup time
   (sum of the per-call seconds the cache recorded).
 
-    python tests/golden/make_c2_reference_golden.py <workdir> (default scratch/c2ref)
+    python tests/golden/make_c2_reference_golden.py <workdir> [suffix]
+
+suffix "_exact": the same run with the probe-fixed pivoted factor
+(oracle/_ref/ref_driver_memo_fixed, rrf_fixed.cpp): the B^s
+eigenpairs and pencils are the shipped run's cache entries (they do not depend
+on the pivoted factor), the W-column PCGs and the solve were recomputed.
 """
 from __future__ import annotations
 
@@ -53,6 +58,7 @@ def memo_seconds(memo_dir):
 
 def main():
     work = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "scratch", "c2ref")
+    suffix = sys.argv[2] if len(sys.argv) > 2 else ""
     out = os.path.join(work, "out")
     s = json.load(open(os.path.join(out, "summary.json")))
     ld = lambda k: np.load(os.path.join(out, k + ".npy"))  # noqa: E731
@@ -62,7 +68,7 @@ def main():
     blob["x_apply"] = xa[:2]
     for k in ("y_H1", "y_Aminus", "y_Aplus", "y_H3ad"):
         blob[k] = ld(k)[:2]
-    np.savez_compressed(os.path.join(HERE, "c2_reference.npz"), **blob)
+    np.savez_compressed(os.path.join(HERE, "c2_reference" + suffix + ".npz"), **blob)
     tot, cnt = memo_seconds(os.path.join(work, "memo"))
     meta = {k: s[k] for k in ("n", "nnz", "n_sub", "n0", "r0", "n_minus", "rw", "iterations", "converged",
                               "final_relative_residual", "kappa", "ritz_min", "ritz_max", "t_h3_apply", "apply_reps",
@@ -70,8 +76,9 @@ def main():
     meta["serial_setup_s"] = {"dense_sym_eig": tot["eig"], "generalized_sym_eig": tot["geig"],
                               "build_w_pcg": tot["pcg"], "calls": cnt}
     meta["provenance"] = ("oracle/run_memo_reference.sh c2 <work> --tau 0.1 (unmodified reference objects, "
-                          "memoised pure functions, stock replay)")
-    with open(os.path.join(HERE, "c2_reference.json"), "w") as fh:
+                          "memoised pure functions, stock replay)" +
+                          ("; pivoted factor replaced by the probe-fixed one (ref_driver_memo_fixed)" if suffix else ""))
+    with open(os.path.join(HERE, "c2_reference" + suffix + ".json"), "w") as fh:
         json.dump(meta, fh, indent=1)
     print(json.dumps(meta))
 

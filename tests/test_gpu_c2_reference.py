@@ -1,0 +1,116 @@
+"""BASELINE.json configs[1] (c2) end to end against runs of the reference
+itself (tests/golden/c2_reference*.{npz,json}, made by
+oracle/run_memo_reference.sh + tests/golden/make_c2_reference_golden.py: the
+reference's own dense_sym_eig / generalized_sym_eig / pcg results memoised by
+content hash — 23 h of one core —, then the stock ProblemContext +
+run_with_context composition, harness.cpp:63-139):
+
+* ``c2_reference``: the unmodified reference (shipped pivoted factor);
+* ``c2_reference_exact``: the same objects with the probe-fixed pivoted
+  factor (oracle/rrf_fixed.cpp).
+
+The GPU path runs its own setup (Householder eigensolver instead of the
+reference's cyclic Jacobi), so what can agree exactly are the integers
+(n_nonpos, n_zero, GenEO mode counts, n0, r0, n_minus) and, to the accuracy of
+the two eigensolvers, the basis-invariant operators H1, A- and A+.  H3 and the
+solve go through K_W = W^T A W's pivoted factor.  With the exact factor that
+is well-posed and the north-star gates apply (iterations +-1, x within 1e-7).
+With the shipped factor (bug 1, dense.cpp:313-338) K_W loses 21 of its 262
+columns at c2 and WHICH ones depends on rounding-level ties: the device's own
+iteration count moved 95 -> 101 -> 128 across eigensolver revisions with every
+operator still within 5e-15 of the restatement on the same factors
+(test_gpu_fullsize.py), and the reference itself lands at 114.  There the
+gates are the counts, the basis-invariant operators and convergence; the
+iteration counts are recorded."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import rel
+from fullsize_parity import record
+from paper_2106_10913_b200 import awg, problems
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+VARIANTS = {k: v for k, v in {"c2_reference": "reference", "c2_reference_exact": "exact"}.items()
+            if os.path.exists(os.path.join(GOLD, k + ".json"))}  # (a golden is a 20+ h offline reference run)
+
+
+def _load(name):
+    with open(os.path.join(GOLD, name + ".json")) as fh:
+        meta = json.load(fh)
+    return meta, np.load(os.path.join(GOLD, name + ".npz"))
+
+
+@pytest.fixture(scope="module", params=list(VARIANTS))
+def run(request):
+    name = request.param
+    meta, g = _load(name)
+    p = problems.make("c2")
+    ctx = awg.context_from_problem(p)
+    ctx.setup(awg.config_for(p, rrf_semantics=VARIANTS[name]))
+    yield name, p, ctx, meta, g
+    ctx.close()
+
+
+def test_setup_counts_identical(run):
+    """splitting.cpp:64-105 (eigsplit), coarse.cpp:113-154 (selection),
+    dense.cpp:299-346 (retained ranks)."""
+    name, p, ctx, meta, g = run
+    assert meta["n"] == p.n and meta["n_sub"] == p.n_sub
+    assert np.array_equal(ctx.get("n_nonpos"), g["n_nonpos"])
+    assert np.array_equal(ctx.get("n_zero"), g["n_zero"])
+    assert np.array_equal(ctx.get("ks"), g["ks"])
+    q = ctx.query()
+    got = {k: q[k] for k in ("n0", "r0", "n_minus", "rw")}
+    record(name + "_counts", {"device": got, "reference": {k: meta[k] for k in got}})
+    assert got["n0"] == meta["n0"] and got["n_minus"] == meta["n_minus"] and got["r0"] == meta["r0"]
+    if VARIANTS[name] == "exact":
+        assert got["rw"] == meta["rw"]
+    else:  # shipped factor: which near-tie pivots drop is rounding-dependent
+        assert abs(got["rw"] - meta["rw"]) <= 8, (got, meta["rw"])
+
+
+def test_basis_invariant_operators(run):
+    """The reference's applies on its own factors vs the device's on its own:
+    H1 = sum R^T D P^s D R, A- and A+ do not depend on the eigenvector basis,
+    so they agree to the accuracy of the two eigensolvers.  H1 is a
+    pseudo-inverse: any normwise backward-stable eigensolver leaves it with a
+    relative error ~ eps ||B^s|| / lambda_min+ (here 1e-16 x 4e6 / ~1e-2; cyclic
+    Jacobi is relatively accurate on such graded matrices, Householder +
+    bisection is not).  Measured: H1 5.8e-9, A- 9.6e-12, A+ 4.9e-14."""
+    name, p, ctx, meta, g = run
+    out = {}
+    for op, key in ((awg.Op.H1, "y_H1"), (awg.Op.AMINUS, "y_Aminus"), (awg.Op.APLUS, "y_Aplus"), (awg.Op.H3, "y_H3ad")):
+        for x, y in zip(g["x_apply"], g[key]):
+            out[key] = max(out.get(key, 0.0), rel(ctx.apply(op, x), y))
+    record(name + "_operators", out)
+    assert out["y_Aplus"] <= 1e-11 and out["y_Aminus"] <= 1e-10 and out["y_H1"] <= 2e-8, out
+    if VARIANTS[name] == "exact":
+        assert out["y_H3ad"] <= 1e-7, out  # W known to w_rtol = 1e-10 on each side
+
+
+def test_pcg_against_reference(run):
+    """krylov.cpp:36-124 through harness.cpp:131-139."""
+    name, p, ctx, meta, g = run
+    x, rep = ctx.pcg(p.b, p.rtol, 10 * p.n)
+    info = {"iterations": rep.iterations, "reference_iterations": meta["iterations"], "x_rel": rel(x, g["pcg_x"]),
+            "kappa": rep.kappa_estimate, "reference_kappa": meta["kappa"],
+            "final_relres": rep.final_relative_residual, "reference_final_relres": meta["final_relative_residual"],
+            "reference_t_h3_apply_s": meta["t_h3_apply"], "reference_t_solve_s": meta["t_solve"],
+            "reference_serial_setup_s": sum(v for k, v in meta["serial_setup_s"].items() if k != "calls")}
+    record(name + "_pcg", info)
+    assert rep.converged and meta["converged"]
+    assert rep.final_relative_residual <= p.rtol or abs(rep.final_relative_residual -
+                                                         rep.recurrence_residual_at_exit) <= 1e-8
+    if VARIANTS[name] == "exact":
+        assert abs(rep.iterations - meta["iterations"]) <= 1, info
+        assert info["x_rel"] <= 1e-7, info
+        assert abs(rep.kappa_estimate - meta["kappa"]) <= 1e-3 * meta["kappa"], info
+    else:
+        # ill-posed under bug 1 (see the module docstring): both solves reach rtol;
+        # the iteration counts stay within the spread the device itself has shown
+        assert abs(rep.iterations - meta["iterations"]) <= 0.25 * meta["iterations"], info
+        assert info["x_rel"] <= 1e-6, info
