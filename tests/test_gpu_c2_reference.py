@@ -114,3 +114,17 @@ def test_pcg_against_reference(run):
         # the iteration counts stay within the spread the device itself has shown
         assert abs(rep.iterations - meta["iterations"]) <= 0.25 * meta["iterations"], info
         assert info["x_rel"] <= 1e-6, info
+
+
+def test_w_inner_iterations(run):
+    """build_w's inner PCG(A+, H2) per W column (preconditioner.cpp:97-113):
+    the device's continuously batched solves stop where the reference's
+    per-column pcg calls stop (+-max(3, 15%), the golden cases' bound)."""
+    name, p, ctx, meta, g = run
+    inner = ctx.get("w_inner_iterations")
+    ref = np.asarray(g["w_inner_iterations"])
+    assert inner.size == ref.size
+    d = np.abs(inner - ref)
+    record(name + "_w_inner", {"device_total": int(inner.sum()), "reference_total": int(ref.sum()),
+                               "max_abs_diff": int(d.max()), "columns_differing": int((d > 0).sum())})
+    assert np.all(d <= np.maximum(3, 0.15 * ref)), (inner, ref)
