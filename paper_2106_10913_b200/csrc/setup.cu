@@ -768,13 +768,15 @@ void run_setup(Ctx& c, const awg_config& cfg) {
     const bool as = (cfg.one_level == 0);
     int lw_max = 1;
     size_t blk_max = 1;
-    for (int s = 0; s < N; ++s) {
-      int lw = 0;
-      AWG_SOLVER(cusolverDnDsygvd_bufferSize(sv.sol[0], CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR,
-                                             CUBLAS_FILL_MODE_LOWER, c.h_ns[s], nullptr, c.h_ld[s], nullptr,
-                                             c.h_ld[s], nullptr, &lw));
-      lw_max = std::max(lw_max, lw);
-      blk_max = std::max(blk_max, size_t(c.h_ld[s]) * c.h_ns[s]);
+    for (int s = 0; s < N; ++s) blk_max = std::max(blk_max, size_t(c.h_ld[s]) * c.h_ns[s]);
+    if (c.opt("setup_cusolver", 0) != 0) {  // workspace of the library path only
+      for (int s = 0; s < N; ++s) {
+        int lw = 0;
+        AWG_SOLVER(cusolverDnDsygvd_bufferSize(sv.sol[0], CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR,
+                                               CUBLAS_FILL_MODE_LOWER, c.h_ns[s], nullptr, c.h_ld[s], nullptr,
+                                               c.h_ld[s], nullptr, &lw));
+        lw_max = std::max(lw_max, lw);
+      }
     }
     DArr<double> plam, plam2;
     plam.alloc(c.P);
@@ -802,6 +804,7 @@ void run_setup(Ctx& c, const awg_config& cfg) {
       });
       for (const auto& wave : waves) {
         const int J = int(wave.size());
+        double tw = now_ms();
         std::vector<DArr<double>> B(size_t(J) * nb);
         std::vector<double*> MA(J), MB(J), T(J), AB(J), AB2(J);
         for (int q = 0; q < J; ++q) {
@@ -822,6 +825,8 @@ void run_setup(Ctx& c, const awg_config& cfg) {
           }
         }
         sv.sync();
+        trace(c, "  pencil blocks of " + std::to_string(J) + " subdomains (weighted A+^s, R A+ R^T)", now_ms() - tw);
+        tw = now_ms();
         if (!as) {
           const double tau = cfg.one_level == 1 ? 1.0 / cfg.tau_flat : cfg.tau_sharp;
           pencil_wave(c, wave, MA, MB, T, plam.p, Ycol, cap, count_rule(tau, cfg.fixed_k));
@@ -830,6 +835,8 @@ void run_setup(Ctx& c, const awg_config& cfg) {
           pencil_wave(c, wave, MA, AB, T, plam.p, Ycol, cap, count_rule(1.0 / cfg.tau_flat, 0));
           pencil_wave(c, wave, AB2, MB, T, plam2.p, Ycol2, cap, count_rule(cfg.tau_sharp, 0));
         }
+        AWG_CUDA(cudaStreamSynchronize(c.stream));
+        trace(c, "  pencil reduction + eigensolve + back substitution", now_ms() - tw);
       }
     } else {
     const int nbuf = as ? 4 : 2;
