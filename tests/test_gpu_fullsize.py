@@ -186,26 +186,41 @@ def test_pcg_full_size(c2fs):
     assert true <= p.rtol or abs(true - rep1.recurrence_residual_at_exit) <= 1e-8  # krylov.cpp:93-101
 
 
-@pytest.mark.parametrize("mode", ["hyb", "inex"])
+@pytest.mark.parametrize("mode", ["hyb", "inex", "inex_exact_lu"])
 def test_h3_variants_full_size(c2fs, mode):
     """AWG HYB and INEX (preconditioner.cpp:199-221) and the projections Pi3 /
     Pi3^T (preconditioner.cpp:161-183) on the device's own c2 factors against
-    the restatement: 1e-11 (INEX 1e-8: the reference's lu_solve, bug 2 included,
-    on the 262 x 262 core of a 1e6-contrast problem)."""
+    the restatement, 1e-11.  INEX under the reference's lu_solve (bug 2,
+    dense.cpp:404-409) overflows on c2's 262 x 262 core — the reference's own
+    c2 run prints NaN for it (profiles/r02e/c2_reference_factors_*.json) — so
+    there the bug-compatible device path must be non-finite exactly when the
+    restatement is, and the comparison proper runs with the exact LU."""
     p = c2fs.p
-    cfg = awg.config_for(p)
-    cfg.awg = {"hyb": awg.AwgMode.HYB, "inex": awg.AwgMode.INEX}[mode]
+    lu = "exact" if mode == "inex_exact_lu" else "reference"
+    cfg = awg.config_for(p, lu_semantics=lu)
+    cfg.awg = awg.AwgMode.HYB if mode == "hyb" else awg.AwgMode.INEX
     ctx = awg.context_from_problem(p)
     ctx.load_factors(cfg, c2fs.f)
+    orc = c2fs.orc
     out = {}
     try:
+        orc.lu_exact, orc._core = (lu == "exact"), None
         for seed in (1000, 1001):
             x = problems.uniform(seed, p.n, -1.0, 1.0)
-            out["H3" + mode] = max(out.get("H3" + mode, 0.0), rel(ctx.apply(awg.Op.H3, x), c2fs.orc.h3(x, mode)))
+            got = ctx.apply(awg.Op.H3, x)
+            with np.errstate(all="ignore"):
+                ref = orc.h3(x, "hyb" if mode == "hyb" else "inex")
+            if not np.isfinite(ref).all():
+                assert mode == "inex" and not np.isfinite(got).all(), "bug-compatible INEX: both sides overflow"
+                out["H3inex_nonfinite_both"] = 1.0
+                continue
+            out["H3" + mode] = max(out.get("H3" + mode, 0.0), rel(got, ref))
             if mode == "hyb":
-                out["PI3"] = max(out.get("PI3", 0.0), rel(ctx.apply(awg.Op.PI3, x), c2fs.orc.apply_pi3(x)))
-                out["PI3T"] = max(out.get("PI3T", 0.0), rel(ctx.apply(awg.Op.PI3T, x), c2fs.orc.apply_pi3_transpose(x)))
+                out["PI3"] = max(out.get("PI3", 0.0), rel(ctx.apply(awg.Op.PI3, x), orc.apply_pi3(x)))
+                out["PI3T"] = max(out.get("PI3T", 0.0), rel(ctx.apply(awg.Op.PI3T, x), orc.apply_pi3_transpose(x)))
     finally:
+        orc.lu_exact, orc._core = False, None
         ctx.close()
     record("c2_h3_" + mode, out)
-    assert all(v <= (1e-8 if k == "H3inex" else 1e-11) for k, v in out.items()), out
+    assert out, mode
+    assert all(np.isfinite(v) and v <= (1.0 if k.endswith("_both") else 1e-11) for k, v in out.items()), out
