@@ -134,6 +134,7 @@ typedef struct awg_stats {
   int w_batches;        /* block passes of the batched W build (continuous batching) */
   int nn_single_pass;   /* 1: the NN local solve streams V^s once per apply (k_nn_fused) */
   int nn_static_split;  /* 1: k_nn_fused runs equal static byte shares per CTA (no work queue) */
+  int coarse_az;        /* 1: the hybrid H2's post-solve half uses the precomputed A Z (option coarse_az) */
 } awg_stats;
 
 int awg_create(struct awg_ctx** ctx, int device);

@@ -156,7 +156,7 @@ class _Stats(ctypes.Structure):
         ("sum_ns", ctypes.c_longlong), ("sum_ns2", ctypes.c_longlong), ("sum_ns_ks", ctypes.c_longlong),
         ("sum_ns_ms", ctypes.c_longlong), ("sum_ns_qs", ctypes.c_longlong),
         ("t_setup_ms", ctypes.c_double * 8), ("w_inner_total", ctypes.c_int), ("w_batches", ctypes.c_int),
-        ("nn_single_pass", ctypes.c_int), ("nn_static_split", ctypes.c_int),
+        ("nn_single_pass", ctypes.c_int), ("nn_static_split", ctypes.c_int), ("coarse_az", ctypes.c_int),
     ]
 
 

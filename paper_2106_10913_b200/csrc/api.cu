@@ -502,7 +502,7 @@ int awg_set_option(awg_ctx* ctx, const char* name, long long value) {
     else if (k == "fused_min_cols") c.fused_min_cols = std::max(8, v);
     else if (k == "fused_tail") c.fused_tail_pct = std::max(0, std::min(90, v));
     else if (k == "fused_static_cols" || k == "synth_nm" || k == "dgemm_variant" || k == "coarse_neg" ||
-             k == "verbose" || k == "wbuild_cublas" || k == "setup_cusolver" || k == "eig_probe" || k == "eig_split")
+             k == "verbose" || k == "wbuild_cublas" || k == "setup_cusolver" || k == "eig_probe" || k == "eig_split" || k == "coarse_az")
       c.opts[k] = value;
     else
       c.fail(AWG_E_ARG, "set_option: unknown option " + k);
@@ -694,6 +694,7 @@ int awg_load_factors(awg_ctx* ctx, const awg_config* cfg, const awg_factors* f) 
     // loaded V^s for the A+ blocks); Cholesky factors are unique
     if (c.one_level != 2) build_local_cholesky(c);
     k::build_coarse_neg(c);
+    k::build_az(c);
     AWG_CUDA(cudaStreamSynchronize(c.stream));
     c.have_factors = true;
   });
@@ -904,6 +905,7 @@ int awg_query(awg_ctx* ctx, awg_stats* st) {
       const LocalPlan& lp = c.one_level == 2 ? c.plan_nn : c.plan_as;
       st->nn_static_split = (lp.fused && lp.static_grid > 0) ? 1 : 0;
     }
+    st->coarse_az = c.az_on ? 1 : 0;
   });
 }
 

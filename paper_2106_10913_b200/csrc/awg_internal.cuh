@@ -243,6 +243,10 @@ void aminus(Ctx& c, const double* x, double* y, const int* gate);     // y = A- 
 void aplus(Ctx& c, const double* x, double* y, int mode, const double* sub, const int* gate, bool neg_ready = false);
 bool coarse_q_neg(Ctx& c, const double* x, double* y, const int* gate);  // Q x and the A- dots of Q x
 void build_coarse_neg(Ctx& c);  // M2 = M1 K+ (A- dots of the retained coarse columns), after K0 is set
+void build_az(Ctx& c);          // A Z on ring-extended supports + the combined dots plan, after build_coarse_neg
+// y = ((hp - Z K+ Z^T A+ hp) + corr) [+ extra] without forming A+ hp (needs c.az_on)
+void coarse_q_combine_az(Ctx& c, const double* hp, double* y, const double* corr, const double* extra,
+                         cudaEvent_t wait_before_combine, const int* gate);
 void coarse_q(Ctx& c, const double* x, double* y, const int* gate);   // y = Z K0+ Z^T x
 // y = ((a - Z K0+ Z^T x) + d) [+ e] in one epilogue (a == nullptr: y = Z K0+ Z^T x);
 // the stream waits on `wait_before_combine` (if set) before the combining kernel
@@ -326,6 +330,16 @@ struct Ctx {
   BsPlan bs_neg, bs_z;   // A- dots (V^s columns k < n_nonpos), Z^T x (Y_s blocks)
   DArr<OwnEnt> ent_neg, ent_z;  // owner entries into V^s (A- modes) and Y_s (Z columns)
   DArr<double> m2t;  // (K+ M1^T): r0 x n_neg column-major; M1(q, jj) = A- dot q of coarse column retained[jj]
+  // A Z on ring-extended supports (k::build_az): the post-solve half of the hybrid H2
+  // needs Z^T A+ hp = (A Z)^T hp + M1^T (V-^T R hp); both dot families run as ONE
+  // block-sparse GEMV^T over 2N "subdomains" (s < N: V-^s on Omega^s, s >= N: (A Z)_s on
+  // E_s = Omega^s + one graph ring), and the M1 term rides in the coarse solve (m2)
+  bool az_on = false;
+  BsPlan bs_az;
+  DArr<int> az_ns, az_ld, az_pidx, az_coff, az_ccol;
+  DArr<long long> az_poff, az_moff;  // az_moff: element offsets from V.p (the AZ blocks live in AZ)
+  DArr<double> AZ, az_out;           // az_out: [unweighted A- dots (nneg); (A Z)^T x (n0)]
+  DArr<double> m2;                   // M1 K+ (n_neg x r0 column-major): m2t transposed
   LocalPlan plan_nn;     // V^s with the eigenvalue mask (NN)
   LocalPlan plan_as;     // U^s = L^-T, triangular (AS / AS+)
   DArr<double> U;        // AS / AS+ local factors, same layout as V

@@ -788,7 +788,8 @@ __global__ void __launch_bounds__(256) k_bs_gemvT(const int* __restrict__ gate, 
 __global__ void k_coarse_solve(const int* __restrict__ gate, int dim, int r, const double* __restrict__ kinv,
                                const int* __restrict__ pos, const int* __restrict__ ret,
                                const double* __restrict__ b, double* __restrict__ x, int early, int nq,
-                               const double* __restrict__ m2t, double* __restrict__ out2) {
+                               const double* __restrict__ m2t, double* __restrict__ out2,
+                               int nd, const double* __restrict__ m2, const double* __restrict__ dvec) {
   if (gated_early(gate, early)) return;
   // b_r = b[retained] staged once per CTA (kCoarseStage doubles of static
   // shared memory) instead of two dependent loads per element in every warp
@@ -819,6 +820,14 @@ __global__ void k_coarse_solve(const int* __restrict__ gate, int dim, int r, con
         a1 = fma(row[j + 32], __ldg(b + ret[j + 32]), a1);
       }
       if (j < r) acc = fma(row[j], __ldg(b + ret[j]), acc);
+    }
+    if (dvec && i < dim) {  // + (M1 K+)^T d at the retained position k (column k of m2, nd x r)
+      const double* col = m2 + (size_t)k * nd;
+      for (j = lane; j + 32 < nd; j += 64) {
+        acc = fma(col[j], __ldg(dvec + j), acc);
+        a1 = fma(col[j + 32], __ldg(dvec + j + 32), a1);
+      }
+      if (j < nd) acc = fma(col[j], __ldg(dvec + j), acc);
     }
     acc = warp_sum(acc + a1);
   }
@@ -1299,11 +1308,19 @@ void h1(Ctx& c, const double* x, double* y, const int* gate) {
   nn_prolong(c, y, gate);
 }
 
+struct BsIndex {  // row index sets of a block family (default: the subdomains' Omega^s)
+  const int* ns;
+  const int* ld;
+  const long long* poff;
+  const int* pidx;
+};
 static void bs_gemvT(Ctx& c, BsPlan& b, const int* coff, const int* ccol, const double* M, const long long* moff,
-                     const double* x, const double* w, double* out, const int* gate) {
+                     const double* x, const double* w, double* out, const int* gate, const BsIndex* ix = nullptr) {
   if (b.ntask == 0) return;
-  launch(c, k_bs_gemvT, dim3(b.ntask, b.ncg), 256, 0, gate, b.ts.p, b.tc.p, b.nch.p, b.maxch, coff, ccol, M, moff, c.ns.p,
-                                            c.ld.p, c.poff.p, c.pidx.p, x, w, b.part.p, b.cnt.p, out, c.pdl_early);
+  const BsIndex dflt{c.ns.p, c.ld.p, c.poff.p, c.pidx.p};
+  if (!ix) ix = &dflt;
+  launch(c, k_bs_gemvT, dim3(b.ntask, b.ncg), 256, 0, gate, b.ts.p, b.tc.p, b.nch.p, b.maxch, coff, ccol, M, moff, ix->ns,
+                                            ix->ld, ix->poff, ix->pidx, x, w, b.part.p, b.cnt.p, out, c.pdl_early);
   ++c.launches;
   check_launch("bs_gemvT");
 }
@@ -1364,7 +1381,7 @@ void rr_solve(Ctx& c, const CoarseFactor& f, const double* b, double* x, const i
   }
   launch(c, k_coarse_solve, (f.dim + wpb - 1) / wpb, kThreads, 0, gate, f.dim, f.rank, f.kinv.p, f.pos.p,
                                                                      f.retained.p, b, x, c.pdl_early, 0,
-         (const double*)nullptr, (double*)nullptr);
+         (const double*)nullptr, (double*)nullptr, 0, (const double*)nullptr, (const double*)nullptr);
   ++c.launches;
   check_launch("coarse_solve");
 }
@@ -1379,7 +1396,8 @@ bool coarse_q_neg(Ctx& c, const double* x, double* y, const int* gate) {
   const int wpb = kThreads / 32;
   const CoarseFactor& f = c.k0;
   launch(c, k_coarse_solve, (f.dim + c.nneg + wpb - 1) / wpb, kThreads, 0, gate, f.dim, f.rank, f.kinv.p, f.pos.p,
-         f.retained.p, (const double*)c.cz.p, coef, c.pdl_early, c.nneg, (const double*)c.m2t.p, c.neg_c.p);
+         f.retained.p, (const double*)c.cz.p, coef, c.pdl_early, c.nneg, (const double*)c.m2t.p, c.neg_c.p, 0,
+         (const double*)nullptr, (const double*)nullptr);
   ++c.launches;
   check_launch("coarse_solve_neg");
   const BlockSum bs{c.own_off.p, c.ent_z.p, nullptr, c.Y.p, coef};
@@ -1402,12 +1420,43 @@ void coarse_q(Ctx& c, const double* x, double* y, const int* gate) {
   coarse_q_combine(c, x, y, nullptr, nullptr, nullptr, nullptr, gate);
 }
 
+static void z_combine(Ctx& c, const double* coef, double* y, const double* a, const double* d, const double* e,
+                      cudaEvent_t wait_before_combine, const int* gate);
+
 void coarse_q_combine(Ctx& c, const double* x, double* y, const double* a, const double* d, const double* e,
                       cudaEvent_t wait_before_combine, const int* gate) {
   if (c.n0 == 0) c.fail(AWG_E_STATE, "coarse_q: empty coarse space");
   zT(c, x, c.cz.p, gate);
   double* coef = c.cz.p + c.n0;  // second half of cz holds the solved coefficients
   rr_solve(c, c.k0, c.cz.p, coef, gate);
+  z_combine(c, coef, y, a, d, e, wait_before_combine, gate);
+}
+
+// The post-solve half of the hybrid H2 without A+ hp:
+//   Z^T A+ hp = (A Z)^T hp + Z^T A- hp,  Z^T A- hp = M1^T (V-^T R hp)
+// (M1(q, j) = |lambda_q| v_q^T R z_j, build_coarse_neg), so c2 = K+ (Z^T A+ hp)_r = K+ g_r + (M1 K+)^T d with
+// g = (A Z)^T hp and d = V-^T R hp from ONE block-sparse GEMV^T launch over both
+// families and the second term inside the coarse-solve launch: 3 kernels where
+// A- dots + A+ SpMV + Z^T + solve + combine were 5.  Same sums regrouped
+// (rounding-level differences only).
+void coarse_q_combine_az(Ctx& c, const double* hp, double* y, const double* corr, const double* extra,
+                         cudaEvent_t wait_before_combine, const int* gate) {
+  if (!c.az_on) c.fail(AWG_E_STATE, "coarse_q_combine_az: A Z not built");
+  const BsIndex ix{c.az_ns.p, c.az_ld.p, c.az_poff.p, c.az_pidx.p};
+  bs_gemvT(c, c.bs_az, c.az_coff.p, c.az_ccol.p, c.V.p, c.az_moff.p, hp, nullptr, c.az_out.p, gate, &ix);
+  double* coef = c.cz.p + c.n0;
+  const CoarseFactor& f = c.k0;
+  const int wpb = kThreads / 32;
+  launch(c, k_coarse_solve, (f.dim + wpb - 1) / wpb, kThreads, 0, gate, f.dim, f.rank, f.kinv.p, f.pos.p, f.retained.p,
+         (const double*)(c.az_out.p + c.nneg), coef, c.pdl_early, 0, (const double*)nullptr, (double*)nullptr, c.nneg,
+         (const double*)c.m2.p, (const double*)c.az_out.p);
+  ++c.launches;
+  check_launch("coarse_solve_az");
+  z_combine(c, coef, y, hp, corr, extra, wait_before_combine, gate);
+}
+
+static void z_combine(Ctx& c, const double* coef, double* y, const double* a, const double* d, const double* e,
+                      cudaEvent_t wait_before_combine, const int* gate) {
   if (wait_before_combine) AWG_CUDA(cudaStreamWaitEvent(c.stream, wait_before_combine, 0));
   // Z c: block-sparse combination fused with the prolongation and the composition
   const BlockSum bs{c.own_off.p, c.ent_z.p, nullptr, c.Y.p, coef};
@@ -1577,6 +1626,157 @@ void build_coarse_neg(Ctx& c) {
   AWG_CUDA(cudaStreamSynchronize(c.stream));
   cublasDestroy(h);
   if (st != CUBLAS_STATUS_SUCCESS) c.fail(AWG_E_CUDA, "build_coarse_neg: DGEMM");
+}
+
+// ---------------------------------------------------------------------------
+// A Z on ring-extended supports for coarse_q_combine_az.
+namespace {
+// AZ_s(e, k) = sum_j A(E_s[e], j) Y_s(loc_s(j), k): thread per (e, k); Omega^s is sorted (binary search)
+__global__ void k_az_block(int ne, int lde, const int* __restrict__ eidx, int ns, int lds, const int* __restrict__ om,
+                           const int* __restrict__ rp, const int* __restrict__ ci, const double* __restrict__ va,
+                           const double* __restrict__ Ys, double* __restrict__ AZs) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x, k = blockIdx.y;
+  if (e >= ne) return;
+  const int i = eidx[e];
+  double acc = 0.0;
+  for (int p = rp[i]; p < rp[i + 1]; ++p) {
+    const int j = ci[p];
+    int lo = 0, hi = ns;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (om[mid] < j) lo = mid + 1;
+      else hi = mid;
+    }
+    if (lo < ns && om[lo] == j) acc = fma(va[p], Ys[lo + (size_t)k * lds], acc);
+  }
+  AZs[e + (size_t)k * lde] = acc;
+}
+// m2(q, k) = m2t(k, q): M1 K+ (nq x r) from (K+ M1^T), so that the coarse solve reads column k coalesced
+__global__ void k_m2_transpose(int r, int nq, const double* __restrict__ m2t, double* __restrict__ m2) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= (long long)r * nq) return;
+  const int q = int(t % nq), k = int(t / nq);
+  m2[t] = m2t[k + (size_t)q * r];
+}
+}  // namespace
+
+void build_az(Ctx& c) {
+  c.az_on = false;
+  c.AZ.release();
+  c.m2.release();
+  // measured (profiles/r02e/knobs_coarse_az_c{2,3}.json, ms per PCG iteration): c3 3.676 -> 3.643
+  // (H3 apply 3.721 -> 3.643); c2 0.4824 -> 0.4851 — there the post-solve chain already
+  // overlaps the W branch on the side stream, and the wider dots kernel costs more than
+  // the two kernels it saves.  Automatic: on from 16 MB of M2 (option coarse_az = 0 / 1 forces).
+  if (!c.m2t.p || c.n0 == 0 || c.k0.rank == 0 || c.nneg == 0) return;
+  const long long knob = c.opt("coarse_az", -1);
+  if (knob == 0 || (knob < 0 && 8.0 * c.k0.rank * c.nneg < 16.0 * 1024.0 * 1024.0)) return;
+  const int N = c.N, n = c.n;
+  // E_s = Omega^s plus the columns its rows couple to (A's pattern is symmetric)
+  std::vector<int> mark(n, -1), eidx;
+  std::vector<long long> eoff(N + 1, 0), azoff(N + 1, 0);
+  std::vector<int> ne(N, 0), lde(N, 0);
+  for (int s = 0; s < N; ++s) {
+    if (c.h_ks[s] > 0) {
+      const size_t first = eidx.size();
+      for (long long p = c.h_poff[s]; p < c.h_poff[s + 1]; ++p) {
+        const int i = c.h_pidx[p];
+        if (mark[i] != s) {
+          mark[i] = s;
+          eidx.push_back(i);
+        }
+        for (int a = c.h_rp[i]; a < c.h_rp[i + 1]; ++a) {
+          const int j = c.h_ci[a];
+          if (mark[j] != s) {
+            mark[j] = s;
+            eidx.push_back(j);
+          }
+        }
+      }
+      std::sort(eidx.begin() + first, eidx.end());
+      ne[s] = int(eidx.size() - first);
+      lde[s] = round_up(ne[s], 4);
+    }
+    eoff[s + 1] = (long long)eidx.size();
+    azoff[s + 1] = azoff[s] + (long long)lde[s] * c.h_ks[s];
+  }
+  if (azoff[N] == 0) return;
+  c.AZ.alloc(size_t(azoff[N]));
+  c.AZ.zero(c.stream);
+  DArr<int> d_e;
+  d_e.upload(eidx, c.stream);
+  for (int s = 0; s < N; ++s) {
+    if (c.h_ks[s] == 0) continue;
+    k_az_block<<<dim3((ne[s] + 255) / 256, c.h_ks[s]), 256, 0, c.stream>>>(
+        ne[s], lde[s], d_e.p + eoff[s], c.h_ns[s], c.h_ld[s], c.pidx.p + c.h_poff[s], c.rp.p, c.ci.p, c.va.p,
+        c.Y.p + c.h_yoff[s], c.AZ.p + azoff[s]);
+    ++c.launches;
+  }
+  check_launch("az_block");
+  // M1 K+ for the second term of the coarse solve
+  const int r = c.k0.rank, nq = c.nneg;
+  c.m2.alloc(size_t(nq) * r);
+  k_m2_transpose<<<int(((long long)r * nq + 255) / 256), 256, 0, c.stream>>>(r, nq, c.m2t.p, c.m2.p);
+  ++c.launches;
+  check_launch("m2_transpose");
+  // combined family arrays: s < N the A- modes on Omega^s, N + s the (A Z)_s blocks on E_s
+  std::vector<int> ns2(2 * N), ld2(2 * N), coff2(2 * N + 1, 0), ccol2, pidx2(c.h_pidx);
+  std::vector<long long> poff2(2 * N), moff2(2 * N);
+  pidx2.insert(pidx2.end(), eidx.begin(), eidx.end());
+  const long long P = (long long)c.h_pidx.size();
+  const long long az_base = c.AZ.p - c.V.p;  // element offset between the two allocations
+  for (int s = 0; s < N; ++s) {
+    ns2[s] = c.h_ns[s];
+    ld2[s] = c.h_ld[s];
+    poff2[s] = c.h_poff[s];
+    moff2[s] = c.h_voff[s];
+    for (int k = 0; k < c.h_m[s]; ++k)
+      if (c.h_lam[c.h_poff[s] + k] != 0.0) ccol2.push_back(k);
+    coff2[s + 1] = int(ccol2.size());
+  }
+  if (coff2[N] != nq) c.fail(AWG_E_STATE, "build_az: A- mode count changed");
+  for (int s = 0; s < N; ++s) {
+    ns2[N + s] = ne[s];
+    ld2[N + s] = lde[s];
+    poff2[N + s] = P + eoff[s];
+    moff2[N + s] = az_base + azoff[s];
+    for (int k = 0; k < c.h_ks[s]; ++k) ccol2.push_back(k);
+    coff2[N + s + 1] = int(ccol2.size());
+  }
+  c.az_ns.upload(ns2, c.stream);
+  c.az_ld.upload(ld2, c.stream);
+  c.az_poff.upload(poff2, c.stream);
+  c.az_moff.upload(moff2, c.stream);
+  c.az_coff.upload(coff2, c.stream);
+  c.az_ccol.upload(ccol2, c.stream);
+  c.az_pidx.upload(pidx2, c.stream);
+  BsPlan& b = c.bs_az;
+  std::vector<int> ts, tc, nch(2 * N, 0);
+  b.maxch = 1;
+  int maxcols = 1;
+  for (int s = 0; s < 2 * N; ++s) {
+    const int cols = coff2[s + 1] - coff2[s];
+    if (cols == 0) continue;
+    maxcols = std::max(maxcols, cols);
+    nch[s] = (ns2[s] + kBsRows - 1) / kBsRows;
+    b.maxch = std::max(b.maxch, nch[s]);
+    for (int ch = 0; ch < nch[s]; ++ch) {
+      ts.push_back(s);
+      tc.push_back(ch);
+    }
+  }
+  b.ntask = int(ts.size());
+  b.ncg = (maxcols + 7) / 8;
+  b.ts.upload(ts, c.stream);
+  b.tc.upload(tc, c.stream);
+  b.nch.upload(nch, c.stream);
+  b.cnt.alloc(2 * N);
+  AWG_CUDA(cudaMemsetAsync(b.cnt.p, 0, sizeof(int) * 2 * N, c.stream));
+  b.part.alloc(size_t(nq + c.n0) * b.maxch);
+  c.az_out.alloc(size_t(nq + c.n0));
+  AWG_CUDA(cudaStreamSynchronize(c.stream));
+  c.invalidate_graphs();
+  c.az_on = true;
 }
 
 }  // namespace k

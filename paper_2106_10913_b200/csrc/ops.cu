@@ -292,6 +292,10 @@ static void h2(Ctx& c, const double* x, double* y, const int* gate, const double
   c.trigger_next = 0;
   h1(c, c.t2.p, c.t3.p, gate);                     // hp
   if (after_h1) after_h1();  // enqueues work that must follow the local solve
+  if (c.az_on) {  // Z^T A+ hp from the precomputed A Z and M1: no A+ hp, two kernels fewer
+    k::coarse_q_combine_az(c, c.t3.p, y, c.t0.p, extra, extra_ready, gate);
+    return;
+  }
   aplus(c, c.t3.p, c.t4.p, gate);                  // A+ hp
   // (hp - Q A+ hp) + corr [+ extra], fused into the Z c prolongation
   k::coarse_q_combine(c, c.t4.p, y, c.t3.p, c.t0.p, extra, extra_ready, gate);

@@ -968,6 +968,7 @@ void run_setup(Ctx& c, const awg_config& cfg) {
     ++c.launches;
     pivoted_factor(c, G, c.n0, cfg.rrf_semantics, c.k0, c.n0);
     k::build_coarse_neg(c);  // A- dots of the coarse columns for the hybrid H2 (apply path only)
+    k::build_az(c);          // A Z on ring-extended supports (post-solve half of the hybrid H2)
   }
   c.t_setup_ms[2] = now_ms() - t0;
   trace(c, "coarse operator + pivoted factor (r0 = " + std::to_string(c.k0.rank) + ")", c.t_setup_ms[2]);

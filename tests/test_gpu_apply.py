@@ -233,3 +233,26 @@ def test_precomputed_coarse_neg_dots(case):
         for op in (awg.Op.H2, awg.Op.H3):
             y1, y2 = ctx1.apply(op, x), ctx2.apply(op, x)
             assert rel(y1, y2) <= 1e-12
+
+
+@pytest.mark.parametrize("case", ["c1", "t2d", "t3d", "tragged", "telas8"])
+def test_precomputed_az_post_solve_chain(case):
+    """Option coarse_az: Z^T A+ hp of the hybrid H2's post-solve half from the
+    precomputed A Z (ring-extended supports) and M1 K+ inside the coarse solve
+    instead of A+ hp and a second Z^T pass (automatic from 16 MB of M2: c3).
+    Same sums regrouped: H2 / H3 within 1e-11 of the reference's applies either
+    way, and the solve stops at the same iteration."""
+    g, s = golden_with_base(case)
+    tol = 1e-11
+    reps = {}
+    for az in (0, 1):
+        ctx = make_ctx(g, options={"coarse_az": az})
+        assert ctx.query()["coarse_az"] == (az if s["n_minus"] > 0 and s["n0"] > 0 else 0)
+        for name, op in (("H2", awg.Op.H2), ("H3ad", awg.Op.H3)):
+            for x, y in zip(g["x_apply"], g["y_" + name]):
+                assert rel(ctx.apply(op, x), y) <= tol, (case, az, name)
+        x, rep = ctx.pcg(g["b"], s["rtol_solve"], 10000)
+        reps[az] = (rep.iterations, x)
+        ctx.close()
+    assert abs(reps[0][0] - reps[1][0]) <= 1 and abs(reps[1][0] - s["iterations"]) <= 1
+    assert rel(reps[1][1], reps[0][1]) <= 1e-9
