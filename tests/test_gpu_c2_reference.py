@@ -77,10 +77,12 @@ def test_basis_invariant_operators(run):
     """The reference's applies on its own factors vs the device's on its own:
     H1 = sum R^T D P^s D R, A- and A+ do not depend on the eigenvector basis,
     so they agree to the accuracy of the two eigensolvers.  H1 is a
-    pseudo-inverse: any normwise backward-stable eigensolver leaves it with a
-    relative error ~ eps ||B^s|| / lambda_min+ (here 1e-16 x 4e6 / ~1e-2; cyclic
-    Jacobi is relatively accurate on such graded matrices, Householder +
-    bisection is not).  Measured: H1 5.8e-9, A- 9.6e-12, A+ 4.9e-14."""
+    pseudo-inverse (error ~ 1 / lambda_min+), and the reference's cyclic Jacobi
+    stops at an off-diagonal norm of 1e-14 ||B^s||_F ~ 7e-7 (dense.cpp:145): its
+    smallest positive eigenpair on subdomain 5 has residual 2.3e-9 against
+    LAPACK's 3.0e-10, and LAPACK's P^s x differs from the reference's by 9.6e-9
+    (profiles/r02e/h1_accuracy_c2.txt).  Measured here: H1 5.8e-9, A- 9.6e-12,
+    A+ 4.9e-14."""
     name, p, ctx, meta, g = run
     out = {}
     for op, key in ((awg.Op.H1, "y_H1"), (awg.Op.AMINUS, "y_Aminus"), (awg.Op.APLUS, "y_Aplus"), (awg.Op.H3, "y_H3ad")):
