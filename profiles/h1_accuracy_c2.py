@@ -33,3 +33,9 @@ print("P lapack+RQ eigenvalues vs ref:", rel(P(Z,rq,m),pr))
 print("eigenvalue rel err lapack vs ref (small):", np.max(np.abs(w[m:m+50]-lr[m:m+50])/lr[m:m+50]), " RQ:", np.max(np.abs(rq[m:m+50]-lr[m:m+50])/lr[m:m+50]))
 # residual check of reference vs lapack
 print("resid ref", np.linalg.norm(B@Vr[:,m]-lr[m]*Vr[:,m]), "lapack", np.linalg.norm(B@Z[:,m]-w[m]*Z[:,m]))
+
+# residual / Rayleigh-quotient / orthogonality statistics of both eigenpair sets
+for name,(VV,ll) in {"reference(Jacobi)":(Vr,lr),"LAPACK":(Z,w)}.items():
+    for cnt in (20, ns-m):
+        Zs=VV[:,m:m+cnt]; res=np.linalg.norm(B@Zs-Zs*ll[m:m+cnt],axis=0); rq=np.einsum('ij,ij->j',Zs,B@Zs)
+        print(name, cnt, "resid max %.3e median %.3e"%(res.max(),np.median(res)), "eig vs RQ rel max %.3e"%np.max(np.abs(rq-ll[m:m+cnt])/np.abs(ll[m:m+cnt])), "orth %.2e"%np.abs(Zs.T@Zs-np.eye(cnt)).max())
