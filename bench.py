@@ -247,6 +247,15 @@ def aggregate(dev_ms, applies, e2e_s, e2e_applies, dist=None, device=None):
     return float(t[0]), float(w[0]), float(t[1]), float(w[1])
 
 
+def rank_rhs(b0, rank):
+    """The right-hand side rank `rank` solves: rank 0 the config's own b, every
+    other rank its own seeded uniform[-1, 1] vector (independent units: the
+    N-GPU run shards right-hand sides, not the problem)."""
+    if rank == 0:
+        return b0
+    return np.random.default_rng(1000 + rank).uniform(-1.0, 1.0, len(b0))
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -326,8 +335,7 @@ def main():
     rtol = p.rtol
 
     # RHS set: rank r solves b_r (independent units); resident in HBM
-    rng = np.random.default_rng(1000 + rank)
-    b_host = p.b if rank == 0 else rng.uniform(-1.0, 1.0, p.n)
+    b_host = rank_rhs(p.b, rank)
     b_dev = torch.tensor(b_host, dtype=torch.float64, device="cuda")
     x_dev = torch.empty_like(b_dev)
 
